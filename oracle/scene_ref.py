@@ -1,0 +1,106 @@
+"""The per-frame hybrid step over a scene -- TEST INFRASTRUCTURE ONLY.
+
+Follows `Simulation.__init__` / `Simulation.step` (reference
+`pkg/src/hybridsea/harness.py:72-111,131-209`) stage order: t = frame*dt,
+background synthesis, per-patch injection, per-patch advection, per-patch
+synthesis + finish, blend (evaluated at patch nodes, the tile the stream and
+buoyancy probes read), optional FFT-resolution composite (:219-241).
+
+Differences from the reference harness, all SURVEY App. A knobs:
+  * each patch owns a `Generator(Philox(key=[seed, patch_id]))` instead of a
+    shared PCG64 (harness.py:79) -- the counter-based stream the GPU twins;
+  * bucket tables may be log-spaced, gamma/spread may be pinned;
+  * bodies are not part of the hot path.
+
+A scene is a plain dict (see `paper_2511_02852_b200.config.SimConfig.scene_dict`).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import blend_ref, ocean_ref, particles_ref, spectrum_ref, synth_ref
+
+
+def build_params(sc: dict) -> spectrum_ref.Params:
+    return spectrum_ref.jonswap(sc["u10"], sc["fetch"], sc["g"], gamma=sc.get("gamma"),
+                                spread_s=sc.get("spread_s"))
+
+
+def build_buckets(sc: dict, p: spectrum_ref.Params) -> spectrum_ref.Buckets:
+    if sc.get("bucket_spacing", "equal-energy") == "log":
+        return spectrum_ref.log_buckets(p, sc["omega_lo"], sc["omega_hi"], sc["n_omega"], sc["n_theta"])
+    return spectrum_ref.equal_energy_buckets(p, sc["n_omega"], sc["n_theta"])
+
+
+class OracleScene:
+    """CPU twin of one hybrid scene."""
+
+    def __init__(self, sc: dict, h0: np.ndarray | None = None):
+        self.sc = sc
+        self.p = build_params(sc)
+        self.bk = build_buckets(sc, self.p)
+        self.frame = 0
+        self.patches = [particles_ref.Patch(o[0], o[1], s[0], s[1], m)
+                        for o, s, m in zip(sc["patch_origins"], sc["patch_sizes"], sc["patch_margins"])]
+        self.res = list(sc["patch_res"])
+        self.pools = [particles_ref.Pool() for _ in self.patches]
+        self.ledgers = [particles_ref.Ledger(self.bk.n, rho=sc["rho"]) for _ in self.patches]
+        self.rngs = [np.random.Generator(np.random.Philox(key=[sc["seed"], i]))
+                     for i in range(len(self.patches))]
+        self.plans = [synth_ref.plan(self.bk, pc.l1 / (r - 1), r, sc["amplitude_convention"],
+                                     sc["trough_fraction"])
+                      for pc, r in zip(self.patches, self.res)]
+        self.fft = sc["mode"] != "wp-only"
+        if self.fft:
+            self.h0 = h0 if h0 is not None else ocean_ref.initial_amplitudes(
+                self.p, sc["mean_direction"], sc["fft_n"], sc["fft_domain"], sc["seed"],
+                band=sc.get("fft_band"))
+        self.background = None
+        self.fields = []
+
+    def step(self, dt: float | None = None, synth: bool = True) -> dict:
+        sc = self.sc
+        dt = sc["dt"] if dt is None else dt
+        t = self.frame * dt
+        out = {"t": t}
+        if self.fft:
+            h, dx, dy, nrm = ocean_ref.evolve(self.h0, sc["fft_domain"], self.p.g, t, sc["fft_choppiness"])
+            n = sc["fft_n"]
+            self.background = blend_ref.Field(h, nrm, np.zeros(2), sc["fft_domain"] / n)
+            out.update(height=h, dx=dx, dy=dy, normal=nrm)
+        for pc, pool, led, rng in zip(self.patches, self.pools, self.ledgers, self.rngs):
+            pool.append(particles_ref.inject(pc, self.bk, self.p, sc["mean_direction"], led, dt, rng,
+                                             t=t, beta=sc["trough_fraction"]))
+        for pc, pool, led in zip(self.patches, self.pools, self.ledgers):
+            particles_ref.advect(pool, self.bk, dt, pc, led, self.p.g)
+        if synth:
+            self.fields = []
+            for pc, pool, r, pl in zip(self.patches, self.pools, self.res, self.plans):
+                hp, clamped = synth_ref.synthesize(pool, pc, r, pl)
+                nrm, _ = synth_ref.finish(hp, pc)
+                self.fields.append(blend_ref.Field(hp, nrm, pc.lo.copy(), pc.l1 / (r - 1)))
+            pairs = list(zip(self.patches, self.fields))
+            out["patch_heights"] = [f.height for f in self.fields]
+            out["patch_normals"] = [f.normal for f in self.fields]
+            tiles = [blend_ref.sample(self.background, pairs, blend_ref.patch_nodes(pc, r))
+                     for pc, r in zip(self.patches, self.res)]
+            out["blend_heights"] = [tl[0] for tl in tiles]
+            out["blend_normals"] = [tl[1] for tl in tiles]
+        out["counts"] = np.stack([pool.counts(self.bk.n) for pool in self.pools]) if self.pools else None
+        self.frame += 1
+        return out
+
+    def composite(self) -> np.ndarray:
+        sc = self.sc
+        return blend_ref.stitched(self.background, sc["fft_n"], sc["fft_domain"],
+                                  list(zip(self.patches, self.fields)))
+
+
+def ledger_arrays(led: particles_ref.Ledger) -> dict:
+    return {"acc": led.acc.copy(), "groups": led.groups.copy(), "e_in": led.e_in.copy(),
+            "e_out": led.e_out.copy()}
+
+
+__all__ = ["OracleScene", "build_params", "build_buckets", "ledger_arrays"]

@@ -1,0 +1,261 @@
+"""Pin the CPU oracle against the reference: golden vectors produced by the
+reference package itself (tests/golden/make_golden.py) and the reference
+tests' frozen known-answer constants.  CPU only."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import (blend_ref, ocean_ref, particles_ref, philox_ref, scene_ref, spectrum_ref,
+                    synth_ref)
+
+G = 9.81
+
+
+# -- known-answer constants from the reference tests ------------------------
+
+def test_frozen_jonswap_constants():
+    # pkg/tests/test_spectrum.py:32-36, 60-64
+    p = spectrum_ref.jonswap(5.0, 10000.0, G)
+    assert p.alpha == pytest.approx(0.012308162248519699, rel=1e-12)
+    assert p.omega_p == pytest.approx(2.736604379410473, rel=1e-12)
+    assert p.gamma == pytest.approx(2.161665653748187, rel=1e-12)
+    assert spectrum_ref.s1d(p, 2.737) == pytest.approx(0.0047795943200512805, rel=1e-12)
+
+
+def test_frozen_groups_and_advect_constants():
+    # pkg/tests/test_particles.py:76-84 (8 L dt w^3/(pi^3 g)) and :222-231
+    for w, expect in ((2.737, 0.898761588955238), (6.843, 14.046228565318918)):
+        total = 2.0 * (4.0 * 100.0 * (1.0 / 60.0) * w ** 3 / (math.pi ** 3 * G))
+        assert total == pytest.approx(expect, rel=1e-12)
+    assert G / 2.737 == pytest.approx(3.5842162952137375, rel=1e-12)
+
+
+# -- golden vectors ----------------------------------------------------------
+
+def _table(gd, prefix, bk):
+    np.testing.assert_allclose(bk.omega, gd[f"{prefix}_omega"], rtol=1e-13)
+    np.testing.assert_allclose(bk.width, gd[f"{prefix}_width"], rtol=1e-12)
+    np.testing.assert_allclose(bk.radius, gd[f"{prefix}_radius"], rtol=1e-13)
+    np.testing.assert_allclose(bk.speed, gd[f"{prefix}_speed"], rtol=1e-13)
+    np.testing.assert_allclose(bk.energy, gd[f"{prefix}_energy"], rtol=1e-10)
+    np.testing.assert_allclose(bk.spread_s, gd[f"{prefix}_s"], rtol=1e-13)
+    np.testing.assert_allclose(bk.spread_c, gd[f"{prefix}_c"], rtol=1e-13)
+
+
+def test_spectrum_golden(golden):
+    gd = golden("spectrum.npz")
+    for tag, (u, f) in {"a": (5.0, 1e4), "b": (10.0, 1e5), "c": (15.0, 1e5)}.items():
+        p = spectrum_ref.jonswap(u, f, G)
+        np.testing.assert_array_equal([p.alpha, p.omega_p, p.gamma], gd[f"{tag}_params"])
+        np.testing.assert_allclose(spectrum_ref.s1d(p, gd[f"{tag}_s1d_w"]), gd[f"{tag}_s1d"],
+                                   rtol=1e-14, atol=0)
+        lo, hi = 0.5 * p.omega_p, 2.5 * p.omega_p
+        assert spectrum_ref.band_integral(p, lo, hi) == pytest.approx(gd[f"{tag}_band"][0], rel=1e-14)
+        for n in (8, 12, 16):
+            _table(gd, f"{tag}_eq{n}", spectrum_ref.equal_energy_buckets(p, n, 16))
+    pb = spectrum_ref.jonswap(10.0, 1e5, G, gamma=3.3, spread_s=8.0)
+    _table(gd, "pr1_log8", spectrum_ref.log_buckets(pb, 0.5, 4.0, 8, 16))
+    pc = spectrum_ref.jonswap(10.0, 1e5, G)
+    _table(gd, "c3_log16", spectrum_ref.log_buckets(pc, 0.3, 6.0, 16, 2))
+    np.testing.assert_allclose([spectrum_ref.spread_norm(s) for s in gd["spread_s_vals"]],
+                               gd["spread_norm_vals"], rtol=1e-14)
+
+
+def test_fft_golden(golden):
+    gd = golden("fft.npz")
+    p = spectrum_ref.jonswap(5.0, 1e4, G)
+    h0 = ocean_ref.initial_amplitudes(p, 0.0, 16, 500.0, 7)
+    np.testing.assert_allclose(h0, gd["n16_h0"], rtol=1e-13, atol=1e-300)
+    for k, t in enumerate(gd["n16_times"]):
+        h, dx, dy, nrm = ocean_ref.evolve(gd["n16_h0"], 500.0, G, float(t), 1.0)
+        np.testing.assert_allclose(h, gd[f"n16_t{k}_h"], atol=1e-15)
+        np.testing.assert_allclose(np.stack([dx, dy], -1), gd[f"n16_t{k}_d"], atol=1e-15)
+        np.testing.assert_allclose(nrm, gd[f"n16_t{k}_n"], atol=1e-14)
+    p2 = spectrum_ref.jonswap(10.0, 1e5, G)
+    h0 = ocean_ref.initial_amplitudes(p2, 0.3, 64, 1000.0, 3)
+    np.testing.assert_allclose(h0, gd["n64_h0"], rtol=1e-12, atol=1e-300)
+    for k, t in enumerate(gd["n64_times"]):
+        h, dx, dy, nrm = ocean_ref.evolve(gd["n64_h0"], 1000.0, G, float(t), 1.2)
+        np.testing.assert_allclose(h, gd[f"n64_t{k}_h"], atol=1e-14)
+        np.testing.assert_allclose(np.stack([dx, dy], -1), gd[f"n64_t{k}_d"], atol=1e-14)
+        np.testing.assert_allclose(nrm, gd[f"n64_t{k}_n"], atol=1e-13)
+    hv, nv = ocean_ref.sample_periodic(h, nrm, (0.0, 0.0), 1000.0 / 64, gd["n64_sample_pts"])
+    np.testing.assert_allclose(hv, gd["n64_sample_h"], atol=1e-14)
+    np.testing.assert_allclose(nv, gd["n64_sample_n"], atol=1e-13)
+
+
+def test_direct_dft_pin():
+    # the reference's brute-force oracle: pkg/tests/oracles.py:59-64
+    p = spectrum_ref.jonswap(5.0, 1e4, G)
+    h0 = ocean_ref.initial_amplitudes(p, 0.0, 16, 500.0, 7)
+    hh = ocean_ref.rotated_spectrum(h0, 500.0, G, 12.75)
+    idx = np.arange(16)
+    tw = np.exp(2j * math.pi * np.outer(idx, idx) / 16)
+    ref = (tw @ hh @ tw.T).real
+    h, *_ = ocean_ref.evolve(h0, 500.0, G, 12.75, 0.0)
+    np.testing.assert_allclose(h, ref, atol=1e-9)
+
+
+def _pr1():
+    p = spectrum_ref.jonswap(10.0, 1e5, G, gamma=3.3, spread_s=8.0)
+    bk = spectrum_ref.log_buckets(p, 0.5, 4.0, 8, 16)
+    patch = particles_ref.Patch(100.0, 200.0, 64.0, 64.0, 8.0)
+    return p, bk, patch
+
+
+def _pool_eq(pool, gd, prefix, exact=True):
+    assert len(pool) == len(gd[f"{prefix}_amp"])
+    np.testing.assert_array_equal(pool.bucket, gd[f"{prefix}_bucket"])
+    if exact:
+        np.testing.assert_array_equal(pool.pos, gd[f"{prefix}_pos"])
+        np.testing.assert_array_equal(pool.dir, gd[f"{prefix}_dir"])
+        np.testing.assert_array_equal(pool.amp, gd[f"{prefix}_amp"])
+    else:
+        np.testing.assert_allclose(pool.pos, gd[f"{prefix}_pos"], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(pool.amp, gd[f"{prefix}_amp"], rtol=1e-13)
+
+
+def test_inject_advect_chain_bit_exact(golden):
+    gd = golden("particles.npz")
+    p, bk, patch = _pr1()
+    led = particles_ref.Ledger(8)
+    rng = np.random.Generator(np.random.Philox(key=[0, 0]))
+    pool = particles_ref.Pool()
+    dt = 1.0 / 60.0
+    for k in range(120):
+        new = particles_ref.inject(patch, bk, p, 0.0, led, dt, rng, t=k * dt)
+        assert len(new) == gd["chain_ninj"][k]
+        if k == 30:
+            _pool_eq(new, gd, "inj30")
+        pool.append(new)
+        particles_ref.advect(pool, bk, dt, patch, led, G)
+        np.testing.assert_array_equal(pool.counts(8), gd["chain_counts"][k])
+    _pool_eq(pool, gd, "chain_final")
+    np.testing.assert_array_equal(led.acc, gd["chain_acc"])
+    np.testing.assert_array_equal(led.groups, gd["chain_groups"])
+    np.testing.assert_allclose(led.e_in, gd["chain_e_in"], rtol=1e-13)
+    np.testing.assert_allclose(led.e_out, gd["chain_e_out"], rtol=1e-13)
+
+
+def test_advect_golden(golden):
+    gd = golden("particles.npz")
+    p, bk, patch = _pr1()
+    pool = particles_ref.Pool(gd["chain_final_pos"].copy(), gd["chain_final_dir"].copy(),
+                              gd["chain_final_amp"].copy(), gd["chain_final_bucket"].copy(),
+                              np.zeros(len(gd["chain_final_amp"])))
+    led = particles_ref.Ledger(8)
+    dropped = particles_ref.advect(pool, bk, 7.0 / 60.0, patch, led, G)
+    _pool_eq(pool, gd, "adv7_kept")
+    _pool_eq(dropped, gd, "adv7_dropped")
+    np.testing.assert_allclose(led.e_out, gd["adv7_e_out"], rtol=1e-13)
+
+
+def test_high_rate_inject_golden(golden):
+    gd = golden("particles.npz")
+    pc = spectrum_ref.jonswap(10.0, 1e5, G)
+    bk = spectrum_ref.log_buckets(pc, 0.3, 6.0, 16, 2)
+    patch = particles_ref.Patch(-50.0, 30.0, 256.0, 192.0, 10.0)
+    led = particles_ref.Ledger(16)
+    rng = np.random.Generator(np.random.Philox(key=[5, 1]))
+    for k in range(3):
+        new = particles_ref.inject(patch, bk, pc, 0.7, led, 0.1, rng, t=k * 0.1, beta=0.8)
+    _pool_eq(new, gd, "hr_inj")
+    np.testing.assert_array_equal(led.acc, gd["hr_acc"])
+    np.testing.assert_array_equal(led.groups, gd["hr_groups"])
+    np.testing.assert_allclose(led.e_in, gd["hr_e_in"], rtol=1e-13)
+
+
+def test_philox_stream_model():
+    gen = np.random.Generator(np.random.Philox(key=[0xDEADBEEF, 42]))
+    gen.uniform(size=3)                       # leave a partially used buffer
+    st = philox_ref.state_from_generator(gen)
+    expect = gen.bit_generator.random_raw(11)
+    np.testing.assert_array_equal(philox_ref.stream_words(st, 0, 11), expect)
+    gen2 = np.random.Generator(np.random.Philox(key=[7, 3]))
+    st2 = philox_ref.state_from_generator(gen2)
+    u = gen2.uniform(-0.25, 0.25, size=9)
+    np.testing.assert_array_equal(philox_ref.uniform_from_words(philox_ref.stream_words(st2, 0, 9),
+                                                                -0.25, 0.25), u)
+
+
+def test_synth_golden(golden):
+    gp = golden("particles.npz")
+    gd = golden("synth.npz")
+    p, bk, patch = _pr1()
+    pool = particles_ref.Pool(gp["chain_final_pos"], gp["chain_final_dir"], gp["chain_final_amp"],
+                              gp["chain_final_bucket"], np.zeros(len(gp["chain_final_amp"])))
+    res = 129
+    pl = synth_ref.plan(bk, patch.l1 / (res - 1), res)
+    np.testing.assert_array_equal(pl.factors, gd["plan_factors"])
+    np.testing.assert_array_equal([k.half for k in pl.kernels], gd["plan_half"])
+    np.testing.assert_allclose([k.gain for k in pl.kernels], gd["plan_gain"], rtol=1e-14)
+    h, c = synth_ref.synthesize(pool, patch, res, pl)
+    scale = np.abs(gd["h_plan"]).max()
+    np.testing.assert_allclose(h, gd["h_plan"], atol=1e-12 * scale)
+    assert c == gd["clamped_plan"][0]
+    ex = synth_ref.plan(bk, patch.l1 / (res - 1), res, adaptive=False)
+    h2, c2 = synth_ref.synthesize(pool, patch, res, ex)
+    np.testing.assert_allclose(h2, gd["h_exact"], atol=1e-12 * scale)
+    assert c2 == gd["clamped_exact"][0]
+    pk = synth_ref.plan(bk, patch.l1 / (res - 1), res, convention="peak", adaptive=False)
+    np.testing.assert_allclose([k.gain for k in pk.kernels], gd["gain_peak"], rtol=1e-14)
+    nrm, _ = synth_ref.finish(gd["h_plan"], patch)
+    np.testing.assert_allclose(nrm, gd["finish_n"], atol=1e-14)
+    _, disp = synth_ref.finish(gd["h_plan"], patch, choppiness=0.7, scale=2.0)
+    np.testing.assert_allclose(disp, gd["finish_chop_d"], atol=1e-15)
+
+
+def test_smoothing_forms_agree():
+    rng = np.random.default_rng(0)
+    grid = rng.standard_normal((40, 33))
+    for h in (1, 4, 9):
+        taps = synth_ref.raised_cosine(h)
+        a = synth_ref.smooth_axis(synth_ref.smooth_axis(grid, taps, 0), taps, 1)
+        b = synth_ref.smooth_axis_direct(synth_ref.smooth_axis_direct(grid, taps, 0), taps, 1)
+        np.testing.assert_allclose(a, b, atol=1e-12)
+
+
+def test_blend_golden(golden):
+    gd = golden("synth.npz")
+    gf = golden("fft.npz")
+    _, _, patch = _pr1()
+    res = 129
+    texel = patch.l1 / (res - 1)
+    h, dx, dy, nrm = ocean_ref.evolve(gf["n64_h0"], 1000.0, G, 1.5, 1.2)
+    bg = blend_ref.Field(h, nrm, np.zeros(2), 1000.0 / 64)
+    pn, _ = synth_ref.finish(gd["h_plan"], patch)
+    pf = blend_ref.Field(gd["h_plan"], pn, patch.lo, texel)
+    hb, nb = blend_ref.sample(bg, [(patch, pf)], blend_ref.patch_nodes(patch, res))
+    np.testing.assert_allclose(hb, gd["blend_h"], atol=1e-13)
+    np.testing.assert_allclose(nb, gd["blend_n"], atol=1e-13)
+    hs, ns = blend_ref.sample(bg, [(patch, pf)], gd["sample_pts"])
+    np.testing.assert_allclose(hs, gd["sample_h"], atol=1e-13)
+    np.testing.assert_allclose(ns, gd["sample_n"], atol=1e-13)
+    comp = blend_ref.stitched(bg, 64, 1000.0, [(patch, pf)])
+    np.testing.assert_allclose(comp, gd["stitched"], atol=1e-13)
+
+
+def sim_scene():
+    return {"u10": 5.0, "fetch": 10000.0, "g": G, "mean_direction": 0.0, "n_omega": 8, "n_theta": 8,
+            "bucket_spacing": "equal-energy", "rho": 1000.0, "dt": 0.05, "mode": "hybrid", "seed": 11,
+            "trough_fraction": 1.0, "amplitude_convention": "energy", "fft_n": 64,
+            "fft_domain": 500.0, "fft_choppiness": 1.0, "patch_origins": [(200.0, 180.0)],
+            "patch_sizes": [(100.0, 80.0)], "patch_res": [65], "patch_margins": [10.0]}
+
+
+def test_scene_chain_matches_reference_simulation(golden):
+    gd = golden("sim.npz")
+    scene = scene_ref.OracleScene(sim_scene())
+    for k in range(6):
+        out = scene.step()
+        np.testing.assert_array_equal(out["counts"][0], gd["counts"][k])
+        np.testing.assert_allclose(scene.ledgers[0].e_in, gd["e_in"][k], rtol=1e-12)
+        np.testing.assert_allclose(scene.ledgers[0].e_out, gd["e_out"][k], rtol=1e-12)
+    np.testing.assert_allclose(out["height"], gd["bg_h"], atol=1e-13)
+    scale = np.abs(gd["patch_h"]).max()
+    np.testing.assert_allclose(out["patch_heights"][0], gd["patch_h"], atol=1e-12 * scale)
+    np.testing.assert_allclose(scene.composite(), gd["stitched"], atol=1e-12)
+    seg = scene.pools[0]
+    np.testing.assert_array_equal(seg.pos, gd["pool_pos"])
+    np.testing.assert_array_equal(seg.bucket, gd["pool_bucket"])
