@@ -1,0 +1,292 @@
+/*
+ * hybridsea_b200 -- C ABI of the B200-native hybrid ocean step.
+ *
+ * The reference (`hybridsea` 0.1.0, pure Python + numpy) has no FFI layer:
+ * its operator API is the set of Python functions re-exported by
+ * `pkg/src/hybridsea/__init__.py:8-59`.  Each entry point below replaces one
+ * of those functions on the per-frame hot path; the
+ * Python package `paper_2511_02852_b200` keeps the reference signatures and
+ * calls these through ctypes.
+ *
+ * Conventions
+ *   - every pointer named in an args struct is a DEVICE pointer unless the
+ *     comment says "host"; the caller (PyTorch's caching allocator) owns all
+ *     memory, kernels never allocate;
+ *   - `stream` is a cudaStream_t passed as void*; every call only enqueues
+ *     work (memsets + kernels) on it, never synchronises, so a whole frame is
+ *     CUDA-graph capturable;
+ *   - return 0 on success, nonzero on a host-side validation or launch error;
+ *     hs_last_error() then describes it (thread-local).
+ *   - arrays of per-patch / per-bucket descriptors are device arrays of the
+ *     structs below (plain-old-data, 8-byte aligned).
+ */
+#ifndef HYBRIDSEA_B200_H
+#define HYBRIDSEA_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HS_API __attribute__((visibility("default")))
+#else
+#define HS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_ABI_VERSION 1
+#define HS_MAX_BUCKETS 32
+#define HS_MAX_PATCHES 256
+
+/* status word bits written by kernels (device int, checked by the host
+ * outside the captured graph) */
+#define HS_STATUS_POOL_OVERFLOW  1
+#define HS_STATUS_STAGE_OVERFLOW 2
+#define HS_STATUS_NONFINITE      4
+
+HS_API int hs_abi_version(void);
+HS_API const char* hs_last_error(void);
+/* sizeof of ABI struct `which` (0 HsBucket, 1 HsPatch, 2 HsLayer, 3 HsPool,
+ * 4..12 the args structs in declaration order); -1 if unknown */
+HS_API int hs_struct_size(int which);
+
+/* ------------------------------------------------------------------------ */
+/* Per-bucket constants (replaces the BucketTable array views,
+ * reference spectrum.py:233-257).                                           */
+typedef struct {
+    double omega;      /* representative frequency (rad/s) */
+    double width;      /* bucket width delta_omega */
+    double radius;     /* pi g / omega^2 */
+    double speed;      /* g / omega */
+    double s1d;        /* S_J(omega) (spectrum.py:108-121), fp64 */
+    double spread_s;   /* cos-2s exponent s at omega */
+    double spread_c;   /* C(s) normalisation */
+    double pad;
+} HsBucket;
+
+/* Axis-aligned patch rectangle + its pool / grid / layer bookkeeping
+ * (replaces PatchRegion, particles.py:43-74, and PatchState, harness.py:49-62). */
+typedef struct {
+    double x0, y0;       /* min corner (world, m) */
+    double x1, y1;       /* max corner = min + (l1, l2) */
+    double l1, l2;       /* side lengths */
+    double margin;       /* blend band width */
+    double texel;        /* l1 / (res - 1) */
+    long long pool_base; /* element offset of this patch's pool region */
+    long long stage_base;/* element offset of this patch's staging region */
+    long long grid_base; /* element offset of this patch's (res x ny) grids */
+    int pool_capacity;
+    int stage_capacity;
+    int res, ny;         /* node grid: res along x, ny along y */
+    int layer_base;      /* first HsLayer of this patch */
+    int pad0;
+} HsPatch;
+
+/* One per (patch, bucket) synthesis layer (LayerPlan, patch_synthesis.py:227-258). */
+typedef struct {
+    long long raw_off;   /* float offset of the padded raw layer (wx*wy) */
+    long long sm_off;    /* float offset of the smoothed crop (ncx*ncy) */
+    int f;               /* decimation factor */
+    int H;               /* kernel half width (taps 2H+1) */
+    int pad;             /* H + 1 */
+    int ncx, ncy;        /* coarse node grid (crop) */
+    int wx, wy;          /* padded layer dims ncx+2pad, ncy+2pad */
+    int taps_off;        /* offset into the taps array */
+    float gain;          /* output gain */
+    int pad0;
+} HsLayer;
+
+/* Structure-of-arrays particle pool.  Pools of all patches live in one set of
+ * arrays; patch p owns [pool_base, pool_base + pool_capacity).  Within a patch
+ * particles are bucket-segmented: bucket b occupies count[p*nb + b] elements
+ * starting after buckets < b, each segment in stable birth order (the
+ * reference's order restricted to that bucket, particles.py:167-178).        */
+typedef struct {
+    double* x;  double* y;     /* world position (fp64: keeps cull decisions exact) */
+    double* ux; double* uy;    /* unit direction (fp64) */
+    float* amp;                /* signed amplitude */
+} HsPool;
+
+/* ------------------------------------------------------------------------ */
+/* FFT background at time t.  Replaces evolve_and_synthesize
+ * (fft_background.py:181-208) incl. spectral_at (:155-159) and periodic
+ * grid_normals (:162-178).                                                  */
+typedef struct {
+    int n;                    /* power of two, 4..4096 */
+    int emit_normals;         /* write `normal` (n*n*3) */
+    double g, t, choppiness;  /* t is used when frame_ptr is NULL */
+    const long long* frame_ptr; /* optional device frame counter: t = frame * dt
+                                 (reference harness.py:134), graph-replay safe */
+    double dt;
+    double spacing;           /* domain / n */
+    const double* kf;         /* [n] 2*pi*fftfreq(n, d=domain/n) */
+    const float* h0;          /* [n*n] complex64 (re,im) */
+    const float* twiddle;     /* [n/2] complex64 exp(+2 pi i k/n) */
+    float* work_a;            /* [n*n] complex64 scratch */
+    float* work_b;            /* [(n/2+1)*n] complex64 scratch */
+    float* height;            /* [n*n] */
+    float* dx;                /* [n*n] */
+    float* dy;                /* [n*n] */
+    float* normal;            /* [n*n*3] or NULL */
+    double* sumsq;            /* scalar accumulator += sum(height^2), or NULL */
+} HsFftArgs;
+HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Boundary injection for all patches (one CTA per patch).  Replaces inject
+ * (particles.py:219-300).  Random draws follow numpy's Philox4x64-10 stream:
+ * rng[8*p + 0..1] = key, [2..5] = counter0 (256-bit LE), [6] = draw index.   */
+typedef struct {
+    int n_patches, nb, n_theta;
+    const HsBucket* buckets;       /* [nb] */
+    const HsPatch* patches;        /* [n_patches] */
+    const double* half_rate;       /* [n_patches*nb*4] */
+    double mean_dir, beta, rho, g;
+    double* acc;                   /* [n_patches*nb*4] ledger accumulators */
+    long long* groups;             /* [n_patches*nb] */
+    double* e_in;                  /* [n_patches*nb] */
+    unsigned long long* rng;       /* [n_patches*8] */
+    HsPool stage;                  /* staging arrays (per-patch regions) */
+    int* stage_count;              /* [n_patches*nb] out */
+    double* scratch;               /* [n_patches*member_capacity*2] */
+    int member_capacity;           /* per patch: >= max groups * n_theta */
+    int* status;
+} HsInjectArgs;
+HS_API int hs_inject(const HsInjectArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Advect + cull + stable bucket-segmented compaction (+ fused splat) for all
+ * patches.  Replaces advect (particles.py:303-328), ParticleSet.compact
+ * (:167-178) and the per-bucket _splat of synthesize
+ * (patch_synthesis.py:165-186, 298-310).                                    */
+typedef struct {
+    int n_patches, nb;
+    const HsBucket* buckets;
+    const HsPatch* patches;
+    double dt, rho, g;
+    HsPool in;  const int* in_count;       /* [n_patches*nb] */
+    HsPool stage; const int* stage_count;  /* [n_patches*nb]; may be NULL */
+    HsPool out; int* out_count;            /* [n_patches*nb]; zeroed here */
+    HsPool dropped; int* dropped_count;    /* optional (x == NULL to skip): despawned
+                                              particles, same segmented layout */
+    double* e_out;                         /* [n_patches*nb] despawn ledger */
+    int splat;                             /* fuse the layer splat */
+    float* raw_layers;                     /* zeroed here when splat */
+    long long raw_layers_len;              /* floats */
+    const HsLayer* layers;                 /* [n_patches*nb] */
+    int* clamped;                          /* [n_patches] += clamp counts */
+    unsigned long long* tile_state;        /* [max_tiles] */
+    int max_tiles;
+    int* tile_counter;                     /* scalar */
+    int* status;
+} HsAdvectArgs;
+HS_API int hs_advect(const HsAdvectArgs* a, void* stream);
+
+/* Splat-only pass over a bucket-segmented pool (synthesize on a pool that was
+ * not just advected).                                                       */
+typedef struct {
+    int n_patches, nb;
+    const HsPatch* patches;
+    HsPool pool; const int* count;         /* [n_patches*nb] */
+    float* raw_layers; long long raw_layers_len;
+    const HsLayer* layers;
+    int* clamped;
+    int max_count;                         /* host upper bound of any patch count */
+} HsSplatArgs;
+HS_API int hs_splat(const HsSplatArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Separable raised-cosine smoothing of every layer (all patches, all
+ * buckets) from the raw padded layers into the cropped smoothed layers.
+ * Replaces smooth_layer/convolve1d_zero (patch_synthesis.py:105-130,206-209). */
+typedef struct {
+    int n_layers;
+    const HsLayer* layers;
+    const float* taps;
+    const float* raw_layers;
+    float* smooth_layers;
+    const int* tile_prefix;   /* [n_layers+1] cumulative 32x32 tile counts */
+    int total_tiles;
+    int max_H;
+} HsSmoothArgs;
+HS_API int hs_smooth(const HsSmoothArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Compose: gain-sum of the bilinearly upsampled layers (synthesize,
+ * patch_synthesis.py:301-313), clamped-border normals (finish_field,
+ * :323-340) and the smoothstep blend against the periodic background at the
+ * patch nodes (SurfaceSampler._raw, coupling.py:120-141).                   */
+typedef struct {
+    int n_patches, nb;
+    const HsPatch* patches;
+    const HsLayer* layers;
+    const float* smooth_layers;
+    const int* tile_prefix;     /* [n_patches+1] cumulative 32x32 tile counts */
+    int total_tiles;
+    /* background (may be NULL: flat water) */
+    const float* bg_height; const float* bg_normal; int bg_n; double bg_spacing;
+    /* outputs, per patch at grid_base (res*ny), NULL to skip */
+    float* patch_height;        /* pre-blend patch heights */
+    float* patch_normal;        /* (res*ny*3) patch FD normals */
+    float* blend_height;        /* blended heights */
+    float* blend_normal;        /* (res*ny*3) blended normals */
+    int blend_mode;             /* 0: no blend, 1: blend */
+    double* interior_sumsq;     /* [n_patches] += sum h^2 over the interior inset, or NULL */
+    long long* interior_count;  /* [n_patches] matching counts, or NULL */
+} HsComposeArgs;
+HS_API int hs_compose(const HsComposeArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Surface queries at arbitrary world points: periodic background plus
+ * clamped patch sampling with smoothstep weights.  Replaces
+ * SurfaceSampler.sample (coupling.py:143-161, normal_mode "blend"),
+ * sample_periodic (fft_background.py:222-249), sample_clamped (coupling.py:63-82). */
+typedef struct {
+    int n_points;
+    const double* points;       /* [n_points*2] world x,y */
+    const float* bg_height; const float* bg_normal; int bg_n; double bg_spacing;
+    double bg_x0, bg_y0;
+    int n_patches;
+    const HsPatch* patches;
+    const float* patch_height;  /* per patch at grid_base */
+    const float* patch_normal;
+    float* out_height;
+    float* out_normal;          /* [n_points*3] or NULL */
+    int clamped_only;           /* 1: sample_clamped of patch 0 only, no weights */
+} HsSampleArgs;
+HS_API int hs_sample(const HsSampleArgs* a, void* stream);
+
+/* Global FFT-resolution composite: copy the background and resample the
+ * patch boxes (Simulation.stitched_heights, harness.py:219-241).            */
+typedef struct {
+    int n; double spacing;
+    const float* bg_height; const float* bg_normal;
+    int n_patches;
+    const HsPatch* patches;
+    const float* patch_height; const float* patch_normal;
+    const int* box;             /* [n_patches*4] i0, i1, j0, j1 (half-open) */
+    const int* box_prefix;      /* [n_patches+1] cumulative box sizes */
+    int total_box;
+    float* out;                 /* [n*n] */
+} HsCompositeArgs;
+HS_API int hs_composite(const HsCompositeArgs* a, void* stream);
+
+/* Non-periodic (clamped-border) normals and optional choppy displacement of
+ * patch grids (finish_field, patch_synthesis.py:323-340).                   */
+typedef struct {
+    int nx, ny; double spacing; double chop_scale;  /* -chi*displacement_scale */
+    const float* height; float* normal; float* disp; /* disp may be NULL */
+} HsFinishArgs;
+HS_API int hs_finish(const HsFinishArgs* a, void* stream);
+
+/* Reductions used by FrameStats (harness.py:171-206). */
+HS_API int hs_sumsq(const float* x, long long n, double* out, void* stream);
+
+/* frame += 1 on the device (end of a captured frame). */
+HS_API int hs_advance_frame(long long* frame, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYBRIDSEA_B200_H */

@@ -1,0 +1,121 @@
+"""Host-side packing of bucket / patch / layer descriptors into the C ABI
+structs (include/hybridsea_b200.h) and their device copies.
+
+Everything here runs once per configuration (init time); the per-frame path
+only passes the resulting device pointers.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError
+
+TILE = 32          # smooth / compose tile edge (csrc/synth.cu)
+
+
+def stream_ptr() -> int:
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+def to_device_bytes(arr: np.ndarray, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device)
+
+
+def bucket_structs(table, params) -> list:
+    """HsBucket per bucket: the array views the kernels read (spectrum.py:233-257)
+    plus S_J(omega_b) in fp64 (particles.py:262)."""
+    from .spectrum import evaluate_1d
+    s_arr, c_arr = table.spread_params
+    s1d = evaluate_1d(params, table.omegas)
+    out = []
+    for k, b in enumerate(table.buckets):
+        out.append(N.HsBucket(b.omega, b.delta_omega, b.radius, b.speed, float(s1d[k]),
+                              float(s_arr[k]), float(c_arr[k]), 0.0))
+    return out
+
+
+def half_rates(patch, omegas: np.ndarray, dt: float, g: float) -> np.ndarray:
+    """(nb, 4) per-side group quota per step (particles.py:237-241), computed
+    with the reference's fp64 operation order so the device ledger is exact."""
+    hr = np.empty((len(omegas), 4))
+    for side in range(4):
+        pair = 4.0 * patch.side_length(side) * dt * omegas ** 3 / (math.pi ** 3 * g)
+        hr[:, side] = 0.5 * pair
+    return hr
+
+
+def max_groups_per_step(hr: np.ndarray) -> int:
+    """Upper bound of groups emitted in one step: each (bucket, side) cell can
+    emit floor(acc + hr) <= floor(hr) + 1 with acc in [0, 1)."""
+    return int(np.sum(np.floor(hr) + 1.0))
+
+
+def grid_dims(patch, res: int) -> tuple[float, int]:
+    texel = patch.l1 / (res - 1)
+    return texel, int(round(patch.l2 / texel)) + 1
+
+
+@dataclass
+class LayerPack:
+    """Packed layers of several patches (one HsLayer per (patch, bucket))."""
+    layers: list               # HsLayer structs
+    taps: np.ndarray           # float32
+    raw_len: int               # floats
+    smooth_len: int            # floats
+    smooth_tile_prefix: np.ndarray   # int32 [n_layers + 1]
+    max_H: int
+
+
+def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
+    """Lay out the per-bucket decimated layers of every patch (LayerPlan,
+    patch_synthesis.py:227-258; layer dims :306-308)."""
+    layers, taps, prefix = [], [], [0]
+    raw_off = sm_off = tap_off = 0
+    max_h = 1
+    for plan, (res, ny) in zip(plans, grids):
+        for k, f in zip(plan.kernels, plan.factors):
+            pad = k.half_width + 1
+            ncx = -((res - 1) // -f) + 1
+            ncy = -((ny - 1) // -f) + 1
+            wx, wy = ncx + 2 * pad, ncy + 2 * pad
+            if len(k.taps) > min(wx, wy):
+                raise ConfigError(f"kernel of {len(k.taps)} taps wider than grid axis of {min(wx, wy)}")
+            layers.append(N.HsLayer(raw_off, sm_off, f, k.half_width, pad, ncx, ncy, wx, wy, tap_off,
+                                    float(k.gain), 0))
+            taps.append(np.asarray(k.taps, dtype=np.float32))
+            raw_off += wx * wy
+            sm_off += ncx * ncy
+            tap_off += len(k.taps)
+            max_h = max(max_h, k.half_width)
+            prefix.append(prefix[-1] + (-(-ncx // TILE)) * (-(-ncy // TILE)))
+    if max_h > 88:
+        raise ConfigError(f"kernel half width {max_h} exceeds the device limit of 88 texels")
+    return LayerPack(layers, np.concatenate(taps) if taps else np.zeros(0, np.float32), raw_off, sm_off,
+                     np.array(prefix, dtype=np.int32), max_h)
+
+
+def compose_tile_prefix(grids: list[tuple[int, int]]) -> np.ndarray:
+    pre = [0]
+    for res, ny in grids:
+        pre.append(pre[-1] + (-(-res // TILE)) * (-(-ny // TILE)))
+    return np.array(pre, dtype=np.int32)
+
+
+def patch_struct(region, res: int, *, pool_base=0, pool_capacity=0, stage_base=0, stage_capacity=0,
+                 grid_base=0, layer_base=0) -> N.HsPatch:
+    texel, ny = grid_dims(region, res)
+    lo = region.min_corner
+    hi = region.max_corner
+    return N.HsPatch(float(lo[0]), float(lo[1]), float(hi[0]), float(hi[1]), float(region.l1),
+                     float(region.l2), float(region.margin), float(texel), int(pool_base), int(stage_base),
+                     int(grid_base), int(pool_capacity), int(stage_capacity), int(res), int(ny),
+                     int(layer_base), 0)
+
+
+def structs_to_device(items: list, device) -> torch.Tensor:
+    return to_device_bytes(N.struct_array_bytes(items), device)

@@ -1,0 +1,191 @@
+"""ctypes binding of the C ABI in include/hybridsea_b200.h.
+
+The library is built in-tree (`build_lib.py`, `__graft_entry__.build()`).
+There is no fallback: if the library is missing or a call fails, this module
+raises.  Struct layouts mirror the header field by field; `_check_layout`
+asserts the sizes the CUDA side was compiled with.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libhybridsea_b200.so")
+
+HS_STATUS_POOL_OVERFLOW = 1
+HS_STATUS_STAGE_OVERFLOW = 2
+HS_MAX_BUCKETS = 32
+HS_MAX_PATCHES = 256
+
+vp = C.c_void_p
+dbl = C.c_double
+i32 = C.c_int
+i64 = C.c_longlong
+
+
+class HsBucket(C.Structure):
+    _fields_ = [("omega", dbl), ("width", dbl), ("radius", dbl), ("speed", dbl), ("s1d", dbl),
+                ("spread_s", dbl), ("spread_c", dbl), ("pad", dbl)]
+
+
+class HsPatch(C.Structure):
+    _fields_ = [("x0", dbl), ("y0", dbl), ("x1", dbl), ("y1", dbl), ("l1", dbl), ("l2", dbl),
+                ("margin", dbl), ("texel", dbl), ("pool_base", i64), ("stage_base", i64),
+                ("grid_base", i64), ("pool_capacity", i32), ("stage_capacity", i32), ("res", i32),
+                ("ny", i32), ("layer_base", i32), ("pad0", i32)]
+
+
+class HsLayer(C.Structure):
+    _fields_ = [("raw_off", i64), ("sm_off", i64), ("f", i32), ("H", i32), ("pad", i32), ("ncx", i32),
+                ("ncy", i32), ("wx", i32), ("wy", i32), ("taps_off", i32), ("gain", C.c_float),
+                ("pad0", i32)]
+
+
+class HsPool(C.Structure):
+    _fields_ = [("x", vp), ("y", vp), ("ux", vp), ("uy", vp), ("amp", vp)]
+
+
+class HsFftArgs(C.Structure):
+    _fields_ = [("n", i32), ("emit_normals", i32), ("g", dbl), ("t", dbl), ("choppiness", dbl),
+                ("frame_ptr", vp), ("dt", dbl), ("spacing", dbl), ("kf", vp), ("h0", vp),
+                ("twiddle", vp), ("work_a", vp), ("work_b", vp), ("height", vp), ("dx", vp),
+                ("dy", vp), ("normal", vp), ("sumsq", vp)]
+
+
+class HsInjectArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("n_theta", i32), ("buckets", vp), ("patches", vp),
+                ("half_rate", vp), ("mean_dir", dbl), ("beta", dbl), ("rho", dbl), ("g", dbl),
+                ("acc", vp), ("groups", vp), ("e_in", vp), ("rng", vp), ("stage", HsPool),
+                ("stage_count", vp), ("scratch", vp), ("member_capacity", i32), ("status", vp)]
+
+
+class HsAdvectArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("buckets", vp), ("patches", vp), ("dt", dbl),
+                ("rho", dbl), ("g", dbl), ("in_", HsPool), ("in_count", vp), ("stage", HsPool),
+                ("stage_count", vp), ("out", HsPool), ("out_count", vp), ("dropped", HsPool),
+                ("dropped_count", vp), ("e_out", vp), ("splat", i32), ("raw_layers", vp),
+                ("raw_layers_len", i64), ("layers", vp), ("clamped", vp), ("tile_state", vp),
+                ("max_tiles", i32), ("tile_counter", vp), ("status", vp)]
+
+
+class HsSplatArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("patches", vp), ("pool", HsPool), ("count", vp),
+                ("raw_layers", vp), ("raw_layers_len", i64), ("layers", vp), ("clamped", vp),
+                ("max_count", i32)]
+
+
+class HsSmoothArgs(C.Structure):
+    _fields_ = [("n_layers", i32), ("layers", vp), ("taps", vp), ("raw_layers", vp),
+                ("smooth_layers", vp), ("tile_prefix", vp), ("total_tiles", i32), ("max_H", i32)]
+
+
+class HsComposeArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("patches", vp), ("layers", vp),
+                ("smooth_layers", vp), ("tile_prefix", vp), ("total_tiles", i32),
+                ("bg_height", vp), ("bg_normal", vp), ("bg_n", i32), ("bg_spacing", dbl),
+                ("patch_height", vp), ("patch_normal", vp), ("blend_height", vp),
+                ("blend_normal", vp), ("blend_mode", i32), ("interior_sumsq", vp),
+                ("interior_count", vp)]
+
+
+class HsSampleArgs(C.Structure):
+    _fields_ = [("n_points", i32), ("points", vp), ("bg_height", vp), ("bg_normal", vp), ("bg_n", i32),
+                ("bg_spacing", dbl), ("bg_x0", dbl), ("bg_y0", dbl), ("n_patches", i32),
+                ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("out_height", vp),
+                ("out_normal", vp), ("clamped_only", i32)]
+
+
+class HsCompositeArgs(C.Structure):
+    _fields_ = [("n", i32), ("spacing", dbl), ("bg_height", vp), ("bg_normal", vp), ("n_patches", i32),
+                ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("box", vp),
+                ("box_prefix", vp), ("total_box", i32), ("out", vp)]
+
+
+class HsFinishArgs(C.Structure):
+    _fields_ = [("nx", i32), ("ny", i32), ("spacing", dbl), ("chop_scale", dbl), ("height", vp),
+                ("normal", vp), ("disp", vp)]
+
+
+ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
+               HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs]
+
+EXPECTED_SIZES = {HsBucket: 64, HsPatch: 112, HsLayer: 56, HsPool: 40}
+
+# every symbol include/hybridsea_b200.h declares
+EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
+           "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
+           "hs_advance_frame"]
+
+_lib = None
+
+
+def _check_layout() -> None:
+    for st, size in EXPECTED_SIZES.items():
+        if C.sizeof(st) != size:
+            raise RuntimeError(f"{st.__name__} is {C.sizeof(st)} bytes, C ABI expects {size}")
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"hybridsea_b200 CUDA library not found at {LIB_PATH}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    _check_layout()
+    L = C.CDLL(LIB_PATH)
+    L.hs_last_error.restype = C.c_char_p
+    L.hs_abi_version.restype = C.c_int
+    for name in EXPORTS[3:]:
+        getattr(L, name).restype = C.c_int
+    L.hs_struct_size.restype = C.c_int
+    L.hs_struct_size.argtypes = [C.c_int]
+    for k, st in enumerate(ABI_STRUCTS):
+        if L.hs_struct_size(k) != C.sizeof(st):
+            raise RuntimeError(f"{st.__name__}: ctypes {C.sizeof(st)} bytes != C {L.hs_struct_size(k)}")
+    L.hs_sumsq.argtypes = [vp, i64, vp, vp]
+    L.hs_advance_frame.argtypes = [vp, vp]
+    if L.hs_abi_version() != 1:
+        raise RuntimeError("hybridsea_b200 ABI version mismatch")
+    _lib = L
+    return L
+
+
+def call(name: str, args, stream) -> None:
+    """Invoke `name(&args, stream)`; raise with the library's message on error."""
+    L = lib()
+    rc = getattr(L, name)(C.byref(args), vp(stream))
+    if rc != 0:
+        raise RuntimeError(f"{name} failed ({rc}): {L.hs_last_error().decode(errors='replace')}")
+
+
+def call_raw(name: str, *args) -> None:
+    L = lib()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        raise RuntimeError(f"{name} failed ({rc}): {L.hs_last_error().decode(errors='replace')}")
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor (0 for None)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def struct_array_bytes(items) -> np.ndarray:
+    """Pack a list of ctypes structs into a uint8 numpy array (for upload)."""
+    if not items:
+        return np.zeros(0, dtype=np.uint8)
+    size = C.sizeof(items[0])
+    buf = bytearray(size * len(items))
+    for k, it in enumerate(items):
+        buf[k * size:(k + 1) * size] = bytes(it)
+    return np.frombuffer(bytes(buf), dtype=np.uint8).copy()
+
+
+def pool_struct(x=None, y=None, ux=None, uy=None, amp=None) -> HsPool:
+    return HsPool(ptr(x), ptr(y), ptr(ux), ptr(uy), ptr(amp))

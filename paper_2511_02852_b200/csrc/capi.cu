@@ -1,0 +1,55 @@
+// C ABI bookkeeping: error strings, ABI version, device properties.
+#include <stdarg.h>
+#include <string.h>
+
+#include "hs_common.cuh"
+
+namespace hs {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+}  // namespace hs
+
+extern "C" int hs_abi_version(void) { return HS_ABI_VERSION; }
+
+extern "C" const char* hs_last_error(void) { return hs::g_err; }
+
+// sizeof of each ABI struct, so the ctypes mirror can verify its layout
+extern "C" HS_API int hs_struct_size(int which) {
+    switch (which) {
+        case 0: return (int)sizeof(HsBucket);
+        case 1: return (int)sizeof(HsPatch);
+        case 2: return (int)sizeof(HsLayer);
+        case 3: return (int)sizeof(HsPool);
+        case 4: return (int)sizeof(HsFftArgs);
+        case 5: return (int)sizeof(HsInjectArgs);
+        case 6: return (int)sizeof(HsAdvectArgs);
+        case 7: return (int)sizeof(HsSplatArgs);
+        case 8: return (int)sizeof(HsSmoothArgs);
+        case 9: return (int)sizeof(HsComposeArgs);
+        case 10: return (int)sizeof(HsSampleArgs);
+        case 11: return (int)sizeof(HsCompositeArgs);
+        case 12: return (int)sizeof(HsFinishArgs);
+        default: return -1;
+    }
+}

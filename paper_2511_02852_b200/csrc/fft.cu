@@ -1,0 +1,304 @@
+// FFT background: per-frame dispersion rotation + inverse 2-D FFT to height,
+// choppy displacement and (optionally) periodic normals.
+//
+// Replaces evolve_and_synthesize (reference fft_background.py:181-208), which
+// runs spectral_at (:155-159) and three complex128 np.fft.ifft2 calls.
+//
+// B200 design:
+//   * the three real outputs ride on 1.5 complex transforms:
+//       A = hh * (1 + lambda kx/|k|)         -> IFFT2(A) = height + i dx
+//       B = -i lambda (ky/|k|) hh            -> IFFT2(B) = dy (real)
+//     (the imaginary part of the displacement spectra is dropped at the four
+//     self-conjugate bins first -- the Hermitian part the reference's .real
+//     keeps);
+//   * pass 1 (rows, axis 1): one CTA per row pair (i, n-i) so the h0(-k)
+//     gather stays in shared memory; h0 is read exactly once (8 B/bin).  B is
+//     only transformed for rows 0..n/2: rows n-i are conj of rows i;
+//   * pass 2 (columns, axis 0): A columns in tiles; B columns two at a time
+//     packed as Y[:,j1] + i Y[:,j2] (each column of Y is Hermitian in i, so
+//     one complex IFFT yields two real dy columns);
+//   * in-place radix-2/4 DIT in shared memory (two radix-2 stages fused into
+//     a radix-4 butterfly per thread, one barrier per pair of stages) with an
+//     fp64-accurate fp32 twiddle table;
+//   * the phase omega*t is formed and reduced mod 2 pi in fp64 before the
+//     fp32 sincos.
+#include "hs_common.cuh"
+
+namespace hs {
+
+__device__ __forceinline__ int bitrev(int x, int logn) { return (int)(__brev((unsigned)x) >> (32 - logn)); }
+
+// In-place inverse DFT (e^{+i}) of `count` sequences of length n stored at
+// buf + f*stride in bit-reversed order; result in natural order.
+__device__ void ifft_smem(float2* buf, int count, int stride, int n, int logn, const float2* tw) {
+    int s = 0;
+    if (logn & 1) {
+        const int half = n >> 1;
+        const int items = count * half;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+            int f = it >> (logn - 1), k = it & (half - 1);
+            float2* p = buf + f * stride + 2 * k;
+            float2 a = p[0], b = p[1];
+            p[0] = cadd(a, b);
+            p[1] = csub(a, b);
+        }
+        __syncthreads();
+        s = 1;
+    }
+    const int quarter = n >> 2;
+    for (; s < logn; s += 2) {
+        const int m = 1 << s;
+        const int items = count * quarter;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+            int f = it >> (logn - 2), r = it & (quarter - 1);
+            int q = r & (m - 1);
+            int base = ((r >> s) << (s + 2)) + q;
+            float2* p = buf + f * stride + base;
+            float2 x0 = p[0], x1 = p[m], x2 = p[2 * m], x3 = p[3 * m];
+            float2 w1 = tw[q << (logn - s - 1)];
+            float2 t = cmul(x1, w1);
+            float2 y0 = cadd(x0, t), y1 = csub(x0, t);
+            t = cmul(x3, w1);
+            float2 y2 = cadd(x2, t), y3 = csub(x2, t);
+            float2 w2 = tw[q << (logn - s - 2)];
+            t = cmul(y2, w2);
+            p[0] = cadd(y0, t);
+            p[2 * m] = csub(y0, t);
+            t = cmul_i(cmul(y3, w2));
+            p[m] = cadd(y1, t);
+            p[3 * m] = csub(y1, t);
+        }
+        __syncthreads();
+    }
+}
+
+struct FftDev {
+    int n, logn, chop_on;
+    double g, t, chop, dt;
+    const long long* frame_ptr;
+    const double* kf;
+    const float2* h0;
+    const float2* tw;
+    float2* wa;
+    float2* wb;
+};
+
+// ---------------------------------------------------------------- pass 1 --
+__global__ void __launch_bounds__(256) fft_rows_kernel(FftDev d) {
+    extern __shared__ float2 sm[];
+    const int n = d.n, logn = d.logn, half = n >> 1;
+    float2* tw = sm;               // n/2
+    float2* r0 = tw + half;        // h0 row i
+    float2* r1 = r0 + n;           // h0 row i'
+    float2* A0 = r1 + n;           // A row i   (bit reversed)
+    float2* A1 = A0 + n;           // A row i'
+    float2* B0 = A1 + n;           // B row i
+    const int i = blockIdx.x;
+    const int ip = (n - i) & (n - 1);
+    const bool self = (i == ip);
+    for (int k = threadIdx.x; k < half; k += blockDim.x) tw[k] = d.tw[k];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        r0[j] = d.h0[(size_t)i * n + j];
+        r1[j] = d.h0[(size_t)ip * n + j];
+    }
+    __syncthreads();
+    const double kxi = d.kf[i], kxip = d.kf[ip];
+    const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame*dt
+    const bool row_sc = (i == 0) || (i == half);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int jm = (n - j) & (n - 1);
+        const double kyj = d.kf[j];
+        const double km = hypot(kxi, kyj);
+        const double w = sqrt(d.g * km);
+        double ph = w * t;
+        ph -= two_pi * rint(ph * (1.0 / two_pi));
+        float s, c;
+        sincosf((float)ph, &s, &c);
+        const float2 rot = make_float2(c, -s);    // e^{-i w t}
+        const float2 rotc = make_float2(c, s);    // e^{+i w t}
+        const int jr = bitrev(j, logn);
+        // hh(i, j) = h0(i,j) rot + conj(h0(-i,-j)) conj(rot)
+        float2 hh0 = cadd(cmul(r0[j], rot), cmul(cconj(r1[jm]), rotc));
+        const bool sc = row_sc && (j == 0 || j == half);   // self-conjugate bin
+        const double kinv = km > 0.0 ? 1.0 / km : 1.0;       // k_safe (fft_background.py:194-195)
+        if (d.chop_on) {
+            float fa = sc ? 1.f : (float)(1.0 + d.chop * kxi * kinv);
+            A0[jr] = make_float2(hh0.x * fa, hh0.y * fa);
+            float fb = sc ? 0.f : (float)(d.chop * kyj * kinv);
+            // -i * fb * hh = fb * (hh.y, -hh.x)
+            B0[jr] = make_float2(fb * hh0.y, -fb * hh0.x);
+        } else {
+            A0[jr] = hh0;
+        }
+        if (!self) {
+            float2 hh1 = cadd(cmul(r1[j], rot), cmul(cconj(r0[jm]), rotc));
+            float fa = d.chop_on ? (float)(1.0 + d.chop * kxip * kinv) : 1.f;
+            A1[jr] = make_float2(hh1.x * fa, hh1.y * fa);
+        }
+    }
+    __syncthreads();
+    // A0, A1 are contiguous (count 2, stride n); B0 follows A1
+    if (self) {
+        ifft_smem(A0, 1, n, n, logn, tw);
+        if (d.chop_on) ifft_smem(B0, 1, n, n, logn, tw);
+    } else {
+        ifft_smem(A0, d.chop_on ? 3 : 2, n, n, logn, tw);
+    }
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        d.wa[(size_t)i * n + j] = A0[j];
+        if (!self) d.wa[(size_t)ip * n + j] = A1[j];
+        if (d.chop_on) d.wb[(size_t)i * n + j] = B0[j];
+    }
+}
+
+// ---------------------------------------------------------------- pass 2 --
+struct ColOut {
+    float* h; float* dx; float* dy; double* sumsq;
+};
+
+template <int CA, int CBP>
+__global__ void __launch_bounds__(256) fft_cols_kernel(FftDev d, ColOut o, int n_a_tiles) {
+    extern __shared__ float2 sm[];
+    __shared__ double red[8];
+    const int n = d.n, logn = d.logn, half = n >> 1;
+    const int stride = n + 1;                 // padded column stride
+    float2* tw = sm;
+    float2* cols = tw + half;
+    for (int k = threadIdx.x; k < half; k += blockDim.x) tw[k] = d.tw[k];
+    double acc = 0.0;
+    if ((int)blockIdx.x < n_a_tiles) {
+        const int j0 = blockIdx.x * CA;
+        for (int e = threadIdx.x; e < n * CA; e += blockDim.x) {
+            int i = e / CA, c = e - i * CA;
+            cols[c * stride + bitrev(i, logn)] = d.wa[(size_t)i * n + j0 + c];
+        }
+        __syncthreads();
+        ifft_smem(cols, CA, stride, n, logn, tw);
+        for (int e = threadIdx.x; e < n * CA; e += blockDim.x) {
+            int i = e / CA, c = e - i * CA;
+            float2 v = cols[c * stride + i];
+            size_t o_idx = (size_t)i * n + j0 + c;
+            o.h[o_idx] = v.x;
+            o.dx[o_idx] = d.chop_on ? v.y : 0.f;
+            acc += (double)v.x * (double)v.x;
+        }
+    } else {
+        const int j0 = (blockIdx.x - n_a_tiles) * (2 * CBP);
+        if (!d.chop_on) {
+            for (int e = threadIdx.x; e < n * 2 * CBP; e += blockDim.x) {
+                int i = e / (2 * CBP), c = e - i * (2 * CBP);
+                o.dy[(size_t)i * n + j0 + c] = 0.f;
+            }
+            return;
+        }
+        for (int e = threadIdx.x; e < n * CBP; e += blockDim.x) {
+            int i = e / CBP, q = e - i * CBP;
+            int src = i <= half ? i : n - i;
+            float2 y1 = d.wb[(size_t)src * n + j0 + 2 * q];
+            float2 y2 = d.wb[(size_t)src * n + j0 + 2 * q + 1];
+            if (i == 0 || i == half) { y1.y = 0.f; y2.y = 0.f; }   // rows are real there
+            else if (i > half) { y1.y = -y1.y; y2.y = -y2.y; }     // Y[-i] = conj(Y[i])
+            cols[q * stride + bitrev(i, logn)] = make_float2(y1.x - y2.y, y1.y + y2.x);
+        }
+        __syncthreads();
+        ifft_smem(cols, CBP, stride, n, logn, tw);
+        for (int e = threadIdx.x; e < n * 2 * CBP; e += blockDim.x) {
+            int i = e / (2 * CBP), c = e - i * (2 * CBP);
+            float2 v = cols[(c >> 1) * stride + i];
+            o.dy[(size_t)i * n + j0 + c] = (c & 1) ? v.y : v.x;
+        }
+    }
+    if (o.sumsq) {
+        acc = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            if (t != 0.0) atomicAdd(o.sumsq, t);
+        }
+    }
+}
+
+// -------------------------------------------------------------- normals --
+__global__ void normals_periodic_kernel(const float* __restrict__ h, float* __restrict__ nrm,
+                                        int n, float inv2s) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (j >= n) return;
+    const int ip = (i + 1) & (n - 1), im = (i - 1) & (n - 1);
+    const int jp = (j + 1) & (n - 1), jm = (j - 1) & (n - 1);
+    float hx = (h[(size_t)ip * n + j] - h[(size_t)im * n + j]) * inv2s;
+    float hy = (h[(size_t)i * n + jp] - h[(size_t)i * n + jm]) * inv2s;
+    float r = rsqrtf(hx * hx + hy * hy + 1.f);
+    float* o = nrm + ((size_t)i * n + j) * 3;
+    o[0] = -hx * r;
+    o[1] = -hy * r;
+    o[2] = r;
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
+    HS_CHECK_ARG(a != nullptr, "hs_fft_evolve: null args");
+    const int n = a->n;
+    HS_CHECK_ARG(n >= 4 && n <= 4096 && (n & (n - 1)) == 0, "hs_fft_evolve: n=%d must be a power of two in [4, 4096]", n);
+    HS_CHECK_ARG(a->kf && a->h0 && a->twiddle && a->work_a && a->height && a->dx && a->dy,
+                 "hs_fft_evolve: missing buffer");
+    const int chop_on = a->choppiness != 0.0;
+    HS_CHECK_ARG(!chop_on || a->work_b, "hs_fft_evolve: work_b required when choppiness != 0");
+    HS_CHECK_ARG(!a->emit_normals || a->normal, "hs_fft_evolve: normal buffer required");
+    cudaStream_t st = as_stream(stream);
+    FftDev d;
+    d.n = n;
+    d.logn = 31 - __builtin_clz((unsigned)n);
+    d.chop_on = chop_on;
+    d.g = a->g; d.t = a->t; d.chop = a->choppiness; d.dt = a->dt; d.frame_ptr = a->frame_ptr;
+    d.kf = a->kf;
+    d.h0 = reinterpret_cast<const float2*>(a->h0);
+    d.tw = reinterpret_cast<const float2*>(a->twiddle);
+    d.wa = reinterpret_cast<float2*>(a->work_a);
+    d.wb = reinterpret_cast<float2*>(a->work_b);
+
+    size_t sm_rows = (size_t)(n / 2 + 5 * n) * sizeof(float2);
+    static size_t rows_attr = 48 * 1024;   // attribute calls stay out of graph capture after the first frame
+    if (sm_rows > rows_attr) {
+        HS_CUDA(cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows));
+        rows_attr = sm_rows;
+    }
+    fft_rows_kernel<<<n / 2 + 1, 256, sm_rows, st>>>(d);
+    HS_LAUNCH_CHECK();
+
+    ColOut o{a->height, a->dx, a->dy, a->sumsq};
+    // columns per CTA: keep a tile <= 64 KiB of complex64
+    auto launch_cols = [&](auto kern, int ca, int cbp) -> int {
+        int n_a = n / ca;
+        int n_b = n / (2 * cbp);
+        size_t sm = (size_t)(n / 2 + (size_t)(ca > cbp ? ca : cbp) * (n + 1)) * sizeof(float2);
+        static size_t cols_attr[2] = {48 * 1024, 48 * 1024};
+        const int slot = ca == 8 ? 0 : 1;
+        if (sm > cols_attr[slot]) {
+            HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cols_attr[slot] = sm;
+        }
+        kern<<<n_a + n_b, 256, sm, st>>>(d, o, n_a);
+        HS_LAUNCH_CHECK();
+        return 0;
+    };
+    int rc;
+    if (n <= 8) rc = launch_cols(fft_cols_kernel<4, 2>, 4, 2);
+    else if (n <= 512) rc = launch_cols(fft_cols_kernel<8, 4>, 8, 4);
+    else if (n <= 1024) rc = launch_cols(fft_cols_kernel<8, 4>, 8, 4);
+    else rc = launch_cols(fft_cols_kernel<4, 2>, 4, 2);
+    if (rc) return rc;
+
+    if (a->emit_normals) {
+        dim3 grid((n + 127) / 128, n);
+        normals_periodic_kernel<<<grid, 128, 0, st>>>(a->height, a->normal, n, (float)(1.0 / (2.0 * a->spacing)));
+        HS_LAUNCH_CHECK();
+    }
+    return 0;
+}

@@ -1,0 +1,149 @@
+// Shared device helpers for the hybridsea_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "hybridsea_b200.h"
+
+namespace hs {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const char* fmt, ...);
+
+#define HS_CHECK_ARG(cond, ...)                \
+    do {                                       \
+        if (!(cond)) {                         \
+            ::hs::set_error(__VA_ARGS__);      \
+            return 1;                          \
+        }                                      \
+    } while (0)
+
+#define HS_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t _e = (call);                                                   \
+        if (_e != cudaSuccess) {                                                   \
+            ::hs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                            cudaGetErrorString(_e));                               \
+            return 2;                                                              \
+        }                                                                          \
+    } while (0)
+
+#define HS_LAUNCH_CHECK()                                                          \
+    do {                                                                           \
+        cudaError_t _e = cudaGetLastError();                                       \
+        if (_e != cudaSuccess) {                                                   \
+            ::hs::set_error("%s:%d launch: %s", __FILE__, __LINE__,                \
+                            cudaGetErrorString(_e));                               \
+            return 2;                                                              \
+        }                                                                          \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms();
+
+// ---------------------------------------------------------------- complex --
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// multiply by +i
+__device__ __forceinline__ float2 cmul_i(float2 a) { return make_float2(-a.y, a.x); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+
+// ------------------------------------------------- exact fp64 (no FMA) --
+// The reference evaluates with separate IEEE mul/add (numpy); contraction to
+// FMA would change positions and flip cull decisions, so spell them out.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// ------------------------------------------------------ Philox4x64-10 --
+struct U256 { unsigned long long w[4]; };
+
+__device__ __forceinline__ void philox_round(unsigned long long c[4], unsigned long long k0,
+                                             unsigned long long k1) {
+    const unsigned long long M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+    unsigned long long lo0 = M0 * c[0], hi0 = __umul64hi(M0, c[0]);
+    unsigned long long lo1 = M1 * c[2], hi1 = __umul64hi(M1, c[2]);
+    unsigned long long n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+}
+
+// word (d % 4) of block counter0 + 1 + d/4  -- numpy Philox stream layout
+__device__ __forceinline__ unsigned long long philox_draw(const unsigned long long* st,
+                                                          unsigned long long d) {
+    unsigned long long c[4];
+    unsigned long long add = 1ULL + (d >> 2);
+    // 256-bit add with carry
+    unsigned long long s0 = st[2] + add;
+    unsigned long long carry = s0 < add ? 1ULL : 0ULL;
+    c[0] = s0;
+    for (int i = 1; i < 4; ++i) {
+        unsigned long long v = st[2 + i] + carry;
+        carry = (carry && v == 0ULL) ? 1ULL : 0ULL;
+        c[i] = v;
+    }
+    unsigned long long k0 = st[0], k1 = st[1];
+    const unsigned long long W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += W0; k1 += W1; }
+        philox_round(c, k0, k1);
+    }
+    return c[d & 3];
+}
+
+// numpy: lo + (hi - lo) * ((raw >> 11) * 2^-53)
+__device__ __forceinline__ double uniform_from(unsigned long long raw, double lo, double range) {
+    double unit = (double)(raw >> 11) * (1.0 / 9007199254740992.0);
+    return dadd(lo, dmul(range, unit));
+}
+
+// ------------------------------------------------------------ reductions --
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one int per thread; returns the exclusive
+// prefix and writes the block total to *total.  `sm` needs 33 ints.
+__device__ __forceinline__ int block_excl_scan(int v, int* sm, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    int inc = warp_incl_scan(v, lane);
+    if (lane == 31) sm[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < nw ? sm[lane] : 0;
+        int wi = warp_incl_scan(w, lane);
+        if (lane < nw) sm[lane] = wi - w;
+        if (lane == nw - 1) sm[32] = wi;
+    }
+    __syncthreads();
+    int res = inc - v + sm[wid];
+    *total = sm[32];
+    __syncthreads();
+    return res;
+}
+
+__device__ __forceinline__ float smoothstep01(float t) {
+    t = fminf(fmaxf(t, 0.f), 1.f);
+    return t * t * (3.f - 2.f * t);
+}
+
+}  // namespace hs

@@ -1,0 +1,475 @@
+// Wave-particle pool kernels: boundary injection and the fused
+// advect + cull + stable bucket-segmented compaction + layer splat.
+//
+// Replaces inject (reference particles.py:219-300), advect (:303-328),
+// ParticleSet.extend/compact (:163-178) and the per-bucket _splat of
+// synthesize (patch_synthesis.py:165-186, 298-310).
+//
+// Pool layout: SoA, fp64 position + direction,
+// fp32 amplitude, no per-particle bucket id -- each patch region is
+// bucket-segmented and each segment keeps the reference's stable birth
+// order.  The advect kernel reads the virtual sequence
+//     for b: [old segment b][new crests b][new troughs b]
+// (exactly the reference pool order restricted to bucket b after
+// pool.extend(inject(...))) and compacts it with a single-pass
+// decoupled-look-back scan, so buckets stay contiguous and in order.
+#include "hs_common.cuh"
+
+namespace hs {
+
+// ============================================================== inject ==
+struct InjectDev {
+    HsInjectArgs a;
+};
+
+__device__ __forceinline__ int find_cell(const int* gstart, int ncell, int g) {
+    // largest c with gstart[c] <= g and gstart[c+1] > g
+    int lo = 0, hi = ncell - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (gstart[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
+    const int p = blockIdx.x;
+    const int nb = a.nb, nth = a.n_theta, ncell = nb * 4;
+    __shared__ int n_emit[HS_MAX_BUCKETS * 4];
+    __shared__ int gstart[HS_MAX_BUCKETS * 4 + 1];
+    __shared__ int live_cnt[HS_MAX_BUCKETS];
+    __shared__ int live_before[HS_MAX_BUCKETS + 1];
+    __shared__ int soff[HS_MAX_BUCKETS + 1];
+    __shared__ int scan_sm[33];
+    __shared__ int abort_s;
+    const HsPatch P = a.patches[p];
+    double* acc = a.acc + (size_t)p * ncell;
+    const double* hr = a.half_rate + (size_t)p * ncell;
+    unsigned long long* rng = a.rng + (size_t)p * 8;
+
+    // 1. quota ledger: acc += half_rate; n = floor(acc); acc -= n   (particles.py:243-245)
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+        double v = dadd(acc[c], hr[c]);
+        double fl = floor(v);
+        acc[c] = dsub(v, fl);
+        n_emit[c] = (int)fl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        gstart[0] = 0;
+        for (int c = 0; c < ncell; ++c) gstart[c + 1] = gstart[c] + n_emit[c];
+        for (int b = 0; b < nb; ++b) {
+            long long s = n_emit[4 * b] + n_emit[4 * b + 1] + n_emit[4 * b + 2] + n_emit[4 * b + 3];
+            a.groups[(size_t)p * nb + b] += s;
+        }
+        abort_s = (long long)gstart[ncell] * nth > a.member_capacity;
+        if (abort_s) atomicOr(a.status, HS_STATUS_STAGE_OVERFLOW);
+    }
+    __syncthreads();
+    const int g_tot = gstart[ncell];
+    int* scount = a.stage_count + (size_t)p * nb;
+    if (g_tot == 0 || abort_s) {     // no groups: no RNG draws (particles.py:248-249)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = 0;
+        return;
+    }
+    const int M = g_tot * nth;
+    const double pi = 3.141592653589793;
+    const double dth = dmul(2.0, pi) / (double)nth;
+    const double j_lo = dmul(-0.5, dth), j_range = dsub(dmul(0.5, dth), j_lo);
+    const unsigned long long D = rng[6];
+    double* scr = a.scratch + (size_t)p * a.member_capacity * 2;
+
+    // 2. amplitudes + booked energy for every member  (particles.py:256-264, 291-292)
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        const int g = m / nth, k = m - g * nth;
+        const int cell = find_cell(gstart, ncell, g);
+        const HsBucket B = a.buckets[cell >> 2];
+        double jit = uniform_from(philox_draw(rng, D + (unsigned long long)g), j_lo, j_range);
+        double th0 = dadd(-pi, dmul((double)k + 0.5, dth));
+        double th = dadd(th0, jit);
+        double cv = fabs(cos(dmul(0.5, th)));
+        double dv = dmul(B.spread_c, pow(cv, dmul(2.0, B.spread_s)));
+        double amp = sqrt(dmul(dmul(dmul(dmul(2.0, B.s1d), dv), B.width), dth));
+        double e = dmul(dmul(dmul(dmul(dmul(0.125, a.rho), a.g), dmul(amp, amp)), pi), dmul(B.radius, B.radius));
+        scr[2 * m] = e;
+        scr[2 * m + 1] = amp;
+    }
+    __syncthreads();
+    // 3. per-bucket energy in member order (bincount order) and live counts
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        int m0 = gstart[4 * b] * nth, m1 = gstart[4 * b + 4] * nth;
+        double s = 0.0;
+        int live = 0;
+        for (int m = m0; m < m1; ++m) {
+            s = dadd(s, scr[2 * m]);
+            live += scr[2 * m + 1] > 0.0;
+        }
+        a.e_in[(size_t)p * nb + b] = dadd(a.e_in[(size_t)p * nb + b], s);
+        live_cnt[b] = live;
+    }
+    __syncthreads();
+    const int per_live = a.beta != 0.0 ? 2 : 1;
+    if (threadIdx.x == 0) {
+        live_before[0] = 0;
+        soff[0] = 0;
+        for (int b = 0; b < nb; ++b) {
+            live_before[b + 1] = live_before[b] + live_cnt[b];
+            soff[b + 1] = soff[b] + per_live * live_cnt[b];
+        }
+        abort_s = soff[nb] > P.stage_capacity;
+        if (abort_s) atomicOr(a.status, HS_STATUS_STAGE_OVERFLOW);
+    }
+    __syncthreads();
+    if (abort_s) {
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = 0;
+        if (threadIdx.x == 0) rng[6] = D + (unsigned long long)g_tot * (1 + nth);
+        return;
+    }
+    // 4. positions / directions for live members, in order  (particles.py:266-299)
+    const long long sb = P.stage_base;
+    int carry = 0;
+    for (int base = 0; base < M; base += blockDim.x) {
+        const int m = base + threadIdx.x;
+        double amp = 0.0;
+        if (m < M) amp = scr[2 * m + 1];
+        int live = (m < M) && amp > 0.0;
+        int tot;
+        int ex = block_excl_scan(live, scan_sm, &tot) + carry;
+        if (live) {
+            const int g = m / nth, k = m - g * nth;
+            const int cell = find_cell(gstart, ncell, g);
+            const int b = cell >> 2, s = cell & 3;
+            const HsBucket B = a.buckets[b];
+            double jit = uniform_from(philox_draw(rng, D + (unsigned long long)g), j_lo, j_range);
+            double th = dadd(dadd(-pi, dmul((double)k + 0.5, dth)), jit);
+            double thw = dadd(th, a.mean_dir);
+            double dx = cos(thw), dy = sin(thw);
+            double dot = (s == 0) ? dx : (s == 1) ? -dx : (s == 2) ? dy : -dy;
+            int side = dot > 0.0 ? s : (s ^ 1);
+            double u = uniform_from(philox_draw(rng, D + (unsigned long long)g_tot + (unsigned long long)m), 0.0, 1.0);
+            double px, py;
+            if (side == 0)      { px = P.x0;                 py = dadd(P.y0, dmul(u, P.l2)); }
+            else if (side == 1) { px = dadd(P.x0, P.l1);     py = dadd(P.y0, dmul(u, P.l2)); }
+            else if (side == 2) { px = dadd(P.x0, dmul(u, P.l1)); py = P.y0; }
+            else                { px = dadd(P.x0, dmul(u, P.l1)); py = dadd(P.y0, P.l2); }
+            const int rank = ex - live_before[b];
+            long long o = sb + soff[b] + rank;
+            a.stage.x[o] = px; a.stage.y[o] = py; a.stage.ux[o] = dx; a.stage.uy[o] = dy;
+            a.stage.amp[o] = (float)amp;
+            if (per_live == 2) {
+                o += live_cnt[b];
+                a.stage.x[o] = dsub(px, dmul(B.radius, dx));
+                a.stage.y[o] = dsub(py, dmul(B.radius, dy));
+                a.stage.ux[o] = dx; a.stage.uy[o] = dy;
+                a.stage.amp[o] = (float)(-a.beta * amp);
+            }
+        }
+        carry += tot;
+    }
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = per_live * live_cnt[b];
+    if (threadIdx.x == 0) rng[6] = D + (unsigned long long)g_tot * (1 + nth);
+}
+
+// ============================================================== advect ==
+constexpr int ADV_THREADS = 256;
+constexpr int ADV_ITEMS = 4;
+constexpr int ADV_TILE = ADV_THREADS * ADV_ITEMS;
+constexpr unsigned long long FLAG_AGG = 1ULL << 32;
+constexpr unsigned long long FLAG_PRE = 2ULL << 32;
+
+__device__ __forceinline__ int find_seg(const int* off, int nseg, int v) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= v) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
+                                          double x, double y, float amp, int* clamp_acc) {
+    // gx = (x - x0)/texel / f + pad  (patch_synthesis.py:298-299, 309, 169-177)
+    double gx = (x - P.x0) / P.texel;
+    double gy = (y - P.y0) / P.texel;
+    double u = gx / (double)L.f + (double)L.pad;
+    double v = gy / (double)L.f + (double)L.pad;
+    const double umax = (double)(L.wx - 1), vmax = (double)(L.wy - 1);
+    if (u < 0.0 || u > umax || v < 0.0 || v > vmax) ++(*clamp_acc);
+    u = fmin(fmax(u, 0.0), umax - 1e-9);
+    v = fmin(fmax(v, 0.0), vmax - 1e-9);
+    const int i0 = (int)u, j0 = (int)v;
+    const float fu = (float)(u - i0), fv = (float)(v - j0);
+    float* q = raw + L.raw_off + (long long)i0 * L.wy + j0;
+    atomicAdd(q, amp * (1.f - fu) * (1.f - fv));
+    atomicAdd(q + L.wy, amp * fu * (1.f - fv));
+    atomicAdd(q + 1, amp * (1.f - fu) * fv);
+    atomicAdd(q + L.wy + 1, amp * fu * fv);
+}
+
+__global__ void __launch_bounds__(ADV_THREADS) advect_kernel(HsAdvectArgs a) {
+    const int nb = a.nb;
+    __shared__ int tile_prefix[HS_MAX_PATCHES + 1];
+    __shared__ int in_off[HS_MAX_BUCKETS + 1];
+    __shared__ int st_off[HS_MAX_BUCKETS + 1];
+    __shared__ int voff[HS_MAX_BUCKETS + 1];
+    __shared__ int in_cnt_s[HS_MAX_BUCKETS];
+    __shared__ int keep_hist[HS_MAX_BUCKETS];
+    __shared__ int drop_hist[HS_MAX_BUCKETS];
+    __shared__ double eout_s[HS_MAX_BUCKETS];
+    __shared__ int warp_tot[ADV_ITEMS][ADV_THREADS / 32];
+    __shared__ int tile_s, prefix_s, clamp_s;
+    __shared__ HsPatch P_s;
+
+    if (threadIdx.x == 0) {
+        tile_prefix[0] = 0;
+        for (int p = 0; p < a.n_patches; ++p) {
+            const HsPatch& P = a.patches[p];
+            int cap = P.pool_capacity + (a.stage_count ? P.stage_capacity : 0);
+            tile_prefix[p + 1] = tile_prefix[p] + (cap + ADV_TILE - 1) / ADV_TILE;
+        }
+    }
+    __syncthreads();
+    const int total_tiles = tile_prefix[a.n_patches];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+    while (true) {
+        if (threadIdx.x == 0) tile_s = atomicAdd(a.tile_counter, 1);
+        __syncthreads();
+        const int tile = tile_s;
+        if (tile >= total_tiles) break;
+        const int p = find_seg(tile_prefix, a.n_patches + 1, tile);
+        const int ltile = tile - tile_prefix[p];
+        if (threadIdx.x == 0) {
+            P_s = a.patches[p];
+            int si = 0, ss = 0, sv = 0;
+            for (int b = 0; b < nb; ++b) {
+                int ci = a.in_count[(size_t)p * nb + b];
+                int cs = a.stage_count ? a.stage_count[(size_t)p * nb + b] : 0;
+                in_off[b] = si; st_off[b] = ss; voff[b] = sv; in_cnt_s[b] = ci;
+                si += ci; ss += cs; sv += ci + cs;
+            }
+            in_off[nb] = si; st_off[nb] = ss; voff[nb] = sv;
+            clamp_s = 0;
+        }
+        if (threadIdx.x < nb) { keep_hist[threadIdx.x] = 0; drop_hist[threadIdx.x] = 0; eout_s[threadIdx.x] = 0.0; }
+        __syncthreads();
+        const HsPatch P = P_s;
+        const int N = voff[nb];
+        const int tbase = ltile * ADV_TILE;
+        if (tbase >= N) {
+            // empty tile: publish an inclusive prefix equal to the predecessor's
+            // (never read: later tiles of this patch are empty too)
+            __syncthreads();
+            continue;
+        }
+        double nx[ADV_ITEMS], ny_[ADV_ITEMS], dxv[ADV_ITEMS], dyv[ADV_ITEMS];
+        float am[ADV_ITEMS];
+        int bk[ADV_ITEMS];
+        int keep[ADV_ITEMS];
+#pragma unroll
+        for (int it = 0; it < ADV_ITEMS; ++it) {
+            const int v = tbase + it * ADV_THREADS + threadIdx.x;
+            keep[it] = 0;
+            bk[it] = 0;
+            if (v < N) {
+                const int b = find_seg(voff, nb + 1, v);
+                // empty buckets share voff entries; find_seg returns the last such b
+                const int local = v - voff[b];
+                long long src;
+                const double* X; const double* Y; const double* UX; const double* UY; const float* AM;
+                if (local < in_cnt_s[b]) {
+                    src = P.pool_base + in_off[b] + local;
+                    X = a.in.x; Y = a.in.y; UX = a.in.ux; UY = a.in.uy; AM = a.in.amp;
+                } else {
+                    src = P.stage_base + st_off[b] + (local - in_cnt_s[b]);
+                    X = a.stage.x; Y = a.stage.y; UX = a.stage.ux; UY = a.stage.uy; AM = a.stage.amp;
+                }
+                const HsBucket B = a.buckets[b];
+                const double step = dmul(B.speed, a.dt);                 // speeds * dt
+                const double ux = UX[src], uy = UY[src];
+                const double x = dadd(X[src], dmul(ux, step));           // pos += dir * (c dt)
+                const double y = dadd(Y[src], dmul(uy, step));
+                const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
+                const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
+                keep[it] = dadd(dmul(ox, ox), dmul(oy, oy)) <= dmul(B.radius, B.radius);
+                nx[it] = x; ny_[it] = y; dxv[it] = ux; dyv[it] = uy; am[it] = AM[src]; bk[it] = b;
+            }
+        }
+        // tile-local ranks: per (row, warp) ballots
+#pragma unroll
+        for (int it = 0; it < ADV_ITEMS; ++it) {
+            unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
+            if (lane == 0) warp_tot[it][wid] = __popc(bal);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int it = 0; it < ADV_ITEMS; ++it) {
+                for (int w = 0; w < ADV_THREADS / 32; ++w) {
+                    int c = warp_tot[it][w];
+                    warp_tot[it][w] = run;
+                    run += c;
+                }
+            }
+            // decoupled look-back within this patch
+            unsigned long long* ts = a.tile_state;
+            unsigned long long agg = (unsigned long long)run;
+            unsigned long long prefix = 0;
+            if (ltile == 0) {
+                atomicExch(&ts[tile], FLAG_PRE | agg);
+            } else {
+                atomicExch(&ts[tile], FLAG_AGG | agg);
+                int j = tile - 1;
+                while (true) {
+                    unsigned long long s = *((volatile unsigned long long*)&ts[j]);
+                    unsigned long long flag = s & (3ULL << 32);
+                    if (flag == 0) continue;
+                    prefix += s & 0xffffffffULL;
+                    if (flag == FLAG_PRE) break;
+                    --j;
+                }
+                atomicExch(&ts[tile], FLAG_PRE | (prefix + agg));
+            }
+            prefix_s = (int)prefix;
+        }
+        __syncthreads();
+        const int tprefix = prefix_s;
+        int clamp_local = 0;
+        float* raw = a.raw_layers;
+#pragma unroll
+        for (int it = 0; it < ADV_ITEMS; ++it) {
+            const int v = tbase + it * ADV_THREADS + threadIdx.x;
+            unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
+            if (v < N) {
+                const int b = bk[it];
+                if (keep[it]) {
+                    const int rank = tprefix + warp_tot[it][wid] + __popc(bal & ((1u << lane) - 1u));
+                    if (rank < P.pool_capacity) {
+                        const long long o = P.pool_base + rank;
+                        a.out.x[o] = nx[it]; a.out.y[o] = ny_[it];
+                        a.out.ux[o] = dxv[it]; a.out.uy[o] = dyv[it]; a.out.amp[o] = am[it];
+                    } else {
+                        atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+                    }
+                    atomicAdd(&keep_hist[b], 1);
+                    if (a.splat) splat_one(raw, a.layers[P.layer_base + b], P, nx[it], ny_[it], am[it], &clamp_local);
+                } else {
+                    if (am[it] > 0.f) {
+                        // crest despawn energy rho g A^2 pi r^2 / 8 (particles.py:322-327)
+                        const double r = a.buckets[b].radius;
+                        const double amp = (double)am[it];
+                        double e = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * (r * r);
+                        atomicAdd(&eout_s[b], e);
+                    }
+                    if (a.dropped.x) {
+                        // dropped rank = items before v that were not kept (stable)
+                        const int rank = tprefix + warp_tot[it][wid] + __popc(bal & ((1u << lane) - 1u));
+                        const long long o = P.pool_base + (v - rank);
+                        a.dropped.x[o] = nx[it]; a.dropped.y[o] = ny_[it];
+                        a.dropped.ux[o] = dxv[it]; a.dropped.uy[o] = dyv[it]; a.dropped.amp[o] = am[it];
+                        atomicAdd(&drop_hist[b], 1);
+                    }
+                }
+            }
+        }
+        if (clamp_local) atomicAdd(&clamp_s, clamp_local);
+        __syncthreads();
+        if (threadIdx.x < nb) {
+            const int b = threadIdx.x;
+            if (keep_hist[b]) atomicAdd(&a.out_count[(size_t)p * nb + b], keep_hist[b]);
+            if (drop_hist[b]) atomicAdd(&a.dropped_count[(size_t)p * nb + b], drop_hist[b]);
+            if (eout_s[b] != 0.0) atomicAdd(&a.e_out[(size_t)p * nb + b], eout_s[b]);
+        }
+        if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
+        __syncthreads();
+    }
+}
+
+// ======================================================== splat only ==
+__global__ void __launch_bounds__(256) splat_kernel(HsSplatArgs a) {
+    const int p = blockIdx.y;
+    const int nb = a.nb;
+    __shared__ int off[HS_MAX_BUCKETS + 1];
+    __shared__ int clamp_s;
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int b = 0; b < nb; ++b) { off[b] = s; s += a.count[(size_t)p * nb + b]; }
+        off[nb] = s;
+        clamp_s = 0;
+    }
+    __syncthreads();
+    const HsPatch P = a.patches[p];
+    const int N = off[nb];
+    int cl = 0;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        const int b = find_seg(off, nb + 1, v);
+        const long long src = P.pool_base + v;
+        splat_one(a.raw_layers, a.layers[P.layer_base + b], P, a.pool.x[src], a.pool.y[src], a.pool.amp[src], &cl);
+    }
+    if (cl) atomicAdd(&clamp_s, cl);
+    __syncthreads();
+    if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" int hs_inject(const HsInjectArgs* a, void* stream) {
+    HS_CHECK_ARG(a != nullptr, "hs_inject: null args");
+    HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "hs_inject: nb=%d out of range", a->nb);
+    HS_CHECK_ARG(a->n_theta >= 1, "hs_inject: n_theta must be >= 1");
+    HS_CHECK_ARG(a->n_patches >= 0 && a->n_patches <= HS_MAX_PATCHES, "hs_inject: n_patches out of range");
+    if (a->n_patches == 0) return 0;
+    HS_CHECK_ARG(a->buckets && a->patches && a->half_rate && a->acc && a->groups && a->e_in && a->rng &&
+                 a->stage_count && a->scratch && a->status && a->stage.x && a->stage.amp,
+                 "hs_inject: missing buffer");
+    inject_kernel<<<a->n_patches, 512, 0, as_stream(stream)>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
+    HS_CHECK_ARG(a != nullptr, "hs_advect: null args");
+    HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "hs_advect: nb=%d out of range", a->nb);
+    HS_CHECK_ARG(a->n_patches >= 0 && a->n_patches <= HS_MAX_PATCHES, "hs_advect: n_patches out of range");
+    HS_CHECK_ARG(a->dt >= 0.0, "hs_advect: dt must be nonnegative");
+    if (a->n_patches == 0) return 0;
+    HS_CHECK_ARG(a->buckets && a->patches && a->in_count && a->out_count && a->e_out && a->tile_state &&
+                 a->tile_counter && a->status, "hs_advect: missing buffer");
+    HS_CHECK_ARG(!a->splat || (a->raw_layers && a->layers), "hs_advect: splat needs layers");
+    cudaStream_t st = as_stream(stream);
+    HS_CUDA(cudaMemsetAsync(a->out_count, 0, sizeof(int) * (size_t)a->n_patches * a->nb, st));
+    if (a->dropped.x) {
+        HS_CHECK_ARG(a->dropped_count && a->dropped.y && a->dropped.ux && a->dropped.uy && a->dropped.amp,
+                     "hs_advect: incomplete dropped pool");
+        HS_CUDA(cudaMemsetAsync(a->dropped_count, 0, sizeof(int) * (size_t)a->n_patches * a->nb, st));
+    }
+    HS_CUDA(cudaMemsetAsync(a->tile_state, 0, sizeof(unsigned long long) * (size_t)a->max_tiles, st));
+    HS_CUDA(cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st));
+    if (a->splat) HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
+    static int occ = 0;
+    if (occ == 0) {
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_kernel, ADV_THREADS, 0));
+        if (occ < 1) occ = 1;
+    }
+    int grid = num_sms() * occ;
+    advect_kernel<<<grid, ADV_THREADS, 0, st>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_splat(const HsSplatArgs* a, void* stream) {
+    HS_CHECK_ARG(a != nullptr, "hs_splat: null args");
+    HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "hs_splat: nb out of range");
+    if (a->n_patches == 0) return 0;
+    cudaStream_t st = as_stream(stream);
+    HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
+    int bx = (a->max_count + 255) / 256;
+    if (bx < 1) bx = 1;
+    if (bx > 4096) bx = 4096;
+    dim3 grid(bx, a->n_patches);
+    splat_kernel<<<grid, 256, 0, st>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}

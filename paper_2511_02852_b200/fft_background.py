@@ -1,0 +1,240 @@
+"""Global periodic FFT height field on the B200.
+
+Mirror of `hybridsea.fft_background` (`pkg/src/hybridsea/fft_background.py`).
+`init_fft` stays a host fp64 computation (it runs once and draws the same
+numpy Gaussian stream as the reference, so h0 matches it); every per-frame
+operation -- `evolve_and_synthesize`, `sample_periodic` -- is a CUDA kernel
+from libhybridsea_b200 (csrc/fft.cu, csrc/synth.cu).  Outputs are fp32
+device tensors.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._layout import stream_ptr
+from .errors import ConfigError
+from .spectrum import DirectionalSpectrum, directional_density
+
+
+def _device(device) -> torch.device:
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass(frozen=True, eq=False)
+class FftState:
+    """Spectral state of the background tile (fft_background.py:30-47).
+
+    `h0` is kept on the host in complex128 (reference semantics) and on the
+    device as interleaved complex64 (`h0_dev`).  conj(h0(-k)) is gathered by
+    the kernel itself, so `h0_mirror_conj` is derived, not stored.
+    """
+    n: int
+    domain_size: float
+    g: float
+    rng_seed: int
+    choppiness: float
+    h0: np.ndarray
+    device: torch.device = field(default=None)
+    h0_dev: torch.Tensor = field(default=None, repr=False)
+    kf_dev: torch.Tensor = field(default=None, repr=False)
+    twiddle_dev: torch.Tensor = field(default=None, repr=False)
+
+    @property
+    def spacing(self) -> float:
+        return self.domain_size / self.n
+
+    @property
+    def kf(self) -> np.ndarray:
+        return 2.0 * math.pi * np.fft.fftfreq(self.n, d=self.domain_size / self.n)
+
+    @property
+    def kx(self) -> np.ndarray:
+        return np.meshgrid(self.kf, self.kf, indexing="ij")[0]
+
+    @property
+    def ky(self) -> np.ndarray:
+        return np.meshgrid(self.kf, self.kf, indexing="ij")[1]
+
+    @property
+    def omega(self) -> np.ndarray:
+        return np.sqrt(self.g * np.hypot(self.kx, self.ky))
+
+    @property
+    def h0_mirror_conj(self) -> np.ndarray:
+        idx = (-np.arange(self.n)) % self.n
+        return np.conj(self.h0[np.ix_(idx, idx)])
+
+
+def _upload(state: FftState, device) -> FftState:
+    dev = _device(device)
+    n = state.n
+    h0 = np.stack([state.h0.real, state.h0.imag], axis=-1).astype(np.float32)
+    k = np.arange(n // 2)
+    tw = np.stack([np.cos(2.0 * math.pi * k / n), np.sin(2.0 * math.pi * k / n)], -1).astype(np.float32)
+    object.__setattr__(state, "device", dev)
+    object.__setattr__(state, "h0_dev", torch.from_numpy(np.ascontiguousarray(h0)).to(dev))
+    object.__setattr__(state, "kf_dev", torch.from_numpy(state.kf.copy()).to(dev))
+    object.__setattr__(state, "twiddle_dev", torch.from_numpy(np.ascontiguousarray(tw)).to(dev))
+    return state
+
+
+@dataclass(eq=False)
+class HeightField:
+    """Elevation, horizontal displacement and unit normals on a grid
+    (fft_background.py:50-74).  Arrays are torch tensors (fp32, on the GPU
+    for fields produced here); index [i, j] sits at origin + (i, j) spacing."""
+    resolution: int
+    origin: np.ndarray
+    spacing: float
+    height: torch.Tensor
+    displacement: torch.Tensor
+    normal: torch.Tensor
+    periodic: bool = False
+
+    def validate(self) -> None:
+        if not (bool(torch.isfinite(self.height).all()) and bool(torch.isfinite(self.displacement).all())
+                and bool(torch.isfinite(self.normal).all())):
+            raise ValueError("height field contains non-finite values")
+        norms = torch.linalg.vector_norm(self.normal.double(), dim=-1)
+        if not bool(torch.allclose(norms, torch.ones_like(norms), atol=1e-6)):
+            raise ValueError("normals are not unit length")
+
+    def to_numpy(self) -> dict:
+        return {"height": self.height.double().cpu().numpy(),
+                "displacement": self.displacement.double().cpu().numpy(),
+                "normal": self.normal.double().cpu().numpy()}
+
+
+def resolved_band(spectrum: DirectionalSpectrum, n: int, domain_size: float,
+                  band: tuple | None = None) -> tuple[float, float]:
+    """Sampled band clipped to the fundamental and the inscribed Nyquist
+    circle (fft_background.py:90-99); `band` overrides [0.5, 2.5] omega_p."""
+    g = spectrum.params.g
+    lo, hi = spectrum.params.band
+    if band is not None:
+        lo = band[0] if band[0] is not None else lo
+        hi = band[1] if band[1] is not None else hi
+    w_min = math.sqrt(g * 2.0 * math.pi / domain_size)
+    w_max = math.sqrt(g * math.pi * n / domain_size)
+    return max(lo, w_min), min(hi, w_max)
+
+
+def init_fft(spectrum: DirectionalSpectrum, n: int, domain_size: float, seed: int,
+             choppiness: float = 1.0, *, band: tuple | None = None, device=None) -> FftState:
+    """Initial complex amplitudes, variance-matched to the directional
+    spectrum (fft_background.py:102-146).  Host fp64 with numpy's
+    default_rng(seed) so h0 equals the reference's; uploaded once."""
+    if n < 2 or (n & (n - 1)) != 0:
+        raise ConfigError(f"fft grid size must be a power of two >= 2, got {n}")
+    if domain_size <= 0:
+        raise ConfigError(f"fft domain_size must be positive, got {domain_size}")
+    p = spectrum.params
+    g = p.g
+    kf = 2.0 * math.pi * np.fft.fftfreq(n, d=domain_size / n)
+    kx, ky = np.meshgrid(kf, kf, indexing="ij")
+    kmag = np.hypot(kx, ky)
+    dk = 2.0 * math.pi / domain_size
+    w_lo, w_hi = resolved_band(spectrum, n, domain_size, band)
+    live = (kmag >= (w_lo ** 2 / g) * (1.0 - 1e-12)) & (kmag <= (w_hi ** 2 / g) * (1.0 + 1e-12))
+    live[0, 0] = False
+    kl = kmag[live]
+    om = np.sqrt(g * kl)
+    theta = np.arctan2(ky[live], kx[live]) - spectrum.mean_direction
+    var = np.zeros((n, n))
+    var[live] = directional_density(p, om, theta) * (g / (2.0 * om)) / kl * dk * dk / 2.0
+    xi = np.random.default_rng(seed).standard_normal((n, n, 2))
+    h0 = np.sqrt(var / 2.0) * (xi[..., 0] + 1j * xi[..., 1])
+    h0[~live] = 0.0
+    st = FftState(n=n, domain_size=domain_size, g=g, rng_seed=seed, choppiness=choppiness, h0=h0)
+    if n < 4:
+        raise ConfigError("the B200 FFT path needs fft.n >= 4")
+    return _upload(st, device)
+
+
+def with_h0(state: FftState, h0: np.ndarray) -> FftState:
+    """Copy of the state with custom amplitudes (test hook; the reference
+    tests set h0 directly, test_fft_background.py:121-127)."""
+    st = replace(state, h0=np.asarray(h0, dtype=complex))
+    return _upload(st, state.device)
+
+
+def zeroed(state: FftState) -> FftState:
+    return with_h0(state, np.zeros_like(state.h0))
+
+
+class FftWorkspace:
+    """Scratch + outputs for one background transform (reused across calls)."""
+
+    def __init__(self, n: int, device, normals: bool = True):
+        self.n = n
+        self.work_a = torch.empty((n, n, 2), dtype=torch.float32, device=device)
+        self.work_b = torch.empty((n // 2 + 1, n, 2), dtype=torch.float32, device=device)
+        self.height = torch.empty((n, n), dtype=torch.float32, device=device)
+        self.disp = torch.empty((2, n, n), dtype=torch.float32, device=device)
+        self.normal = torch.empty((n, n, 3), dtype=torch.float32, device=device) if normals else None
+        self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
+
+    def field(self, state: FftState) -> HeightField:
+        nrm = self.normal
+        return HeightField(resolution=state.n, origin=np.zeros(2), spacing=state.spacing, height=self.height,
+                           displacement=self.disp.permute(1, 2, 0), normal=nrm, periodic=True)
+
+
+def fft_args(state: FftState, ws: FftWorkspace, t: float = 0.0, frame_ptr=None, dt: float = 0.0) -> N.HsFftArgs:
+    return N.HsFftArgs(n=state.n, emit_normals=int(ws.normal is not None), g=state.g, t=float(t),
+                       choppiness=float(state.choppiness), frame_ptr=N.ptr(frame_ptr), dt=float(dt),
+                       spacing=state.spacing, kf=N.ptr(state.kf_dev), h0=N.ptr(state.h0_dev),
+                       twiddle=N.ptr(state.twiddle_dev), work_a=N.ptr(ws.work_a), work_b=N.ptr(ws.work_b),
+                       height=N.ptr(ws.height), dx=N.ptr(ws.disp[0]), dy=N.ptr(ws.disp[1]),
+                       normal=N.ptr(ws.normal), sumsq=N.ptr(ws.sumsq))
+
+
+def evolve_and_synthesize(state: FftState, t: float, *, normals: bool = True,
+                          workspace: FftWorkspace | None = None) -> HeightField:
+    """Height field of the background tile at time t (fft_background.py:181-208).
+
+    One CUDA call: dispersion rotation e^{-i w t} with the mirrored
+    conjugate, inverse 2-D FFT to height + choppy displacement, periodic
+    central-difference normals.  Returns fresh fp32 device tensors unless a
+    workspace is given (then its buffers are overwritten)."""
+    ws = workspace if workspace is not None else FftWorkspace(state.n, state.device, normals)
+    N.call("hs_fft_evolve", fft_args(state, ws, t=t), stream_ptr())
+    return ws.field(state)
+
+
+def sample_periodic(field: HeightField, points) -> tuple[torch.Tensor, torch.Tensor]:
+    """Bilinear height and renormalised normal at world points with
+    wrap-around (fft_background.py:222-249); points (..., 2)."""
+    dev = field.height.device
+    pts = torch.as_tensor(np.asarray(points, dtype=np.float64) if not torch.is_tensor(points) else points,
+                          dtype=torch.float64, device=dev)
+    shape = pts.shape[:-1]
+    flat = pts.reshape(-1, 2).contiguous()
+    out_h = torch.empty(flat.shape[0], dtype=torch.float32, device=dev)
+    out_n = torch.empty((flat.shape[0], 3), dtype=torch.float32, device=dev)
+    nrm = field.normal.contiguous() if field.normal is not None else None
+    args = N.HsSampleArgs(n_points=flat.shape[0], points=N.ptr(flat), bg_height=N.ptr(field.height.contiguous()),
+                          bg_normal=N.ptr(nrm), bg_n=field.resolution, bg_spacing=field.spacing,
+                          bg_x0=float(field.origin[0]), bg_y0=float(field.origin[1]), n_patches=0, patches=0,
+                          patch_height=0, patch_normal=0, out_height=N.ptr(out_h), out_normal=N.ptr(out_n),
+                          clamped_only=0)
+    N.call("hs_sample", args, stream_ptr())
+    return out_h.reshape(shape), out_n.reshape(shape + (3,))
+
+
+def max_imag_residue(state: FftState, t: float) -> float:
+    """Reference diagnostic (fft_background.py:223-231); the B200 transform
+    produces real outputs by construction, so report the Hermitian defect of
+    the rotated spectrum instead (host fp64)."""
+    phase = state.omega * t
+    rot = np.cos(phase) - 1j * np.sin(phase)
+    hh = state.h0 * rot + state.h0_mirror_conj * np.conj(rot)
+    idx = (-np.arange(state.n)) % state.n
+    defect = np.abs(hh - np.conj(hh[np.ix_(idx, idx)])).max()
+    peak = np.abs(hh).max()
+    return 0.0 if peak == 0 else float(defect / peak)

@@ -1,0 +1,410 @@
+"""Wave-particle pools on the B200: boundary injection, advection, lifecycle.
+
+Mirror of `hybridsea.particles` (`pkg/src/hybridsea/particles.py`).  The
+pool is device-resident and *bucket-segmented*: within a patch, bucket b's
+particles are contiguous and in the reference's stable birth order, so every
+per-bucket subsequence equals the reference pool's (the reference keeps one
+interleaved list, `particles.py:88-184`).  Accessors return arrays in
+segment order.
+
+`inject` and `advect` are single CUDA launches (csrc/particles.cu).  Random
+draws follow numpy's Philox4x64-10 stream: pass a
+`numpy.random.Generator(numpy.random.Philox(...))` (its state is advanced on
+the host exactly as the reference call would) or a device-resident
+`PhiloxStream` (no host synchronisation).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._layout import bucket_structs, half_rates, max_groups_per_step, patch_struct, stream_ptr, structs_to_device
+from .spectrum import BucketTable, DirectionalSpectrum, FrequencyBucket
+
+DEFAULT_TROUGH_FRACTION = 1.0
+SIDE_INWARD = np.array([[1.0, 0.0], [-1.0, 0.0], [0.0, 1.0], [0.0, -1.0]])
+N_SIDES = 4
+
+
+def _dev(device=None) -> torch.device:
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass(frozen=True)
+class PatchRegion:
+    """Axis-aligned wave-particle region (particles.py:43-74)."""
+    origin: tuple
+    l1: float
+    l2: float
+    margin: float
+
+    def __post_init__(self):
+        if self.l1 <= 0 or self.l2 <= 0:
+            raise ValueError(f"patch side lengths must be positive, got {self.l1}, {self.l2}")
+        if not (0.0 < self.margin < 0.5 * min(self.l1, self.l2)):
+            raise ValueError(f"margin must lie in (0, min(l1, l2)/2), got {self.margin}")
+
+    @property
+    def min_corner(self) -> np.ndarray:
+        return np.asarray(self.origin, dtype=float)
+
+    @property
+    def max_corner(self) -> np.ndarray:
+        return self.min_corner + np.array([self.l1, self.l2])
+
+    def side_length(self, side: int) -> float:
+        return self.l2 if side < 2 else self.l1
+
+    def contains(self, points) -> np.ndarray:
+        p = np.asarray(points, dtype=float)
+        return np.all((p >= self.min_corner) & (p <= self.max_corner), axis=-1)
+
+
+@dataclass
+class WaveParticle:
+    position: np.ndarray
+    direction: np.ndarray
+    amplitude: float
+    bucket: int
+    birth_time: float = 0.0
+
+
+class ParticleSet:
+    """Bucket-segmented SoA pool in device memory.
+
+    Host-side `append`/`append_arrays` (reference API) buffer particles in
+    insertion order; the first device operation stable-sorts them into
+    bucket segments.  `n_buckets` is fixed on first device use.
+    """
+
+    def __init__(self, capacity: int = 1024, n_buckets: int | None = None, device=None):
+        self.device = _dev(device)
+        self.n_buckets = n_buckets
+        self._host: list = []          # pending host batches (pos, dir, amp, bucket)
+        self.x = self.y = self.ux = self.uy = None
+        self.amp = None
+        self.counts = None             # host np.int64 [nb]
+        self.capacity_hint = capacity
+
+    # ---------------------------------------------------------- building --
+    def append_arrays(self, pos, direction, amp, bucket, birth=None) -> None:
+        amp = np.asarray(amp, dtype=float)
+        if len(amp) == 0:
+            return
+        self._host.append((np.asarray(pos, float).reshape(-1, 2), np.asarray(direction, float).reshape(-1, 2),
+                           amp, np.asarray(bucket, dtype=np.int64)))
+
+    def append(self, p: WaveParticle) -> None:
+        self.append_arrays(p.position[None, :], p.direction[None, :], [p.amplitude], [p.bucket])
+
+    @classmethod
+    def from_arrays(cls, pos, direction, amp, bucket, n_buckets: int, device=None) -> "ParticleSet":
+        ps = cls(n_buckets=n_buckets, device=device)
+        ps.append_arrays(pos, direction, amp, bucket)
+        ps.materialize()
+        return ps
+
+    @classmethod
+    def from_segments(cls, x, y, ux, uy, amp, counts: np.ndarray, device=None) -> "ParticleSet":
+        ps = cls(n_buckets=len(counts), device=device)
+        ps.x, ps.y, ps.ux, ps.uy, ps.amp = x, y, ux, uy, amp
+        ps.counts = np.asarray(counts, dtype=np.int64).copy()
+        return ps
+
+    def _empty_device(self, nb: int) -> None:
+        z64 = torch.zeros(0, dtype=torch.float64, device=self.device)
+        self.x, self.y, self.ux, self.uy = z64, z64.clone(), z64.clone(), z64.clone()
+        self.amp = torch.zeros(0, dtype=torch.float32, device=self.device)
+        self.counts = np.zeros(nb, dtype=np.int64)
+
+    def materialize(self, n_buckets: int | None = None) -> "ParticleSet":
+        """Fold pending host batches into the device segments (stable)."""
+        if n_buckets is not None:
+            if self.n_buckets is not None and self.n_buckets != n_buckets:
+                raise ValueError(f"pool has {self.n_buckets} buckets, table has {n_buckets}")
+            self.n_buckets = n_buckets
+        if self.n_buckets is None:
+            raise ValueError("ParticleSet needs n_buckets before device use")
+        if self.x is None:
+            self._empty_device(self.n_buckets)
+        if not self._host:
+            return self
+        pos = np.concatenate([h[0] for h in self._host])
+        d = np.concatenate([h[1] for h in self._host])
+        a = np.concatenate([h[2] for h in self._host])
+        b = np.concatenate([h[3] for h in self._host])
+        self._host = []
+        if np.any((b < 0) | (b >= self.n_buckets)):
+            raise ValueError("bucket index out of range")
+        order = np.argsort(b, kind="stable")
+        new_counts = np.bincount(b, minlength=self.n_buckets)
+        other = ParticleSet.from_segments(
+            torch.from_numpy(pos[order, 0].copy()).to(self.device), torch.from_numpy(pos[order, 1].copy()).to(self.device),
+            torch.from_numpy(d[order, 0].copy()).to(self.device), torch.from_numpy(d[order, 1].copy()).to(self.device),
+            torch.from_numpy(a[order].astype(np.float32)).to(self.device), new_counts, self.device)
+        self._merge(other)
+        return self
+
+    def _merge(self, other: "ParticleSet") -> None:
+        """Per-bucket concatenation [self_b, other_b] (ParticleSet.extend, :163-165)."""
+        if self.counts is None:
+            self._empty_device(other.n_buckets)
+        so = np.concatenate([[0], np.cumsum(self.counts)])
+        oo = np.concatenate([[0], np.cumsum(other.counts)])
+        parts = {k: [] for k in ("x", "y", "ux", "uy", "amp")}
+        for bkt in range(self.n_buckets):
+            for src, off in ((self, so), (other, oo)):
+                lo, hi = int(off[bkt]), int(off[bkt + 1])
+                if hi > lo:
+                    for k in parts:
+                        parts[k].append(getattr(src, k)[lo:hi])
+        for k in parts:
+            dt = torch.float32 if k == "amp" else torch.float64
+            setattr(self, k, torch.cat(parts[k]) if parts[k] else torch.zeros(0, dtype=dt, device=self.device))
+        self.counts = self.counts + other.counts
+
+    def extend(self, other: "ParticleSet") -> None:
+        if other._host and other.n_buckets is None:
+            other.n_buckets = self.n_buckets
+        if self.n_buckets is None:
+            self.n_buckets = other.n_buckets
+        if self.n_buckets is None:      # both host-only: keep buffering
+            self._host.extend(other._host)
+            return
+        self.materialize()
+        other.materialize(self.n_buckets)
+        self._merge(other)
+
+    # ----------------------------------------------------------- access --
+    def __len__(self) -> int:
+        pending = sum(len(h[2]) for h in self._host)
+        return pending + (int(self.counts.sum()) if self.counts is not None else 0)
+
+    def _dev_view(self):
+        self.materialize()
+        return self
+
+    @property
+    def positions(self) -> np.ndarray:
+        s = self._dev_view()
+        return torch.stack([s.x, s.y], 1).cpu().numpy()
+
+    @property
+    def directions(self) -> np.ndarray:
+        s = self._dev_view()
+        return torch.stack([s.ux, s.uy], 1).cpu().numpy()
+
+    @property
+    def amplitudes(self) -> np.ndarray:
+        return self._dev_view().amp.double().cpu().numpy()
+
+    @property
+    def buckets(self) -> np.ndarray:
+        s = self._dev_view()
+        return np.repeat(np.arange(s.n_buckets), s.counts).astype(np.int32)
+
+    @property
+    def birth_times(self) -> np.ndarray:
+        # births are not stored on the device (they are not read on the hot path)
+        return np.full(len(self), np.nan)
+
+    def counts_per_bucket(self, n_buckets: int) -> np.ndarray:
+        self.materialize(n_buckets)
+        return self.counts.copy()
+
+    def segment(self, b: int) -> dict:
+        """Bucket b's particles (numpy, stable order)."""
+        s = self._dev_view()
+        off = np.concatenate([[0], np.cumsum(s.counts)])
+        lo, hi = int(off[b]), int(off[b + 1])
+        return {"pos": torch.stack([s.x[lo:hi], s.y[lo:hi]], 1).cpu().numpy(),
+                "dir": torch.stack([s.ux[lo:hi], s.uy[lo:hi]], 1).cpu().numpy(),
+                "amp": s.amp[lo:hi].double().cpu().numpy()}
+
+    def clear(self) -> None:
+        self._host = []
+        if self.n_buckets is not None:
+            self._empty_device(self.n_buckets)
+
+    def __iter__(self):
+        pos, d, a, b = self.positions, self.directions, self.amplitudes, self.buckets
+        for i in range(len(a)):
+            yield WaveParticle(pos[i].copy(), d[i].copy(), float(a[i]), int(b[i]), float("nan"))
+
+    def pool_struct(self) -> N.HsPool:
+        return N.pool_struct(self.x, self.y, self.ux, self.uy, self.amp)
+
+
+class InjectionLedger:
+    """Fractional group quotas + per-bucket energy books in device memory
+    (particles.py:187-202).  Host views synchronise."""
+
+    def __init__(self, n_buckets: int, rho: float = 1000.0, device=None):
+        dev = _dev(device)
+        self.n_buckets = n_buckets
+        self.rho = rho
+        self.device = dev
+        self.acc = torch.zeros((n_buckets, N_SIDES), dtype=torch.float64, device=dev)
+        self.groups = torch.zeros(n_buckets, dtype=torch.int64, device=dev)
+        self.e_in = torch.zeros(n_buckets, dtype=torch.float64, device=dev)
+        self.e_out = torch.zeros(n_buckets, dtype=torch.float64, device=dev)
+
+    @property
+    def accumulators(self) -> np.ndarray:
+        return self.acc.cpu().numpy()
+
+    @property
+    def injected_groups(self) -> np.ndarray:
+        return self.groups.cpu().numpy()
+
+    @property
+    def injected_energy(self) -> np.ndarray:
+        return self.e_in.cpu().numpy()
+
+    @property
+    def despawned_energy(self) -> np.ndarray:
+        return self.e_out.cpu().numpy()
+
+
+class PhiloxStream:
+    """Device-resident Philox4x64-10 stream state: [key0, key1, counter0 (4
+    words), draw index, pad] -- the layout of HsInjectArgs.rng."""
+
+    def __init__(self, key=(0, 0), device=None, *, counter0: int = (1 << 256) - 1, draw: int = 4):
+        words = [int(key[0]) & ((1 << 64) - 1), int(key[1]) & ((1 << 64) - 1)]
+        words += [(counter0 >> (64 * i)) & ((1 << 64) - 1) for i in range(4)]
+        words += [draw, 0]
+        self.state = torch.tensor(np.array(words, dtype=np.uint64).view(np.int64), device=_dev(device))
+
+    @classmethod
+    def from_generator(cls, gen: np.random.Generator, device=None) -> "PhiloxStream":
+        st = gen.bit_generator.state
+        if st["bit_generator"] != "Philox":
+            raise TypeError("the B200 inject kernel reproduces numpy's Philox stream only; "
+                            "pass Generator(Philox(...)) or a PhiloxStream")
+        ctr = st["state"]["counter"]
+        c = sum(int(ctr[i]) << (64 * i) for i in range(4))
+        key = st["state"]["key"]
+        return cls((int(key[0]), int(key[1])), device, counter0=(c - 1) % (1 << 256), draw=int(st["buffer_pos"]))
+
+    @property
+    def draws(self) -> int:
+        return int(self.state[6].item())
+
+
+def particle_energy(rho: float, g: float, amplitude, radius):
+    """rho g A^2 pi r^2 / 8 (particles.py:205-207)."""
+    return 0.125 * rho * g * np.asarray(amplitude) ** 2 * math.pi * np.asarray(radius) ** 2
+
+
+def groups_per_step(bucket: FrequencyBucket, side_length: float, dt: float, g: float) -> float:
+    """4 L dt w^3 / (pi^3 g) (particles.py:210-216)."""
+    if side_length <= 0 or dt < 0:
+        raise ValueError("side_length must be positive and dt nonnegative")
+    return 4.0 * side_length * dt * bucket.omega ** 3 / (math.pi ** 3 * g)
+
+
+def inject(patch: PatchRegion, table: BucketTable, spectrum: DirectionalSpectrum, ledger: InjectionLedger,
+           dt: float, rng, t: float = 0.0, trough_fraction: float = DEFAULT_TROUGH_FRACTION) -> ParticleSet:
+    """Advance the boundary quotas one step and emit due groups
+    (particles.py:219-300) -- one CUDA launch.  Returns the new crests and
+    troughs as a bucket-segmented ParticleSet (per bucket: crests then
+    troughs, each in group/member order)."""
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    dev = ledger.device
+    nb, nth = table.n_omega, table.n_theta
+    omegas = table.omegas
+    hr = half_rates(patch, omegas, dt, spectrum.params.g)
+    max_g = max_groups_per_step(hr)
+    members = max(1, max_g * nth)
+    stage_cap = 2 * members
+    host_gen = None
+    if isinstance(rng, PhiloxStream):
+        stream = rng
+    else:
+        host_gen = rng
+        stream = PhiloxStream.from_generator(rng, dev)
+    z64 = lambda n: torch.empty(n, dtype=torch.float64, device=dev)  # noqa: E731
+    sx, sy, sux, suy = z64(stage_cap), z64(stage_cap), z64(stage_cap), z64(stage_cap)
+    samp = torch.empty(stage_cap, dtype=torch.float32, device=dev)
+    scount = torch.zeros(nb, dtype=torch.int32, device=dev)
+    scratch = z64(2 * members)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    buckets = structs_to_device(bucket_structs(table, spectrum.params), dev)
+    pstruct = structs_to_device([patch_struct(patch, 2, stage_capacity=stage_cap)], dev)
+    hr_dev = torch.from_numpy(hr.copy()).to(dev)
+    groups_before = ledger.groups.sum() if host_gen is not None else None
+    args = N.HsInjectArgs(n_patches=1, nb=nb, n_theta=nth, buckets=N.ptr(buckets), patches=N.ptr(pstruct),
+                          half_rate=N.ptr(hr_dev), mean_dir=float(spectrum.mean_direction),
+                          beta=float(trough_fraction), rho=float(ledger.rho), g=float(spectrum.params.g),
+                          acc=N.ptr(ledger.acc), groups=N.ptr(ledger.groups), e_in=N.ptr(ledger.e_in),
+                          rng=N.ptr(stream.state), stage=N.pool_struct(sx, sy, sux, suy, samp),
+                          stage_count=N.ptr(scount), scratch=N.ptr(scratch), member_capacity=members,
+                          status=N.ptr(status))
+    N.call("hs_inject", args, stream_ptr())
+    if int(status.item()) != 0:
+        raise RuntimeError("inject staging overflow (internal capacity bound violated)")
+    counts = scount.cpu().numpy().astype(np.int64)
+    total = int(counts.sum())
+    if host_gen is not None:
+        g_tot = int((ledger.groups.sum() - groups_before).item())
+        if g_tot:
+            host_gen.bit_generator.random_raw(g_tot * (1 + nth))   # keep the numpy stream in step
+    return ParticleSet.from_segments(sx[:total], sy[:total], sux[:total], suy[:total], samp[:total], counts, dev)
+
+
+def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRegion,
+           ledger: InjectionLedger | None = None, g: float = 9.81) -> ParticleSet:
+    """Move at the bucket phase speed, despawn particles whose support no
+    longer touches the patch, compact stably (particles.py:303-328).
+    Mutates `particles`; returns the despawned set (segmented)."""
+    if dt < 0:
+        raise ValueError("dt must be nonnegative")
+    nb = table.n_omega
+    particles.materialize(nb)
+    dev = particles.device
+    n = len(particles)
+    if n == 0:
+        return ParticleSet(1, n_buckets=nb, device=dev).materialize()
+    z64 = lambda k: torch.empty(k, dtype=torch.float64, device=dev)  # noqa: E731
+    ox, oy, oux, ouy = z64(n), z64(n), z64(n), z64(n)
+    oamp = torch.empty(n, dtype=torch.float32, device=dev)
+    dx, dy, dux, duy = z64(n), z64(n), z64(n), z64(n)
+    damp = torch.empty(n, dtype=torch.float32, device=dev)
+    in_count = torch.from_numpy(particles.counts.astype(np.int32)).to(dev)
+    out_count = torch.zeros(nb, dtype=torch.int32, device=dev)
+    drop_count = torch.zeros(nb, dtype=torch.int32, device=dev)
+    own_ledger = ledger if ledger is not None else InjectionLedger(nb, device=dev)
+    buckets = structs_to_device(bucket_structs(table, _params_for(table, g)), dev)
+    pstruct = structs_to_device([patch_struct(patch, 2, pool_capacity=n)], dev)
+    max_tiles = (n + 1023) // 1024 + 1
+    tile_state = torch.zeros(max_tiles, dtype=torch.int64, device=dev)
+    tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    args = N.HsAdvectArgs(n_patches=1, nb=nb, buckets=N.ptr(buckets), patches=N.ptr(pstruct), dt=float(dt),
+                          rho=float(own_ledger.rho), g=float(g), in_=particles.pool_struct(),
+                          in_count=N.ptr(in_count), stage=N.pool_struct(), stage_count=0,
+                          out=N.pool_struct(ox, oy, oux, ouy, oamp), out_count=N.ptr(out_count),
+                          dropped=N.pool_struct(dx, dy, dux, duy, damp), dropped_count=N.ptr(drop_count),
+                          e_out=N.ptr(own_ledger.e_out), splat=0, raw_layers=0, raw_layers_len=0, layers=0,
+                          clamped=0, tile_state=N.ptr(tile_state), max_tiles=max_tiles,
+                          tile_counter=N.ptr(tile_counter), status=N.ptr(status))
+    N.call("hs_advect", args, stream_ptr())
+    kc = out_count.cpu().numpy().astype(np.int64)
+    dc = drop_count.cpu().numpy().astype(np.int64)
+    k, d = int(kc.sum()), int(dc.sum())
+    particles.x, particles.y, particles.ux, particles.uy, particles.amp = ox[:k], oy[:k], oux[:k], ouy[:k], oamp[:k]
+    particles.counts = kc
+    return ParticleSet.from_segments(dx[:d], dy[:d], dux[:d], duy[:d], damp[:d], dc, dev)
+
+
+def _params_for(table: BucketTable, g: float):
+    """advect only reads speeds/radii; S_J is irrelevant there, so any valid
+    params record with the right g works for packing the bucket structs."""
+    from .spectrum import derive_params
+    return derive_params(10.0, 1e5, g)

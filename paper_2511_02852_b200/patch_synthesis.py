@@ -1,0 +1,222 @@
+"""Patch height synthesis on the B200: per-bucket splat, separable
+raised-cosine smoothing, bilinear upsampling, gain-sum, finish.
+
+Mirror of `hybridsea.patch_synthesis` (`pkg/src/hybridsea/patch_synthesis.py`).
+Kernel/plan construction is host fp64 (init time, :50-90, :242-258); the
+per-frame work is three CUDA launches (hs_splat, hs_smooth, hs_compose) --
+inside `Simulation.step` the splat is fused into the advect kernel.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._layout import (compose_tile_prefix, grid_dims, pack_layers, patch_struct, stream_ptr,
+                      structs_to_device)
+from .errors import ConfigError
+from .fft_background import HeightField
+from .particles import DEFAULT_TROUGH_FRACTION, ParticleSet, PatchRegion
+from .spectrum import BucketTable
+
+AMPLITUDE_CONVENTIONS = ("energy", "peak")
+
+
+@dataclass(frozen=True)
+class SmoothingKernel:
+    """Normalised symmetric taps + output gain (patch_synthesis.py:37-47)."""
+    taps: np.ndarray
+    half_width: int
+    gain: float
+
+    def __post_init__(self):
+        if len(self.taps) != 2 * self.half_width + 1:
+            raise ValueError("taps length must be 2*half_width + 1")
+
+
+def raised_cosine_taps(half_width: int) -> np.ndarray:
+    """1 + cos(pi m/(R+1)) over m = -R..R, summing to 1 (:50-54)."""
+    m = np.arange(-half_width, half_width + 1)
+    taps = 1.0 + np.cos(math.pi * m / (half_width + 1))
+    return taps / taps.sum()
+
+
+def _pair_square_sum(taps: np.ndarray, shift: int, trough_fraction: float) -> float:
+    """Sum of squares of a unit crest + trailing trough bump pair (:57-66)."""
+    bump = np.outer(taps, taps)
+    w = bump.shape[0]
+    canvas = np.zeros((w + shift, w))
+    canvas[:w] += bump
+    if trough_fraction != 0.0:
+        canvas[shift:] -= trough_fraction * bump
+    return float(np.sum(canvas ** 2))
+
+
+def _kernel_for(radius: float, texel_size: float, convention: str, trough_fraction: float) -> SmoothingKernel:
+    if convention not in AMPLITUDE_CONVENTIONS:
+        raise ConfigError(f"unknown amplitude convention {convention!r}")
+    half = max(1, int(round(radius / texel_size)))
+    taps = raised_cosine_taps(half)
+    if convention == "peak":
+        gain = 1.0 / float(taps[half] ** 2)
+    else:
+        ss = _pair_square_sum(taps, half, trough_fraction) * texel_size ** 2
+        gain = math.sqrt((math.pi * radius ** 2 / 8.0) / ss)
+    return SmoothingKernel(taps=taps, half_width=half, gain=gain)
+
+
+def build_kernels(table: BucketTable, texel_size: float, convention: str = "energy",
+                  trough_fraction: float = DEFAULT_TROUGH_FRACTION) -> list:
+    return [_kernel_for(b.radius, texel_size, convention, trough_fraction) for b in table.buckets]
+
+
+@dataclass(frozen=True)
+class LayerPlan:
+    """Per-bucket decimation factor + kernel at the coarse texel (:227-240)."""
+    kernels: tuple
+    factors: tuple
+
+
+def plan_layers(table: BucketTable, texel_size: float, resolution: int, convention: str = "energy",
+                trough_fraction: float = DEFAULT_TROUGH_FRACTION, min_taps: int = 4,
+                adaptive: bool = True) -> LayerPlan:
+    """Coarse grids at ~min_taps texels per radius (:242-258)."""
+    factors = []
+    for b in table.buckets:
+        if not adaptive:
+            factors.append(1)
+            continue
+        f = max(1, int((b.radius / texel_size) / min_taps))
+        factors.append(min(f, max(1, (resolution - 1) // (4 * min_taps))))
+    kernels = tuple(_kernel_for(b.radius, texel_size * f, convention, trough_fraction)
+                    for b, f in zip(table.buckets, factors))
+    return LayerPlan(kernels=kernels, factors=tuple(factors))
+
+
+def as_plan(plan) -> LayerPlan:
+    if isinstance(plan, LayerPlan):
+        return plan
+    return LayerPlan(kernels=tuple(plan), factors=(1,) * len(plan))
+
+
+def mean_radius(table: BucketTable) -> float:
+    e = table.energies
+    return float(np.sum(e * table.radii) / np.sum(e))
+
+
+class SynthWorkspace:
+    """Device layers and descriptors for synthesising a set of patches."""
+
+    def __init__(self, regions: list, resolutions: list, plans: list, device):
+        self.device = device
+        self.regions = list(regions)
+        self.grids = [(res, grid_dims(r, res)[1]) for r, res in zip(regions, resolutions)]
+        plans = [as_plan(p) for p in plans]
+        self.nb = len(plans[0].kernels)
+        if any(len(p.kernels) != self.nb for p in plans):
+            raise ConfigError("all patches need one kernel per bucket")
+        self.pack = pack_layers(plans, self.grids)
+        self.layers = structs_to_device(self.pack.layers, device)
+        self.taps = torch.from_numpy(self.pack.taps).to(device)
+        self.raw = torch.zeros(max(1, self.pack.raw_len), dtype=torch.float32, device=device)
+        self.smooth = torch.zeros(max(1, self.pack.smooth_len), dtype=torch.float32, device=device)
+        self.smooth_prefix = torch.from_numpy(self.pack.smooth_tile_prefix).to(device)
+        self.compose_prefix_np = compose_tile_prefix(self.grids)
+        self.compose_prefix = torch.from_numpy(self.compose_prefix_np).to(device)
+        self.grid_base = np.concatenate([[0], np.cumsum([r * ny for r, ny in self.grids])]).astype(np.int64)
+        self.clamped = torch.zeros(len(regions), dtype=torch.int32, device=device)
+
+    def patch_structs(self, **kw) -> list:
+        return [patch_struct(r, res, grid_base=int(self.grid_base[k]), layer_base=k * self.nb, **kw)
+                for k, (r, (res, _)) in enumerate(zip(self.regions, self.grids))]
+
+    def smooth_args(self) -> N.HsSmoothArgs:
+        return N.HsSmoothArgs(n_layers=len(self.pack.layers), layers=N.ptr(self.layers), taps=N.ptr(self.taps),
+                              raw_layers=N.ptr(self.raw), smooth_layers=N.ptr(self.smooth),
+                              tile_prefix=N.ptr(self.smooth_prefix),
+                              total_tiles=int(self.pack.smooth_tile_prefix[-1]), max_H=self.pack.max_H)
+
+
+def synthesize(particles: ParticleSet, patch: PatchRegion, resolution: int, plan) -> tuple:
+    """Splat + smooth + upsample + gain-sum of one patch (:277-314).
+    Returns (heights (res, ny) fp32 device tensor, clamped splat count)."""
+    if resolution < 2:
+        raise ConfigError(f"patch resolution must be >= 2, got {resolution}")
+    plan = as_plan(plan)
+    nb = len(plan.kernels)
+    particles.materialize(nb)
+    dev = particles.device
+    ws = SynthWorkspace([patch], [resolution], [plan], dev)
+    res, ny = ws.grids[0]
+    heights = torch.zeros((res, ny), dtype=torch.float32, device=dev)
+    if len(particles) == 0:
+        return heights, 0
+    pst = structs_to_device(ws.patch_structs(), dev)
+    count = torch.from_numpy(particles.counts.astype(np.int32)).to(dev)
+    st = stream_ptr()
+    N.call("hs_splat", N.HsSplatArgs(n_patches=1, nb=nb, patches=N.ptr(pst), pool=particles.pool_struct(),
+                                     count=N.ptr(count), raw_layers=N.ptr(ws.raw), raw_layers_len=ws.pack.raw_len,
+                                     layers=N.ptr(ws.layers), clamped=N.ptr(ws.clamped),
+                                     max_count=int(particles.counts.sum())), st)
+    N.call("hs_smooth", ws.smooth_args(), st)
+    N.call("hs_compose", N.HsComposeArgs(
+        n_patches=1, nb=nb, patches=N.ptr(pst), layers=N.ptr(ws.layers), smooth_layers=N.ptr(ws.smooth),
+        tile_prefix=N.ptr(ws.compose_prefix), total_tiles=int(ws.compose_prefix_np[-1]), bg_height=0,
+        bg_normal=0, bg_n=0, bg_spacing=1.0, patch_height=N.ptr(heights), patch_normal=0, blend_height=0,
+        blend_normal=0, blend_mode=0, interior_sumsq=0, interior_count=0), st)
+    return heights, int(ws.clamped.item())
+
+
+def finish_field(heights, patch: PatchRegion, choppiness: float = 0.0,
+                 displacement_scale: float = 1.0) -> HeightField:
+    """Clamped-border FD normals and optional choppy displacement (:323-340)."""
+    h = torch.as_tensor(heights)
+    if not h.is_cuda:
+        h = h.to(torch.device("cuda", torch.cuda.current_device()))
+    h = h.to(torch.float32).contiguous()
+    if not bool(torch.isfinite(h).all()):
+        raise ValueError("patch heights contain non-finite values")
+    nx, ny = h.shape
+    spacing = patch.l1 / (nx - 1)
+    normal = torch.empty((nx, ny, 3), dtype=torch.float32, device=h.device)
+    disp = torch.zeros((nx, ny, 2), dtype=torch.float32, device=h.device)
+    args = N.HsFinishArgs(nx=nx, ny=ny, spacing=spacing, chop_scale=-choppiness * displacement_scale,
+                          height=N.ptr(h), normal=N.ptr(normal), disp=N.ptr(disp) if choppiness != 0.0 else 0)
+    N.call("hs_finish", args, stream_ptr())
+    return HeightField(resolution=nx, origin=patch.min_corner.copy(), spacing=spacing, height=h,
+                       displacement=disp, normal=normal, periodic=False)
+
+
+class LayerStack:
+    """Texel-exact (factor 1) layered synthesis (:133-162): holds the kernels
+    and the accumulated particles; `smooth_and_sum` runs the device path."""
+
+    def __init__(self, patch: PatchRegion, resolution: int, kernels: list):
+        if resolution < 2:
+            raise ConfigError(f"patch resolution must be >= 2, got {resolution}")
+        self.patch = patch
+        self.resolution = resolution
+        self.texel_size = patch.l1 / (resolution - 1)
+        self.ny = int(round(patch.l2 / self.texel_size)) + 1
+        self.kernels = list(kernels)
+        self.pads = [k.half_width + 1 for k in self.kernels]
+        self.particles = ParticleSet(n_buckets=len(self.kernels))
+        self.clamped_splats = 0
+
+
+def accumulate(particles: ParticleSet, patch: PatchRegion, stack: LayerStack) -> LayerStack:
+    particles.materialize(len(stack.kernels))
+    stack.particles.extend(particles)
+    return stack
+
+
+def smooth_and_sum(stack: LayerStack, kernels: list | None = None) -> torch.Tensor:
+    kernels = kernels if kernels is not None else stack.kernels
+    if len(kernels) != len(stack.kernels):
+        raise ConfigError("need exactly one kernel per layer")
+    h, c = synthesize(stack.particles, stack.patch, stack.resolution, list(kernels))
+    stack.clamped_splats = c
+    return h
