@@ -94,7 +94,7 @@ typedef struct {
     int wx, wy;          /* padded layer dims ncx+2pad, ncy+2pad */
     int taps_off;        /* offset into the taps array */
     float gain;          /* output gain */
-    int pad0;
+    int mid_off;         /* float offset into HsSmoothArgs.mid (wide kernels), -1 otherwise */
 } HsLayer;
 
 /* Structure-of-arrays particle pool.  Pools of all patches live in one set of
@@ -200,15 +200,25 @@ HS_API int hs_splat(const HsSplatArgs* a, void* stream);
 /* Separable raised-cosine smoothing of every layer (all patches, all
  * buckets) from the raw padded layers into the cropped smoothed layers.
  * Replaces smooth_layer/convolve1d_zero (patch_synthesis.py:105-130,206-209). */
+/* Layers with H <= HS_SMOOTH_FUSED_MAX_H run one fused 2-D tile pass; wider
+ * kernels (texel-exact plans) run two 1-D passes through `mid`
+ * (HsLayer.mid_off, ncx*wy floats per wide layer).                          */
+#define HS_SMOOTH_FUSED_MAX_H 40
 typedef struct {
     int n_layers;
     const HsLayer* layers;
     const float* taps;
     const float* raw_layers;
     float* smooth_layers;
-    const int* tile_prefix;   /* [n_layers+1] cumulative 32x32 tile counts */
+    const int* tile_prefix;   /* [n_layers+1] cumulative fused 32x32 tiles (0 for wide layers) */
     int total_tiles;
-    int max_H;
+    int max_H;                /* max H over fused layers */
+    float* mid;               /* wide-layer intermediate, or NULL */
+    const int* xtile_prefix;  /* [n_layers+1] x-pass tiles of wide layers (ncx x wy) */
+    int total_xtiles;
+    const int* ytile_prefix;  /* [n_layers+1] y-pass tiles of wide layers (ncx x ncy) */
+    int total_ytiles;
+    int max_H_wide;           /* max H over wide layers (<= 780) */
 } HsSmoothArgs;
 HS_API int hs_smooth(const HsSmoothArgs* a, void* stream);
 

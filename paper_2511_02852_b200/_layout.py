@@ -67,16 +67,25 @@ class LayerPack:
     taps: np.ndarray           # float32
     raw_len: int               # floats
     smooth_len: int            # floats
-    smooth_tile_prefix: np.ndarray   # int32 [n_layers + 1]
+    smooth_tile_prefix: np.ndarray   # int32 [n_layers + 1] fused tiles
     max_H: int
+    mid_len: int = 0           # floats of the wide-kernel intermediate
+    xtile_prefix: np.ndarray = None
+    ytile_prefix: np.ndarray = None
+    max_H_wide: int = 0
+
+
+def _tiles(a: int, b: int) -> int:
+    return (-(-a // TILE)) * (-(-b // TILE))
 
 
 def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
     """Lay out the per-bucket decimated layers of every patch (LayerPlan,
-    patch_synthesis.py:227-258; layer dims :306-308)."""
-    layers, taps, prefix = [], [], [0]
-    raw_off = sm_off = tap_off = 0
-    max_h = 1
+    patch_synthesis.py:227-258; layer dims :306-308).  Kernels wider than
+    HS_SMOOTH_FUSED_MAX_H take the two-pass path through a scratch layer."""
+    layers, taps, prefix, xpre, ypre = [], [], [0], [0], [0]
+    raw_off = sm_off = tap_off = mid_off = 0
+    max_h, max_hw = 1, 0
     for plan, (res, ny) in zip(plans, grids):
         for k, f in zip(plan.kernels, plan.factors):
             pad = k.half_width + 1
@@ -85,18 +94,26 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
             wx, wy = ncx + 2 * pad, ncy + 2 * pad
             if len(k.taps) > min(wx, wy):
                 raise ConfigError(f"kernel of {len(k.taps)} taps wider than grid axis of {min(wx, wy)}")
+            wide = k.half_width > N.HS_SMOOTH_FUSED_MAX_H
+            if wide and k.half_width > 780:
+                raise ConfigError(f"kernel half width {k.half_width} exceeds the device limit of 780 texels")
             layers.append(N.HsLayer(raw_off, sm_off, f, k.half_width, pad, ncx, ncy, wx, wy, tap_off,
-                                    float(k.gain), 0))
+                                    float(k.gain), mid_off if wide else -1))
             taps.append(np.asarray(k.taps, dtype=np.float32))
             raw_off += wx * wy
             sm_off += ncx * ncy
             tap_off += len(k.taps)
-            max_h = max(max_h, k.half_width)
-            prefix.append(prefix[-1] + (-(-ncx // TILE)) * (-(-ncy // TILE)))
-    if max_h > 88:
-        raise ConfigError(f"kernel half width {max_h} exceeds the device limit of 88 texels")
+            if wide:
+                mid_off += ncx * wy
+                max_hw = max(max_hw, k.half_width)
+            else:
+                max_h = max(max_h, k.half_width)
+            prefix.append(prefix[-1] + (0 if wide else _tiles(ncx, ncy)))
+            xpre.append(xpre[-1] + (_tiles(ncx, wy) if wide else 0))
+            ypre.append(ypre[-1] + (_tiles(ncx, ncy) if wide else 0))
     return LayerPack(layers, np.concatenate(taps) if taps else np.zeros(0, np.float32), raw_off, sm_off,
-                     np.array(prefix, dtype=np.int32), max_h)
+                     np.array(prefix, dtype=np.int32), max_h, mid_off, np.array(xpre, dtype=np.int32),
+                     np.array(ypre, dtype=np.int32), max_hw)
 
 
 def compose_tile_prefix(grids: list[tuple[int, int]]) -> np.ndarray:

@@ -19,6 +19,7 @@ HS_STATUS_POOL_OVERFLOW = 1
 HS_STATUS_STAGE_OVERFLOW = 2
 HS_MAX_BUCKETS = 32
 HS_MAX_PATCHES = 256
+HS_SMOOTH_FUSED_MAX_H = 40
 
 vp = C.c_void_p
 dbl = C.c_double
@@ -41,7 +42,7 @@ class HsPatch(C.Structure):
 class HsLayer(C.Structure):
     _fields_ = [("raw_off", i64), ("sm_off", i64), ("f", i32), ("H", i32), ("pad", i32), ("ncx", i32),
                 ("ncy", i32), ("wx", i32), ("wy", i32), ("taps_off", i32), ("gain", C.c_float),
-                ("pad0", i32)]
+                ("mid_off", i32)]
 
 
 class HsPool(C.Structure):
@@ -79,7 +80,9 @@ class HsSplatArgs(C.Structure):
 
 class HsSmoothArgs(C.Structure):
     _fields_ = [("n_layers", i32), ("layers", vp), ("taps", vp), ("raw_layers", vp),
-                ("smooth_layers", vp), ("tile_prefix", vp), ("total_tiles", i32), ("max_H", i32)]
+                ("smooth_layers", vp), ("tile_prefix", vp), ("total_tiles", i32), ("max_H", i32),
+                ("mid", vp), ("xtile_prefix", vp), ("total_xtiles", i32), ("ytile_prefix", vp),
+                ("total_ytiles", i32), ("max_H_wide", i32)]
 
 
 class HsComposeArgs(C.Structure):

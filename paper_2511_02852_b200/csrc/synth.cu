@@ -71,6 +71,68 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     }
 }
 
+// Wide kernels (H > HS_SMOOTH_FUSED_MAX_H): two 1-D passes through `mid`.
+// x pass: mid[r][c] = sum_m taps[m] raw[r + pad - H + m][c], r in crop rows,
+// c over the full padded width; y pass: out[r][c] = sum_m taps[m] mid[r][c + pad - H + m].
+__global__ void __launch_bounds__(256) smooth_wide_x_kernel(HsSmoothArgs a) {
+    extern __shared__ float smem[];
+    const int tile = blockIdx.x;
+    const int l = find_seg_i(a.xtile_prefix, a.n_layers + 1, tile);
+    const HsLayer L = a.layers[l];
+    const int local = tile - a.xtile_prefix[l];
+    const int tiles_c = (L.wy + SM_TILE - 1) / SM_TILE;
+    const int r0 = (local / tiles_c) * SM_TILE, c0 = (local % tiles_c) * SM_TILE;
+    const int H = L.H, K = 2 * H + 1, R = SM_TILE + 2 * H;
+    float* taps = smem;
+    float* in = taps + ((K + 3) & ~3);          // R x 32
+    for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
+    const float* raw = a.raw_layers + L.raw_off;
+    for (int e = threadIdx.x; e < R * SM_TILE; e += blockDim.x) {
+        int r = e / SM_TILE, c = e - r * SM_TILE;
+        int gx = r0 + L.pad - H + r, gy = c0 + c;
+        in[e] = (gx >= 0 && gx < L.wx && gy < L.wy) ? raw[(long long)gx * L.wy + gy] : 0.f;
+    }
+    __syncthreads();
+    float* mid = a.mid + L.mid_off;
+    for (int e = threadIdx.x; e < SM_TILE * SM_TILE; e += blockDim.x) {
+        int r = e / SM_TILE, c = e - r * SM_TILE;
+        if (r0 + r >= L.ncx || c0 + c >= L.wy) continue;
+        float s = 0.f;
+        for (int m = 0; m < K; ++m) s = fmaf(taps[m], in[(r + m) * SM_TILE + c], s);
+        mid[(long long)(r0 + r) * L.wy + c0 + c] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) smooth_wide_y_kernel(HsSmoothArgs a) {
+    extern __shared__ float smem[];
+    const int tile = blockIdx.x;
+    const int l = find_seg_i(a.ytile_prefix, a.n_layers + 1, tile);
+    const HsLayer L = a.layers[l];
+    const int local = tile - a.ytile_prefix[l];
+    const int tiles_c = (L.ncy + SM_TILE - 1) / SM_TILE;
+    const int r0 = (local / tiles_c) * SM_TILE, c0 = (local % tiles_c) * SM_TILE;
+    const int H = L.H, K = 2 * H + 1, C = SM_TILE + 2 * H;
+    float* taps = smem;
+    float* in = taps + ((K + 3) & ~3);          // 32 x C
+    for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
+    const float* mid = a.mid + L.mid_off;
+    for (int e = threadIdx.x; e < SM_TILE * C; e += blockDim.x) {
+        int r = e / C, c = e - r * C;
+        int gx = r0 + r, gy = c0 + L.pad - H + c;
+        in[e] = (gx < L.ncx && gy >= 0 && gy < L.wy) ? mid[(long long)gx * L.wy + gy] : 0.f;
+    }
+    __syncthreads();
+    float* out = a.smooth_layers + L.sm_off;
+    for (int e = threadIdx.x; e < SM_TILE * SM_TILE; e += blockDim.x) {
+        int r = e / SM_TILE, c = e - r * SM_TILE;
+        if (r0 + r >= L.ncx || c0 + c >= L.ncy) continue;
+        float s = 0.f;
+        const float* row = in + r * C + c;
+        for (int m = 0; m < K; ++m) s = fmaf(taps[m], row[m], s);
+        out[(long long)(r0 + r) * L.ncy + c0 + c] = s;
+    }
+}
+
 // ============================================================== compose ==
 __device__ __forceinline__ float upsample_at(const float* __restrict__ S, const HsLayer& L, int i, int j) {
     if (L.f == 1) return S[(long long)i * L.ncy + j];
@@ -332,18 +394,36 @@ using namespace hs;
 
 extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_smooth: null args");
-    if (a->total_tiles == 0) return 0;
     HS_CHECK_ARG(a->layers && a->taps && a->raw_layers && a->smooth_layers && a->tile_prefix, "hs_smooth: missing buffer");
-    HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= 88, "hs_smooth: max_H=%d out of range [1, 88]", a->max_H);
-    const int W = SM_TILE + 2 * a->max_H, K = 2 * a->max_H + 1;
-    size_t sm = (size_t)(((K + 3) & ~3) + W * W + SM_TILE * W) * sizeof(float);
-    static size_t smooth_attr = 48 * 1024;
-    if (sm > smooth_attr) {
-        HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        smooth_attr = sm;
+    cudaStream_t st = as_stream(stream);
+    if (a->total_tiles > 0) {
+        HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= HS_SMOOTH_FUSED_MAX_H, "hs_smooth: max_H=%d out of range", a->max_H);
+        const int W = SM_TILE + 2 * a->max_H, K = 2 * a->max_H + 1;
+        size_t sm = (size_t)(((K + 3) & ~3) + W * W + SM_TILE * W) * sizeof(float);
+        static size_t smooth_attr = 48 * 1024;
+        if (sm > smooth_attr) {
+            HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            smooth_attr = sm;
+        }
+        smooth_kernel<<<a->total_tiles, 256, sm, st>>>(*a);
+        HS_LAUNCH_CHECK();
     }
-    smooth_kernel<<<a->total_tiles, 256, sm, as_stream(stream)>>>(*a);
-    HS_LAUNCH_CHECK();
+    if (a->total_xtiles > 0) {
+        HS_CHECK_ARG(a->mid && a->xtile_prefix && a->ytile_prefix, "hs_smooth: wide layers need mid + tile prefixes");
+        HS_CHECK_ARG(a->max_H_wide >= 1 && a->max_H_wide <= 780, "hs_smooth: max_H_wide=%d out of range", a->max_H_wide);
+        const int K = 2 * a->max_H_wide + 1, R = SM_TILE + 2 * a->max_H_wide;
+        size_t sm = (size_t)(((K + 3) & ~3) + R * SM_TILE) * sizeof(float);
+        static size_t wide_attr = 48 * 1024;
+        if (sm > wide_attr) {
+            HS_CUDA(cudaFuncSetAttribute(smooth_wide_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            HS_CUDA(cudaFuncSetAttribute(smooth_wide_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            wide_attr = sm;
+        }
+        smooth_wide_x_kernel<<<a->total_xtiles, 256, sm, st>>>(*a);
+        HS_LAUNCH_CHECK();
+        smooth_wide_y_kernel<<<a->total_ytiles, 256, sm, st>>>(*a);
+        HS_LAUNCH_CHECK();
+    }
     return 0;
 }
 

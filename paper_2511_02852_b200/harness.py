@@ -248,12 +248,17 @@ class Simulation:
         return N.pool_struct(*self.pools[k])
 
     # --------------------------------------------------------- the frame --
-    def _enqueue_frame(self, parity: int, dt: float) -> None:
-        """Enqueue one frame on the current stream (graph-capturable)."""
+    def _enqueue_frame(self, parity: int, dt: float, mark=None) -> None:
+        """Enqueue one frame on the current stream (graph-capturable).
+        `mark(stage)` (optional) is called after each stage's launches, e.g.
+        to record CUDA events for per-stage timing."""
         st = stream_ptr()
+        mark = mark or (lambda _name: None)
+        mark("start")
         if self.fft_state is not None:
             self.fft_ws.sumsq.zero_()
             N.call("hs_fft_evolve", fft_args(self.fft_state, self.fft_ws, frame_ptr=self.frame_dev, dt=dt), st)
+        mark("fft")
         if self.n_patches:
             src, dst = parity, parity ^ 1
             self.isum.zero_()
@@ -267,6 +272,7 @@ class Simulation:
                 e_in=N.ptr(self.e_in), rng=N.ptr(self.rng), stage=N.pool_struct(*self.stage),
                 stage_count=N.ptr(self.stage_count), scratch=N.ptr(self.scratch), member_capacity=self.member_cap,
                 status=N.ptr(self.status)), st)
+            mark("inject")
             N.call("hs_advect", N.HsAdvectArgs(
                 n_patches=self.n_patches, nb=self.nb, buckets=N.ptr(self.buckets_dev), patches=N.ptr(self.patches_dev),
                 dt=float(dt), rho=float(self.config.rho), g=float(self.config.g), in_=self._pool(src),
@@ -276,7 +282,9 @@ class Simulation:
                 raw_layers_len=self.synth.pack.raw_len, layers=N.ptr(self.synth.layers),
                 clamped=N.ptr(self.synth.clamped), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
                 tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status)), st)
+            mark("advect")
             N.call("hs_smooth", self.synth.smooth_args(), st)
+            mark("smooth")
             bg = self.fft_ws
             N.call("hs_compose", N.HsComposeArgs(
                 n_patches=self.n_patches, nb=self.nb, patches=N.ptr(self.patches_dev), layers=N.ptr(self.synth.layers),
@@ -289,7 +297,9 @@ class Simulation:
                 patch_height=N.ptr(self.patch_h), patch_normal=N.ptr(self.patch_n),
                 blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
                 interior_sumsq=N.ptr(self.isum), interior_count=N.ptr(self.icount)), st)
+            mark("compose")
         N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(st))
+        mark("end")
 
     def _graph(self, parity: int):
         g = self._graphs.get(parity)
@@ -302,6 +312,38 @@ class Simulation:
             torch.cuda.current_stream(self.device).wait_stream(s)
             self._graphs[parity] = g
         return g
+
+    def kernel_launches_per_frame(self) -> int:
+        """Library kernels one frame launches (csrc/*.cu): fft rows + cols
+        (+ periodic normals), inject, advect, smooth (1 or 3), compose,
+        advance_frame."""
+        k = 1
+        if self.fft_state is not None:
+            k += 2 + (1 if self.fft_ws.normal is not None else 0)
+        if self.n_patches:
+            pk = self.synth.pack
+            k += 3 + (1 if pk.smooth_tile_prefix[-1] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
+        return k
+
+    def timed_frame(self, dt: float | None = None) -> dict:
+        """Run one eager frame with CUDA events after every stage; returns
+        {stage: ms} (synchronises).  Used by bench.py for the per-kernel
+        roofline; not part of the normal step path."""
+        use_dt = self.config.dt if dt is None else float(dt)
+        evs = []
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            evs.append((name, e))
+        self._enqueue_frame(self._parity, use_dt, mark)
+        self._parity ^= 1
+        self.frame += 1
+        evs[-1][1].synchronize()
+        out = {}
+        for (_, a), (name, b) in zip(evs[:-1], evs[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
 
     def step(self, dt: float | None = None, *, stats: bool = True):
         """Advance one frame.  With the configured dt and `config.graph` the

@@ -124,6 +124,9 @@ class SynthWorkspace:
         self.raw = torch.zeros(max(1, self.pack.raw_len), dtype=torch.float32, device=device)
         self.smooth = torch.zeros(max(1, self.pack.smooth_len), dtype=torch.float32, device=device)
         self.smooth_prefix = torch.from_numpy(self.pack.smooth_tile_prefix).to(device)
+        self.xtile_prefix = torch.from_numpy(self.pack.xtile_prefix).to(device)
+        self.ytile_prefix = torch.from_numpy(self.pack.ytile_prefix).to(device)
+        self.mid = torch.zeros(self.pack.mid_len, dtype=torch.float32, device=device) if self.pack.mid_len else None
         self.compose_prefix_np = compose_tile_prefix(self.grids)
         self.compose_prefix = torch.from_numpy(self.compose_prefix_np).to(device)
         self.grid_base = np.concatenate([[0], np.cumsum([r * ny for r, ny in self.grids])]).astype(np.int64)
@@ -137,7 +140,10 @@ class SynthWorkspace:
         return N.HsSmoothArgs(n_layers=len(self.pack.layers), layers=N.ptr(self.layers), taps=N.ptr(self.taps),
                               raw_layers=N.ptr(self.raw), smooth_layers=N.ptr(self.smooth),
                               tile_prefix=N.ptr(self.smooth_prefix),
-                              total_tiles=int(self.pack.smooth_tile_prefix[-1]), max_H=self.pack.max_H)
+                              total_tiles=int(self.pack.smooth_tile_prefix[-1]), max_H=self.pack.max_H,
+                              mid=N.ptr(self.mid), xtile_prefix=N.ptr(self.xtile_prefix),
+                              total_xtiles=int(self.pack.xtile_prefix[-1]), ytile_prefix=N.ptr(self.ytile_prefix),
+                              total_ytiles=int(self.pack.ytile_prefix[-1]), max_H_wide=self.pack.max_H_wide)
 
 
 def synthesize(particles: ParticleSet, patch: PatchRegion, resolution: int, plan) -> tuple:
