@@ -160,7 +160,7 @@ def reference_arm(args):
     t_warm = time.perf_counter()
     n_warm = int(round(args.warm_seconds / WARM_DT))
     for _ in range(n_warm):                       # same warm-up as the GPU arm, no synthesis
-        sc.step(dt=WARM_DT, synth=False)
+        sc.step(dt=WARM_DT, synth=False, fft=False)
     warm_s = time.perf_counter() - t_warm
     for _ in range(min(args.warmup, 1)):
         sc.step()

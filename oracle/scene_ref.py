@@ -60,12 +60,12 @@ class OracleScene:
         self.background = None
         self.fields = []
 
-    def step(self, dt: float | None = None, synth: bool = True) -> dict:
+    def step(self, dt: float | None = None, synth: bool = True, fft: bool = True) -> dict:
         sc = self.sc
         dt = sc["dt"] if dt is None else dt
         t = self.frame * dt
         out = {"t": t}
-        if self.fft:
+        if self.fft and fft:
             h, dx, dy, nrm = ocean_ref.evolve(self.h0, sc["fft_domain"], self.p.g, t, sc["fft_choppiness"])
             n = sc["fft_n"]
             self.background = blend_ref.Field(h, nrm, np.zeros(2), sc["fft_domain"] / n)

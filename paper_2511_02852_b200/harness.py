@@ -304,6 +304,8 @@ class Simulation:
     def _graph(self, parity: int):
         g = self._graphs.get(parity)
         if g is None:
+            if self.n_patches:
+                self._hr(self.config.dt)        # host->device uploads must precede capture
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream(self.device))
