@@ -129,7 +129,8 @@ typedef struct {
     float* dx;                /* [n*n] */
     float* dy;                /* [n*n] */
     float* normal;            /* [n*n*3] or NULL */
-    double* sumsq;            /* scalar accumulator += sum(height^2), or NULL */
+    double* sumsq;            /* scalar, set to sum(height^2) (zeroed by this call), or NULL */
+    long long* frame_advance; /* optional: device frame counter, += 1 after the transform */
 } HsFftArgs;
 HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
 
@@ -152,6 +153,8 @@ typedef struct {
     double* scratch;               /* [n_patches*member_capacity*2] */
     int member_capacity;           /* per patch: >= max groups * n_theta */
     int* status;
+    int* zero_words;               /* optional: 4-byte words zeroed by this launch (per-frame */
+    int n_zero_words;              /*   stat accumulators read by later kernels)             */
 } HsInjectArgs;
 HS_API int hs_inject(const HsInjectArgs* a, void* stream);
 
@@ -210,7 +213,7 @@ typedef struct {
     const float* taps;
     const float* raw_layers;
     float* smooth_layers;
-    const int* tile_prefix;   /* [n_layers+1] cumulative fused 32x32 tiles (0 for wide layers) */
+    const int* tile_info;     /* [total_tiles*3] fused 32x32 tiles: layer, cx0, cy0 */
     int total_tiles;
     int max_H;                /* max H over fused layers */
     float* mid;               /* wide-layer intermediate, or NULL */
@@ -232,7 +235,7 @@ typedef struct {
     const HsPatch* patches;
     const HsLayer* layers;
     const float* smooth_layers;
-    const int* tile_prefix;     /* [n_patches+1] cumulative 32x32 tile counts */
+    const int* tile_info;       /* [total_tiles*3] 32x32 output tiles: patch, i0, j0 */
     int total_tiles;
     /* background (may be NULL: flat water) */
     const float* bg_height; const float* bg_normal; int bg_n; double bg_spacing;
@@ -244,6 +247,7 @@ typedef struct {
     int blend_mode;             /* 0: no blend, 1: blend */
     double* interior_sumsq;     /* [n_patches] += sum h^2 over the interior inset, or NULL */
     long long* interior_count;  /* [n_patches] matching counts, or NULL */
+    long long* frame_advance;   /* optional: device frame counter, += 1 by this launch */
 } HsComposeArgs;
 HS_API int hs_compose(const HsComposeArgs* a, void* stream);
 

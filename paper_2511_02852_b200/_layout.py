@@ -69,6 +69,7 @@ class LayerPack:
     smooth_len: int            # floats
     smooth_tile_prefix: np.ndarray   # int32 [n_layers + 1] fused tiles
     max_H: int
+    smooth_tile_info: np.ndarray = None   # int32 [tiles, 3]: layer, cx0, cy0 (fused path)
     mid_len: int = 0           # floats of the wide-kernel intermediate
     xtile_prefix: np.ndarray = None
     ytile_prefix: np.ndarray = None
@@ -111,16 +112,20 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
             prefix.append(prefix[-1] + (0 if wide else _tiles(ncx, ncy)))
             xpre.append(xpre[-1] + (_tiles(ncx, wy) if wide else 0))
             ypre.append(ypre[-1] + (_tiles(ncx, ncy) if wide else 0))
+    info = [(l, tx * TILE, ty * TILE) for l, L in enumerate(layers) if L.mid_off < 0
+            for tx in range(-(-L.ncx // TILE)) for ty in range(-(-L.ncy // TILE))]
+    # largest kernels first: the long-tap tiles start earliest
+    info.sort(key=lambda t: -layers[t[0]].H)
     return LayerPack(layers, np.concatenate(taps) if taps else np.zeros(0, np.float32), raw_off, sm_off,
-                     np.array(prefix, dtype=np.int32), max_h, mid_off, np.array(xpre, dtype=np.int32),
-                     np.array(ypre, dtype=np.int32), max_hw)
+                     np.array(prefix, dtype=np.int32), max_h, np.array(info, dtype=np.int32).reshape(-1, 3),
+                     mid_off, np.array(xpre, dtype=np.int32), np.array(ypre, dtype=np.int32), max_hw)
 
 
-def compose_tile_prefix(grids: list[tuple[int, int]]) -> np.ndarray:
-    pre = [0]
-    for res, ny in grids:
-        pre.append(pre[-1] + (-(-res // TILE)) * (-(-ny // TILE)))
-    return np.array(pre, dtype=np.int32)
+def compose_tile_info(grids: list[tuple[int, int]]) -> np.ndarray:
+    """[tiles, 3] int32: patch, i0, j0 of every 32x32 output tile."""
+    info = [(p, tx * TILE, ty * TILE) for p, (res, ny) in enumerate(grids)
+            for tx in range(-(-res // TILE)) for ty in range(-(-ny // TILE))]
+    return np.array(info, dtype=np.int32).reshape(-1, 3)
 
 
 def patch_struct(region, res: int, *, pool_base=0, pool_capacity=0, stage_base=0, stage_capacity=0,

@@ -53,14 +53,15 @@ class HsFftArgs(C.Structure):
     _fields_ = [("n", i32), ("emit_normals", i32), ("g", dbl), ("t", dbl), ("choppiness", dbl),
                 ("frame_ptr", vp), ("dt", dbl), ("spacing", dbl), ("kf", vp), ("h0", vp),
                 ("twiddle", vp), ("work_a", vp), ("work_b", vp), ("height", vp), ("dx", vp),
-                ("dy", vp), ("normal", vp), ("sumsq", vp)]
+                ("dy", vp), ("normal", vp), ("sumsq", vp), ("frame_advance", vp)]
 
 
 class HsInjectArgs(C.Structure):
     _fields_ = [("n_patches", i32), ("nb", i32), ("n_theta", i32), ("buckets", vp), ("patches", vp),
                 ("half_rate", vp), ("mean_dir", dbl), ("beta", dbl), ("rho", dbl), ("g", dbl),
                 ("acc", vp), ("groups", vp), ("e_in", vp), ("rng", vp), ("stage", HsPool),
-                ("stage_count", vp), ("scratch", vp), ("member_capacity", i32), ("status", vp)]
+                ("stage_count", vp), ("scratch", vp), ("member_capacity", i32), ("status", vp),
+                ("zero_words", vp), ("n_zero_words", i32)]
 
 
 class HsAdvectArgs(C.Structure):
@@ -80,18 +81,18 @@ class HsSplatArgs(C.Structure):
 
 class HsSmoothArgs(C.Structure):
     _fields_ = [("n_layers", i32), ("layers", vp), ("taps", vp), ("raw_layers", vp),
-                ("smooth_layers", vp), ("tile_prefix", vp), ("total_tiles", i32), ("max_H", i32),
+                ("smooth_layers", vp), ("tile_info", vp), ("total_tiles", i32), ("max_H", i32),
                 ("mid", vp), ("xtile_prefix", vp), ("total_xtiles", i32), ("ytile_prefix", vp),
                 ("total_ytiles", i32), ("max_H_wide", i32)]
 
 
 class HsComposeArgs(C.Structure):
     _fields_ = [("n_patches", i32), ("nb", i32), ("patches", vp), ("layers", vp),
-                ("smooth_layers", vp), ("tile_prefix", vp), ("total_tiles", i32),
+                ("smooth_layers", vp), ("tile_info", vp), ("total_tiles", i32),
                 ("bg_height", vp), ("bg_normal", vp), ("bg_n", i32), ("bg_spacing", dbl),
                 ("patch_height", vp), ("patch_normal", vp), ("blend_height", vp),
                 ("blend_normal", vp), ("blend_mode", i32), ("interior_sumsq", vp),
-                ("interior_count", vp)]
+                ("interior_count", vp), ("frame_advance", vp)]
 
 
 class HsSampleArgs(C.Structure):

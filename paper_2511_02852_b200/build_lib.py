@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libhybridsea_b200.so")
-SOURCES = ["capi.cu", "fft.cu", "particles.cu", "synth.cu"]
+SOURCES = ["capi.cu", "fft.cu", "particles.cu", "synth.cu", "compose.cu"]
 # -fmad=false keeps every fp64 mul/add a separate IEEE op (bit-exact with
 # numpy on the integer-relevant paths); fp32 code uses explicit fmaf where
 # contraction is wanted.

@@ -76,6 +76,7 @@ struct FftDev {
     int n, logn, chop_on;
     double g, t, chop, dt;
     const long long* frame_ptr;
+    double* sumsq_zero;
     const double* kf;
     const float2* h0;
     const float2* tw;
@@ -96,11 +97,13 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(FftDev d) {
     const int i = blockIdx.x;
     const int ip = (n - i) & (n - 1);
     const bool self = (i == ip);
-    for (int k = threadIdx.x; k < half; k += blockDim.x) tw[k] = d.tw[k];
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        r0[j] = d.h0[(size_t)i * n + j];
-        r1[j] = d.h0[(size_t)ip * n + j];
+    if (d.sumsq_zero && i == 0 && threadIdx.x == 0) *d.sumsq_zero = 0.0;   // accumulated by pass 2
+    for (int k = threadIdx.x; k < half / 2; k += blockDim.x) cp_async16(tw + 2 * k, d.tw + 2 * k);
+    for (int k = threadIdx.x; k < half; k += blockDim.x) {
+        cp_async16(r0 + 2 * k, d.h0 + (size_t)i * n + 2 * k);
+        cp_async16(r1 + 2 * k, d.h0 + (size_t)ip * n + 2 * k);
     }
+    cp_async_wait_all();
     __syncthreads();
     const double kxi = d.kf[i], kxip = d.kf[ip];
     const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame*dt
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(FftDev d) {
 
 // ---------------------------------------------------------------- pass 2 --
 struct ColOut {
-    float* h; float* dx; float* dy; double* sumsq;
+    float* h; float* dx; float* dy; double* sumsq; long long* frame_advance;
 };
 
 template <int CA, int CBP>
@@ -165,14 +168,16 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftDev d, ColOut o, int n
     const int stride = n + 1;                 // padded column stride
     float2* tw = sm;
     float2* cols = tw + half;
-    for (int k = threadIdx.x; k < half; k += blockDim.x) tw[k] = d.tw[k];
+    if (o.frame_advance && blockIdx.x == 0 && threadIdx.x == 0) *o.frame_advance += 1;
+    for (int k = threadIdx.x; k < half / 2; k += blockDim.x) cp_async16(tw + 2 * k, d.tw + 2 * k);
     double acc = 0.0;
     if ((int)blockIdx.x < n_a_tiles) {
         const int j0 = blockIdx.x * CA;
         for (int e = threadIdx.x; e < n * CA; e += blockDim.x) {
             int i = e / CA, c = e - i * CA;
-            cols[c * stride + bitrev(i, logn)] = d.wa[(size_t)i * n + j0 + c];
+            cp_async8(cols + c * stride + bitrev(i, logn), d.wa + (size_t)i * n + j0 + c, true);
         }
+        cp_async_wait_all();
         __syncthreads();
         ifft_smem(cols, CA, stride, n, logn, tw);
         for (int e = threadIdx.x; e < n * CA; e += blockDim.x) {
@@ -190,8 +195,10 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftDev d, ColOut o, int n
                 int i = e / (2 * CBP), c = e - i * (2 * CBP);
                 o.dy[(size_t)i * n + j0 + c] = 0.f;
             }
+            cp_async_wait_all();
             return;
         }
+        cp_async_wait_all();
         for (int e = threadIdx.x; e < n * CBP; e += blockDim.x) {
             int i = e / CBP, q = e - i * CBP;
             int src = i <= half ? i : n - i;
@@ -257,6 +264,7 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     d.logn = 31 - __builtin_clz((unsigned)n);
     d.chop_on = chop_on;
     d.g = a->g; d.t = a->t; d.chop = a->choppiness; d.dt = a->dt; d.frame_ptr = a->frame_ptr;
+    d.sumsq_zero = a->sumsq;
     d.kf = a->kf;
     d.h0 = reinterpret_cast<const float2*>(a->h0);
     d.tw = reinterpret_cast<const float2*>(a->twiddle);
@@ -272,7 +280,7 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     fft_rows_kernel<<<n / 2 + 1, 256, sm_rows, st>>>(d);
     HS_LAUNCH_CHECK();
 
-    ColOut o{a->height, a->dx, a->dy, a->sumsq};
+    ColOut o{a->height, a->dx, a->dy, a->sumsq, a->frame_advance};
     // columns per CTA: keep a tile <= 64 KiB of complex64
     auto launch_cols = [&](auto kern, int ca, int cbp) -> int {
         int n_a = n / ca;

@@ -141,6 +141,24 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sm, int* total) {
     return res;
 }
 
+// ------------------------------------------------------------ cp.async --
+// Asynchronous global -> shared copies (LDGSTS): a thread issues all of its
+// tile loads back to back and waits once, so a CTA keeps KBs in flight
+// instead of one dependent load per loop trip.  `valid == false` zero-fills.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __device__ __forceinline__ float smoothstep01(float t) {
     t = fminf(fmaxf(t, 0.f), 1.f);
     return t * t * (3.f - 2.f * t);

@@ -32,6 +32,8 @@ __device__ __forceinline__ int find_cell(const int* gstart, int ncell, int g) {
     return lo;
 }
 
+constexpr int INJ_SMEM_MEMBERS = 1536;
+
 __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     const int p = blockIdx.x;
     const int nb = a.nb, nth = a.n_theta, ncell = nb * 4;
@@ -47,6 +49,8 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     const double* hr = a.half_rate + (size_t)p * ncell;
     unsigned long long* rng = a.rng + (size_t)p * 8;
 
+    if (p == 0)
+        for (int w = threadIdx.x; w < a.n_zero_words; w += blockDim.x) a.zero_words[w] = 0;
     // 1. quota ledger: acc += half_rate; n = floor(acc); acc -= n   (particles.py:243-245)
     for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
         double v = dadd(acc[c], hr[c]);
@@ -77,7 +81,10 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     const double dth = dmul(2.0, pi) / (double)nth;
     const double j_lo = dmul(-0.5, dth), j_range = dsub(dmul(0.5, dth), j_lo);
     const unsigned long long D = rng[6];
-    double* scr = a.scratch + (size_t)p * a.member_capacity * 2;
+    // member (energy, amplitude) pairs: shared memory when they fit (the
+    // per-bucket sums below walk them serially), global scratch otherwise
+    __shared__ double scr_sm[2 * INJ_SMEM_MEMBERS];
+    double* scr = M <= INJ_SMEM_MEMBERS ? scr_sm : a.scratch + (size_t)p * a.member_capacity * 2;
 
     // 2. amplitudes + booked energy for every member  (particles.py:256-264, 291-292)
     for (int m = threadIdx.x; m < M; m += blockDim.x) {
@@ -186,41 +193,62 @@ __device__ __forceinline__ int find_seg(const int* off, int nseg, int v) {
     return lo;
 }
 
-__device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
-                                          double x, double y, float amp, int* clamp_acc) {
-    // gx = (x - x0)/texel / f + pad  (patch_synthesis.py:298-299, 309, 169-177)
-    double gx = (x - P.x0) / P.texel;
-    double gy = (y - P.y0) / P.texel;
-    double u = gx / (double)L.f + (double)L.pad;
-    double v = gy / (double)L.f + (double)L.pad;
-    const double umax = (double)(L.wx - 1), vmax = (double)(L.wy - 1);
-    if (u < 0.0 || u > umax || v < 0.0 || v > vmax) ++(*clamp_acc);
-    u = fmin(fmax(u, 0.0), umax - 1e-9);
-    v = fmin(fmax(v, 0.0), vmax - 1e-9);
+// Bilinear scatter-add of one particle into its bucket layer
+// (patch_synthesis.py:165-186 at gx/f, 298-310).  u = (x - x0)/(texel f) + pad
+// in fp64 (index and clamp decision), weights in fp32.
+struct SplatLayer {
+    long long raw_off;
+    double inv_tf;          // 1 / (texel * f)
+    double umax, vmax;      // wx - 1, wy - 1
+    int wy, pad;
+};
+
+__device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLayer& L, double x0, double y0,
+                                         double x, double y, float amp, int* clamp_acc) {
+    double u = (x - x0) * L.inv_tf + (double)L.pad;
+    double v = (y - y0) * L.inv_tf + (double)L.pad;
+    if (u < 0.0 || u > L.umax || v < 0.0 || v > L.vmax) ++(*clamp_acc);
+    u = fmin(fmax(u, 0.0), L.umax - 1e-9);
+    v = fmin(fmax(v, 0.0), L.vmax - 1e-9);
     const int i0 = (int)u, j0 = (int)v;
     const float fu = (float)(u - i0), fv = (float)(v - j0);
     float* q = raw + L.raw_off + (long long)i0 * L.wy + j0;
-    atomicAdd(q, amp * (1.f - fu) * (1.f - fv));
-    atomicAdd(q + L.wy, amp * fu * (1.f - fv));
-    atomicAdd(q + 1, amp * (1.f - fu) * fv);
-    atomicAdd(q + L.wy + 1, amp * fu * fv);
+    const float a1 = amp * fu, a0 = amp - a1;          // amp (1 - fu), amp fu
+    atomicAdd(q, a0 * (1.f - fv));
+    atomicAdd(q + L.wy, a1 * (1.f - fv));
+    atomicAdd(q + 1, a0 * fv);
+    atomicAdd(q + L.wy + 1, a1 * fv);
 }
 
-__global__ void __launch_bounds__(ADV_THREADS) advect_kernel(HsAdvectArgs a) {
+__device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
+                                          double x, double y, float amp, int* clamp_acc) {
+    SplatLayer S{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1), L.wy, L.pad};
+    splat_at(raw, S, P.x0, P.y0, x, y, amp, clamp_acc);
+}
+
+// Persistent CTAs take tiles of ADV_TILE virtual items in order from a global
+// counter; tiles never straddle patches.  Per item: advect in fp64 with the
+// reference's operation order, keep test, tile-local rank by ballots, tile
+// prefix by a warp-parallel decoupled look-back, stable scatter of survivors
+// (and optionally of the dropped), fused splat of survivors.
+__global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) {
     const int nb = a.nb;
     __shared__ int tile_prefix[HS_MAX_PATCHES + 1];
     __shared__ int in_off[HS_MAX_BUCKETS + 1];
     __shared__ int st_off[HS_MAX_BUCKETS + 1];
     __shared__ int voff[HS_MAX_BUCKETS + 1];
     __shared__ int in_cnt_s[HS_MAX_BUCKETS];
+    __shared__ double step_s[HS_MAX_BUCKETS], r2_s[HS_MAX_BUCKETS];
+    __shared__ SplatLayer sl_s[HS_MAX_BUCKETS];
     __shared__ int keep_hist[HS_MAX_BUCKETS];
     __shared__ int drop_hist[HS_MAX_BUCKETS];
     __shared__ double eout_s[HS_MAX_BUCKETS];
     __shared__ int warp_tot[ADV_ITEMS][ADV_THREADS / 32];
-    __shared__ int tile_s, prefix_s, clamp_s;
+    __shared__ int tile_s, prefix_s, clamp_s, cur_p_s, seg_b_s, seg_end_s;
     __shared__ HsPatch P_s;
 
     if (threadIdx.x == 0) {
+        cur_p_s = -1;
         tile_prefix[0] = 0;
         for (int p = 0; p < a.n_patches; ++p) {
             const HsPatch& P = a.patches[p];
@@ -239,29 +267,44 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_kernel(HsAdvectArgs a) {
         if (tile >= total_tiles) break;
         const int p = find_seg(tile_prefix, a.n_patches + 1, tile);
         const int ltile = tile - tile_prefix[p];
-        if (threadIdx.x == 0) {
-            P_s = a.patches[p];
-            int si = 0, ss = 0, sv = 0;
-            for (int b = 0; b < nb; ++b) {
-                int ci = a.in_count[(size_t)p * nb + b];
-                int cs = a.stage_count ? a.stage_count[(size_t)p * nb + b] : 0;
-                in_off[b] = si; st_off[b] = ss; voff[b] = sv; in_cnt_s[b] = ci;
-                si += ci; ss += cs; sv += ci + cs;
+        if (p != cur_p_s && wid == 0) {
+            // per-patch tables (warp 0; reused while tiles stay in patch p)
+            const HsPatch P = a.patches[p];
+            if (lane == 0) P_s = P;
+            const int ci = lane < nb ? a.in_count[(size_t)p * nb + lane] : 0;
+            const int cs = (lane < nb && a.stage_count) ? a.stage_count[(size_t)p * nb + lane] : 0;
+            const int si = warp_incl_scan(ci, lane), ss = warp_incl_scan(cs, lane);
+            if (lane < nb) {
+                in_off[lane] = si - ci; st_off[lane] = ss - cs; voff[lane] = si - ci + ss - cs; in_cnt_s[lane] = ci;
+                const HsBucket B = a.buckets[lane];
+                step_s[lane] = dmul(B.speed, a.dt);                   // speeds * dt (particles.py:312-313)
+                r2_s[lane] = dmul(B.radius, B.radius);
+                if (a.splat) {
+                    const HsLayer L = a.layers[P.layer_base + lane];
+                    sl_s[lane] = SplatLayer{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1),
+                                            (double)(L.wy - 1), L.wy, L.pad};
+                }
             }
-            in_off[nb] = si; st_off[nb] = ss; voff[nb] = sv;
-            clamp_s = 0;
+            if (lane == nb - 1) { in_off[nb] = si; st_off[nb] = ss; voff[nb] = si + ss; }
+            if (lane == 0) cur_p_s = p;
         }
         if (threadIdx.x < nb) { keep_hist[threadIdx.x] = 0; drop_hist[threadIdx.x] = 0; eout_s[threadIdx.x] = 0.0; }
         __syncthreads();
-        const HsPatch P = P_s;
         const int N = voff[nb];
         const int tbase = ltile * ADV_TILE;
-        if (tbase >= N) {
-            // empty tile: publish an inclusive prefix equal to the predecessor's
-            // (never read: later tiles of this patch are empty too)
+        if (tbase >= N) {               // empty tile (the patch's later tiles are empty too)
             __syncthreads();
             continue;
         }
+        if (threadIdx.x == 0) {
+            const int b = find_seg(voff, nb + 1, tbase);
+            seg_b_s = b;
+            seg_end_s = voff[b + 1];
+            clamp_s = 0;
+        }
+        __syncthreads();
+        const HsPatch P = P_s;
+        const int seg_b = seg_b_s, seg_end = seg_end_s;
         double nx[ADV_ITEMS], ny_[ADV_ITEMS], dxv[ADV_ITEMS], dyv[ADV_ITEMS];
         float am[ADV_ITEMS];
         int bk[ADV_ITEMS];
@@ -272,65 +315,63 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_kernel(HsAdvectArgs a) {
             keep[it] = 0;
             bk[it] = 0;
             if (v < N) {
-                const int b = find_seg(voff, nb + 1, v);
-                // empty buckets share voff entries; find_seg returns the last such b
+                const int b = v < seg_end ? seg_b : find_seg(voff, nb + 1, v);
                 const int local = v - voff[b];
-                long long src;
-                const double* X; const double* Y; const double* UX; const double* UY; const float* AM;
-                if (local < in_cnt_s[b]) {
-                    src = P.pool_base + in_off[b] + local;
-                    X = a.in.x; Y = a.in.y; UX = a.in.ux; UY = a.in.uy; AM = a.in.amp;
-                } else {
-                    src = P.stage_base + st_off[b] + (local - in_cnt_s[b]);
-                    X = a.stage.x; Y = a.stage.y; UX = a.stage.ux; UY = a.stage.uy; AM = a.stage.amp;
-                }
-                const HsBucket B = a.buckets[b];
-                const double step = dmul(B.speed, a.dt);                 // speeds * dt
-                const double ux = UX[src], uy = UY[src];
-                const double x = dadd(X[src], dmul(ux, step));           // pos += dir * (c dt)
-                const double y = dadd(Y[src], dmul(uy, step));
+                const bool from_pool = local < in_cnt_s[b];
+                const long long src = from_pool ? P.pool_base + in_off[b] + local
+                                                : P.stage_base + st_off[b] + (local - in_cnt_s[b]);
+                const HsPool& S = from_pool ? a.in : a.stage;
+                const double step = step_s[b];
+                const double ux = S.ux[src], uy = S.uy[src];
+                const double x = dadd(S.x[src], dmul(ux, step));        // pos += dir * (c dt)
+                const double y = dadd(S.y[src], dmul(uy, step));
                 const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
                 const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
-                keep[it] = dadd(dmul(ox, ox), dmul(oy, oy)) <= dmul(B.radius, B.radius);
-                nx[it] = x; ny_[it] = y; dxv[it] = ux; dyv[it] = uy; am[it] = AM[src]; bk[it] = b;
+                keep[it] = dadd(dmul(ox, ox), dmul(oy, oy)) <= r2_s[b];  // support disk (:315-320)
+                nx[it] = x; ny_[it] = y; dxv[it] = ux; dyv[it] = uy; am[it] = S.amp[src]; bk[it] = b;
             }
         }
         // tile-local ranks: per (row, warp) ballots
 #pragma unroll
         for (int it = 0; it < ADV_ITEMS; ++it) {
-            unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
             if (lane == 0) warp_tot[it][wid] = __popc(bal);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int it = 0; it < ADV_ITEMS; ++it) {
-                for (int w = 0; w < ADV_THREADS / 32; ++w) {
-                    int c = warp_tot[it][w];
-                    warp_tot[it][w] = run;
-                    run += c;
-                }
-            }
-            // decoupled look-back within this patch
+        if (wid == 0) {
+            // exclusive scan of the ADV_ITEMS x 8 warp totals (row-major), one lane per entry
+            constexpr int NW = ADV_THREADS / 32;
+            const int cnt = lane < ADV_ITEMS * NW ? warp_tot[lane / NW][lane % NW] : 0;
+            const int inc = warp_incl_scan(cnt, lane);
+            const int agg = __shfl_sync(0xffffffffu, inc, ADV_ITEMS * NW - 1);
+            if (lane < ADV_ITEMS * NW) warp_tot[lane / NW][lane % NW] = inc - cnt;
+            // decoupled look-back over this patch's earlier tiles, 32 at a time
             unsigned long long* ts = a.tile_state;
-            unsigned long long agg = (unsigned long long)run;
+            const int first = tile - ltile;
             unsigned long long prefix = 0;
             if (ltile == 0) {
-                atomicExch(&ts[tile], FLAG_PRE | agg);
+                if (lane == 0) atomicExch(&ts[tile], FLAG_PRE | (unsigned long long)agg);
             } else {
-                atomicExch(&ts[tile], FLAG_AGG | agg);
-                int j = tile - 1;
+                if (lane == 0) atomicExch(&ts[tile], FLAG_AGG | (unsigned long long)agg);
+                int hi = tile - 1;
                 while (true) {
-                    unsigned long long s = *((volatile unsigned long long*)&ts[j]);
-                    unsigned long long flag = s & (3ULL << 32);
-                    if (flag == 0) continue;
-                    prefix += s & 0xffffffffULL;
-                    if (flag == FLAG_PRE) break;
-                    --j;
+                    const int j = hi - lane;
+                    unsigned long long sv = FLAG_PRE;     // before the patch: prefix 0
+                    if (j >= first) {
+                        do { sv = *((volatile unsigned long long*)&ts[j]); } while ((sv >> 32) == 0);
+                    }
+                    const unsigned pre = __ballot_sync(0xffffffffu, (sv & (3ULL << 32)) == FLAG_PRE);
+                    const int stop = pre ? __ffs(pre) - 1 : 31;          // closest full prefix
+                    unsigned long long val = lane <= stop ? (sv & 0xffffffffULL) : 0ULL;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    prefix += val;
+                    if (pre) break;
+                    hi -= 32;
                 }
-                atomicExch(&ts[tile], FLAG_PRE | (prefix + agg));
+                if (lane == 0) atomicExch(&ts[tile], FLAG_PRE | (prefix + (unsigned long long)agg));
             }
-            prefix_s = (int)prefix;
+            if (lane == 0) prefix_s = (int)prefix;
         }
         __syncthreads();
         const int tprefix = prefix_s;
@@ -339,11 +380,11 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_kernel(HsAdvectArgs a) {
 #pragma unroll
         for (int it = 0; it < ADV_ITEMS; ++it) {
             const int v = tbase + it * ADV_THREADS + threadIdx.x;
-            unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
             if (v < N) {
                 const int b = bk[it];
+                const int rank = tprefix + warp_tot[it][wid] + __popc(bal & ((1u << lane) - 1u));
                 if (keep[it]) {
-                    const int rank = tprefix + warp_tot[it][wid] + __popc(bal & ((1u << lane) - 1u));
                     if (rank < P.pool_capacity) {
                         const long long o = P.pool_base + rank;
                         a.out.x[o] = nx[it]; a.out.y[o] = ny_[it];
@@ -352,19 +393,16 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_kernel(HsAdvectArgs a) {
                         atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
                     }
                     atomicAdd(&keep_hist[b], 1);
-                    if (a.splat) splat_one(raw, a.layers[P.layer_base + b], P, nx[it], ny_[it], am[it], &clamp_local);
+                    if (a.splat) splat_at(raw, sl_s[b], P.x0, P.y0, nx[it], ny_[it], am[it], &clamp_local);
                 } else {
                     if (am[it] > 0.f) {
                         // crest despawn energy rho g A^2 pi r^2 / 8 (particles.py:322-327)
-                        const double r = a.buckets[b].radius;
                         const double amp = (double)am[it];
-                        double e = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * (r * r);
+                        const double e = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2_s[b];
                         atomicAdd(&eout_s[b], e);
                     }
                     if (a.dropped.x) {
-                        // dropped rank = items before v that were not kept (stable)
-                        const int rank = tprefix + warp_tot[it][wid] + __popc(bal & ((1u << lane) - 1u));
-                        const long long o = P.pool_base + (v - rank);
+                        const long long o = P.pool_base + (v - rank);       // stable among the dropped
                         a.dropped.x[o] = nx[it]; a.dropped.y[o] = ny_[it];
                         a.dropped.ux[o] = dxv[it]; a.dropped.uy[o] = dyv[it]; a.dropped.amp[o] = am[it];
                         atomicAdd(&drop_hist[b], 1);

@@ -12,62 +12,128 @@
 //   hs_sample    SurfaceSampler.sample at arbitrary points (coupling.py:143-161)
 //   hs_composite Simulation.stitched_heights (harness.py:219-241)
 //   hs_finish    finish_field on a standalone grid
-#include "hs_common.cuh"
+#include "synth_common.cuh"
 
 namespace hs {
-
-__device__ __forceinline__ int find_seg_i(const int* off, int nseg, int v) {
-    int lo = 0, hi = nseg - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= v) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
 
 // =============================================================== smooth ==
 constexpr int SM_TILE = 32;
 
-__global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
-    extern __shared__ float smem[];
-    const int tile = blockIdx.x;
-    const int l = find_seg_i(a.tile_prefix, a.n_layers + 1, tile);
-    const HsLayer L = a.layers[l];
-    const int local = tile - a.tile_prefix[l];
-    const int tiles_y = (L.ncy + SM_TILE - 1) / SM_TILE;
-    const int cx0 = (local / tiles_y) * SM_TILE, cy0 = (local % tiles_y) * SM_TILE;
-    const int H = L.H, K = 2 * H + 1, W = SM_TILE + 2 * H;
-    float* taps = smem;            // K (padded to 4)
-    float* in = taps + ((K + 3) & ~3);
-    float* mid = in + W * W;
-    for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
-    const float* raw = a.raw_layers + L.raw_off;
-    const int rx0 = cx0 + L.pad - H, ry0 = cy0 + L.pad - H;
-    for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
-        int r = e / W, c = e - r * W;
-        int gx = rx0 + r, gy = ry0 + c;
-        in[e] = (gx >= 0 && gx < L.wx && gy >= 0 && gy < L.wy) ? raw[(long long)gx * L.wy + gy] : 0.f;
+constexpr int SM_RB = 8;                 // outputs per thread along the convolution axis
+
+// x pass of one tile, register-blocked: thread item = (column c, block of 8
+// output rows); the K taps live in registers and each input value is loaded
+// once and feeds up to 8 accumulators.
+template <int H>
+__device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ in, float* __restrict__ mid,
+                                                     const float* __restrict__ taps_sm, int W, int MS,
+                                                     float* __restrict__ out, long long out_base, int ncy,
+                                                     int rows_valid, int cols_valid) {
+    constexpr int K = 2 * H + 1;
+    float t[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) t[m] = taps_sm[m];
+    // x pass (axis 0): mid[r][c] = sum_m t[m] in[r + m][c]
+    for (int item = threadIdx.x; item < W * (SM_TILE / SM_RB); item += blockDim.x) {
+        const int c = item % W, rb = item / W;
+        float acc[SM_RB];
+#pragma unroll
+        for (int k = 0; k < SM_RB; ++k) acc[k] = 0.f;
+        const float* col = in + (rb * SM_RB) * W + c;
+#pragma unroll
+        for (int u = 0; u < SM_RB + 2 * H; ++u) {
+            const float v = col[u * W];
+#pragma unroll
+            for (int k = 0; k < SM_RB; ++k) {
+                const int m = u - k;
+                if (m >= 0 && m < K) acc[k] = fmaf(t[m], v, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SM_RB; ++k) mid[(rb * SM_RB + k) * MS + c] = acc[k];
     }
     __syncthreads();
-    // pass along axis 0 (x): mid[r][c] = sum_m taps[m] in[r+m][c]
+    // y pass (axis 1): thread item = (row r, block of 8 output columns)
+    for (int item = threadIdx.x; item < SM_TILE * (SM_TILE / SM_RB); item += blockDim.x) {
+        const int r = item % SM_TILE, cb = item / SM_TILE;
+        float acc[SM_RB];
+#pragma unroll
+        for (int k = 0; k < SM_RB; ++k) acc[k] = 0.f;
+        const float* row = mid + r * MS + cb * SM_RB;
+#pragma unroll
+        for (int u = 0; u < SM_RB + 2 * H; ++u) {
+            const float v = row[u];
+#pragma unroll
+            for (int k = 0; k < SM_RB; ++k) {
+                const int m = u - k;
+                if (m >= 0 && m < K) acc[k] = fmaf(t[m], v, acc[k]);
+            }
+        }
+        if (r < rows_valid) {
+#pragma unroll
+            for (int k = 0; k < SM_RB; ++k)
+                if (cb * SM_RB + k < cols_valid) out[out_base + (long long)r * ncy + cb * SM_RB + k] = acc[k];
+        }
+    }
+}
+
+__device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in, float* __restrict__ mid,
+                                                    const float* __restrict__ taps, int H, int W, int MS,
+                                                    float* __restrict__ out, long long out_base, int ncy,
+                                                    int rows_valid, int cols_valid) {
+    const int K = 2 * H + 1;
     for (int e = threadIdx.x; e < SM_TILE * W; e += blockDim.x) {
-        int r = e / W, c = e - r * W;
+        const int r = e / W, c = e - r * W;
         const float* col = in + r * W + c;
         float s = 0.f;
         for (int m = 0; m < K; ++m) s = fmaf(taps[m], col[m * W], s);
-        mid[e] = s;
+        mid[r * MS + c] = s;
     }
     __syncthreads();
-    // pass along axis 1 (y)
-    float* out = a.smooth_layers + L.sm_off;
     for (int e = threadIdx.x; e < SM_TILE * SM_TILE; e += blockDim.x) {
-        int r = e / SM_TILE, c = e - r * SM_TILE;
-        int ox = cx0 + r, oy = cy0 + c;
-        if (ox >= L.ncx || oy >= L.ncy) continue;
-        const float* row = mid + r * W + c;
+        const int r = e / SM_TILE, c = e - r * SM_TILE;
+        if (r >= rows_valid || c >= cols_valid) continue;
+        const float* row = mid + r * MS + c;
         float s = 0.f;
         for (int m = 0; m < K; ++m) s = fmaf(taps[m], row[m], s);
-        out[(long long)ox * L.ncy + oy] = s;
+        out[out_base + (long long)r * ncy + c] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
+    extern __shared__ float smem[];
+    const int* ti = a.tile_info + 3 * blockIdx.x;
+    const HsLayer L = a.layers[ti[0]];
+    const int cx0 = ti[1], cy0 = ti[2];
+    const int H = L.H, K = 2 * H + 1, W = SM_TILE + 2 * H;
+    const int MS = W | 1;                      // odd row stride: conflict-free column walks
+    float* taps = smem;                        // K (padded to 4)
+    float* in = taps + ((K + 3) & ~3);         // W x W
+    float* mid = in + W * W;                   // 32 x MS
+    for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
+    const float* raw = a.raw_layers + L.raw_off;
+    const int rx0 = cx0 + L.pad - H, ry0 = cy0 + L.pad - H;
+    for (int r = threadIdx.x >> 5; r < W; r += blockDim.x >> 5) {       // warp per row, lanes along it
+        const int gx = rx0 + r;
+        const bool rok = gx >= 0 && gx < L.wx;
+        for (int c = threadIdx.x & 31; c < W; c += 32) {
+            const int gy = ry0 + c;
+            const bool ok = rok && gy >= 0 && gy < L.wy;
+            cp_async4(in + r * W + c, ok ? raw + (long long)gx * L.wy + gy : raw, ok);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    float* out = a.smooth_layers + L.sm_off;
+    const long long ob = (long long)cx0 * L.ncy + cy0;
+    const int rv = min(SM_TILE, L.ncx - cx0), cv = min(SM_TILE, L.ncy - cy0);
+    switch (H) {
+#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(in, mid, taps, W, MS, out, ob, L.ncy, rv, cv); break;
+        HS_SM_CASE(1) HS_SM_CASE(2) HS_SM_CASE(3) HS_SM_CASE(4) HS_SM_CASE(5) HS_SM_CASE(6) HS_SM_CASE(7)
+        HS_SM_CASE(8) HS_SM_CASE(9) HS_SM_CASE(10) HS_SM_CASE(11) HS_SM_CASE(12) HS_SM_CASE(13)
+        HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16)
+#undef HS_SM_CASE
+        default: smooth_tile_generic(in, mid, taps, H, W, MS, out, ob, L.ncy, rv, cv);
     }
 }
 
@@ -90,8 +156,10 @@ __global__ void __launch_bounds__(256) smooth_wide_x_kernel(HsSmoothArgs a) {
     for (int e = threadIdx.x; e < R * SM_TILE; e += blockDim.x) {
         int r = e / SM_TILE, c = e - r * SM_TILE;
         int gx = r0 + L.pad - H + r, gy = c0 + c;
-        in[e] = (gx >= 0 && gx < L.wx && gy < L.wy) ? raw[(long long)gx * L.wy + gy] : 0.f;
+        const bool ok = gx >= 0 && gx < L.wx && gy < L.wy;
+        cp_async4(in + e, ok ? raw + (long long)gx * L.wy + gy : raw, ok);
     }
+    cp_async_wait_all();
     __syncthreads();
     float* mid = a.mid + L.mid_off;
     for (int e = threadIdx.x; e < SM_TILE * SM_TILE; e += blockDim.x) {
@@ -119,8 +187,10 @@ __global__ void __launch_bounds__(256) smooth_wide_y_kernel(HsSmoothArgs a) {
     for (int e = threadIdx.x; e < SM_TILE * C; e += blockDim.x) {
         int r = e / C, c = e - r * C;
         int gx = r0 + r, gy = c0 + L.pad - H + c;
-        in[e] = (gx < L.ncx && gy >= 0 && gy < L.wy) ? mid[(long long)gx * L.wy + gy] : 0.f;
+        const bool ok = gx < L.ncx && gy >= 0 && gy < L.wy;
+        cp_async4(in + e, ok ? mid + (long long)gx * L.wy + gy : mid, ok);
     }
+    cp_async_wait_all();
     __syncthreads();
     float* out = a.smooth_layers + L.sm_off;
     for (int e = threadIdx.x; e < SM_TILE * SM_TILE; e += blockDim.x) {
@@ -130,149 +200,6 @@ __global__ void __launch_bounds__(256) smooth_wide_y_kernel(HsSmoothArgs a) {
         const float* row = in + r * C + c;
         for (int m = 0; m < K; ++m) s = fmaf(taps[m], row[m], s);
         out[(long long)(r0 + r) * L.ncy + c0 + c] = s;
-    }
-}
-
-// ============================================================== compose ==
-__device__ __forceinline__ float upsample_at(const float* __restrict__ S, const HsLayer& L, int i, int j) {
-    if (L.f == 1) return S[(long long)i * L.ncy + j];
-    const int ci = i / L.f, cj = j / L.f;
-    const float wi = (float)((double)(i - ci * L.f) / (double)L.f);
-    const float wj = (float)((double)(j - cj * L.f) / (double)L.f);
-    const int ci1 = min(ci + 1, L.ncx - 1), cj1 = min(cj + 1, L.ncy - 1);
-    const float* r0 = S + (long long)ci * L.ncy;
-    const float* r1 = S + (long long)ci1 * L.ncy;
-    float a0 = r0[cj] * (1.f - wi) + r1[cj] * wi;
-    float a1 = r0[cj1] * (1.f - wi) + r1[cj1] * wi;
-    return a0 * (1.f - wj) + a1 * wj;
-}
-
-struct BgView {
-    const float* h; const float* nrm; int n; double spacing; double x0, y0;
-};
-
-// periodic bilinear (fft_background.py:222-249)
-__device__ __forceinline__ void sample_bg(const BgView& bg, double x, double y, float& h, float3& nv) {
-    if (!bg.h) { h = 0.f; nv = make_float3(0.f, 0.f, 1.f); return; }
-    const double u = (x - bg.x0) / bg.spacing, v = (y - bg.y0) / bg.spacing;
-    const double fi = floor(u), fj = floor(v);
-    const float fu = (float)(u - fi), fv = (float)(v - fj);
-    const int m = bg.n - 1;
-    const int i0 = ((long long)fi) & m, j0 = ((long long)fj) & m;
-    const int i1 = (i0 + 1) & m, j1 = (j0 + 1) & m;
-    const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
-    const long long a00 = (long long)i0 * bg.n + j0, a10 = (long long)i1 * bg.n + j0;
-    const long long a01 = (long long)i0 * bg.n + j1, a11 = (long long)i1 * bg.n + j1;
-    h = bg.h[a00] * w00 + bg.h[a10] * w10 + bg.h[a01] * w01 + bg.h[a11] * w11;
-    if (bg.nrm) {
-        const float* N = bg.nrm;
-        float nx = N[3 * a00] * w00 + N[3 * a10] * w10 + N[3 * a01] * w01 + N[3 * a11] * w11;
-        float ny = N[3 * a00 + 1] * w00 + N[3 * a10 + 1] * w10 + N[3 * a01 + 1] * w01 + N[3 * a11 + 1] * w11;
-        float nz = N[3 * a00 + 2] * w00 + N[3 * a10 + 2] * w10 + N[3 * a01 + 2] * w01 + N[3 * a11 + 2] * w11;
-        float r = rsqrtf(nx * nx + ny * ny + nz * nz);
-        nv = make_float3(nx * r, ny * r, nz * r);
-    } else {
-        nv = make_float3(0.f, 0.f, 1.f);
-    }
-}
-
-// smoothstep weight from inward boundary depth (coupling.py:27-40)
-__device__ __forceinline__ double blend_w(const HsPatch& P, double x, double y) {
-    double d = fmin(fmin(x - P.x0, P.x1 - x), fmin(y - P.y0, P.y1 - y));
-    if (!(d > 0.0)) return 0.0;
-    double t = fmin(fmax(d / P.margin, 0.0), 1.0);
-    return t * t * (3.0 - 2.0 * t);
-}
-
-constexpr int CT = 32;
-
-__global__ void __launch_bounds__(256) compose_kernel(HsComposeArgs a) {
-    __shared__ float hs_[CT + 2][CT + 3];
-    __shared__ double red_s[8];
-    __shared__ long long redc_s[8];
-    const int tile = blockIdx.x;
-    const int p = find_seg_i(a.tile_prefix, a.n_patches + 1, tile);
-    const HsPatch P = a.patches[p];
-    const int local = tile - a.tile_prefix[p];
-    const int tiles_y = (P.ny + CT - 1) / CT;
-    const int i0 = (local / tiles_y) * CT, j0 = (local % tiles_y) * CT;
-    const HsLayer* Ls = a.layers + P.layer_base;
-    const int nb = a.nb;
-    // 1. patch heights with a 1-texel halo
-    for (int e = threadIdx.x; e < (CT + 2) * (CT + 2); e += blockDim.x) {
-        int r = e / (CT + 2), c = e - r * (CT + 2);
-        int i = i0 - 1 + r, j = j0 - 1 + c;
-        float h = 0.f;
-        if (i >= 0 && i < P.res && j >= 0 && j < P.ny) {
-            for (int b = 0; b < nb; ++b) {
-                const HsLayer L = Ls[b];
-                h += L.gain * upsample_at(a.smooth_layers + L.sm_off, L, i, j);
-            }
-        }
-        hs_[r][c] = h;
-    }
-    __syncthreads();
-    BgView bg{a.bg_height, a.bg_normal, a.bg_n, a.bg_spacing, 0.0, 0.0};
-    const float s = (float)P.texel;
-    const int inset = max(1, (int)rint(P.margin / P.texel));
-    double acc = 0.0;
-    long long cnt = 0;
-    const long long gb = P.grid_base;
-    for (int e = threadIdx.x; e < CT * CT; e += blockDim.x) {
-        int r = e / CT, c = e - r * CT;
-        int i = i0 + r, j = j0 + c;
-        if (i >= P.res || j >= P.ny) continue;
-        const float h = hs_[r + 1][c + 1];
-        float hx, hy;
-        if (i == 0) hx = (hs_[r + 2][c + 1] - h) / s;
-        else if (i == P.res - 1) hx = (h - hs_[r][c + 1]) / s;
-        else hx = (hs_[r + 2][c + 1] - hs_[r][c + 1]) / (2.f * s);
-        if (j == 0) hy = (hs_[r + 1][c + 2] - h) / s;
-        else if (j == P.ny - 1) hy = (h - hs_[r + 1][c]) / s;
-        else hy = (hs_[r + 1][c + 2] - hs_[r + 1][c]) / (2.f * s);
-        const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
-        const float3 pn = make_float3(-hx * rn, -hy * rn, rn);
-        const long long o = gb + (long long)i * P.ny + j;
-        if (a.patch_height) a.patch_height[o] = h;
-        if (a.patch_normal) { a.patch_normal[3 * o] = pn.x; a.patch_normal[3 * o + 1] = pn.y; a.patch_normal[3 * o + 2] = pn.z; }
-        if (i >= inset && i < P.res - inset && j >= inset && j < P.ny - inset) {
-            acc += (double)h * (double)h;
-            ++cnt;
-        }
-        if (a.blend_mode) {
-            const double x = P.x0 + (double)i * P.texel;     // patch nodes (coupling.py:57-59)
-            const double y = P.y0 + (double)j * P.texel;
-            float hb; float3 nb3;
-            sample_bg(bg, x, y, hb, nb3);
-            const double w = blend_w(P, x, y);
-            if (w > 0.0) {
-                const float wf = (float)w;
-                hb = wf * h + (1.f - wf) * hb;
-                float mx = wf * pn.x + (1.f - wf) * nb3.x;
-                float my = wf * pn.y + (1.f - wf) * nb3.y;
-                float mz = wf * pn.z + (1.f - wf) * nb3.z;
-                float rr = rsqrtf(mx * mx + my * my + mz * mz);
-                nb3 = make_float3(mx * rr, my * rr, mz * rr);
-            }
-            if (a.blend_height) a.blend_height[o] = hb;
-            if (a.blend_normal) { a.blend_normal[3 * o] = nb3.x; a.blend_normal[3 * o + 1] = nb3.y; a.blend_normal[3 * o + 2] = nb3.z; }
-        }
-    }
-    if (a.interior_sumsq) {
-        acc = warp_sum(acc);
-        long long c2 = cnt;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-        if ((threadIdx.x & 31) == 0) { red_s[threadIdx.x >> 5] = acc; redc_s[threadIdx.x >> 5] = c2; }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0; long long tc = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += red_s[w]; tc += redc_s[w]; }
-            if (tc) {
-                atomicAdd(&a.interior_sumsq[p], t);
-                if (a.interior_count) atomicAdd((unsigned long long*)&a.interior_count[p], (unsigned long long)tc);
-            }
-        }
     }
 }
 
@@ -394,12 +321,12 @@ using namespace hs;
 
 extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_smooth: null args");
-    HS_CHECK_ARG(a->layers && a->taps && a->raw_layers && a->smooth_layers && a->tile_prefix, "hs_smooth: missing buffer");
+    HS_CHECK_ARG(a->layers && a->taps && a->raw_layers && a->smooth_layers && a->tile_info, "hs_smooth: missing buffer");
     cudaStream_t st = as_stream(stream);
     if (a->total_tiles > 0) {
         HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= HS_SMOOTH_FUSED_MAX_H, "hs_smooth: max_H=%d out of range", a->max_H);
         const int W = SM_TILE + 2 * a->max_H, K = 2 * a->max_H + 1;
-        size_t sm = (size_t)(((K + 3) & ~3) + W * W + SM_TILE * W) * sizeof(float);
+        size_t sm = (size_t)(((K + 3) & ~3) + W * W + SM_TILE * (W | 1)) * sizeof(float);
         static size_t smooth_attr = 48 * 1024;
         if (sm > smooth_attr) {
             HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -424,17 +351,6 @@ extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
         smooth_wide_y_kernel<<<a->total_ytiles, 256, sm, st>>>(*a);
         HS_LAUNCH_CHECK();
     }
-    return 0;
-}
-
-extern "C" int hs_compose(const HsComposeArgs* a, void* stream) {
-    HS_CHECK_ARG(a != nullptr, "hs_compose: null args");
-    if (a->total_tiles == 0) return 0;
-    HS_CHECK_ARG(a->patches && a->layers && a->smooth_layers && a->tile_prefix, "hs_compose: missing buffer");
-    HS_CHECK_ARG(!a->blend_mode || a->bg_height == nullptr || (a->bg_n >= 2 && (a->bg_n & (a->bg_n - 1)) == 0),
-                 "hs_compose: background size must be a power of two");
-    compose_kernel<<<a->total_tiles, 256, 0, as_stream(stream)>>>(*a);
-    HS_LAUNCH_CHECK();
     return 0;
 }
 

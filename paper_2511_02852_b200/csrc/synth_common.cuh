@@ -1,0 +1,66 @@
+// Helpers shared by the synthesis / blend kernels.
+#pragma once
+#include "hs_common.cuh"
+
+namespace hs {
+
+__device__ __forceinline__ int find_seg_i(const int* off, int nseg, int v) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= v) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ float upsample_at(const float* __restrict__ S, const HsLayer& L, int i, int j) {
+    if (L.f == 1) return S[(long long)i * L.ncy + j];
+    const int ci = i / L.f, cj = j / L.f;
+    const float wi = (float)((double)(i - ci * L.f) / (double)L.f);
+    const float wj = (float)((double)(j - cj * L.f) / (double)L.f);
+    const int ci1 = min(ci + 1, L.ncx - 1), cj1 = min(cj + 1, L.ncy - 1);
+    const float* r0 = S + (long long)ci * L.ncy;
+    const float* r1 = S + (long long)ci1 * L.ncy;
+    float a0 = r0[cj] * (1.f - wi) + r1[cj] * wi;
+    float a1 = r0[cj1] * (1.f - wi) + r1[cj1] * wi;
+    return a0 * (1.f - wj) + a1 * wj;
+}
+
+struct BgView {
+    const float* h; const float* nrm; int n; double spacing; double x0, y0;
+};
+
+// periodic bilinear (fft_background.py:222-249)
+__device__ __forceinline__ void sample_bg(const BgView& bg, double x, double y, float& h, float3& nv) {
+    if (!bg.h) { h = 0.f; nv = make_float3(0.f, 0.f, 1.f); return; }
+    const double u = (x - bg.x0) / bg.spacing, v = (y - bg.y0) / bg.spacing;
+    const double fi = floor(u), fj = floor(v);
+    const float fu = (float)(u - fi), fv = (float)(v - fj);
+    const int m = bg.n - 1;
+    const int i0 = ((long long)fi) & m, j0 = ((long long)fj) & m;
+    const int i1 = (i0 + 1) & m, j1 = (j0 + 1) & m;
+    const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
+    const long long a00 = (long long)i0 * bg.n + j0, a10 = (long long)i1 * bg.n + j0;
+    const long long a01 = (long long)i0 * bg.n + j1, a11 = (long long)i1 * bg.n + j1;
+    h = bg.h[a00] * w00 + bg.h[a10] * w10 + bg.h[a01] * w01 + bg.h[a11] * w11;
+    if (bg.nrm) {
+        const float* N = bg.nrm;
+        float nx = N[3 * a00] * w00 + N[3 * a10] * w10 + N[3 * a01] * w01 + N[3 * a11] * w11;
+        float ny = N[3 * a00 + 1] * w00 + N[3 * a10 + 1] * w10 + N[3 * a01 + 1] * w01 + N[3 * a11 + 1] * w11;
+        float nz = N[3 * a00 + 2] * w00 + N[3 * a10 + 2] * w10 + N[3 * a01 + 2] * w01 + N[3 * a11 + 2] * w11;
+        float r = rsqrtf(nx * nx + ny * ny + nz * nz);
+        nv = make_float3(nx * r, ny * r, nz * r);
+    } else {
+        nv = make_float3(0.f, 0.f, 1.f);
+    }
+}
+
+// smoothstep weight from inward boundary depth (coupling.py:27-40)
+__device__ __forceinline__ double blend_w(const HsPatch& P, double x, double y) {
+    double d = fmin(fmin(x - P.x0, P.x1 - x), fmin(y - P.y0, P.y1 - y));
+    if (!(d > 0.0)) return 0.0;
+    double t = fmin(fmax(d / P.margin, 0.0), 1.0);
+    return t * t * (3.0 - 2.0 * t);
+}
+
+}  // namespace hs

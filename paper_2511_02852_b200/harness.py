@@ -211,8 +211,12 @@ class Simulation:
             self.patch_n = f32(3 * n_grid)
             self.blend_h = f32(n_grid)
             self.blend_n = f32(3 * n_grid)
-            self.isum = torch.zeros(self.n_patches, dtype=torch.float64, device=dev)
-            self.icount = torch.zeros(self.n_patches, dtype=torch.int64, device=dev)
+            # per-frame accumulators in one block of 4-byte words, zeroed by hs_inject
+            P = self.n_patches
+            self.stat_words = torch.zeros(5 * P + (P & 1), dtype=torch.int32, device=dev)
+            self.isum = self.stat_words[0:2 * P].view(torch.float64)
+            self.icount = self.stat_words[2 * P:4 * P].view(torch.int64)
+            self.clamped = self.stat_words[4 * P:5 * P]
             self.max_tiles = int(sum(-(-(pc + sc) // ADV_TILE) for pc, sc in zip(self.pool_caps, self.stage_caps)))
             self.tile_state = torch.zeros(self.max_tiles, dtype=torch.int64, device=dev)
             self.tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -249,21 +253,29 @@ class Simulation:
 
     # --------------------------------------------------------- the frame --
     def _enqueue_frame(self, parity: int, dt: float, mark=None) -> None:
-        """Enqueue one frame on the current stream (graph-capturable).
-        `mark(stage)` (optional) is called after each stage's launches, e.g.
-        to record CUDA events for per-stage timing."""
-        st = stream_ptr()
+        """Enqueue one frame (graph-capturable).  The background transform
+        only feeds the blend, so it runs on a side stream concurrently with
+        the particle chain inject -> advect -> smooth; the streams join before
+        hs_compose.  `mark(stage)` (optional) is called after each stage's
+        launches on the stream that ran it (CUDA events for stage timing)."""
         mark = mark or (lambda _name: None)
-        mark("start")
+        main = torch.cuda.current_stream(self.device)
+        fork = self.fft_state is not None and self.n_patches > 0
         if self.fft_state is not None:
-            self.fft_ws.sumsq.zero_()
-            N.call("hs_fft_evolve", fft_args(self.fft_state, self.fft_ws, frame_ptr=self.frame_dev, dt=dt), st)
-        mark("fft")
+            side = self._side_stream() if fork else main
+            if fork:
+                side.wait_stream(main)
+            with torch.cuda.stream(side):
+                mark("fft_start")
+                fa = fft_args(self.fft_state, self.fft_ws, frame_ptr=self.frame_dev, dt=dt)
+                if not self.n_patches:
+                    fa.frame_advance = N.ptr(self.frame_dev)
+                N.call("hs_fft_evolve", fa, stream_ptr())
+                mark("fft")
+        st = stream_ptr()
         if self.n_patches:
+            mark("particles_start")
             src, dst = parity, parity ^ 1
-            self.isum.zero_()
-            self.icount.zero_()
-            self.synth.clamped.zero_()
             N.call("hs_inject", N.HsInjectArgs(
                 n_patches=self.n_patches, nb=self.nb, n_theta=self.table.n_theta, buckets=N.ptr(self.buckets_dev),
                 patches=N.ptr(self.patches_dev), half_rate=N.ptr(self._hr(dt)),
@@ -271,7 +283,8 @@ class Simulation:
                 rho=float(self.config.rho), g=float(self.config.g), acc=N.ptr(self.acc), groups=N.ptr(self.groups),
                 e_in=N.ptr(self.e_in), rng=N.ptr(self.rng), stage=N.pool_struct(*self.stage),
                 stage_count=N.ptr(self.stage_count), scratch=N.ptr(self.scratch), member_capacity=self.member_cap,
-                status=N.ptr(self.status)), st)
+                status=N.ptr(self.status), zero_words=N.ptr(self.stat_words),
+                n_zero_words=self.stat_words.numel()), st)
             mark("inject")
             N.call("hs_advect", N.HsAdvectArgs(
                 n_patches=self.n_patches, nb=self.nb, buckets=N.ptr(self.buckets_dev), patches=N.ptr(self.patches_dev),
@@ -280,26 +293,36 @@ class Simulation:
                 out=self._pool(dst), out_count=N.ptr(self.counts[dst]), dropped=N.pool_struct(), dropped_count=0,
                 e_out=N.ptr(self.e_out), splat=1, raw_layers=N.ptr(self.synth.raw),
                 raw_layers_len=self.synth.pack.raw_len, layers=N.ptr(self.synth.layers),
-                clamped=N.ptr(self.synth.clamped), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
+                clamped=N.ptr(self.clamped), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
                 tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status)), st)
             mark("advect")
             N.call("hs_smooth", self.synth.smooth_args(), st)
             mark("smooth")
+            if fork:
+                main.wait_stream(self._side_stream())
+                mark("join")
             bg = self.fft_ws
             N.call("hs_compose", N.HsComposeArgs(
                 n_patches=self.n_patches, nb=self.nb, patches=N.ptr(self.patches_dev), layers=N.ptr(self.synth.layers),
-                smooth_layers=N.ptr(self.synth.smooth), tile_prefix=N.ptr(self.synth.compose_prefix),
-                total_tiles=int(self.synth.compose_prefix_np[-1]),
+                smooth_layers=N.ptr(self.synth.smooth), tile_info=N.ptr(self.synth.compose_info),
+                total_tiles=self.synth.compose_tiles,
                 bg_height=N.ptr(bg.height) if bg is not None else 0,
                 bg_normal=N.ptr(bg.normal) if bg is not None else 0,
                 bg_n=self.config.fft_n if bg is not None else 0,
                 bg_spacing=self.config.fft_domain / self.config.fft_n if bg is not None else 1.0,
-                patch_height=N.ptr(self.patch_h), patch_normal=N.ptr(self.patch_n),
+                patch_height=N.ptr(self.patch_h), patch_normal=0,
                 blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
-                interior_sumsq=N.ptr(self.isum), interior_count=N.ptr(self.icount)), st)
+                interior_sumsq=N.ptr(self.isum), interior_count=N.ptr(self.icount),
+                frame_advance=N.ptr(self.frame_dev)), st)
             mark("compose")
-        N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(st))
-        mark("end")
+            self._patch_n_frame = -1          # patch normals are derived lazily (patch_field)
+        if self.fft_state is None and not self.n_patches:
+            N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(st))
+
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
 
     def _graph(self, parity: int):
         g = self._graphs.get(parity)
@@ -319,32 +342,53 @@ class Simulation:
         """Library kernels one frame launches (csrc/*.cu): fft rows + cols
         (+ periodic normals), inject, advect, smooth (1 or 3), compose,
         advance_frame."""
-        k = 1
+        k = 0
         if self.fft_state is not None:
             k += 2 + (1 if self.fft_ws.normal is not None else 0)
         if self.n_patches:
             pk = self.synth.pack
-            k += 3 + (1 if pk.smooth_tile_prefix[-1] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
-        return k
+            k += 3 + (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
+        return max(k, 1)
 
-    def timed_frame(self, dt: float | None = None) -> dict:
-        """Run one eager frame with CUDA events after every stage; returns
-        {stage: ms} (synchronises).  Used by bench.py for the per-kernel
-        roofline; not part of the normal step path."""
-        use_dt = self.config.dt if dt is None else float(dt)
-        evs = []
+    def timed_frame(self) -> dict:
+        """Replay one frame from a CUDA graph that carries timing-event record
+        nodes after every stage; returns {stage: ms} (synchronises).  Each
+        stage is timed against the previous event on its own stream, so the
+        concurrently running background transform and particle chain are
+        both per-kernel device times without host launch gaps.  Used by
+        bench.py for the per-kernel roofline."""
+        key = ("timed", self._parity)
+        if key not in self._graphs:
+            if self.n_patches:
+                self._hr(self.config.dt)
+            evs = []
 
-        def mark(name):
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            evs.append((name, e))
-        self._enqueue_frame(self._parity, use_dt, mark)
+            def mark(name):
+                e = torch.cuda.Event(enable_timing=True, external=True)
+                strm = torch.cuda.current_stream(self.device)
+                e.record(strm)
+                evs.append((name, e, strm.cuda_stream))
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.graph(g, stream=s):
+                self._enqueue_frame(self._parity, self.config.dt, mark)
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            self._graphs[key] = (g, evs)
+        g, evs = self._graphs[key]
+        g.replay()
         self._parity ^= 1
         self.frame += 1
-        evs[-1][1].synchronize()
-        out = {}
-        for (_, a), (name, b) in zip(evs[:-1], evs[1:]):
-            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        torch.cuda.synchronize(self.device)
+        out, last = {}, {}
+        for name, e, sid in evs:
+            if sid in last and not name.endswith("_start") and name != "join":
+                out[name] = out.get(name, 0.0) + last[sid].elapsed_time(e)
+            last[sid] = e
+        if "fft_start" in [n for n, _, _ in evs] and "compose" in out:
+            first = next(e for n, e, _ in evs if n in ("fft_start", "particles_start"))
+            end = next(e for n, e, _ in evs if n == "compose")
+            out["frame"] = first.elapsed_time(end)
         return out
 
     def step(self, dt: float | None = None, *, stats: bool = True):
@@ -417,8 +461,17 @@ class Simulation:
         return self._grid(self.patch_h, k)
 
     def patch_field(self, k: int) -> HeightField:
+        """Patch k's finished field (finish_field): heights from the last
+        frame, clamped-border normals derived on demand (hs_finish)."""
         res, ny = self.synth.grids[k]
         r = self.regions[k]
+        if getattr(self, "_patch_n_frame", -1) != self.frame:
+            for q, (rq, nyq) in enumerate(self.synth.grids):
+                N.call("hs_finish", N.HsFinishArgs(nx=rq, ny=nyq, spacing=self.regions[q].l1 / (rq - 1),
+                                                   chop_scale=0.0, height=N.ptr(self._grid(self.patch_h, q)),
+                                                   normal=N.ptr(self._grid(self.patch_n, q, 3)), disp=0),
+                       stream_ptr())
+            self._patch_n_frame = self.frame
         return HeightField(resolution=res, origin=r.min_corner.copy(), spacing=r.l1 / (res - 1),
                            height=self._grid(self.patch_h, k), normal=self._grid(self.patch_n, k, 3),
                            displacement=torch.zeros((res, ny, 2), dtype=torch.float32, device=self.device),

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._layout import (compose_tile_prefix, grid_dims, pack_layers, patch_struct, stream_ptr,
+from ._layout import (compose_tile_info, grid_dims, pack_layers, patch_struct, stream_ptr,
                       structs_to_device)
 from .errors import ConfigError
 from .fft_background import HeightField
@@ -123,12 +123,13 @@ class SynthWorkspace:
         self.taps = torch.from_numpy(self.pack.taps).to(device)
         self.raw = torch.zeros(max(1, self.pack.raw_len), dtype=torch.float32, device=device)
         self.smooth = torch.zeros(max(1, self.pack.smooth_len), dtype=torch.float32, device=device)
-        self.smooth_prefix = torch.from_numpy(self.pack.smooth_tile_prefix).to(device)
+        self.smooth_info = torch.from_numpy(np.ascontiguousarray(self.pack.smooth_tile_info)).to(device)
         self.xtile_prefix = torch.from_numpy(self.pack.xtile_prefix).to(device)
         self.ytile_prefix = torch.from_numpy(self.pack.ytile_prefix).to(device)
         self.mid = torch.zeros(self.pack.mid_len, dtype=torch.float32, device=device) if self.pack.mid_len else None
-        self.compose_prefix_np = compose_tile_prefix(self.grids)
-        self.compose_prefix = torch.from_numpy(self.compose_prefix_np).to(device)
+        self.compose_info_np = compose_tile_info(self.grids)
+        self.compose_info = torch.from_numpy(self.compose_info_np).to(device)
+        self.compose_tiles = int(self.compose_info_np.shape[0])
         self.grid_base = np.concatenate([[0], np.cumsum([r * ny for r, ny in self.grids])]).astype(np.int64)
         self.clamped = torch.zeros(len(regions), dtype=torch.int32, device=device)
 
@@ -139,8 +140,8 @@ class SynthWorkspace:
     def smooth_args(self) -> N.HsSmoothArgs:
         return N.HsSmoothArgs(n_layers=len(self.pack.layers), layers=N.ptr(self.layers), taps=N.ptr(self.taps),
                               raw_layers=N.ptr(self.raw), smooth_layers=N.ptr(self.smooth),
-                              tile_prefix=N.ptr(self.smooth_prefix),
-                              total_tiles=int(self.pack.smooth_tile_prefix[-1]), max_H=self.pack.max_H,
+                              tile_info=N.ptr(self.smooth_info),
+                              total_tiles=int(self.pack.smooth_tile_info.shape[0]), max_H=self.pack.max_H,
                               mid=N.ptr(self.mid), xtile_prefix=N.ptr(self.xtile_prefix),
                               total_xtiles=int(self.pack.xtile_prefix[-1]), ytile_prefix=N.ptr(self.ytile_prefix),
                               total_ytiles=int(self.pack.ytile_prefix[-1]), max_H_wide=self.pack.max_H_wide)
@@ -170,7 +171,7 @@ def synthesize(particles: ParticleSet, patch: PatchRegion, resolution: int, plan
     N.call("hs_smooth", ws.smooth_args(), st)
     N.call("hs_compose", N.HsComposeArgs(
         n_patches=1, nb=nb, patches=N.ptr(pst), layers=N.ptr(ws.layers), smooth_layers=N.ptr(ws.smooth),
-        tile_prefix=N.ptr(ws.compose_prefix), total_tiles=int(ws.compose_prefix_np[-1]), bg_height=0,
+        tile_info=N.ptr(ws.compose_info), total_tiles=ws.compose_tiles, bg_height=0,
         bg_normal=0, bg_n=0, bg_spacing=1.0, patch_height=N.ptr(heights), patch_normal=0, blend_height=0,
         blend_normal=0, blend_mode=0, interior_sumsq=0, interior_count=0), st)
     return heights, int(ws.clamped.item())
