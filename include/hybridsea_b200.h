@@ -122,7 +122,7 @@ typedef struct {
     double spacing;           /* domain / n */
     const double* kf;         /* [n] 2*pi*fftfreq(n, d=domain/n) */
     const float* h0;          /* [n*n] complex64 (re,im) */
-    const float* twiddle;     /* [n/2] complex64 exp(+2 pi i k/n) */
+    const float* twiddle;     /* [n] complex64 exp(+2 pi i k/n), fp64-accurate */
     float* work_a;            /* [n*n] complex64 scratch */
     float* work_b;            /* [(n/2+1)*n] complex64 scratch */
     float* height;            /* [n*n] */

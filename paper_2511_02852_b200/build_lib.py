@@ -17,12 +17,12 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libhybridsea_b200.so")
 SOURCES = ["capi.cu", "fft.cu", "particles.cu", "synth.cu", "compose.cu"]
-# -fmad=false keeps every fp64 mul/add a separate IEEE op (bit-exact with
-# numpy on the integer-relevant paths); fp32 code uses explicit fmaf where
-# contraction is wanted.
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-fmad=false",
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-cudart", "static"]
+# particle arithmetic must round like numpy (separate IEEE mul / add); the
+# kernels spell it out with __dmul_rn/__dadd_rn and this flag backs that up
+PER_FILE_FLAGS = {"particles.cu": ["-fmad=false"]}
 
 
 def nvcc() -> str:
@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-dc" if False else "-c",
+        cmd = [nvcc(), *NVCC_FLAGS, *PER_FILE_FLAGS.get(src, []), "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-dc" if False else "-c",
                os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -22,7 +22,7 @@
 //     fp64-accurate fp32 twiddle table;
 //   * the phase omega*t is formed and reduced mod 2 pi in fp64 before the
 //     fp32 sincos.
-#include "hs_common.cuh"
+#include "fft_reg.cuh"
 
 namespace hs {
 
@@ -245,6 +245,174 @@ __global__ void normals_periodic_kernel(const float* __restrict__ h, float* __re
     o[2] = r;
 }
 
+// ------------------------------------------------ register-FFT kernels --
+// n >= 64: each transform is N/16 threads x 16 register elements per pass
+// (fft_reg.cuh).  Same data flow as the radix-2/4 kernels above.
+__device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0, const float2* r1, int i, int ip,
+                                              int j, double t, float2& A0, float2& A1, float2& B0) {
+    const int n = d.n, half = n >> 1;
+    const int jm = (n - j) & (n - 1);
+    const double kxi = d.kf[i], kxip = d.kf[ip], kyj = d.kf[j];
+    const double km = hypot(kxi, kyj);
+    const double w = sqrt(d.g * km);
+    const double two_pi = 6.283185307179586476925286766559;
+    double ph = w * t;
+    ph -= two_pi * rint(ph * (1.0 / two_pi));       // reduce in fp64 before the fp32 sincos (App. B.2)
+    float s, c;
+    sincosf((float)ph, &s, &c);
+    const float2 rot = make_float2(c, -s), rotc = make_float2(c, s);
+    const float2 hh0 = cadd(cmul(r0[j], rot), cmul(cconj(r1[jm]), rotc));
+    const float2 hh1 = cadd(cmul(r1[j], rot), cmul(cconj(r0[jm]), rotc));
+    const bool sc = ((i == 0) || (i == half)) && (j == 0 || j == half);   // self-conjugate bin
+    const double kinv = km > 0.0 ? 1.0 / km : 1.0;
+    if (d.chop_on) {
+        const float fa = sc ? 1.f : (float)(1.0 + d.chop * kxi * kinv);
+        A0 = make_float2(hh0.x * fa, hh0.y * fa);
+        const float fb = sc ? 0.f : (float)(d.chop * kyj * kinv);
+        B0 = make_float2(fb * hh0.y, -fb * hh0.x);
+        const float fa1 = (float)(1.0 + d.chop * kxip * kinv);
+        A1 = make_float2(hh1.x * fa1, hh1.y * fa1);
+    } else {
+        A0 = hh0;
+        A1 = hh1;
+        B0 = make_float2(0.f, 0.f);
+    }
+}
+
+template <int N>
+__global__ void fft_rows_reg_kernel(FftDev d) {
+    constexpr int T = N / 16, NP = N + N / 32;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;            // N
+    float2* r0 = tw + N;        // h0 row i
+    float2* r1 = r0 + N;        // h0 row i'
+    float2* buf = r1 + N;       // 3 transforms of NP: A(i), A(i'), B(i)
+    const int i = blockIdx.x, ip = (N - i) & (N - 1);
+    const bool self = (i == ip);
+    if (d.sumsq_zero && i == 0 && threadIdx.x == 0) *d.sumsq_zero = 0.0;
+    for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
+        cp_async16(tw + 2 * k, d.tw + 2 * k);
+        cp_async16(r0 + 2 * k, d.h0 + (size_t)i * N + 2 * k);
+        cp_async16(r1 + 2 * k, d.h0 + (size_t)ip * N + 2 * k);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame * dt
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        float2 A0, A1, B0;
+        spectrum_pair(d, r0, r1, i, ip, j, t, A0, A1, B0);
+        buf[fpad(j)] = A0;
+        buf[NP + fpad(j)] = A1;
+        buf[2 * NP + fpad(j)] = B0;
+    }
+    __syncthreads();
+    const int f = threadIdx.x / T, tt = threadIdx.x - f * T;
+    const bool active = (f == 0) || (f == 1 && !self) || (f == 2 && d.chop_on);
+    fft_inplace<N>(buf + (f < 3 ? f : 0) * NP, tw, tt, active && f < 3);
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        const int pos = fpad(out_pos<N>(k));
+        d.wa[(size_t)i * N + k] = buf[pos];
+        if (!self) d.wa[(size_t)ip * N + k] = buf[NP + pos];
+        if (d.chop_on) d.wb[(size_t)i * N + k] = buf[2 * NP + pos];
+    }
+}
+
+// columns: CT transforms per CTA; blocks < n_a_tiles do A (height + i dx),
+// the rest do B (two real dy columns per transform)
+template <int N, int CT>
+__global__ void fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
+    constexpr int T = N / 16, NP = N + N / 32;
+    extern __shared__ float2 sm[];
+    __shared__ double red[32];
+    float2* tw = sm;
+    float2* buf = tw + N;       // CT transforms of NP
+    if (o.frame_advance && blockIdx.x == 0 && threadIdx.x == 0) *o.frame_advance += 1;
+    for (int k = threadIdx.x; k < N / 2; k += blockDim.x) cp_async16(tw + 2 * k, d.tw + 2 * k);
+    const bool is_a = (int)blockIdx.x < n_a_tiles;
+    double acc = 0.0;
+    if (is_a) {
+        const int j0 = blockIdx.x * CT;
+        for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
+            const int i = e / CT, c = e - i * CT;
+            cp_async8(buf + c * NP + fpad(i), d.wa + (size_t)i * N + j0 + c, true);
+        }
+    } else if (d.chop_on) {
+        const int j0 = (blockIdx.x - n_a_tiles) * (2 * CT);
+        const int half = N >> 1;
+        for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
+            const int i = e / CT, q = e - i * CT;
+            const int src = i <= half ? i : N - i;
+            float2 y1 = d.wb[(size_t)src * N + j0 + 2 * q];
+            float2 y2 = d.wb[(size_t)src * N + j0 + 2 * q + 1];
+            if (i == 0 || i == half) { y1.y = 0.f; y2.y = 0.f; }      // rows 0, n/2 are real
+            else if (i > half) { y1.y = -y1.y; y2.y = -y2.y; }        // Y[-i] = conj(Y[i])
+            buf[q * NP + fpad(i)] = make_float2(y1.x - y2.y, y1.y + y2.x);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (!is_a && !d.chop_on) {
+        const int j0 = (blockIdx.x - n_a_tiles) * (2 * CT);
+        for (int e = threadIdx.x; e < N * 2 * CT; e += blockDim.x) {
+            const int i = e / (2 * CT), c = e - i * (2 * CT);
+            o.dy[(size_t)i * N + j0 + c] = 0.f;
+        }
+        return;
+    }
+    const int f = threadIdx.x / T, tt = threadIdx.x - f * T;
+    fft_inplace<N>(buf + (f < CT ? f : 0) * NP, tw, tt, f < CT);
+    if (is_a) {
+        const int j0 = blockIdx.x * CT;
+        for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
+            const int i = e / CT, c = e - i * CT;
+            const float2 v = buf[c * NP + fpad(out_pos<N>(i))];
+            const size_t oi = (size_t)i * N + j0 + c;
+            o.h[oi] = v.x;
+            o.dx[oi] = d.chop_on ? v.y : 0.f;
+            acc += (double)v.x * (double)v.x;
+        }
+    } else {
+        const int j0 = (blockIdx.x - n_a_tiles) * (2 * CT);
+        for (int e = threadIdx.x; e < N * 2 * CT; e += blockDim.x) {
+            const int i = e / (2 * CT), c = e - i * (2 * CT);
+            const float2 v = buf[(c >> 1) * NP + fpad(out_pos<N>(i))];
+            o.dy[(size_t)i * N + j0 + c] = (c & 1) ? v.y : v.x;
+        }
+    }
+    if (o.sumsq) {
+        acc = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tsum = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tsum += red[w];
+            if (tsum != 0.0) atomicAdd(o.sumsq, tsum);
+        }
+    }
+}
+
+template <int N>
+int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
+    constexpr int T = N / 16, NP = N + N / 32;
+    constexpr int CT = (512 / T) < N / 2 ? (512 / T) : N / 2;   // transforms per column CTA (B needs 2 CT <= N)
+    const int rows_threads = 3 * T < 32 ? 32 : 3 * T;
+    const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2);
+    const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+        HS_CUDA(cudaFuncSetAttribute(fft_rows_reg_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows));
+        HS_CUDA(cudaFuncSetAttribute(fft_cols_reg_kernel<N, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cols));
+        attr = true;
+    }
+    fft_rows_reg_kernel<N><<<N / 2 + 1, rows_threads, sm_rows, st>>>(d);
+    HS_LAUNCH_CHECK();
+    const int n_a = N / CT, n_b = N / (2 * CT);
+    const int cols_threads = CT * T < 32 ? 32 : CT * T;
+    fft_cols_reg_kernel<N, CT><<<n_a + n_b, cols_threads, sm_cols, st>>>(d, o, n_a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
 }  // namespace hs
 
 using namespace hs;
@@ -270,6 +438,28 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     d.tw = reinterpret_cast<const float2*>(a->twiddle);
     d.wa = reinterpret_cast<float2*>(a->work_a);
     d.wb = reinterpret_cast<float2*>(a->work_b);
+
+    ColOut oreg{a->height, a->dx, a->dy, a->sumsq, a->frame_advance};
+    int rc_reg = -1;
+    switch (n) {
+        case 64: rc_reg = launch_fft_reg<64>(d, oreg, st); break;
+        case 128: rc_reg = launch_fft_reg<128>(d, oreg, st); break;
+        case 256: rc_reg = launch_fft_reg<256>(d, oreg, st); break;
+        case 512: rc_reg = launch_fft_reg<512>(d, oreg, st); break;
+        case 1024: rc_reg = launch_fft_reg<1024>(d, oreg, st); break;
+        case 2048: rc_reg = launch_fft_reg<2048>(d, oreg, st); break;
+        case 4096: rc_reg = launch_fft_reg<4096>(d, oreg, st); break;
+        default: break;
+    }
+    if (rc_reg > 0) return rc_reg;
+    if (rc_reg == 0) {
+        if (a->emit_normals) {
+            dim3 grid((n + 127) / 128, n);
+            normals_periodic_kernel<<<grid, 128, 0, st>>>(a->height, a->normal, n, (float)(1.0 / (2.0 * a->spacing)));
+            HS_LAUNCH_CHECK();
+        }
+        return 0;
+    }
 
     size_t sm_rows = (size_t)(n / 2 + 5 * n) * sizeof(float2);
     static size_t rows_attr = 48 * 1024;   // attribute calls stay out of graph capture after the first frame

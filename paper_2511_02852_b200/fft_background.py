@@ -74,7 +74,7 @@ def _upload(state: FftState, device) -> FftState:
     dev = _device(device)
     n = state.n
     h0 = np.stack([state.h0.real, state.h0.imag], axis=-1).astype(np.float32)
-    k = np.arange(n // 2)
+    k = np.arange(n)
     tw = np.stack([np.cos(2.0 * math.pi * k / n), np.sin(2.0 * math.pi * k / n)], -1).astype(np.float32)
     object.__setattr__(state, "device", dev)
     object.__setattr__(state, "h0_dev", torch.from_numpy(np.ascontiguousarray(h0)).to(dev))
