@@ -179,10 +179,12 @@ typedef struct {
     long long raw_layers_len;              /* floats */
     const HsLayer* layers;                 /* [n_patches*nb] */
     int* clamped;                          /* [n_patches] += clamp counts */
-    unsigned long long* tile_state;        /* [max_tiles] */
-    int max_tiles;
+    unsigned long long* tile_state;        /* [max_tiles] look-back state / per-tile counts */
+    int max_tiles;                         /* >= sum over patches of ceil((pool+stage capacity)/1024) */
     int* tile_counter;                     /* scalar */
     int* status;
+    unsigned* keep_words;                  /* optional [max_tiles*32]: selects the count + scatter
+                                              two-kernel compaction (no serial look-back chain) */
 } HsAdvectArgs;
 HS_API int hs_advect(const HsAdvectArgs* a, void* stream);
 
@@ -235,7 +237,7 @@ typedef struct {
     const HsPatch* patches;
     const HsLayer* layers;
     const float* smooth_layers;
-    const int* tile_info;       /* [total_tiles*3] 32x32 output tiles: patch, i0, j0 */
+    const int* tile_info;       /* [total_tiles*3] 30x30 output tiles: patch, i0, j0 */
     int total_tiles;
     /* background (may be NULL: flat water) */
     const float* bg_height; const float* bg_normal; int bg_n; double bg_spacing;
@@ -296,6 +298,11 @@ HS_API int hs_finish(const HsFinishArgs* a, void* stream);
 
 /* Reductions used by FrameStats (harness.py:171-206). */
 HS_API int hs_sumsq(const float* x, long long n, double* out, void* stream);
+
+/* Periodic central-difference normals of an n x n height grid (the
+ * grid_normals(periodic=True) part of evolve_and_synthesize,
+ * fft_background.py:162-178), for lazily materialised background normals. */
+HS_API int hs_periodic_normals(const float* height, float* normal, int n, double spacing, void* stream);
 
 /* frame += 1 on the device (end of a captured frame). */
 HS_API int hs_advance_frame(long long* frame, void* stream);

@@ -15,7 +15,8 @@ import torch
 from . import _native as N
 from .errors import ConfigError
 
-TILE = 32          # smooth / compose tile edge (csrc/synth.cu)
+TILE = 32          # smooth tile edge (csrc/synth.cu)
+COMPOSE_TILE = 30  # compose output tile edge (csrc/compose.cu: 32 x 32 haloed heights)
 
 
 def stream_ptr() -> int:
@@ -122,9 +123,10 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
 
 
 def compose_tile_info(grids: list[tuple[int, int]]) -> np.ndarray:
-    """[tiles, 3] int32: patch, i0, j0 of every 32x32 output tile."""
-    info = [(p, tx * TILE, ty * TILE) for p, (res, ny) in enumerate(grids)
-            for tx in range(-(-res // TILE)) for ty in range(-(-ny // TILE))]
+    """[tiles, 3] int32: patch, i0, j0 of every compose output tile."""
+    T = COMPOSE_TILE
+    info = [(p, tx * T, ty * T) for p, (res, ny) in enumerate(grids)
+            for tx in range(-(-res // T)) for ty in range(-(-ny // T))]
     return np.array(info, dtype=np.int32).reshape(-1, 3)
 
 

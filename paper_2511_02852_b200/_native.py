@@ -70,7 +70,7 @@ class HsAdvectArgs(C.Structure):
                 ("stage_count", vp), ("out", HsPool), ("out_count", vp), ("dropped", HsPool),
                 ("dropped_count", vp), ("e_out", vp), ("splat", i32), ("raw_layers", vp),
                 ("raw_layers_len", i64), ("layers", vp), ("clamped", vp), ("tile_state", vp),
-                ("max_tiles", i32), ("tile_counter", vp), ("status", vp)]
+                ("max_tiles", i32), ("tile_counter", vp), ("status", vp), ("keep_words", vp)]
 
 
 class HsSplatArgs(C.Structure):
@@ -121,7 +121,7 @@ EXPECTED_SIZES = {HsBucket: 64, HsPatch: 112, HsLayer: 56, HsPool: 40}
 # every symbol include/hybridsea_b200.h declares
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
-           "hs_advance_frame"]
+           "hs_advance_frame", "hs_periodic_normals"]
 
 _lib = None
 
@@ -154,6 +154,7 @@ def lib() -> C.CDLL:
             raise RuntimeError(f"{st.__name__}: ctypes {C.sizeof(st)} bytes != C {L.hs_struct_size(k)}")
     L.hs_sumsq.argtypes = [vp, i64, vp, vp]
     L.hs_advance_frame.argtypes = [vp, vp]
+    L.hs_periodic_normals.argtypes = [vp, vp, i32, dbl, vp]
     if L.hs_abi_version() != 1:
         raise RuntimeError("hybridsea_b200 ABI version mismatch")
     _lib = L

@@ -417,6 +417,15 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
 
 using namespace hs;
 
+extern "C" int hs_periodic_normals(const float* height, float* normal, int n, double spacing, void* stream) {
+    HS_CHECK_ARG(height && normal, "hs_periodic_normals: null buffer");
+    HS_CHECK_ARG(n >= 2 && (n & (n - 1)) == 0, "hs_periodic_normals: n=%d must be a power of two", n);
+    dim3 grid((n + 127) / 128, n);
+    normals_periodic_kernel<<<grid, 128, 0, as_stream(stream)>>>(height, normal, n, (float)(1.0 / (2.0 * spacing)));
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
 extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_fft_evolve: null args");
     const int n = a->n;

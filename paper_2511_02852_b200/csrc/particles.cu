@@ -13,6 +13,8 @@
 // (exactly the reference pool order restricted to bucket b after
 // pool.extend(inject(...))) and compacts it with a single-pass
 // decoupled-look-back scan, so buckets stay contiguous and in order.
+#include <stdlib.h>
+
 #include "hs_common.cuh"
 
 namespace hs {
@@ -179,8 +181,8 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
 
 // ============================================================== advect ==
 constexpr int ADV_THREADS = 256;
-constexpr int ADV_ITEMS = 4;
-constexpr int ADV_TILE = ADV_THREADS * ADV_ITEMS;
+constexpr int ADV_ITEMS = 4;                        // items per thread per chunk
+constexpr int ADV_CHUNK = ADV_THREADS * ADV_ITEMS;  // 1024
 constexpr unsigned long long FLAG_AGG = 1ULL << 32;
 constexpr unsigned long long FLAG_PRE = 2ULL << 32;
 
@@ -227,11 +229,36 @@ __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer
 }
 
 // Persistent CTAs take tiles of ADV_TILE virtual items in order from a global
-// counter; tiles never straddle patches.  Per item: advect in fp64 with the
-// reference's operation order, keep test, tile-local rank by ballots, tile
-// prefix by a warp-parallel decoupled look-back, stable scatter of survivors
-// (and optionally of the dropped), fused splat of survivors.
+// counter; tiles never straddle patches.  Two phases per tile:
+//   1. stream the tile's items from HBM: advect in fp64 with the reference's
+//      operation order, keep test, one ballot word per (chunk, item, warp);
+//      publish the tile's survivor count and resolve its prefix with a
+//      warp-parallel decoupled look-back (32 predecessors per round);
+//   2. re-read the items (L2-resident now), recompute the same positions and
+//      scatter survivors stably (ballot ranks) + the fused layer splat; the
+//      dropped are optionally scattered the same way.
+// Large tiles keep the look-back chain short (~210 tiles at C3).
+__device__ __forceinline__ void adv_item(const HsAdvectArgs& a, const HsPatch& P, const int* in_off,
+                                         const int* st_off, const int* voff, const int* in_cnt, const double* step_s,
+                                         int v, int b, double& x, double& y, double& ux, double& uy,
+                                         const float** amp_ptr) {
+    const int local = v - voff[b];
+    const bool from_pool = local < in_cnt[b];
+    const long long src = from_pool ? P.pool_base + in_off[b] + local
+                                    : P.stage_base + st_off[b] + (local - in_cnt[b]);
+    const HsPool& S = from_pool ? a.in : a.stage;
+    const double step = step_s[b];
+    ux = S.ux[src];
+    uy = S.uy[src];
+    x = dadd(S.x[src], dmul(ux, step));        // pos += dir * (c dt)  (particles.py:312-313)
+    y = dadd(S.y[src], dmul(uy, step));
+    *amp_ptr = S.amp + src;
+}
+
+template <int ADV_CHUNKS>
 __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) {
+    constexpr int ADV_TILE = ADV_CHUNK * ADV_CHUNKS;                        // items per look-back tile
+    constexpr int ADV_WORDS = ADV_CHUNKS * ADV_ITEMS * (ADV_THREADS / 32);  // ballot words per tile
     const int nb = a.nb;
     __shared__ int tile_prefix[HS_MAX_PATCHES + 1];
     __shared__ int in_off[HS_MAX_BUCKETS + 1];
@@ -243,7 +270,9 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
     __shared__ int keep_hist[HS_MAX_BUCKETS];
     __shared__ int drop_hist[HS_MAX_BUCKETS];
     __shared__ double eout_s[HS_MAX_BUCKETS];
-    __shared__ int warp_tot[ADV_ITEMS][ADV_THREADS / 32];
+    __shared__ unsigned keepw[ADV_WORDS];
+    __shared__ int wpre[ADV_WORDS];
+    __shared__ unsigned char bk_s[ADV_TILE];
     __shared__ int tile_s, prefix_s, clamp_s, cur_p_s, seg_b_s, seg_end_s;
     __shared__ HsPatch P_s;
 
@@ -277,7 +306,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
             if (lane < nb) {
                 in_off[lane] = si - ci; st_off[lane] = ss - cs; voff[lane] = si - ci + ss - cs; in_cnt_s[lane] = ci;
                 const HsBucket B = a.buckets[lane];
-                step_s[lane] = dmul(B.speed, a.dt);                   // speeds * dt (particles.py:312-313)
+                step_s[lane] = dmul(B.speed, a.dt);                   // speeds * dt
                 r2_s[lane] = dmul(B.radius, B.radius);
                 if (a.splat) {
                     const HsLayer L = a.layers[P.layer_base + lane];
@@ -305,46 +334,51 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
         __syncthreads();
         const HsPatch P = P_s;
         const int seg_b = seg_b_s, seg_end = seg_end_s;
-        double nx[ADV_ITEMS], ny_[ADV_ITEMS], dxv[ADV_ITEMS], dyv[ADV_ITEMS];
-        float am[ADV_ITEMS];
-        int bk[ADV_ITEMS];
-        int keep[ADV_ITEMS];
+
+        // ---- phase 1: keep flags (HBM stream) ----
 #pragma unroll
-        for (int it = 0; it < ADV_ITEMS; ++it) {
-            const int v = tbase + it * ADV_THREADS + threadIdx.x;
-            keep[it] = 0;
-            bk[it] = 0;
-            if (v < N) {
-                const int b = v < seg_end ? seg_b : find_seg(voff, nb + 1, v);
-                const int local = v - voff[b];
-                const bool from_pool = local < in_cnt_s[b];
-                const long long src = from_pool ? P.pool_base + in_off[b] + local
-                                                : P.stage_base + st_off[b] + (local - in_cnt_s[b]);
-                const HsPool& S = from_pool ? a.in : a.stage;
-                const double step = step_s[b];
-                const double ux = S.ux[src], uy = S.uy[src];
-                const double x = dadd(S.x[src], dmul(ux, step));        // pos += dir * (c dt)
-                const double y = dadd(S.y[src], dmul(uy, step));
-                const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
-                const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
-                keep[it] = dadd(dmul(ox, ox), dmul(oy, oy)) <= r2_s[b];  // support disk (:315-320)
-                nx[it] = x; ny_[it] = y; dxv[it] = ux; dyv[it] = uy; am[it] = S.amp[src]; bk[it] = b;
+        for (int c = 0; c < ADV_CHUNKS; ++c) {
+            int keep[ADV_ITEMS];
+#pragma unroll
+            for (int it = 0; it < ADV_ITEMS; ++it) {
+                const int li = c * ADV_CHUNK + it * ADV_THREADS + threadIdx.x;
+                const int v = tbase + li;
+                keep[it] = 0;
+                if (v < N) {
+                    const int b = v < seg_end ? seg_b : find_seg(voff, nb + 1, v);
+                    bk_s[li] = (unsigned char)b;
+                    double x, y, ux, uy;
+                    const float* ap;
+                    adv_item(a, P, in_off, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
+                    const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
+                    const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
+                    keep[it] = dadd(dmul(ox, ox), dmul(oy, oy)) <= r2_s[b];   // support disk (:315-320)
+                }
             }
-        }
-        // tile-local ranks: per (row, warp) ballots
 #pragma unroll
-        for (int it = 0; it < ADV_ITEMS; ++it) {
-            const unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
-            if (lane == 0) warp_tot[it][wid] = __popc(bal);
+            for (int it = 0; it < ADV_ITEMS; ++it) {
+                const unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
+                if (lane == 0) keepw[(c * ADV_ITEMS + it) * (ADV_THREADS / 32) + wid] = bal;
+            }
         }
         __syncthreads();
         if (wid == 0) {
-            // exclusive scan of the ADV_ITEMS x 8 warp totals (row-major), one lane per entry
-            constexpr int NW = ADV_THREADS / 32;
-            const int cnt = lane < ADV_ITEMS * NW ? warp_tot[lane / NW][lane % NW] : 0;
-            const int inc = warp_incl_scan(cnt, lane);
-            const int agg = __shfl_sync(0xffffffffu, inc, ADV_ITEMS * NW - 1);
-            if (lane < ADV_ITEMS * NW) warp_tot[lane / NW][lane % NW] = inc - cnt;
+            // exclusive scan of the tile's ballot-word popcounts (item order)
+            constexpr int PER = (ADV_WORDS + 31) / 32;
+            int cnt[PER], loc = 0;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                cnt[q] = lane * PER + q < ADV_WORDS ? __popc(keepw[lane * PER + q]) : 0;
+                loc += cnt[q];
+            }
+            const int inc = warp_incl_scan(loc, lane);
+            const int agg = __shfl_sync(0xffffffffu, inc, 31);
+            int run = inc - loc;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                if (lane * PER + q < ADV_WORDS) wpre[lane * PER + q] = run;
+                run += cnt[q];
+            }
             // decoupled look-back over this patch's earlier tiles, 32 at a time
             unsigned long long* ts = a.tile_state;
             const int first = tile - ltile;
@@ -375,36 +409,46 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
         }
         __syncthreads();
         const int tprefix = prefix_s;
+
+        // ---- phase 2: stable scatter + splat (L2 re-read) ----
         int clamp_local = 0;
         float* raw = a.raw_layers;
 #pragma unroll
-        for (int it = 0; it < ADV_ITEMS; ++it) {
-            const int v = tbase + it * ADV_THREADS + threadIdx.x;
-            const unsigned bal = __ballot_sync(0xffffffffu, keep[it]);
-            if (v < N) {
-                const int b = bk[it];
-                const int rank = tprefix + warp_tot[it][wid] + __popc(bal & ((1u << lane) - 1u));
-                if (keep[it]) {
+        for (int c = 0; c < ADV_CHUNKS; ++c) {
+#pragma unroll
+            for (int it = 0; it < ADV_ITEMS; ++it) {
+                const int li = c * ADV_CHUNK + it * ADV_THREADS + threadIdx.x;
+                const int v = tbase + li;
+                if (v >= N) continue;
+                const int w = (c * ADV_ITEMS + it) * (ADV_THREADS / 32) + wid;
+                const unsigned bal = keepw[w];
+                const bool kept = (bal >> lane) & 1u;
+                const int rank = tprefix + wpre[w] + __popc(bal & ((1u << lane) - 1u));
+                const int b = bk_s[li];
+                double x, y, ux, uy;
+                const float* ap;
+                adv_item(a, P, in_off, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
+                const float am = *ap;
+                if (kept) {
                     if (rank < P.pool_capacity) {
                         const long long o = P.pool_base + rank;
-                        a.out.x[o] = nx[it]; a.out.y[o] = ny_[it];
-                        a.out.ux[o] = dxv[it]; a.out.uy[o] = dyv[it]; a.out.amp[o] = am[it];
+                        a.out.x[o] = x; a.out.y[o] = y; a.out.ux[o] = ux; a.out.uy[o] = uy; a.out.amp[o] = am;
                     } else {
                         atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
                     }
                     atomicAdd(&keep_hist[b], 1);
-                    if (a.splat) splat_at(raw, sl_s[b], P.x0, P.y0, nx[it], ny_[it], am[it], &clamp_local);
+                    if (a.splat) splat_at(raw, sl_s[b], P.x0, P.y0, x, y, am, &clamp_local);
                 } else {
-                    if (am[it] > 0.f) {
+                    if (am > 0.f) {
                         // crest despawn energy rho g A^2 pi r^2 / 8 (particles.py:322-327)
-                        const double amp = (double)am[it];
+                        const double amp = (double)am;
                         const double e = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2_s[b];
                         atomicAdd(&eout_s[b], e);
                     }
                     if (a.dropped.x) {
                         const long long o = P.pool_base + (v - rank);       // stable among the dropped
-                        a.dropped.x[o] = nx[it]; a.dropped.y[o] = ny_[it];
-                        a.dropped.ux[o] = dxv[it]; a.dropped.uy[o] = dyv[it]; a.dropped.amp[o] = am[it];
+                        a.dropped.x[o] = x; a.dropped.y[o] = y; a.dropped.ux[o] = ux; a.dropped.uy[o] = uy;
+                        a.dropped.amp[o] = am;
                         atomicAdd(&drop_hist[b], 1);
                     }
                 }
@@ -421,6 +465,188 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
         if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
         __syncthreads();
     }
+}
+
+// ------------------------------------------------ two-kernel compaction --
+// Count + scatter (used when HsAdvectArgs.keep_words is set): no serial
+// look-back chain -- the scatter kernel sums the per-tile survivor counts of
+// its patch's earlier tiles directly (a few hundred ints, L2-resident).
+struct AdvTables {
+    int in_off[HS_MAX_BUCKETS + 1], st_off[HS_MAX_BUCKETS + 1], voff[HS_MAX_BUCKETS + 1];
+    int in_cnt[HS_MAX_BUCKETS];
+    double step[HS_MAX_BUCKETS], r2[HS_MAX_BUCKETS];
+    SplatLayer sl[HS_MAX_BUCKETS];
+    HsPatch P;
+    int p, ltile, first, seg_b, seg_end;
+};
+
+// every thread calls; returns false when the block's tile is empty
+__device__ __forceinline__ bool adv_setup(const HsAdvectArgs& a, AdvTables& T, int tile) {
+    const int nb = a.nb, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        int pre = 0, p = 0;
+        for (; p < a.n_patches; ++p) {
+            const HsPatch& Pq = a.patches[p];
+            const int cap = Pq.pool_capacity + (a.stage_count ? Pq.stage_capacity : 0);
+            const int nt = (cap + ADV_CHUNK - 1) / ADV_CHUNK;
+            if (tile < pre + nt) break;
+            pre += nt;
+        }
+        T.p = p;
+        T.first = pre;
+        T.ltile = tile - pre;
+    }
+    __syncthreads();
+    const int p = T.p;
+    if (p >= a.n_patches) return false;
+    if (wid == 0) {
+        const HsPatch P = a.patches[p];
+        if (lane == 0) T.P = P;
+        const int ci = lane < nb ? a.in_count[(size_t)p * nb + lane] : 0;
+        const int cs = (lane < nb && a.stage_count) ? a.stage_count[(size_t)p * nb + lane] : 0;
+        const int si = warp_incl_scan(ci, lane), ss = warp_incl_scan(cs, lane);
+        if (lane < nb) {
+            T.in_off[lane] = si - ci; T.st_off[lane] = ss - cs; T.voff[lane] = si - ci + ss - cs; T.in_cnt[lane] = ci;
+            const HsBucket B = a.buckets[lane];
+            T.step[lane] = dmul(B.speed, a.dt);
+            T.r2[lane] = dmul(B.radius, B.radius);
+            if (a.splat) {
+                const HsLayer L = a.layers[P.layer_base + lane];
+                T.sl[lane] = SplatLayer{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1),
+                                        (double)(L.wy - 1), L.wy, L.pad};
+            }
+        }
+        if (lane == nb - 1) { T.in_off[nb] = si; T.st_off[nb] = ss; T.voff[nb] = si + ss; }
+        __syncwarp();
+        if (lane == 0) {
+            const int tb = T.ltile * ADV_CHUNK;
+            if (tb < T.voff[nb]) {
+                const int b = find_seg(T.voff, nb + 1, tb);
+                T.seg_b = b;
+                T.seg_end = T.voff[b + 1];
+            }
+        }
+    }
+    __syncthreads();
+    return T.ltile * ADV_CHUNK < T.voff[nb];
+}
+
+__global__ void __launch_bounds__(ADV_THREADS) advect_count_kernel(HsAdvectArgs a) {
+    __shared__ AdvTables T;
+    __shared__ int wsum[ADV_THREADS / 32];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool live = adv_setup(a, T, tile);
+    unsigned* words = a.keep_words + (size_t)tile * (ADV_ITEMS * ADV_THREADS / 32);
+    if (!live) {
+        if (threadIdx.x == 0) a.tile_state[tile] = 0ULL;
+        return;
+    }
+    const int nb = a.nb, N = T.voff[nb], tbase = T.ltile * ADV_CHUNK;
+    const HsPatch& P = T.P;
+    int mine = 0;
+#pragma unroll
+    for (int it = 0; it < ADV_ITEMS; ++it) {
+        const int v = tbase + it * ADV_THREADS + threadIdx.x;
+        int keep = 0;
+        if (v < N) {
+            const int b = v < T.seg_end ? T.seg_b : find_seg(T.voff, nb + 1, v);
+            double x, y, ux, uy;
+            const float* ap;
+            adv_item(a, P, T.in_off, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
+            const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
+            const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
+            keep = dadd(dmul(ox, ox), dmul(oy, oy)) <= T.r2[b];       // support disk (:315-320)
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) { words[it * (ADV_THREADS / 32) + wid] = bal; mine += __popc(bal); }
+    }
+    if (lane == 0) wsum[wid] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < ADV_THREADS / 32; ++w) t += wsum[w];
+        a.tile_state[tile] = (unsigned long long)t;
+    }
+}
+
+__global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArgs a) {
+    __shared__ AdvTables T;
+    __shared__ int wpre[ADV_ITEMS * ADV_THREADS / 32];
+    __shared__ unsigned wbits[ADV_ITEMS * ADV_THREADS / 32];
+    __shared__ int red[ADV_THREADS / 32];
+    __shared__ int keep_hist[HS_MAX_BUCKETS], drop_hist[HS_MAX_BUCKETS], clamp_s;
+    __shared__ double eout_s[HS_MAX_BUCKETS];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nb = a.nb;
+    if (threadIdx.x < nb) { keep_hist[threadIdx.x] = 0; drop_hist[threadIdx.x] = 0; eout_s[threadIdx.x] = 0.0; }
+    if (threadIdx.x == 0) clamp_s = 0;
+    if (!adv_setup(a, T, tile)) return;
+    const int N = T.voff[nb], tbase = T.ltile * ADV_CHUNK, p = T.p;
+    const HsPatch& P = T.P;
+    // tile prefix: survivors of this patch's earlier tiles
+    int acc = 0;
+    for (int q = T.first + threadIdx.x; q < tile; q += ADV_THREADS) acc += (int)a.tile_state[q];
+    acc = warp_sum(acc);
+    if (lane == 0) red[wid] = acc;
+    const unsigned* words = a.keep_words + (size_t)tile * (ADV_ITEMS * ADV_THREADS / 32);
+    if (wid == 0) {
+        const unsigned wv = words[lane];              // 32 = ADV_ITEMS * 8 words, item order
+        const int c = __popc(wv);
+        wbits[lane] = wv;
+        wpre[lane] = warp_incl_scan(c, lane) - c;
+    }
+    __syncthreads();
+    int tprefix = 0;
+#pragma unroll
+    for (int w = 0; w < ADV_THREADS / 32; ++w) tprefix += red[w];
+    int clamp_local = 0;
+    float* raw = a.raw_layers;
+#pragma unroll
+    for (int it = 0; it < ADV_ITEMS; ++it) {
+        const int v = tbase + it * ADV_THREADS + threadIdx.x;
+        if (v >= N) continue;
+        const int w = it * (ADV_THREADS / 32) + wid;
+        const unsigned bal = wbits[w];
+        const bool kept = (bal >> lane) & 1u;
+        const int rank = tprefix + wpre[w] + __popc(bal & ((1u << lane) - 1u));
+        const int b = v < T.seg_end ? T.seg_b : find_seg(T.voff, nb + 1, v);
+        double x, y, ux, uy;
+        const float* ap;
+        adv_item(a, P, T.in_off, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
+        const float am = *ap;
+        if (kept) {
+            if (rank < P.pool_capacity) {
+                const long long o = P.pool_base + rank;
+                a.out.x[o] = x; a.out.y[o] = y; a.out.ux[o] = ux; a.out.uy[o] = uy; a.out.amp[o] = am;
+            } else {
+                atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+            }
+            atomicAdd(&keep_hist[b], 1);
+            if (a.splat) splat_at(raw, T.sl[b], P.x0, P.y0, x, y, am, &clamp_local);
+        } else {
+            if (am > 0.f) {
+                const double amp = (double)am;          // crest despawn energy (particles.py:322-327)
+                atomicAdd(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * T.r2[b]);
+            }
+            if (a.dropped.x) {
+                const long long o = P.pool_base + (v - rank);
+                a.dropped.x[o] = x; a.dropped.y[o] = y; a.dropped.ux[o] = ux; a.dropped.uy[o] = uy;
+                a.dropped.amp[o] = am;
+                atomicAdd(&drop_hist[b], 1);
+            }
+        }
+    }
+    if (clamp_local) atomicAdd(&clamp_s, clamp_local);
+    __syncthreads();
+    if (threadIdx.x < nb) {
+        const int b = threadIdx.x;
+        if (keep_hist[b]) atomicAdd(&a.out_count[(size_t)p * nb + b], keep_hist[b]);
+        if (drop_hist[b]) atomicAdd(&a.dropped_count[(size_t)p * nb + b], drop_hist[b]);
+        if (eout_s[b] != 0.0) atomicAdd(&a.e_out[(size_t)p * nb + b], eout_s[b]);
+    }
+    if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
 }
 
 // ======================================================== splat only ==
@@ -486,13 +712,27 @@ extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
     HS_CUDA(cudaMemsetAsync(a->tile_state, 0, sizeof(unsigned long long) * (size_t)a->max_tiles, st));
     HS_CUDA(cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st));
     if (a->splat) HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
-    static int occ = 0;
-    if (occ == 0) {
-        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_kernel, ADV_THREADS, 0));
-        if (occ < 1) occ = 1;
+    static int chunks = 0, occ1 = 0, occ4 = 0;
+    if (chunks == 0) {
+        const char* e = getenv("HS_ADVECT_CHUNKS");
+        chunks = (e && atoi(e) == 4) ? 4 : 1;
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, advect_kernel<1>, ADV_THREADS, 0));
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, advect_kernel<4>, ADV_THREADS, 0));
+        if (occ1 < 1) occ1 = 1;
+        if (occ4 < 1) occ4 = 1;
     }
-    int grid = num_sms() * occ;
-    advect_kernel<<<grid, ADV_THREADS, 0, st>>>(*a);
+    if (a->keep_words) {
+        // tiles of every patch, 1024 items each (empty tiles exit at once)
+        advect_count_kernel<<<a->max_tiles, ADV_THREADS, 0, st>>>(*a);
+        HS_LAUNCH_CHECK();
+        advect_scatter_kernel<<<a->max_tiles, ADV_THREADS, 0, st>>>(*a);
+        HS_LAUNCH_CHECK();
+        return 0;
+    }
+    const int occ = chunks == 4 ? occ4 : occ1;
+    const int grid = num_sms() * occ;
+    if (chunks == 4) advect_kernel<4><<<grid, ADV_THREADS, 0, st>>>(*a);
+    else advect_kernel<1><<<grid, ADV_THREADS, 0, st>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

@@ -219,6 +219,7 @@ class Simulation:
             self.clamped = self.stat_words[4 * P:5 * P]
             self.max_tiles = int(sum(-(-(pc + sc) // ADV_TILE) for pc, sc in zip(self.pool_caps, self.stage_caps)))
             self.tile_state = torch.zeros(self.max_tiles, dtype=torch.int64, device=dev)
+            self.keep_words = torch.zeros(self.max_tiles * 32, dtype=torch.int32, device=dev)
             self.tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
             self._init_boxes()
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -268,6 +269,8 @@ class Simulation:
             with torch.cuda.stream(side):
                 mark("fft_start")
                 fa = fft_args(self.fft_state, self.fft_ws, frame_ptr=self.frame_dev, dt=dt)
+                fa.emit_normals = 0          # normals are derived lazily (background) / in hs_compose
+                fa.normal = 0
                 if not self.n_patches:
                     fa.frame_advance = N.ptr(self.frame_dev)
                 N.call("hs_fft_evolve", fa, stream_ptr())
@@ -294,7 +297,8 @@ class Simulation:
                 e_out=N.ptr(self.e_out), splat=1, raw_layers=N.ptr(self.synth.raw),
                 raw_layers_len=self.synth.pack.raw_len, layers=N.ptr(self.synth.layers),
                 clamped=N.ptr(self.clamped), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
-                tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status)), st)
+                tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status),
+                keep_words=N.ptr(self.keep_words)), st)
             mark("advect")
             N.call("hs_smooth", self.synth.smooth_args(), st)
             mark("smooth")
@@ -307,7 +311,7 @@ class Simulation:
                 smooth_layers=N.ptr(self.synth.smooth), tile_info=N.ptr(self.synth.compose_info),
                 total_tiles=self.synth.compose_tiles,
                 bg_height=N.ptr(bg.height) if bg is not None else 0,
-                bg_normal=N.ptr(bg.normal) if bg is not None else 0,
+                bg_normal=0,                  # hs_compose derives them from the staged heights
                 bg_n=self.config.fft_n if bg is not None else 0,
                 bg_spacing=self.config.fft_domain / self.config.fft_n if bg is not None else 1.0,
                 patch_height=N.ptr(self.patch_h), patch_normal=0,
@@ -316,6 +320,7 @@ class Simulation:
                 frame_advance=N.ptr(self.frame_dev)), st)
             mark("compose")
             self._patch_n_frame = -1          # patch normals are derived lazily (patch_field)
+        self._bg_n_frame = -1                 # so are the background normals (background)
         if self.fft_state is None and not self.n_patches:
             N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(st))
 
@@ -344,10 +349,11 @@ class Simulation:
         advance_frame."""
         k = 0
         if self.fft_state is not None:
-            k += 2 + (1 if self.fft_ws.normal is not None else 0)
+            k += 2                            # rows + columns (normals are lazy)
         if self.n_patches:
             pk = self.synth.pack
-            k += 3 + (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
+            # inject, advect count + scatter, compose, smooth (fused + 2 wide passes)
+            k += 4 + (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
         return max(k, 1)
 
     def timed_frame(self) -> dict:
@@ -433,7 +439,15 @@ class Simulation:
     # ----------------------------------------------------------- outputs --
     @property
     def background(self) -> HeightField | None:
-        return self.fft_ws.field(self.fft_state) if self.fft_ws is not None else None
+        """The frame's background HeightField; its normals (grid_normals,
+        fft_background.py:205) are materialised on first access per frame."""
+        if self.fft_ws is None:
+            return None
+        if getattr(self, "_bg_n_frame", -1) != self.frame and self.fft_ws.normal is not None:
+            N.call_raw("hs_periodic_normals", N.vp(N.ptr(self.fft_ws.height)), N.vp(N.ptr(self.fft_ws.normal)),
+                       self.config.fft_n, self.config.fft_domain / self.config.fft_n, N.vp(stream_ptr()))
+            self._bg_n_frame = self.frame
+        return self.fft_ws.field(self.fft_state)
 
     def counts_host(self) -> np.ndarray:
         """(n_patches, nb) live particles per bucket (synchronises)."""
@@ -495,7 +509,7 @@ class Simulation:
             raise ConfigError("stitched_heights needs the FFT background (mode != wp-only)")
         bg = self.fft_ws
         args = N.HsCompositeArgs(
-            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=N.ptr(bg.normal),
+            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0,
             n_patches=self.n_patches, patches=N.ptr(self.patches_dev) if self.n_patches else 0,
             patch_height=N.ptr(self.patch_h) if self.n_patches else 0, patch_normal=0,
             box=N.ptr(self.box_dev) if self.n_patches else 0,

@@ -386,6 +386,7 @@ def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRe
     tile_state = torch.zeros(max_tiles, dtype=torch.int64, device=dev)
     tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
+    keep_words = torch.zeros(max_tiles * 32, dtype=torch.int32, device=dev)
     args = N.HsAdvectArgs(n_patches=1, nb=nb, buckets=N.ptr(buckets), patches=N.ptr(pstruct), dt=float(dt),
                           rho=float(own_ledger.rho), g=float(g), in_=particles.pool_struct(),
                           in_count=N.ptr(in_count), stage=N.pool_struct(), stage_count=0,
@@ -393,7 +394,7 @@ def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRe
                           dropped=N.pool_struct(dx, dy, dux, duy, damp), dropped_count=N.ptr(drop_count),
                           e_out=N.ptr(own_ledger.e_out), splat=0, raw_layers=0, raw_layers_len=0, layers=0,
                           clamped=0, tile_state=N.ptr(tile_state), max_tiles=max_tiles,
-                          tile_counter=N.ptr(tile_counter), status=N.ptr(status))
+                          tile_counter=N.ptr(tile_counter), status=N.ptr(status), keep_words=N.ptr(keep_words))
     N.call("hs_advect", args, stream_ptr())
     kc = out_count.cpu().numpy().astype(np.int64)
     dc = drop_count.cpu().numpy().astype(np.int64)

@@ -23,6 +23,7 @@ def main() -> int:
     from paper_2511_02852_b200 import Simulation, scenes
     sim = Simulation(scenes.PRESETS[args.config](), device="cuda:0")
     sim.run_frames(args.warm_frames, dt=0.1)
+    sim.run_frames(3)
     torch.cuda.synchronize()
     sim.config = sim.config.__class__(**{**sim.config.__dict__, "graph": False})
     for _ in range(args.frames):
