@@ -8,23 +8,31 @@
 //            n = normalize(w n_patch + (1 - w) n_fft)  (coupling.py:37-40, 120-141)
 //   stats    interior sum of h^2 for FrameStats.patch_variance (harness.py:176-178)
 //
-// One CTA per 32x32 output tile (+1-texel halo).  Per CTA the coarse (f > 1)
-// smoothed layers' footprint under the tile is staged in shared memory and
-// the bilinear row / column indices and weights are tabulated once; f == 1
-// layers are read straight from L2 with coalesced rows.  Blend distances and
-// background sample positions are formed per row / column in fp64 (world
-// coordinates, as the reference) and applied per texel in fp32.
+// One CTA per 30x30 output tile (+1-texel halo).  The coarse (f > 1)
+// smoothed layers' footprint under the tile is staged in shared memory in
+// one cp.async batch; f == 1 layers are read straight from L2 with coalesced
+// rows.  Blend distances and background sample positions are formed per row
+// / column in fp64 (world coordinates, as the reference) and applied per
+// texel in fp32.
 #include "synth_common.cuh"
 
 namespace hs {
 
 constexpr int CT = 30;            // output tile edge
-constexpr int CH = CT + 2;        // haloed height tile (32): lane = haloed row, 32 columns in registers
-constexpr int WPB = 2;            // warps (tiles) per block
+constexpr int CH = CT + 2;        // haloed height tile (32): lane = haloed column
+constexpr int NW = 4;             // warps per tile (CTA)
+constexpr int NT = 32 * NW;
+constexpr int RPW = CH / NW;      // haloed rows per warp in the height pass
 constexpr int BG_CAP = 8;         // staged background footprint per axis (+1 halo each side)
-constexpr int CS_WARP = 1536;     // floats of staged coarse footprints per warp
+constexpr int CS_CTA = 1536;      // floats of staged coarse footprints per tile
+constexpr int TC_CAP = 2560;      // floats of row-interpolated coarse rows per tile (32 per coarse row)
 
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
+
+// floor(x / f) for 0 <= x < 2^22, f >= 1, from the fp32 reciprocal: the
+// quotient of x + 1/2 sits >= 1/(2f) from an integer, far above the rounding
+// error, so the truncation is exact
+__device__ __forceinline__ int fdiv(int x, float inv_f) { return (int)(((float)x + 0.5f) * inv_f); }
 
 __device__ __forceinline__ float3 bg_node_normal(const float* H, int n, long long i, long long j, float inv2s) {
     const int m = n - 1;
@@ -34,280 +42,316 @@ __device__ __forceinline__ float3 bg_node_normal(const float* H, int n, long lon
     return make_float3(-hx * r, -hy * r, r);
 }
 
-struct WarpSmem {
-    float hs[CH][CH + 1];             // haloed patch heights
-    float tcol[20][CH];               // row-interpolated coarse rows of one layer (lane = column)
-    float4 rw[CH];                    // per haloed row: coarse row (rel), g0, g1, unused
-    float cs[CS_WARP];                // staged coarse footprints of all layers
-    HsLayer Ls[HS_MAX_BUCKETS];
-    int st[HS_MAX_BUCKETS][4];        // per layer: staged offset (-1: none), cr0, cc0, ncol
-    float bgh[(BG_CAP + 2) * (BG_CAP + 2)];
-    float bgn[BG_CAP * BG_CAP * 3];
-    float row_d[CT], col_d[CT], row_fu[CT], col_fv[CT];
-    int row_q0[CT], row_q1[CT], col_q0[CT], col_q1[CT];
-    int bg_q[4];
+// per-tile plan of one smoothed layer
+struct LayerPlan {
+    long long sm_off;
+    int f, ncx, ncy;
+    int cs_off;                       // staged footprint offset in cs (-1: layer read from global)
+    int cr0, cc0, ncol, nr;           // coarse footprint: first row / column, extents
+    int tc_off;                       // row-interpolated rows offset in tc
+    float inv_f, gain;
 };
 
-// One warp per 30 x 30 output tile (32 x 32 haloed heights):
-//   heights  lane = haloed row; per layer the warp walks the row's coarse
-//            cells left to right (cell boundaries are warp-uniform), forms the
-//            two row-interpolated coarse values per cell and lerps them into
-//            32 register accumulators: sum_b gain_b upsample_b
-//            (patch_synthesis.py:261-274, 301-313); f == 1 layers are staged
-//            through shared memory (coalesced) and read transposed
+struct TileSmem {
+    union {
+        float cs[CS_CTA];             // staged coarse footprints (until the tc table is built)
+        float hs[CH][CH + 1];         // haloed patch heights (after the height pass)
+    } u1;
+    union {
+        float tc[TC_CAP];             // coarse rows of every layer interpolated at the 32 haloed columns
+        float4 trow[CT][BG_CAP];      // background (h, nx, ny, nz) x-lerped per output row (epilogue)
+    } u2;
+    float bgh[(BG_CAP + 2) * (BG_CAP + 2)];   // background heights (+1 halo)
+    float bgn[BG_CAP * BG_CAP * 3];           // background node normals (given ones)
+    float row_d[CT], col_d[CT], col_fv[CT];
+    int col_p0[CT];
+    double red[NW];
+    int redc[NW];
+    // dynamic tail, nb entries each:
+    //   LayerPlan pl[nb];
+    //   int2 rowt[nb][CH]   per layer and haloed row: tc offsets of rows r, r+1 (16 bit each), g1
+};
+
+__host__ __device__ constexpr size_t compose_smem_bytes(int nb) {
+    return sizeof(TileSmem) + (size_t)nb * (sizeof(LayerPlan) + CH * sizeof(int2));
+}
+
+// background footprint of an output tile: first node and node count per
+// axis (0 counts: not stageable, read from global)
+__device__ __forceinline__ int4 bg_footprint(const HsPatch& P, int i0, int j0, double inv_sp, int bm) {
+    const int il = min(i0 + CT - 1, P.res - 1), jl = min(j0 + CT - 1, P.ny - 1);
+    const long long qa = (long long)floor((P.x0 + (double)i0 * P.texel) * inv_sp);
+    const long long qb = (long long)floor((P.x0 + (double)il * P.texel) * inv_sp) + 1;
+    const long long qc = (long long)floor((P.y0 + (double)j0 * P.texel) * inv_sp);
+    const long long qd = (long long)floor((P.y0 + (double)jl * P.texel) * inv_sp) + 1;
+    if (qb - qa + 1 <= BG_CAP && qd - qc + 1 <= BG_CAP)
+        return make_int4((int)(qa & bm), (int)(qb - qa + 1), (int)(qc & bm), (int)(qd - qc + 1));
+    return make_int4(0, 0, 0, 0);
+}
+
+// One CTA (4 warps) per 30 x 30 output tile (32 x 32 haloed heights).
+//   heights  sum_b gain_b upsample_b (patch_synthesis.py:261-274, 301-313),
+//            x-first bilinear: every coarse (f > 1) layer's footprint is
+//            staged by one cp.async batch, its rows are interpolated once at
+//            the 32 haloed columns (tc table), and each haloed texel then
+//            sums two table entries per layer (lane = column, warp w = rows
+//            8w..8w+7); f == 1 layers are read as coalesced rows
 //   epilogue clamped FD normals (finish_field :323-340) and the smoothstep
 //            blend against the periodic background at the patch nodes
-//            (coupling.py:37-40, 120-141), background footprint staged
-// Warps never synchronise with each other.
-__global__ void __launch_bounds__(32 * WPB) compose_kernel(HsComposeArgs a) {
-    __shared__ WarpSmem wsm[WPB];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int tile = blockIdx.x * WPB + wid;
-    if (a.frame_advance && blockIdx.x == 0 && threadIdx.x == 0) *a.frame_advance += 1;
-    if (tile >= a.total_tiles) return;
-    WarpSmem& W = wsm[wid];
+//            (coupling.py:37-40, 120-141); the background bilinear is done
+//            separably from per-row x-lerped tables
+__global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& W = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int nb = a.nb;
+    LayerPlan* const Wpl = reinterpret_cast<LayerPlan*>(smem_raw + sizeof(TileSmem));
+    int2 (*const Wrowt)[CH] = reinterpret_cast<int2 (*)[CH]>(Wpl + nb);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int tile = blockIdx.x;
+    if (a.frame_advance && tile == 0 && tid == 0) *a.frame_advance += 1;
     const int* ti = a.tile_info + 3 * tile;
     const int p = ti[0], i0 = ti[1], j0 = ti[2];
     const HsPatch P = a.patches[p];
-    const int nb = a.nb;
-    const bool have_bg = a.bg_height != nullptr;
+    const bool have_bg = a.bg_height != nullptr && a.blend_mode;
     const int bm = a.bg_n - 1;
     const double inv_sp = have_bg ? 1.0 / a.bg_spacing : 0.0;
+    const int4 bq = have_bg ? bg_footprint(P, i0, j0, inv_sp, bm) : make_int4(0, 0, 0, 0);
+    const bool bg_staged = bq.y > 0;
+    const bool own_normals = a.bg_normal == nullptr;
 
-    // background footprint of the output tile (+1 halo for the node normals)
-    if (lane == 0) {
-        W.bg_q[0] = W.bg_q[1] = W.bg_q[2] = W.bg_q[3] = 0;
-        if (have_bg) {
-            const int il = min(i0 + CT - 1, P.res - 1), jl = min(j0 + CT - 1, P.ny - 1);
-            const long long qa = (long long)floor((P.x0 + (double)i0 * P.texel) * inv_sp);
-            const long long qb = (long long)floor((P.x0 + (double)il * P.texel) * inv_sp) + 1;
-            const long long qc = (long long)floor((P.y0 + (double)j0 * P.texel) * inv_sp);
-            const long long qd = (long long)floor((P.y0 + (double)jl * P.texel) * inv_sp) + 1;
-            if (qb - qa + 1 <= BG_CAP && qd - qc + 1 <= BG_CAP) {
-                W.bg_q[0] = (int)(qa & bm); W.bg_q[1] = (int)(qb - qa + 1);
-                W.bg_q[2] = (int)(qc & bm); W.bg_q[3] = (int)(qd - qc + 1);
+    const int ib = i0 - 1;                         // haloed row 0 / column 0
+    const int jb = j0 - 1;
+    const int ilo = min(max(ib, 0), P.res - 1), ihi = min(max(ib + CH - 1, 0), P.res - 1);
+    const int jlo = min(max(jb, 0), P.ny - 1), jhi = min(max(jb + CH - 1, 0), P.ny - 1);
+
+    if (wid == 0) {
+        // layer plans (lane b: layer b); footprint offsets by warp scans
+        LayerPlan pl{};
+        int need_cs = 0, need_tc = 0;
+        if (lane < nb) {
+            const HsLayer L = a.layers[P.layer_base + lane];
+            pl.sm_off = L.sm_off; pl.f = L.f; pl.ncx = L.ncx; pl.ncy = L.ncy;
+            pl.inv_f = 1.f / (float)L.f; pl.gain = L.gain;
+            if (L.f > 1) {
+                pl.cr0 = ilo / L.f;
+                pl.nr = min(ihi / L.f + 1, L.ncx - 1) - pl.cr0 + 1;
+                pl.cc0 = jlo / L.f;
+                pl.ncol = min(jhi / L.f + 1, L.ncy - 1) - pl.cc0 + 1;
+                need_cs = pl.nr * pl.ncol;
+                need_tc = pl.nr * CH;
             }
         }
+        const int inc_cs = warp_incl_scan(need_cs, lane);
+        const int inc_tc = warp_incl_scan(need_tc, lane);
+        // a layer is tabulated only if every layer before it was (prefix offsets stay valid)
+        const bool fits = need_cs > 0 && inc_cs <= CS_CTA && inc_tc <= TC_CAP;
+        pl.cs_off = fits ? inc_cs - need_cs : -1;
+        pl.tc_off = fits ? inc_tc - need_tc : -1;
+        if (lane < nb) Wpl[lane] = pl;
+    } else if (wid == 1 && lane < CT) {
+        // per output row / column (fp64 world coordinates, coupling.py:57-59): boundary
+        // depth (coupling.py:27-34) and the column-side background lerp
+        const double yy = P.y0 + (double)(j0 + lane) * P.texel;
+        W.col_d[lane] = (float)fmin(yy - P.y0, P.y1 - yy);
+        const double xx = P.x0 + (double)(i0 + lane) * P.texel;
+        W.row_d[lane] = (float)fmin(xx - P.x0, P.x1 - xx);
+        if (have_bg) {
+            const double v = yy * inv_sp, fl = floor(v);
+            W.col_fv[lane] = (float)(v - fl);
+            const long long q = (long long)fl;
+            W.col_p0[lane] = bg_staged ? (int)(q - (long long)floor((P.y0 + (double)j0 * P.texel) * inv_sp)) : (int)(q & bm);
+        }
     }
-    __syncwarp();
-    const bool bg_staged = W.bg_q[1] > 0;
-    const bool own_normals = a.bg_normal == nullptr;
+    // background footprint (+1 halo) by cp.async; independent of the plans
     if (bg_staged) {
-        const int nr = W.bg_q[1] + 2, nc = W.bg_q[3] + 2;
-        for (int e = lane; e < nr * nc; e += 32) {
+        const int nr = bq.y + 2, nc = bq.w + 2;
+        for (int e = tid; e < nr * nc; e += NT) {
             const int rr = e / nc, cc = e - rr * nc;
-            const long long g = (long long)((W.bg_q[0] - 1 + rr) & bm) * a.bg_n + ((W.bg_q[2] - 1 + cc) & bm);
+            const long long g = (long long)((bq.x - 1 + rr) & bm) * a.bg_n + ((bq.z - 1 + cc) & bm);
             cp_async4(W.bgh + e, a.bg_height + g, true);
         }
         if (!own_normals) {
-            const int nr0 = W.bg_q[1], nc0 = W.bg_q[3];
-            for (int e = lane; e < nr0 * nc0; e += 32) {
-                const int rr = e / nc0, cc = e - rr * nc0;
-                const long long g = (long long)((W.bg_q[0] + rr) & bm) * a.bg_n + ((W.bg_q[2] + cc) & bm);
-                cp_async4(W.bgn + 3 * e, a.bg_normal + 3 * g, true);
-                cp_async4(W.bgn + 3 * e + 1, a.bg_normal + 3 * g + 1, true);
-                cp_async4(W.bgn + 3 * e + 2, a.bg_normal + 3 * g + 2, true);
+            for (int e = tid; e < bq.y * bq.w; e += NT) {
+                const int rr = e / bq.w, cc = e - rr * bq.w;
+                const long long g = 3 * ((long long)((bq.x + rr) & bm) * a.bg_n + ((bq.z + cc) & bm));
+                cp_async4(W.bgn + 3 * e, a.bg_normal + g, true);
+                cp_async4(W.bgn + 3 * e + 1, a.bg_normal + g + 1, true);
+                cp_async4(W.bgn + 3 * e + 2, a.bg_normal + g + 2, true);
             }
         }
     }
-    // blend / background tables: lane k < 30 does output row k and column k (fp64 world coordinates)
-    if (lane < CT) {
-#pragma unroll
-        for (int axis = 0; axis < 2; ++axis) {
-            const int idx = (axis == 0 ? i0 : j0) + lane;
-            const double lo = axis == 0 ? P.x0 : P.y0, hi = axis == 0 ? P.x1 : P.y1;
-            const double x = lo + (double)idx * P.texel;        // node positions (coupling.py:57-59)
-            const float d = (float)fmin(x - lo, hi - x);        // boundary_depth (coupling.py:27-34)
-            int q0 = 0, q1 = 0;
-            float fr = 0.f;
-            if (have_bg) {
-                const double u = x * inv_sp;                     // background origin (0, 0)
-                const double fl = floor(u);
-                fr = (float)(u - fl);
-                const long long q = (long long)fl;
-                if (bg_staged) {
-                    const long long base = axis == 0 ? (long long)floor((P.x0 + (double)i0 * P.texel) * inv_sp)
-                                                     : (long long)floor((P.y0 + (double)j0 * P.texel) * inv_sp);
-                    q0 = (int)(q - base);
-                    q1 = q0 + 1;
-                } else {
-                    q0 = (int)(q & bm);
-                    q1 = (q0 + 1) & bm;
-                }
-            }
-            if (axis == 0) { W.row_d[lane] = d; W.row_fu[lane] = fr; W.row_q0[lane] = q0; W.row_q1[lane] = q1; }
-            else           { W.col_d[lane] = d; W.col_fv[lane] = fr; W.col_q0[lane] = q0; W.col_q1[lane] = q1; }
+    __syncthreads();
+    // every coarse footprint, one batch
+    for (int b = 0; b < nb; ++b) {
+        const LayerPlan& L = Wpl[b];
+        if (L.cs_off < 0) continue;
+        const float* Sg = a.smooth_layers + L.sm_off + (long long)L.cr0 * L.ncy + L.cc0;
+        const float inv_nc = 1.f / (float)L.ncol;
+        for (int e = tid; e < L.nr * L.ncol; e += NT) {
+            const int rr = fdiv(e, inv_nc) , cc = e - rr * L.ncol;
+            cp_async4(W.u1.cs + L.cs_off + e, Sg + (long long)rr * L.ncy + cc, true);
         }
     }
-
-    // ---- heights: lane = haloed column c, acc[r] = haloed row r ----
-    // all global reads are batched: layer descriptors (one round trip), then
-    // every coarse footprint by cp.async while the f == 1 layers stream in
+    // f == 1 layers straight into the accumulators (lane = haloed column, coalesced rows)
     const int c = lane;
-    const int j_raw = j0 - 1 + c;
-    const int j = min(max(j_raw, 0), P.ny - 1);
-    const int ib = i0 - 1;                         // haloed row 0
-    const int ilo = min(max(ib, 0), P.res - 1), ihi = min(max(ib + CH - 1, 0), P.res - 1);
-    const int jlo = min(max(j0 - 1, 0), P.ny - 1), jhi = min(max(j0 - 1 + CH - 1, 0), P.ny - 1);
-    if (lane < nb) W.Ls[lane] = a.layers[P.layer_base + lane];
-    __syncwarp();
-    {
-        // staging plan: lane b sizes layer b's footprint; offsets by a warp scan
-        int need = 0, cr0 = 0, cc0 = 0, ncol = 0;
-        if (lane < nb && W.Ls[lane].f > 1) {
-            const HsLayer& L = W.Ls[lane];
-            cr0 = ilo / L.f;
-            const int nr = min(ihi / L.f + 1, L.ncx - 1) - cr0 + 1;
-            cc0 = jlo / L.f;
-            ncol = min(jhi / L.f + 1, L.ncy - 1) - cc0 + 1;
-            need = nr * ncol;
-        }
-        const int inc = warp_incl_scan(need, lane);
-        if (lane < nb) {
-            W.st[lane][0] = (need > 0 && inc <= CS_WARP) ? inc - need : -1;
-            W.st[lane][1] = cr0; W.st[lane][2] = cc0; W.st[lane][3] = ncol;
-        }
-    }
-    __syncwarp();
-    for (int b = 0; b < nb; ++b) {
-        const HsLayer& L = W.Ls[b];
-        const int off = W.st[b][0];
-        if (off < 0) continue;
-        const int cr0 = W.st[b][1], cc0 = W.st[b][2], ncol = W.st[b][3];
-        const int nr = min(ihi / L.f + 1, L.ncx - 1) - cr0 + 1;
-        const float* S = a.smooth_layers + L.sm_off;
-        for (int e = lane; e < nr * ncol; e += 32) {
-            const int rr = e / ncol, cc = e - rr * ncol;
-            cp_async4(W.cs + off + e, S + (long long)(cr0 + rr) * L.ncy + cc0 + cc, true);
-        }
-    }
-    float acc[CH];
+    const int j = min(max(jb + c, 0), P.ny - 1);
+    const int qb = RPW * wid;                      // first haloed row of this warp
+    float acc[RPW];
 #pragma unroll
-    for (int q = 0; q < CH; ++q) acc[q] = 0.f;
-    for (int b = 0; b < nb; ++b) {                 // f == 1 layers: coalesced rows, 32 loads in flight
-        const HsLayer& L = W.Ls[b];
+    for (int k = 0; k < RPW; ++k) acc[k] = 0.f;
+    for (int b = 0; b < nb; ++b) {
+        const LayerPlan& L = Wpl[b];
         if (L.f != 1) continue;
-        const float* S = a.smooth_layers + L.sm_off;
-        float v[CH];
+        const float* Sg = a.smooth_layers + L.sm_off;
+        float v[RPW];
 #pragma unroll
-        for (int q = 0; q < CH; ++q) v[q] = S[(long long)min(max(ib + q, 0), P.res - 1) * L.ncy + j];
+        for (int k = 0; k < RPW; ++k) v[k] = Sg[(long long)min(max(ib + qb + k, 0), P.res - 1) * L.ncy + j];
 #pragma unroll
-        for (int q = 0; q < CH; ++q) acc[q] = fmaf(L.gain, v[q], acc[q]);
+        for (int k = 0; k < RPW; ++k) acc[k] = fmaf(L.gain, v[k], acc[k]);
     }
     cp_async_wait_all();
-    __syncwarp();
+    __syncthreads();
+    // tables: tc[b][r][c] = coarse row r of layer b lerped at haloed column c;
+    // rowt[b][q] = (rows r, r+1 of haloed row q, g1 = gain * wi)
     for (int b = 0; b < nb; ++b) {
-        const HsLayer& L = W.Ls[b];
+        const LayerPlan& L = Wpl[b];
+        if (L.tc_off < 0) continue;
+        const int jj = min(max(jb + (tid & 31), 0), P.ny - 1);
+        const int cj = fdiv(jj, L.inv_f);
+        const int d1 = min(cj + 1, L.ncy - 1) - cj;
+        const float wj = (float)(jj - cj * L.f) * L.inv_f;
+        const float* src = W.u1.cs + L.cs_off + (cj - L.cc0);
+        for (int r = tid >> 5; r < L.nr; r += NW)
+            W.u2.tc[L.tc_off + r * CH + (tid & 31)] = lerpf(src[r * L.ncol], src[r * L.ncol + d1], wj);
+    }
+    for (int e = tid; e < nb * CH; e += NT) {
+        const int b = e >> 5, q = e & 31;
+        const LayerPlan& L = Wpl[b];
         if (L.f == 1) continue;
-        const int f = L.f;
-        const float inv_f = 1.f / (float)f;
-        const int cr0 = ilo / f, nr = min(ihi / f + 1, L.ncx - 1) - cr0 + 1;
-        const int cj = j / f;
-        const int cj1 = min(cj + 1, L.ncy - 1);
-        const float wj = (float)(j - cj * f) * inv_f;
-        {   // per haloed row (lane = row): coarse row offset and gain-folded weights
-            const int ii = min(max(ib + lane, 0), P.res - 1);
-            const int ci = ii / f;
-            const float wi = (float)(ii - ci * f) * inv_f;
-            const float g1 = L.gain * wi;
-            W.rw[lane] = make_float4(__int_as_float(ci - cr0), L.gain - g1, g1, 0.f);
-        }
-        const int off = W.st[b][0];
-        if (off >= 0 && nr <= 20) {
-            // x-first bilinear (:270-273): interpolate this lane's column on each staged coarse row
-            const int ncol = W.st[b][3], cc0 = W.st[b][2];
-            const float* src = W.cs + off + (cj - cc0);
-            const int d1 = cj1 - cj;
-            for (int rr = 0; rr < nr; ++rr) W.tcol[rr][c] = lerpf(src[rr * ncol], src[rr * ncol + d1], wj);
-            __syncwarp();
+        const int ii = min(max(ib + q, 0), P.res - 1);
+        const int ci = fdiv(ii, L.inv_f);
+        const float wi = (float)(ii - ci * L.f) * L.inv_f;
+        const int cr0 = L.tc_off >= 0 ? L.cr0 : 0;
+        const int r = ci - cr0;
+        const int rn = min(ci + 1, L.ncx - 1) - cr0;
+        Wrowt[b][q] = make_int2((L.tc_off + r * CH) | ((L.tc_off + rn * CH) << 16), __float_as_int(L.gain * wi));
+    }
+    __syncthreads();
+    // ---- heights: acc[k] = haloed row qb + k at haloed column c ----
+    for (int b = 0; b < nb; ++b) {
+        const LayerPlan& L = Wpl[b];
+        if (L.f == 1) continue;
+        const float gain = L.gain;
+        if (L.tc_off >= 0) {
+            const float* T = W.u2.tc + c;
 #pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                const float4 e = W.rw[q];
-                const int rr = __float_as_int(e.x);
-                const int rn = min(rr + 1, nr - 1);
-                acc[q] = fmaf(e.y, W.tcol[rr][c], fmaf(e.z, W.tcol[rn][c], acc[q]));
+            for (int k = 0; k < RPW; ++k) {
+                const int2 e = Wrowt[b][qb + k];
+                const float g1 = __int_as_float(e.y);
+                acc[k] = fmaf(gain - g1, T[e.x & 0xffff], fmaf(g1, T[e.x >> 16], acc[k]));
             }
-        } else {                                   // not staged: direct reads (rare)
-            __syncwarp();
-            const float* S = a.smooth_layers + L.sm_off;
+        } else {                                   // layer not tabulated: rows from global (rare)
+            const float* Sg = a.smooth_layers + L.sm_off;
+            const int cj = fdiv(j, L.inv_f), cj1 = min(cj + 1, L.ncy - 1);
+            const float wj = (float)(j - cj * L.f) * L.inv_f;
 #pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                const float4 e = W.rw[q];
-                const int ci = cr0 + __float_as_int(e.x), ci1 = min(ci + 1, L.ncx - 1);
-                const float* r0 = S + (long long)ci * L.ncy;
-                const float* r1 = S + (long long)ci1 * L.ncy;
-                acc[q] = fmaf(e.y, lerpf(r0[cj], r0[cj1], wj), fmaf(e.z, lerpf(r1[cj], r1[cj1], wj), acc[q]));
+            for (int k = 0; k < RPW; ++k) {
+                const int2 e = Wrowt[b][qb + k];
+                const float g1 = __int_as_float(e.y);
+                const int ii = min(max(ib + qb + k, 0), P.res - 1);
+                const int r0 = fdiv(ii, L.inv_f), r1 = min(r0 + 1, L.ncx - 1);
+                const float* R0 = Sg + (long long)r0 * L.ncy;
+                const float* R1 = Sg + (long long)r1 * L.ncy;
+                acc[k] = fmaf(gain - g1, lerpf(R0[cj], R0[cj1], wj), fmaf(g1, lerpf(R1[cj], R1[cj1], wj), acc[k]));
             }
         }
-        __syncwarp();
     }
     {
-        const bool jok = j_raw >= 0 && j_raw < P.ny;
+        const int jr = jb + c;
+        const bool jok = jr >= 0 && jr < P.ny;
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            const int ii = ib + q;
-            W.hs[q][c] = (jok && ii >= 0 && ii < P.res) ? acc[q] : 0.f;
+        for (int k = 0; k < RPW; ++k) {
+            const int ii = ib + qb + k;
+            W.u1.hs[qb + k][c] = (jok && ii >= 0 && ii < P.res) ? acc[k] : 0.f;
         }
     }
-    cp_async_wait_all();
-    __syncwarp();
-    if (bg_staged && own_normals) {
-        const int nr0 = W.bg_q[1], nc0 = W.bg_q[3], ncs = nc0 + 2;
-        const float inv2s = (float)(0.5 / a.bg_spacing);
-        for (int e = lane; e < nr0 * nc0; e += 32) {
-            const int rr = e / nc0 + 1, cc = e % nc0 + 1;
-            const float hx = (W.bgh[(rr + 1) * ncs + cc] - W.bgh[(rr - 1) * ncs + cc]) * inv2s;
-            const float hy = (W.bgh[rr * ncs + cc + 1] - W.bgh[rr * ncs + cc - 1]) * inv2s;
-            const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
-            W.bgn[3 * e] = -hx * rn; W.bgn[3 * e + 1] = -hy * rn; W.bgn[3 * e + 2] = rn;
+    __syncthreads();                               // tc dead: trow may overwrite it
+    // background: node normals (given, or from the staged heights), x-lerped per output row
+    const float inv2sp = have_bg ? (float)(0.5 / a.bg_spacing) : 0.f;
+    if (bg_staged) {
+        const int ncs = bq.w + 2;
+        const long long base_x = (long long)floor((P.x0 + (double)i0 * P.texel) * inv_sp);
+        for (int e = tid; e < CT * bq.w; e += NT) {
+            const int rr = e / bq.w, pc = e - rr * bq.w;
+            const double u = (P.x0 + (double)(i0 + rr) * P.texel) * inv_sp, fl = floor(u);
+            const float fu = (float)(u - fl);
+            const int q0 = (int)((long long)fl - base_x);
+            float4 n0, n1;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int qr = q0 + s;
+                float4 v;
+                v.x = W.bgh[(qr + 1) * ncs + pc + 1];
+                if (own_normals) {
+                    const float hx = (W.bgh[(qr + 2) * ncs + pc + 1] - W.bgh[qr * ncs + pc + 1]) * inv2sp;
+                    const float hy = (W.bgh[(qr + 1) * ncs + pc + 2] - W.bgh[(qr + 1) * ncs + pc]) * inv2sp;
+                    const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
+                    v.y = -hx * rn; v.z = -hy * rn; v.w = rn;
+                } else {
+                    const int ai = 3 * (qr * bq.w + pc);
+                    v.y = W.bgn[ai]; v.z = W.bgn[ai + 1]; v.w = W.bgn[ai + 2];
+                }
+                if (s == 0) n0 = v; else n1 = v;
+            }
+            W.u2.trow[rr][pc] = make_float4(lerpf(n0.x, n1.x, fu), lerpf(n0.y, n1.y, fu), lerpf(n0.z, n1.z, fu),
+                                            lerpf(n0.w, n1.w, fu));
         }
-        __syncwarp();
     }
+    __syncthreads();
 
     // ---- normals, blend, outputs ----
     const float inv_s = (float)(1.0 / P.texel), inv_2s = (float)(0.5 / P.texel);
     const float inv_margin = (float)(1.0 / P.margin);
-    const float inv2sp = have_bg ? (float)(0.5 / a.bg_spacing) : 0.f;
     const int inset = max(1, (int)rint(P.margin / P.texel));
     double accv = 0.0;
     int cnt = 0;
     const long long gb = P.grid_base;
-    const int bn = a.bg_n, bnc = W.bg_q[3], bnh = W.bg_q[3] + 2;
-    for (int e = lane; e < CT * CT; e += 32) {
-        const int rr = e / CT, c = e - rr * CT;
-        const int ii = i0 + rr, j = j0 + c;
-        if (ii >= P.res || j >= P.ny) continue;
-        const float h = W.hs[rr + 1][c + 1];
-        float hx, hy;
-        if (ii == 0) hx = (W.hs[rr + 2][c + 1] - h) * inv_s;
-        else if (ii == P.res - 1) hx = (h - W.hs[rr][c + 1]) * inv_s;
-        else hx = (W.hs[rr + 2][c + 1] - W.hs[rr][c + 1]) * inv_2s;
-        if (j == 0) hy = (W.hs[rr + 1][c + 2] - h) * inv_s;
-        else if (j == P.ny - 1) hy = (h - W.hs[rr + 1][c]) * inv_s;
-        else hy = (W.hs[rr + 1][c + 2] - W.hs[rr + 1][c]) * inv_2s;
+    const int bn = a.bg_n;
+    for (int e = tid; e < CT * CT; e += NT) {
+        const int rr = e / CT, cc = e - rr * CT;
+        const int ii = i0 + rr, jj = j0 + cc;
+        if (ii >= P.res || jj >= P.ny) continue;
+        const float h = W.u1.hs[rr + 1][cc + 1];
+        const float hu = ii == P.res - 1 ? h : W.u1.hs[rr + 2][cc + 1];
+        const float hd = ii == 0 ? h : W.u1.hs[rr][cc + 1];
+        const float hr = jj == P.ny - 1 ? h : W.u1.hs[rr + 1][cc + 2];
+        const float hl = jj == 0 ? h : W.u1.hs[rr + 1][cc];
+        const float hx = (hu - hd) * ((ii == 0 || ii == P.res - 1) ? inv_s : inv_2s);
+        const float hy = (hr - hl) * ((jj == 0 || jj == P.ny - 1) ? inv_s : inv_2s);
         const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
         const float pnx = -hx * rn, pny = -hy * rn, pnz = rn;
-        const long long o = gb + (long long)ii * P.ny + j;
+        const long long o = gb + (long long)ii * P.ny + jj;
         if (a.patch_height) a.patch_height[o] = h;
         if (a.patch_normal) { a.patch_normal[3 * o] = pnx; a.patch_normal[3 * o + 1] = pny; a.patch_normal[3 * o + 2] = pnz; }
-        if (ii >= inset && ii < P.res - inset && j >= inset && j < P.ny - inset) {
-            accv += (double)h * (double)h;
+        if (ii >= inset && ii < P.res - inset && jj >= inset && jj < P.ny - inset) {
+            accv = fma((double)h, (double)h, accv);
             ++cnt;
         }
         if (a.blend_mode) {
             float hb = 0.f, nx = 0.f, ny = 0.f, nz = 1.f;
             if (have_bg) {
-                const float fu = W.row_fu[rr], fv = W.col_fv[c];
-                const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
-                const int q0 = W.row_q0[rr], q1 = W.row_q1[rr], p0 = W.col_q0[c], p1 = W.col_q1[c];
+                const float fv = W.col_fv[cc];
                 if (bg_staged) {
-                    hb = W.bgh[(q0 + 1) * bnh + p0 + 1] * w00 + W.bgh[(q1 + 1) * bnh + p0 + 1] * w10
-                       + W.bgh[(q0 + 1) * bnh + p1 + 1] * w01 + W.bgh[(q1 + 1) * bnh + p1 + 1] * w11;
-                    const int a00 = q0 * bnc + p0, a10 = q1 * bnc + p0, a01 = q0 * bnc + p1, a11 = q1 * bnc + p1;
-                    nx = W.bgn[3 * a00] * w00 + W.bgn[3 * a10] * w10 + W.bgn[3 * a01] * w01 + W.bgn[3 * a11] * w11;
-                    ny = W.bgn[3 * a00 + 1] * w00 + W.bgn[3 * a10 + 1] * w10 + W.bgn[3 * a01 + 1] * w01 + W.bgn[3 * a11 + 1] * w11;
-                    nz = W.bgn[3 * a00 + 2] * w00 + W.bgn[3 * a10 + 2] * w10 + W.bgn[3 * a01 + 2] * w01 + W.bgn[3 * a11 + 2] * w11;
+                    const int p0 = W.col_p0[cc];
+                    const float4 t0 = W.u2.trow[rr][p0], t1 = W.u2.trow[rr][p0 + 1];
+                    hb = lerpf(t0.x, t1.x, fv);
+                    nx = lerpf(t0.y, t1.y, fv); ny = lerpf(t0.z, t1.z, fv); nz = lerpf(t0.w, t1.w, fv);
                 } else {
+                    const double u = (P.x0 + (double)ii * P.texel) * inv_sp, fl = floor(u);
+                    const float fu = (float)(u - fl);
+                    const int q0 = (int)((long long)fl & bm), q1 = (q0 + 1) & bm;
+                    const int p0 = W.col_p0[cc], p1 = (p0 + 1) & bm;
+                    const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
                     const float* B = a.bg_height;
                     hb = B[(long long)q0 * bn + p0] * w00 + B[(long long)q1 * bn + p0] * w10
                        + B[(long long)q0 * bn + p1] * w01 + B[(long long)q1 * bn + p1] * w11;
@@ -326,16 +370,16 @@ __global__ void __launch_bounds__(32 * WPB) compose_kernel(HsComposeArgs a) {
                     ny = n00.y * w00 + n10.y * w10 + n01.y * w01 + n11.y * w11;
                     nz = n00.z * w00 + n10.z * w10 + n01.z * w01 + n11.z * w11;
                 }
-                const float rr2 = rsqrtf(nx * nx + ny * ny + nz * nz);
-                nx *= rr2; ny *= rr2; nz *= rr2;
+                const float r2 = rsqrtf(nx * nx + ny * ny + nz * nz);
+                nx *= r2; ny *= r2; nz *= r2;
             }
-            const float d = fminf(W.row_d[rr], W.col_d[c]);
+            const float d = fminf(W.row_d[rr], W.col_d[cc]);
             if (d > 0.f) {
                 const float w = smoothstep01(d * inv_margin);
-                hb = w * h + (1.f - w) * hb;
-                const float mx = w * pnx + (1.f - w) * nx, my = w * pny + (1.f - w) * ny, mz = w * pnz + (1.f - w) * nz;
-                const float rr2 = rsqrtf(mx * mx + my * my + mz * mz);
-                nx = mx * rr2; ny = my * rr2; nz = mz * rr2;
+                hb = lerpf(hb, h, w);
+                const float mx = lerpf(nx, pnx, w), my = lerpf(ny, pny, w), mz = lerpf(nz, pnz, w);
+                const float r2 = rsqrtf(mx * mx + my * my + mz * mz);
+                nx = mx * r2; ny = my * r2; nz = mz * r2;
             }
             if (a.blend_height) a.blend_height[o] = hb;
             if (a.blend_normal) { a.blend_normal[3 * o] = nx; a.blend_normal[3 * o + 1] = ny; a.blend_normal[3 * o + 2] = nz; }
@@ -344,9 +388,17 @@ __global__ void __launch_bounds__(32 * WPB) compose_kernel(HsComposeArgs a) {
     if (a.interior_sumsq) {
         accv = warp_sum(accv);
         cnt = warp_sum(cnt);
-        if (lane == 0 && cnt) {
-            atomicAdd(&a.interior_sumsq[p], accv);
-            if (a.interior_count) atomicAdd((unsigned long long*)&a.interior_count[p], (unsigned long long)cnt);
+        if (lane == 0) { W.red[wid] = accv; W.redc[wid] = cnt; }
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            int n = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) { s += W.red[w]; n += W.redc[w]; }
+            if (n) {
+                atomicAdd(&a.interior_sumsq[p], s);
+                if (a.interior_count) atomicAdd((unsigned long long*)&a.interior_count[p], (unsigned long long)n);
+            }
         }
     }
 }
@@ -365,7 +417,12 @@ extern "C" int hs_compose(const HsComposeArgs* a, void* stream) {
     HS_CHECK_ARG(a->patches && a->layers && a->smooth_layers && a->tile_info, "hs_compose: missing buffer");
     HS_CHECK_ARG(!a->blend_mode || a->bg_height == nullptr || (a->bg_n >= 2 && (a->bg_n & (a->bg_n - 1)) == 0),
                  "hs_compose: background size must be a power of two");
-    compose_kernel<<<(a->total_tiles + WPB - 1) / WPB, 32 * WPB, 0, as_stream(stream)>>>(*a);
+    static bool carve = false;
+    if (!carve) {   // the whole 228 KB as shared memory: 9 tiles per SM
+        HS_CUDA(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        carve = true;
+    }
+    compose_kernel<<<a->total_tiles, NT, compose_smem_bytes(a->nb), as_stream(stream)>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }
