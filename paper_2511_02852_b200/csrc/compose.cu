@@ -25,7 +25,9 @@ constexpr int NT = 32 * NW;
 constexpr int RPW = CH / NW;      // haloed rows per warp in the height pass
 constexpr int BG_CAP = 8;         // staged background footprint per axis (+1 halo each side)
 constexpr int CS_CTA = 1536;      // floats of staged coarse footprints per tile
-constexpr int TC_CAP = 2560;      // floats of row-interpolated coarse rows per tile (32 per coarse row)
+constexpr int TCP = CH + 1;       // tc row pitch: lanes on different coarse rows, same column -> distinct banks
+constexpr int TC_CAP = 88 * TCP;  // floats of row-interpolated coarse rows per tile (88 rows)
+constexpr int CPT = CH / NW;      // haloed columns per thread in the coarse pass (thread = haloed row)
 
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
 
@@ -53,10 +55,8 @@ struct LayerPlan {
 };
 
 struct TileSmem {
-    union {
-        float cs[CS_CTA];             // staged coarse footprints (until the tc table is built)
-        float hs[CH][CH + 1];         // haloed patch heights (after the height pass)
-    } u1;
+    float cs[CS_CTA];                 // staged coarse footprints (until the tc table is built)
+    float hs[CH][CH + 1];             // haloed patch heights
     union {
         float tc[TC_CAP];             // coarse rows of every layer interpolated at the 32 haloed columns
         float4 trow[CT][BG_CAP];      // background (h, nx, ny, nz) x-lerped per output row (epilogue)
@@ -69,11 +69,10 @@ struct TileSmem {
     int redc[NW];
     // dynamic tail, nb entries each:
     //   LayerPlan pl[nb];
-    //   int2 rowt[nb][CH]   per layer and haloed row: tc offsets of rows r, r+1 (16 bit each), g1
 };
 
 __host__ __device__ constexpr size_t compose_smem_bytes(int nb) {
-    return sizeof(TileSmem) + (size_t)nb * (sizeof(LayerPlan) + CH * sizeof(int2));
+    return sizeof(TileSmem) + (size_t)nb * sizeof(LayerPlan);
 }
 
 // background footprint of an output tile: first node and node count per
@@ -105,7 +104,6 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
     TileSmem& W = *reinterpret_cast<TileSmem*>(smem_raw);
     const int nb = a.nb;
     LayerPlan* const Wpl = reinterpret_cast<LayerPlan*>(smem_raw + sizeof(TileSmem));
-    int2 (*const Wrowt)[CH] = reinterpret_cast<int2 (*)[CH]>(Wpl + nb);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int tile = blockIdx.x;
     if (a.frame_advance && tile == 0 && tid == 0) *a.frame_advance += 1;
@@ -138,7 +136,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
                 pl.cc0 = jlo / L.f;
                 pl.ncol = min(jhi / L.f + 1, L.ncy - 1) - pl.cc0 + 1;
                 need_cs = pl.nr * pl.ncol;
-                need_tc = pl.nr * CH;
+                need_tc = pl.nr * TCP;
             }
         }
         const int inc_cs = warp_incl_scan(need_cs, lane);
@@ -189,7 +187,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         const float inv_nc = 1.f / (float)L.ncol;
         for (int e = tid; e < L.nr * L.ncol; e += NT) {
             const int rr = fdiv(e, inv_nc) , cc = e - rr * L.ncol;
-            cp_async4(W.u1.cs + L.cs_off + e, Sg + (long long)rr * L.ncy + cc, true);
+            cp_async4(W.cs + L.cs_off + e, Sg + (long long)rr * L.ncy + cc, true);
         }
     }
     // f == 1 layers straight into the accumulators (lane = haloed column, coalesced rows)
@@ -211,8 +209,17 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
     }
     cp_async_wait_all();
     __syncthreads();
-    // tables: tc[b][r][c] = coarse row r of layer b lerped at haloed column c;
-    // rowt[b][q] = (rows r, r+1 of haloed row q, g1 = gain * wi)
+    // f == 1 sum to shared memory; the coarse pass below picks it up transposed
+    {
+        const int jr = jb + c;
+        const bool jok = jr >= 0 && jr < P.ny;
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int ii = ib + qb + k;
+            W.hs[qb + k][c] = (jok && ii >= 0 && ii < P.res) ? acc[k] : 0.f;
+        }
+    }
+    // tc[b][r][c] = coarse row r of layer b lerped at haloed column c (x-first bilinear, :270-273)
     for (int b = 0; b < nb; ++b) {
         const LayerPlan& L = Wpl[b];
         if (L.tc_off < 0) continue;
@@ -220,59 +227,48 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         const int cj = fdiv(jj, L.inv_f);
         const int d1 = min(cj + 1, L.ncy - 1) - cj;
         const float wj = (float)(jj - cj * L.f) * L.inv_f;
-        const float* src = W.u1.cs + L.cs_off + (cj - L.cc0);
+        const float* src = W.cs + L.cs_off + (cj - L.cc0);
         for (int r = tid >> 5; r < L.nr; r += NW)
-            W.u2.tc[L.tc_off + r * CH + (tid & 31)] = lerpf(src[r * L.ncol], src[r * L.ncol + d1], wj);
-    }
-    for (int e = tid; e < nb * CH; e += NT) {
-        const int b = e >> 5, q = e & 31;
-        const LayerPlan& L = Wpl[b];
-        if (L.f == 1) continue;
-        const int ii = min(max(ib + q, 0), P.res - 1);
-        const int ci = fdiv(ii, L.inv_f);
-        const float wi = (float)(ii - ci * L.f) * L.inv_f;
-        const int cr0 = L.tc_off >= 0 ? L.cr0 : 0;
-        const int r = ci - cr0;
-        const int rn = min(ci + 1, L.ncx - 1) - cr0;
-        Wrowt[b][q] = make_int2((L.tc_off + r * CH) | ((L.tc_off + rn * CH) << 16), __float_as_int(L.gain * wi));
+            W.u2.tc[L.tc_off + r * TCP + (tid & 31)] = lerpf(src[r * L.ncol], src[r * L.ncol + d1], wj);
     }
     __syncthreads();
-    // ---- heights: acc[k] = haloed row qb + k at haloed column c ----
-    for (int b = 0; b < nb; ++b) {
-        const LayerPlan& L = Wpl[b];
-        if (L.f == 1) continue;
-        const float gain = L.gain;
-        if (L.tc_off >= 0) {
-            const float* T = W.u2.tc + c;
+    // ---- coarse layers: thread = haloed row q, columns c0 .. c0+7; per layer the
+    // row weights are formed once and each texel costs two table reads ----
+    {
+        const int q = lane, c0 = CPT * wid;
+        const int ii = min(max(ib + q, 0), P.res - 1);
+        float h[CPT];
 #pragma unroll
-            for (int k = 0; k < RPW; ++k) {
-                const int2 e = Wrowt[b][qb + k];
-                const float g1 = __int_as_float(e.y);
-                acc[k] = fmaf(gain - g1, T[e.x & 0xffff], fmaf(g1, T[e.x >> 16], acc[k]));
-            }
-        } else {                                   // layer not tabulated: rows from global (rare)
-            const float* Sg = a.smooth_layers + L.sm_off;
-            const int cj = fdiv(j, L.inv_f), cj1 = min(cj + 1, L.ncy - 1);
-            const float wj = (float)(j - cj * L.f) * L.inv_f;
+        for (int k = 0; k < CPT; ++k) h[k] = W.hs[q][c0 + k];
+        for (int b = 0; b < nb; ++b) {
+            const LayerPlan& L = Wpl[b];
+            if (L.f == 1) continue;
+            const int ci = fdiv(ii, L.inv_f);
+            const float g1 = L.gain * ((float)(ii - ci * L.f) * L.inv_f);
+            const float g0 = L.gain - g1;
+            const int ci1 = min(ci + 1, L.ncx - 1);
+            if (L.tc_off >= 0) {
+                const float* T0 = W.u2.tc + L.tc_off + (ci - L.cr0) * TCP + c0;
+                const float* T1 = W.u2.tc + L.tc_off + (ci1 - L.cr0) * TCP + c0;
 #pragma unroll
-            for (int k = 0; k < RPW; ++k) {
-                const int2 e = Wrowt[b][qb + k];
-                const float g1 = __int_as_float(e.y);
-                const int ii = min(max(ib + qb + k, 0), P.res - 1);
-                const int r0 = fdiv(ii, L.inv_f), r1 = min(r0 + 1, L.ncx - 1);
-                const float* R0 = Sg + (long long)r0 * L.ncy;
-                const float* R1 = Sg + (long long)r1 * L.ncy;
-                acc[k] = fmaf(gain - g1, lerpf(R0[cj], R0[cj1], wj), fmaf(g1, lerpf(R1[cj], R1[cj1], wj), acc[k]));
+                for (int k = 0; k < CPT; ++k) h[k] = fmaf(g0, T0[k], fmaf(g1, T1[k], h[k]));
+            } else {                               // layer not tabulated: rows from global (rare)
+                const float* R0 = a.smooth_layers + L.sm_off + (long long)ci * L.ncy;
+                const float* R1 = a.smooth_layers + L.sm_off + (long long)ci1 * L.ncy;
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const int jj = min(max(jb + c0 + k, 0), P.ny - 1);
+                    const int cj = fdiv(jj, L.inv_f), cj1 = min(cj + 1, L.ncy - 1);
+                    const float wj = (float)(jj - cj * L.f) * L.inv_f;
+                    h[k] = fmaf(g0, lerpf(R0[cj], R0[cj1], wj), fmaf(g1, lerpf(R1[cj], R1[cj1], wj), h[k]));
+                }
             }
         }
-    }
-    {
-        const int jr = jb + c;
-        const bool jok = jr >= 0 && jr < P.ny;
+        const bool iok = ib + q >= 0 && ib + q < P.res;
 #pragma unroll
-        for (int k = 0; k < RPW; ++k) {
-            const int ii = ib + qb + k;
-            W.u1.hs[qb + k][c] = (jok && ii >= 0 && ii < P.res) ? acc[k] : 0.f;
+        for (int k = 0; k < CPT; ++k) {
+            const int jr = jb + c0 + k;
+            W.hs[q][c0 + k] = (iok && jr >= 0 && jr < P.ny) ? h[k] : 0.f;
         }
     }
     __syncthreads();                               // tc dead: trow may overwrite it
@@ -321,11 +317,11 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         const int rr = e / CT, cc = e - rr * CT;
         const int ii = i0 + rr, jj = j0 + cc;
         if (ii >= P.res || jj >= P.ny) continue;
-        const float h = W.u1.hs[rr + 1][cc + 1];
-        const float hu = ii == P.res - 1 ? h : W.u1.hs[rr + 2][cc + 1];
-        const float hd = ii == 0 ? h : W.u1.hs[rr][cc + 1];
-        const float hr = jj == P.ny - 1 ? h : W.u1.hs[rr + 1][cc + 2];
-        const float hl = jj == 0 ? h : W.u1.hs[rr + 1][cc];
+        const float h = W.hs[rr + 1][cc + 1];
+        const float hu = ii == P.res - 1 ? h : W.hs[rr + 2][cc + 1];
+        const float hd = ii == 0 ? h : W.hs[rr][cc + 1];
+        const float hr = jj == P.ny - 1 ? h : W.hs[rr + 1][cc + 2];
+        const float hl = jj == 0 ? h : W.hs[rr + 1][cc];
         const float hx = (hu - hd) * ((ii == 0 || ii == P.res - 1) ? inv_s : inv_2s);
         const float hy = (hr - hl) * ((jj == 0 || jj == P.ny - 1) ? inv_s : inv_2s);
         const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
