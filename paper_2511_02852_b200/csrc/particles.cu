@@ -61,15 +61,27 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         n_emit[c] = (int)fl;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        gstart[0] = 0;
-        for (int c = 0; c < ncell; ++c) gstart[c + 1] = gstart[c] + n_emit[c];
-        for (int b = 0; b < nb; ++b) {
-            long long s = n_emit[4 * b] + n_emit[4 * b + 1] + n_emit[4 * b + 2] + n_emit[4 * b + 3];
-            a.groups[(size_t)p * nb + b] += s;
+    if (threadIdx.x < 32) {
+        // cell prefix (cell = 4 b + side): lane b owns bucket b's four cells
+        const int lane = threadIdx.x;
+        int e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+        if (lane < nb) { e0 = n_emit[4 * lane]; e1 = n_emit[4 * lane + 1]; e2 = n_emit[4 * lane + 2]; e3 = n_emit[4 * lane + 3]; }
+        const int sb = e0 + e1 + e2 + e3;
+        const int inc = warp_incl_scan(sb, lane);
+        if (lane < nb) {
+            const int g0 = inc - sb;
+            gstart[4 * lane] = g0;
+            gstart[4 * lane + 1] = g0 + e0;
+            gstart[4 * lane + 2] = g0 + e0 + e1;
+            gstart[4 * lane + 3] = g0 + e0 + e1 + e2;
+            a.groups[(size_t)p * nb + lane] += sb;
         }
-        abort_s = (long long)gstart[ncell] * nth > a.member_capacity;
-        if (abort_s) atomicOr(a.status, HS_STATUS_STAGE_OVERFLOW);
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) {
+            gstart[ncell] = tot;
+            abort_s = (long long)tot * nth > a.member_capacity;
+            if (abort_s) atomicOr(a.status, HS_STATUS_STAGE_OVERFLOW);
+        }
     }
     __syncthreads();
     const int g_tot = gstart[ncell];
@@ -85,7 +97,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     const unsigned long long D = rng[6];
     // member (energy, amplitude) pairs: shared memory when they fit (the
     // per-bucket sums below walk them serially), global scratch otherwise
-    __shared__ double scr_sm[2 * INJ_SMEM_MEMBERS];
+    __shared__ __align__(16) double scr_sm[2 * INJ_SMEM_MEMBERS];
     double* scr = M <= INJ_SMEM_MEMBERS ? scr_sm : a.scratch + (size_t)p * a.member_capacity * 2;
 
     // 2. amplitudes + booked energy for every member  (particles.py:256-264, 291-292)
@@ -104,29 +116,43 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         scr[2 * m + 1] = amp;
     }
     __syncthreads();
-    // 3. per-bucket energy in member order (bincount order) and live counts
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        int m0 = gstart[4 * b] * nth, m1 = gstart[4 * b + 4] * nth;
+    // 3. per-bucket energy in member order (bincount order, a serial fp64 sum per
+    //    bucket: lane b walks bucket b, loads four ahead) and live counts; prefixes
+    const int per_live = a.beta != 0.0 ? 2 : 1;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
         double s = 0.0;
         int live = 0;
-        for (int m = m0; m < m1; ++m) {
-            s = dadd(s, scr[2 * m]);
-            live += scr[2 * m + 1] > 0.0;
+        if (lane < nb) {
+            const int m0 = gstart[4 * lane] * nth, m1 = gstart[4 * lane + 4] * nth;
+            int m = m0;
+            for (; m + 4 <= m1; m += 4) {
+                const double2 v0 = *reinterpret_cast<const double2*>(scr + 2 * m);
+                const double2 v1 = *reinterpret_cast<const double2*>(scr + 2 * m + 2);
+                const double2 v2 = *reinterpret_cast<const double2*>(scr + 2 * m + 4);
+                const double2 v3 = *reinterpret_cast<const double2*>(scr + 2 * m + 6);
+                s = dadd(dadd(dadd(dadd(s, v0.x), v1.x), v2.x), v3.x);
+                live += (v0.y > 0.0) + (v1.y > 0.0) + (v2.y > 0.0) + (v3.y > 0.0);
+            }
+            for (; m < m1; ++m) {
+                s = dadd(s, scr[2 * m]);
+                live += scr[2 * m + 1] > 0.0;
+            }
+            a.e_in[(size_t)p * nb + lane] = dadd(a.e_in[(size_t)p * nb + lane], s);
+            live_cnt[lane] = live;
         }
-        a.e_in[(size_t)p * nb + b] = dadd(a.e_in[(size_t)p * nb + b], s);
-        live_cnt[b] = live;
-    }
-    __syncthreads();
-    const int per_live = a.beta != 0.0 ? 2 : 1;
-    if (threadIdx.x == 0) {
-        live_before[0] = 0;
-        soff[0] = 0;
-        for (int b = 0; b < nb; ++b) {
-            live_before[b + 1] = live_before[b] + live_cnt[b];
-            soff[b + 1] = soff[b] + per_live * live_cnt[b];
+        const int inc = warp_incl_scan(live, lane);
+        if (lane < nb) {
+            live_before[lane + 1] = inc;
+            soff[lane + 1] = per_live * inc;
         }
-        abort_s = soff[nb] > P.stage_capacity;
-        if (abort_s) atomicOr(a.status, HS_STATUS_STAGE_OVERFLOW);
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) {
+            live_before[0] = 0;
+            soff[0] = 0;
+            abort_s = per_live * tot > P.stage_capacity;
+            if (abort_s) atomicOr(a.status, HS_STATUS_STAGE_OVERFLOW);
+        }
     }
     __syncthreads();
     if (abort_s) {
@@ -536,6 +562,27 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_count_kernel(HsAdvectArgs 
     __shared__ int wsum[ADV_THREADS / 32];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // the scatter kernel's accumulators, cleared here instead of by memset nodes
+    {
+        const long long gt = (long long)blockIdx.x * ADV_THREADS + threadIdx.x;
+        const long long nthreads = (long long)gridDim.x * ADV_THREADS;
+        const long long ncnt = (long long)a.n_patches * a.nb;
+        if (gt < ncnt) {
+            a.out_count[gt] = 0;
+            if (a.dropped.x) a.dropped_count[gt] = 0;
+        }
+        if (a.splat) {
+            float* r = a.raw_layers;
+            const long long n = a.raw_layers_len;
+            const long long head = min(n, (long long)((16 - ((size_t)r & 15)) & 15) / 4);
+            if (gt < head) r[gt] = 0.f;
+            float4* r4 = reinterpret_cast<float4*>(r + head);
+            const long long n4 = (n - head) / 4;
+            for (long long k = gt; k < n4; k += nthreads) r4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const long long tail = head + n4 * 4;
+            if (gt < n - tail) r[tail + gt] = 0.f;
+        }
+    }
     const bool live = adv_setup(a, T, tile);
     unsigned* words = a.keep_words + (size_t)tile * (ADV_ITEMS * ADV_THREADS / 32);
     if (!live) {
@@ -703,12 +750,22 @@ extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
                  a->tile_counter && a->status, "hs_advect: missing buffer");
     HS_CHECK_ARG(!a->splat || (a->raw_layers && a->layers), "hs_advect: splat needs layers");
     cudaStream_t st = as_stream(stream);
-    HS_CUDA(cudaMemsetAsync(a->out_count, 0, sizeof(int) * (size_t)a->n_patches * a->nb, st));
-    if (a->dropped.x) {
+    if (a->dropped.x)
         HS_CHECK_ARG(a->dropped_count && a->dropped.y && a->dropped.ux && a->dropped.uy && a->dropped.amp,
                      "hs_advect: incomplete dropped pool");
-        HS_CUDA(cudaMemsetAsync(a->dropped_count, 0, sizeof(int) * (size_t)a->n_patches * a->nb, st));
+    if (a->keep_words) {
+        // count kernel: clears out/dropped counts and the raw layers, writes every tile's
+        // state; scatter kernel: tiles of every patch, 1024 items each (empty tiles exit at once)
+        HS_CHECK_ARG((long long)a->max_tiles * ADV_THREADS >= (long long)a->n_patches * a->nb,
+                     "hs_advect: max_tiles too small");
+        advect_count_kernel<<<a->max_tiles, ADV_THREADS, 0, st>>>(*a);
+        HS_LAUNCH_CHECK();
+        advect_scatter_kernel<<<a->max_tiles, ADV_THREADS, 0, st>>>(*a);
+        HS_LAUNCH_CHECK();
+        return 0;
     }
+    HS_CUDA(cudaMemsetAsync(a->out_count, 0, sizeof(int) * (size_t)a->n_patches * a->nb, st));
+    if (a->dropped.x) HS_CUDA(cudaMemsetAsync(a->dropped_count, 0, sizeof(int) * (size_t)a->n_patches * a->nb, st));
     HS_CUDA(cudaMemsetAsync(a->tile_state, 0, sizeof(unsigned long long) * (size_t)a->max_tiles, st));
     HS_CUDA(cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st));
     if (a->splat) HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
@@ -720,14 +777,6 @@ extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
         HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, advect_kernel<4>, ADV_THREADS, 0));
         if (occ1 < 1) occ1 = 1;
         if (occ4 < 1) occ4 = 1;
-    }
-    if (a->keep_words) {
-        // tiles of every patch, 1024 items each (empty tiles exit at once)
-        advect_count_kernel<<<a->max_tiles, ADV_THREADS, 0, st>>>(*a);
-        HS_LAUNCH_CHECK();
-        advect_scatter_kernel<<<a->max_tiles, ADV_THREADS, 0, st>>>(*a);
-        HS_LAUNCH_CHECK();
-        return 0;
     }
     const int occ = chunks == 4 ? occ4 : occ1;
     const int grid = num_sms() * occ;
