@@ -131,6 +131,8 @@ typedef struct {
     float* normal;            /* [n*n*3] or NULL */
     double* sumsq;            /* scalar, set to sum(height^2) (zeroed by this call), or NULL */
     long long* frame_advance; /* optional: device frame counter, += 1 after the transform */
+    const double* omega;      /* optional [(n/2+1)^2] dispersion sqrt(g |k|) at (|i|, |j|) =
+                                 (min(i, n-i), min(j, n-j)); NULL: formed per bin each call */
 } HsFftArgs;
 HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
 

@@ -53,7 +53,8 @@ class HsFftArgs(C.Structure):
     _fields_ = [("n", i32), ("emit_normals", i32), ("g", dbl), ("t", dbl), ("choppiness", dbl),
                 ("frame_ptr", vp), ("dt", dbl), ("spacing", dbl), ("kf", vp), ("h0", vp),
                 ("twiddle", vp), ("work_a", vp), ("work_b", vp), ("height", vp), ("dx", vp),
-                ("dy", vp), ("normal", vp), ("sumsq", vp), ("frame_advance", vp)]
+                ("dy", vp), ("normal", vp), ("sumsq", vp), ("frame_advance", vp),
+                ("omega", vp)]
 
 
 class HsInjectArgs(C.Structure):

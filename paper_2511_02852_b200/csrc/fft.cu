@@ -78,6 +78,7 @@ struct FftDev {
     const long long* frame_ptr;
     double* sumsq_zero;
     const double* kf;
+    const double* omega;      // [(n/2+1)^2] or NULL
     const float2* h0;
     const float2* tw;
     float2* wa;
@@ -253,24 +254,32 @@ __device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0,
     const int n = d.n, half = n >> 1;
     const int jm = (n - j) & (n - 1);
     const double kxi = d.kf[i], kxip = d.kf[ip], kyj = d.kf[j];
-    const double km = hypot(kxi, kyj);
-    const double w = sqrt(d.g * km);
+    double w;
+    if (d.omega) {   // host table, numpy's sqrt(g hypot(kx, ky)) (fft_background.py:40-47)
+        const int ia = i <= half ? i : n - i, ja = j <= half ? j : n - j;
+        w = __ldg(d.omega + (size_t)ia * (half + 1) + ja);
+    } else {
+        w = sqrt(d.g * sqrt(fma(kxi, kxi, kyj * kyj)));
+    }
     const double two_pi = 6.283185307179586476925286766559;
     double ph = w * t;
-    ph -= two_pi * rint(ph * (1.0 / two_pi));       // reduce in fp64 before the fp32 sincos (App. B.2)
+    ph -= two_pi * rint(ph * (1.0 / two_pi));       // reduce in fp64, |ph| <= pi (App. B.2)
     float s, c;
-    sincosf((float)ph, &s, &c);
+    __sincosf((float)ph, &s, &c);                   // |err| < 4e-7 on [-pi, pi]
     const float2 rot = make_float2(c, -s), rotc = make_float2(c, s);
     const float2 hh0 = cadd(cmul(r0[j], rot), cmul(cconj(r1[jm]), rotc));
     const float2 hh1 = cadd(cmul(r1[j], rot), cmul(cconj(r0[jm]), rotc));
     const bool sc = ((i == 0) || (i == half)) && (j == 0 || j == half);   // self-conjugate bin
-    const double kinv = km > 0.0 ? 1.0 / km : 1.0;
     if (d.chop_on) {
-        const float fa = sc ? 1.f : (float)(1.0 + d.chop * kxi * kinv);
+        // lambda k / |k| only scales fp32 values: fp32 reciprocal
+        const float wf = (float)w;
+        const float kinv = wf > 0.f ? (float)d.g / (wf * wf) : 1.f;    // 1/|k| = g / w^2
+        const float ch = (float)d.chop;
+        const float fa = sc ? 1.f : 1.f + ch * (float)kxi * kinv;
         A0 = make_float2(hh0.x * fa, hh0.y * fa);
-        const float fb = sc ? 0.f : (float)(d.chop * kyj * kinv);
+        const float fb = sc ? 0.f : ch * (float)kyj * kinv;
         B0 = make_float2(fb * hh0.y, -fb * hh0.x);
-        const float fa1 = (float)(1.0 + d.chop * kxip * kinv);
+        const float fa1 = 1.f + ch * (float)kxip * kinv;
         A1 = make_float2(hh1.x * fa1, hh1.y * fa1);
     } else {
         A0 = hh0;
@@ -281,7 +290,7 @@ __device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0,
 
 template <int N>
 __global__ void fft_rows_reg_kernel(FftDev d) {
-    constexpr int T = N / 16, NP = N + N / 32;
+    constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
     extern __shared__ float2 sm[];
     float2* tw = sm;            // N
     float2* r0 = tw + N;        // h0 row i
@@ -321,7 +330,7 @@ __global__ void fft_rows_reg_kernel(FftDev d) {
 // the rest do B (two real dy columns per transform)
 template <int N, int CT>
 __global__ void fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
-    constexpr int T = N / 16, NP = N + N / 32;
+    constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
     extern __shared__ float2 sm[];
     __shared__ double red[32];
     float2* tw = sm;
@@ -393,8 +402,10 @@ __global__ void fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
 
 template <int N>
 int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
-    constexpr int T = N / 16, NP = N + N / 32;
-    constexpr int CT = (512 / T) < N / 2 ? (512 / T) : N / 2;   // transforms per column CTA (B needs 2 CT <= N)
+    constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
+    // transforms per column CTA (B needs 2 CT <= N): 256 threads, so that the
+    // 1.5 N column transforms spread evenly over the SMs (all CTAs resident)
+    constexpr int CT = (256 / T) < 1 ? 1 : ((256 / T) < N / 2 ? (256 / T) : N / 2);
     const int rows_threads = 3 * T < 32 ? 32 : 3 * T;
     const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2);
     const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
@@ -443,6 +454,7 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     d.g = a->g; d.t = a->t; d.chop = a->choppiness; d.dt = a->dt; d.frame_ptr = a->frame_ptr;
     d.sumsq_zero = a->sumsq;
     d.kf = a->kf;
+    d.omega = a->omega;
     d.h0 = reinterpret_cast<const float2*>(a->h0);
     d.tw = reinterpret_cast<const float2*>(a->twiddle);
     d.wa = reinterpret_cast<float2*>(a->work_a);

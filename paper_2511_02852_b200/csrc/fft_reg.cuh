@@ -16,8 +16,11 @@
 
 namespace hs {
 
-// one float2 of padding per 32 elements keeps strided passes bank-friendly
-__device__ __forceinline__ int fpad(int i) { return i + (i >> 5); }
+// XOR swizzle of a transform's float2 slots: permutes within aligned groups
+// of 16 so that every pass's strided loads / stores and the digit-reversed
+// output read hit 16 distinct 8-byte bank pairs per half warp (model and
+// check: tools/fft_banks.py); no padding, the layout stays N slots
+__device__ __forceinline__ int fpad(int i) { return i ^ (((i >> 4) ^ (i >> 8)) & 15); }
 
 template <int N> struct FftPlan;
 // radices per pass; the product is N, every radix divides 16

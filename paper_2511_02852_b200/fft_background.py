@@ -43,6 +43,7 @@ class FftState:
     h0_dev: torch.Tensor = field(default=None, repr=False)
     kf_dev: torch.Tensor = field(default=None, repr=False)
     twiddle_dev: torch.Tensor = field(default=None, repr=False)
+    omega_dev: torch.Tensor = field(default=None, repr=False)
 
     @property
     def spacing(self) -> float:
@@ -80,6 +81,11 @@ def _upload(state: FftState, device) -> FftState:
     object.__setattr__(state, "h0_dev", torch.from_numpy(np.ascontiguousarray(h0)).to(dev))
     object.__setattr__(state, "kf_dev", torch.from_numpy(state.kf.copy()).to(dev))
     object.__setattr__(state, "twiddle_dev", torch.from_numpy(np.ascontiguousarray(tw)).to(dev))
+    # dispersion on the (|i|, |j|) quarter grid, the reference's own expression
+    # (fft_background.py:40-47); the kernel mirrors it over the four quadrants
+    kq = state.kf[: n // 2 + 1]
+    om = np.sqrt(state.g * np.hypot(kq[:, None], kq[None, :]))
+    object.__setattr__(state, "omega_dev", torch.from_numpy(np.ascontiguousarray(om)).to(dev))
     return state
 
 
@@ -191,7 +197,7 @@ def fft_args(state: FftState, ws: FftWorkspace, t: float = 0.0, frame_ptr=None, 
                        spacing=state.spacing, kf=N.ptr(state.kf_dev), h0=N.ptr(state.h0_dev),
                        twiddle=N.ptr(state.twiddle_dev), work_a=N.ptr(ws.work_a), work_b=N.ptr(ws.work_b),
                        height=N.ptr(ws.height), dx=N.ptr(ws.disp[0]), dy=N.ptr(ws.disp[1]),
-                       normal=N.ptr(ws.normal), sumsq=N.ptr(ws.sumsq))
+                       normal=N.ptr(ws.normal), sumsq=N.ptr(ws.sumsq), omega=N.ptr(state.omega_dev))
 
 
 def evolve_and_synthesize(state: FftState, t: float, *, normals: bool = True,
