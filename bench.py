@@ -298,12 +298,16 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = adv_bytes / (adv_ms * 1e-3) / 1e9 if adv_ms == adv_ms and adv_ms > 0 else None
+    # DRAM bytes per hs_advect call (count + scatter kernels) from the committed
+    # ncu launch list of this workload (tools/ncu_launches.sh -> tools/traffic_json.py)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "advect_dram_bytes.json")
+    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
+            ks = json.load(open(tp))["kernels"]
+            traffic = sum(ks[k]["dram_read_bytes"] + ks[k]["dram_write_bytes"]
+                          for k in ("advect_count_kernel", "advect_scatter_kernel"))
+        except (OSError, KeyError, ValueError):
             traffic = None
 
     cpu = None

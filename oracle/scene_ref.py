@@ -47,8 +47,10 @@ class OracleScene:
         self.res = list(sc["patch_res"])
         self.pools = [particles_ref.Pool() for _ in self.patches]
         self.ledgers = [particles_ref.Ledger(self.bk.n, rho=sc["rho"]) for _ in self.patches]
-        self.rngs = [np.random.Generator(np.random.Philox(key=[sc["seed"], i]))
-                     for i in range(len(self.patches))]
+        # key = (seed, global patch id): a patch's stream is the same whichever
+        # rank owns it (sharded runs pass their block's ids as "patch_ids")
+        ids = sc.get("patch_ids") or list(range(len(self.patches)))
+        self.rngs = [np.random.Generator(np.random.Philox(key=[sc["seed"], i])) for i in ids]
         self.plans = [synth_ref.plan(self.bk, pc.l1 / (r - 1), r, sc["amplitude_convention"],
                                      sc["trough_fraction"])
                       for pc, r in zip(self.patches, self.res)]

@@ -31,6 +31,19 @@ def partition(n_items: int, world: int) -> list[range]:
     return out
 
 
+def shard_config(cfg, rank: int, world: int):
+    """Rank `rank`'s share of a multi-patch scene: the config restricted to its
+    contiguous patch block, the global ids of those patches and their Philox
+    keys (seed, global id) -- pass the keys as `Simulation(rng_seed_keys=...)`
+    so every patch draws the same stream as in a single-process run."""
+    from dataclasses import replace
+    pcs = tuple(cfg.patches)
+    block = partition(len(pcs), world)[rank]
+    local = replace(cfg, patches=tuple(pcs[k] for k in block))
+    ids = list(block)
+    return local, ids, [(cfg.seed, k) for k in ids]
+
+
 def cascade_owner(cascade: int, world: int) -> int:
     """Round-robin owner of an FFT cascade (C4: 3 cascades on ranks 0-2)."""
     return cascade % world
@@ -39,9 +52,9 @@ def cascade_owner(cascade: int, world: int) -> int:
 def gather_tiles(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """All-gather equal-size flattened tiles: returns [world, numel]."""
     flat = local.reshape(-1).contiguous()
-    out = torch.empty((world, flat.numel()), dtype=flat.dtype, device=flat.device)
+    out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)   # flat: gloo and nccl
     dist.all_gather_into_tensor(out, flat, group=group)
-    return out
+    return out.view(world, flat.numel())
 
 
 def assemble(tiles: torch.Tensor, shapes: list[tuple[int, int]]) -> list[torch.Tensor]:
@@ -59,9 +72,9 @@ class TileGather:
         self.group = group
         res, ny = sim.synth.grids[0]
         self.shape = (res, ny)
-        self.out = torch.empty((world, res * ny), dtype=torch.float32, device=sim.device)
+        self.out = torch.empty(world * res * ny, dtype=torch.float32, device=sim.device)
 
     def exchange(self) -> torch.Tensor:
         h = self.sim.blended_tile(0)[0].reshape(-1)
         dist.all_gather_into_tensor(self.out, h, group=self.group)
-        return self.out
+        return self.out.view(self.world, -1)
