@@ -162,13 +162,14 @@ def reference_arm(args):
     for _ in range(n_warm):                       # same warm-up as the GPU arm, no synthesis
         sc.step(dt=WARM_DT, synth=False, fft=False)
     warm_s = time.perf_counter() - t_warm
-    for _ in range(min(args.warmup, 1)):
+    n_w = 3                                       # W >= 3 untimed full frames (~1 s each at C3: bounded)
+    for _ in range(n_w):
         sc.step()
     budget = 90.0
     frame_s, live, n = time_cpu_frames(sc, seconds=budget, min_frames=1, max_frames=max(1, args.steps))
     pps = live / frame_s
     line = {"impl": "reference", "metric": "particles splatted/s (hybrid step)", "value": pps,
-            "unit": "particles/s", "n_gpus": args.gpus, "steps": n, "warmup": min(args.warmup, 1),
+            "unit": "particles/s", "n_gpus": args.gpus, "steps": n, "warmup": n_w,
             "ms_per_step": frame_s * 1e3, "fps": 1.0 / frame_s, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, steady state via the step itself)",
             "config": {"workload": f"{args.config} hybrid step", "live_particles": live, "fft_n": cfg.fft_n,
