@@ -85,7 +85,7 @@ typedef struct {
 
 /* One per (patch, bucket) synthesis layer (LayerPlan, patch_synthesis.py:227-258). */
 typedef struct {
-    long long raw_off;   /* float offset of the padded raw layer (wx*wy) */
+    long long raw_off;   /* float offset of the padded raw layer (wx rows of raw_pitch), multiple of 4 */
     long long sm_off;    /* float offset of the smoothed crop (ncx*ncy) */
     int f;               /* decimation factor */
     int H;               /* kernel half width (taps 2H+1) */
@@ -95,6 +95,9 @@ typedef struct {
     int taps_off;        /* offset into the taps array */
     float gain;          /* output gain */
     int mid_off;         /* float offset into HsSmoothArgs.mid (wide kernels), -1 otherwise */
+    int raw_pitch;       /* raw row pitch in floats: >= wy, multiple of 4 (16-byte rows for
+                            the splat's vector reductions); columns >= wy stay zero */
+    int pad1;
 } HsLayer;
 
 /* Structure-of-arrays particle pool.  Pools of all patches live in one set of

@@ -99,10 +99,11 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
             wide = k.half_width > N.HS_SMOOTH_FUSED_MAX_H
             if wide and k.half_width > 780:
                 raise ConfigError(f"kernel half width {k.half_width} exceeds the device limit of 780 texels")
+            pitch = -(-wy // 4) * 4                  # 16-byte rows (vector splat reductions)
             layers.append(N.HsLayer(raw_off, sm_off, f, k.half_width, pad, ncx, ncy, wx, wy, tap_off,
-                                    float(k.gain), mid_off if wide else -1))
+                                    float(k.gain), mid_off if wide else -1, pitch, 0))
             taps.append(np.asarray(k.taps, dtype=np.float32))
-            raw_off += wx * wy
+            raw_off += wx * pitch                     # stays a multiple of 4
             sm_off += ncx * ncy
             tap_off += len(k.taps)
             if wide:

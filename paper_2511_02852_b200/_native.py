@@ -42,7 +42,7 @@ class HsPatch(C.Structure):
 class HsLayer(C.Structure):
     _fields_ = [("raw_off", i64), ("sm_off", i64), ("f", i32), ("H", i32), ("pad", i32), ("ncx", i32),
                 ("ncy", i32), ("wx", i32), ("wy", i32), ("taps_off", i32), ("gain", C.c_float),
-                ("mid_off", i32)]
+                ("mid_off", i32), ("raw_pitch", i32), ("pad1", i32)]
 
 
 class HsPool(C.Structure):
@@ -117,7 +117,7 @@ class HsFinishArgs(C.Structure):
 ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs]
 
-EXPECTED_SIZES = {HsBucket: 64, HsPatch: 112, HsLayer: 56, HsPool: 40}
+EXPECTED_SIZES = {HsBucket: 64, HsPatch: 112, HsLayer: 64, HsPool: 40}
 
 # every symbol include/hybridsea_b200.h declares
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",

@@ -228,8 +228,26 @@ struct SplatLayer {
     long long raw_off;
     double inv_tf;          // 1 / (texel * f)
     double umax, vmax;      // wx - 1, wy - 1
-    int wy, pad;
+    int pitch, pad;         // raw row pitch (multiple of 4 floats), grid pad
 };
+
+__device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void red2(float* p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(a), "f"(b) : "memory");
+}
+// add (v0, v1) at row[c], row[c + 1]; row is 16-byte aligned: one 16-byte
+// reduction when the pair sits in one aligned float4, else two 8-byte ones
+// (zero lanes leave their neighbours unchanged)
+__device__ __forceinline__ void red_pair(float* row, int c, float v0, float v1) {
+    const int s = c & 3;
+    float* b = row + (c - s);
+    if (s == 0) red4(b, v0, v1, 0.f, 0.f);
+    else if (s == 1) red4(b, 0.f, v0, v1, 0.f);
+    else if (s == 2) red2(b + 2, v0, v1);
+    else { red2(b + 2, 0.f, v0); red2(b + 4, v1, 0.f); }
+}
 
 __device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLayer& L, double x0, double y0,
                                          double x, double y, float amp, int* clamp_acc) {
@@ -240,17 +258,15 @@ __device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLay
     v = fmin(fmax(v, 0.0), L.vmax - 1e-9);
     const int i0 = (int)u, j0 = (int)v;
     const float fu = (float)(u - i0), fv = (float)(v - j0);
-    float* q = raw + L.raw_off + (long long)i0 * L.wy + j0;
+    float* row = raw + L.raw_off + (long long)i0 * L.pitch;
     const float a1 = amp * fu, a0 = amp - a1;          // amp (1 - fu), amp fu
-    atomicAdd(q, a0 * (1.f - fv));
-    atomicAdd(q + L.wy, a1 * (1.f - fv));
-    atomicAdd(q + 1, a0 * fv);
-    atomicAdd(q + L.wy + 1, a1 * fv);
+    red_pair(row, j0, a0 * (1.f - fv), a0 * fv);
+    red_pair(row + L.pitch, j0, a1 * (1.f - fv), a1 * fv);
 }
 
 __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
                                           double x, double y, float amp, int* clamp_acc) {
-    SplatLayer S{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1), L.wy, L.pad};
+    SplatLayer S{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1), L.raw_pitch, L.pad};
     splat_at(raw, S, P.x0, P.y0, x, y, amp, clamp_acc);
 }
 
@@ -337,7 +353,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                 if (a.splat) {
                     const HsLayer L = a.layers[P.layer_base + lane];
                     sl_s[lane] = SplatLayer{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1),
-                                            (double)(L.wy - 1), L.wy, L.pad};
+                                            (double)(L.wy - 1), L.raw_pitch, L.pad};
                 }
             }
             if (lane == nb - 1) { in_off[nb] = si; st_off[nb] = ss; voff[nb] = si + ss; }
@@ -539,7 +555,7 @@ __device__ __forceinline__ bool adv_setup(const HsAdvectArgs& a, AdvTables& T, i
             if (a.splat) {
                 const HsLayer L = a.layers[P.layer_base + lane];
                 T.sl[lane] = SplatLayer{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1),
-                                        (double)(L.wy - 1), L.wy, L.pad};
+                                        (double)(L.wy - 1), L.raw_pitch, L.pad};
             }
         }
         if (lane == nb - 1) { T.in_off[nb] = si; T.st_off[nb] = ss; T.voff[nb] = si + ss; }
@@ -653,12 +669,21 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
 #pragma unroll
     for (int it = 0; it < ADV_ITEMS; ++it) {
         const int v = tbase + it * ADV_THREADS + threadIdx.x;
-        if (v >= N) continue;
         const int w = it * (ADV_THREADS / 32) + wid;
         const unsigned bal = wbits[w];
+        const int b = v < N ? (v < T.seg_end ? T.seg_b : find_seg(T.voff, nb + 1, v)) : -1;
+        // per-bucket survivor counts, warp-aggregated (a warp's items nearly always share a bucket)
+        {
+            const int b0 = __shfl_sync(0xffffffffu, b, 0);
+            if (__all_sync(0xffffffffu, b == b0 || b < 0)) {
+                if (lane == 0 && bal) atomicAdd(&keep_hist[b0], __popc(bal));
+            } else if (b >= 0 && ((bal >> lane) & 1u)) {
+                atomicAdd(&keep_hist[b], 1);
+            }
+        }
+        if (v >= N) continue;
         const bool kept = (bal >> lane) & 1u;
         const int rank = tprefix + wpre[w] + __popc(bal & ((1u << lane) - 1u));
-        const int b = v < T.seg_end ? T.seg_b : find_seg(T.voff, nb + 1, v);
         double x, y, ux, uy;
         const float* ap;
         adv_item(a, P, T.in_off, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
@@ -670,7 +695,6 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
             } else {
                 atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             }
-            atomicAdd(&keep_hist[b], 1);
             if (a.splat) splat_at(raw, T.sl[b], P.x0, P.y0, x, y, am, &clamp_local);
         } else {
             if (am > 0.f) {

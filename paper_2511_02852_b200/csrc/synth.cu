@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
         for (int c = threadIdx.x & 31; c < W; c += 32) {
             const int gy = ry0 + c;
             const bool ok = rok && gy >= 0 && gy < L.wy;
-            cp_async4(in + r * W + c, ok ? raw + (long long)gx * L.wy + gy : raw, ok);
+            cp_async4(in + r * W + c, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
         }
     }
     cp_async_wait_all();
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) smooth_wide_x_kernel(HsSmoothArgs a) {
         int r = e / SM_TILE, c = e - r * SM_TILE;
         int gx = r0 + L.pad - H + r, gy = c0 + c;
         const bool ok = gx >= 0 && gx < L.wx && gy < L.wy;
-        cp_async4(in + e, ok ? raw + (long long)gx * L.wy + gy : raw, ok);
+        cp_async4(in + e, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
     }
     cp_async_wait_all();
     __syncthreads();

@@ -84,7 +84,9 @@ def test_layer_plan_mirror_matches_golden(golden):
     for L, f, k in zip(pack.layers, plan.factors, plan.kernels):
         ncx = -((128) // -f) + 1
         assert (L.f, L.H, L.pad, L.ncx, L.wx) == (f, k.half_width, k.half_width + 1, ncx, ncx + 2 * L.pad)
-    assert pack.raw_len == sum(L.wx * L.wy for L in pack.layers)
+    # raw rows are padded to 16-byte pitches (vector splat reductions), offsets stay 16-byte aligned
+    assert all(L.raw_pitch >= L.wy and L.raw_pitch % 4 == 0 and L.raw_off % 4 == 0 for L in pack.layers)
+    assert pack.raw_len == sum(L.wx * L.raw_pitch for L in pack.layers)
 
 
 def test_half_rates_bit_exact_with_oracle():
