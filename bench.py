@@ -210,6 +210,7 @@ def main():
     sim.run_frames(n_warm, dt=WARM_DT)
     torch.cuda.synchronize()
     sim.check()
+    sim.prepare_graphs()
     for _ in range(max(3, args.warmup)):
         sim.step(stats=False)
         if gather:
@@ -240,6 +241,8 @@ def main():
     clk = clocks.stop()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(np.sum(step_ms))
+    step_pct = {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
+                "max": float(np.max(step_ms))}
     live_after = sim.live_particles()
     sim.check()
     live = 0.5 * (live_before + live_after)
@@ -277,7 +280,7 @@ def main():
         sim.frame_dev.copy_(host_frame, non_blocking=True)
         sim.step(stats=False)
         host_tile.copy_(sim.blended_tile(0)[0], non_blocking=True)
-        host_counts.copy_(sim.counts[sim._parity], non_blocking=True)
+        host_counts.copy_(sim.live, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e2e_end.record()
     torch.cuda.synchronize()
@@ -288,9 +291,10 @@ def main():
         e2e_ms = float(t[0])
     e2e_value = live_all * 1e3 / e2e_ms
 
-    # roofline of the dominant kernel (advect: algorithmic bytes per launch)
-    n_stage = int(sim.stage_count.sum().item()) if sim.n_patches else 0
-    adv_bytes = 36.0 * (live + n_stage) + 36.0 * live      # read in+staged SoA, write survivors
+    # roofline of the dominant particle kernel, hs_advect_resident (in-place
+    # advect + cull + splat): per live particle it must read x, y, ux, uy (f64)
+    # and amp (f32) = 36 B and write the new x, y = 16 B
+    adv_bytes = 52.0 * live
     adv_ms = stage.get("advect", float("nan"))
     peaks = {}
     try:
@@ -307,7 +311,7 @@ def main():
         try:
             ks = json.load(open(tp))["kernels"]
             traffic = sum(ks[k]["dram_read_bytes"] + ks[k]["dram_write_bytes"]
-                          for k in ("advect_count_kernel", "advect_scatter_kernel"))
+                          for k in ("advect_resident_kernel",))
         except (OSError, KeyError, ValueError):
             traffic = None
 
@@ -330,9 +334,10 @@ def main():
                        "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
                        "warm_start": f"{n_warm} frames at dt={WARM_DT}", "l2": "flushed between timed steps",
                        "parallelism": f"patch-sharded x{world}" if world > 1 else "single GPU"},
+            "step_ms_percentiles": step_pct,
             "gpu_launches": sim.kernel_launches_per_frame() * args.steps,
             "stages_ms": stage,
-            "roofline": {"bound": "hbm", "kernel": "hs_advect (advect+cull+compact+splat)",
+            "roofline": {"bound": "hbm", "kernel": "hs_advect_resident (in-place advect+cull+splat)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes": adv_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},

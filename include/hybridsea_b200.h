@@ -190,8 +190,72 @@ typedef struct {
     int* status;
     unsigned* keep_words;                  /* optional [max_tiles*32]: selects the count + scatter
                                               two-kernel compaction (no serial look-back chain) */
+    /* resident-pool compaction (HsResidentArgs below); all optional */
+    const int* in_seg_base;                /* [n_patches*nb]: input bucket b of patch p occupies the
+                                              absolute slots [in_seg_base, +in_count) of `in`, and
+                                              slots whose x is NaN are holes (skipped, not despawned) */
+    const int* out_slack_prefix;           /* [n_patches*nb]: survivor of bucket b with patch rank r
+                                              goes to pool_base + r + out_slack_prefix (gaps between
+                                              segments for later in-place appends) */
+    int raw_is_clear;                      /* 1: raw layers are already zero (skip the clear) */
 } HsAdvectArgs;
 HS_API int hs_advect(const HsAdvectArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Resident pool (the Simulation frame path).  Between compactions every
+ * (patch, bucket) segment keeps fixed storage [seg_base, seg_base + seg_cap)
+ * with len slots in use; a despawned particle leaves a hole (x = NaN) in
+ * place, so the live particles of a segment, read in slot order, are exactly
+ * the reference's stable compaction of that bucket (particles.py:167-178).
+ * Per frame:
+ *   hs_advect_resident  advect + cull + splat every used slot IN PLACE
+ *                       (reads x,y,ux,uy,amp; writes x,y -- or the hole mark)
+ *   hs_append_resident  advect + cull + splat this frame's injected particles
+ *                       and append them at the segment tails (len_out = len_in
+ *                       + staged); independent of hs_advect_resident, so the
+ *                       two run concurrently
+ * Every K frames hs_advect (count + scatter, in_seg_base/out_slack_prefix)
+ * squeezes the holes out into the other buffer and hs_resident_layout
+ * re-derives the segment table.                                             */
+typedef struct {
+    int n_patches, nb;
+    const HsBucket* buckets;
+    const HsPatch* patches;
+    double dt, rho, g;
+    HsPool pool;                   /* the current buffer */
+    const int* seg_base;           /* [n_patches*nb] absolute element offset */
+    const int* seg_cap;            /* [n_patches*nb] */
+    const int* tile_map;           /* [max_tiles*4], 16-byte aligned: (segment, tile within
+                                      segment, absolute first slot, 0); unused tiles (-1, 0, 0, 0) */
+    int max_tiles;                 /* tile-map entries */
+    const int* len_in;             /* [n_patches*nb] slots in use at frame start */
+    int* len_out;                  /* [n_patches*nb] written by hs_append_resident */
+    int* live;                     /* [n_patches*nb] live particles (atomic updates) */
+    HsPool stage; const int* stage_count;   /* hs_append_resident: this frame's injected set */
+    double* e_out;                 /* [n_patches*nb] despawn ledger */
+    float* raw_layers;             /* must be zero at frame start (not cleared here) */
+    const HsLayer* layers;
+    int* clamped;                  /* [n_patches] */
+    int* status;
+} HsResidentArgs;
+HS_API int hs_advect_resident(const HsResidentArgs* a, void* stream);
+HS_API int hs_append_resident(const HsResidentArgs* a, void* stream);
+
+/* Segment table after a compaction (or at start, count = NULL): segment
+ * (p, b) gets base = pool_base + sum_{b'<b} count + slack_prefix, cap = count
+ * + slack, len = live = count, and tiles of 1024 slots in tile_map.          */
+typedef struct {
+    int n_patches, nb;
+    const HsPatch* patches;
+    const int* count;              /* [n_patches*nb] packed counts, or NULL (empty pool) */
+    const int* slack;              /* [n_patches*nb] */
+    const int* slack_prefix;       /* [n_patches*nb] exclusive prefix of slack within the patch */
+    int* seg_base; int* seg_cap; int* len; int* live;
+    int* tile_map;                 /* [max_tiles*4] */
+    int max_tiles;
+    int* status;
+} HsLayoutArgs;
+HS_API int hs_resident_layout(const HsLayoutArgs* a, void* stream);
 
 /* Splat-only pass over a bucket-segmented pool (synthesize on a pool that was
  * not just advected).                                                       */

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libhybridsea_b200.so")
+# HS_LIB selects an experiment build (tools/, build_lib.build(out=...)); default: the product library
+LIB_PATH = os.environ.get("HS_LIB") or os.path.join(_PKG, "_lib", "libhybridsea_b200.so")
 
 HS_STATUS_POOL_OVERFLOW = 1
 HS_STATUS_STAGE_OVERFLOW = 2
@@ -71,7 +72,22 @@ class HsAdvectArgs(C.Structure):
                 ("stage_count", vp), ("out", HsPool), ("out_count", vp), ("dropped", HsPool),
                 ("dropped_count", vp), ("e_out", vp), ("splat", i32), ("raw_layers", vp),
                 ("raw_layers_len", i64), ("layers", vp), ("clamped", vp), ("tile_state", vp),
-                ("max_tiles", i32), ("tile_counter", vp), ("status", vp), ("keep_words", vp)]
+                ("max_tiles", i32), ("tile_counter", vp), ("status", vp), ("keep_words", vp),
+                ("in_seg_base", vp), ("out_slack_prefix", vp), ("raw_is_clear", i32)]
+
+
+class HsResidentArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("buckets", vp), ("patches", vp), ("dt", dbl),
+                ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp),
+                ("tile_map", vp), ("max_tiles", i32), ("len_in", vp), ("len_out", vp), ("live", vp),
+                ("stage", HsPool), ("stage_count", vp), ("e_out", vp), ("raw_layers", vp), ("layers", vp),
+                ("clamped", vp), ("status", vp)]
+
+
+class HsLayoutArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("patches", vp), ("count", vp), ("slack", vp),
+                ("slack_prefix", vp), ("seg_base", vp), ("seg_cap", vp), ("len", vp), ("live", vp),
+                ("tile_map", vp), ("max_tiles", i32), ("status", vp)]
 
 
 class HsSplatArgs(C.Structure):
@@ -115,14 +131,16 @@ class HsFinishArgs(C.Structure):
 
 
 ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
-               HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs]
+               HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
+               HsLayoutArgs]
 
 EXPECTED_SIZES = {HsBucket: 64, HsPatch: 112, HsLayer: 64, HsPool: 40}
 
 # every symbol include/hybridsea_b200.h declares
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
-           "hs_advance_frame", "hs_periodic_normals"]
+           "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
+           "hs_resident_layout"]
 
 _lib = None
 

@@ -40,29 +40,41 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = True, out: str | None = None, extra: tuple = ()) -> str:
+    """Compile every csrc/*.cu (in parallel) and link the shared library.
+    `out` / `extra` build an experiment variant (extra nvcc flags, e.g. -D
+    switches) at another path; the product library is always `LIB`."""
+    lib = out or LIB
+    if not force and out is None and not extra and not needs_build():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
-    objs = []
+    odir = os.path.dirname(lib)
+    os.makedirs(odir, exist_ok=True)
+    tag = os.path.basename(lib).replace(".so", "")
+    jobs = []
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, *PER_FILE_FLAGS.get(src, []), "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-dc" if False else "-c",
-               os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(odir, f"{tag}_{src.replace('.cu', '.o')}")
+        cmd = [nvcc(), *NVCC_FLAGS, *PER_FILE_FLAGS.get(src, []), *extra, "-I", os.path.join(ROOT, "include"),
+               "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+        jobs.append((cmd, obj))
+    procs = []
+    for cmd, _ in jobs:
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
-    tmp = LIB + ".tmp"
+        procs.append(subprocess.Popen(cmd))
+    bad = [cmd[-3] for (cmd, _), pr in zip(jobs, procs) if pr.wait() != 0]
+    if bad:
+        raise RuntimeError(f"nvcc failed on {bad}")
+    objs = [o for _, o in jobs]
+    tmp = lib + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-Xcompiler", "-fPIC", *objs, "-o", tmp]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

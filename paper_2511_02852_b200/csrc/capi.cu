@@ -50,6 +50,8 @@ extern "C" HS_API int hs_struct_size(int which) {
         case 10: return (int)sizeof(HsSampleArgs);
         case 11: return (int)sizeof(HsCompositeArgs);
         case 12: return (int)sizeof(HsFinishArgs);
+        case 13: return (int)sizeof(HsResidentArgs);
+        case 14: return (int)sizeof(HsLayoutArgs);
         default: return -1;
     }
 }

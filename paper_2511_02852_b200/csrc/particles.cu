@@ -280,13 +280,13 @@ __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer
 //      scatter survivors stably (ballot ranks) + the fused layer splat; the
 //      dropped are optionally scattered the same way.
 // Large tiles keep the look-back chain short (~210 tiles at C3).
-__device__ __forceinline__ void adv_item(const HsAdvectArgs& a, const HsPatch& P, const int* in_off,
+__device__ __forceinline__ void adv_item(const HsAdvectArgs& a, const HsPatch& P, const long long* in_base,
                                          const int* st_off, const int* voff, const int* in_cnt, const double* step_s,
                                          int v, int b, double& x, double& y, double& ux, double& uy,
                                          const float** amp_ptr) {
     const int local = v - voff[b];
     const bool from_pool = local < in_cnt[b];
-    const long long src = from_pool ? P.pool_base + in_off[b] + local
+    const long long src = from_pool ? in_base[b] + local
                                     : P.stage_base + st_off[b] + (local - in_cnt[b]);
     const HsPool& S = from_pool ? a.in : a.stage;
     const double step = step_s[b];
@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
     const int nb = a.nb;
     __shared__ int tile_prefix[HS_MAX_PATCHES + 1];
     __shared__ int in_off[HS_MAX_BUCKETS + 1];
+    __shared__ long long in_base[HS_MAX_BUCKETS];
     __shared__ int st_off[HS_MAX_BUCKETS + 1];
     __shared__ int voff[HS_MAX_BUCKETS + 1];
     __shared__ int in_cnt_s[HS_MAX_BUCKETS];
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
             const int si = warp_incl_scan(ci, lane), ss = warp_incl_scan(cs, lane);
             if (lane < nb) {
                 in_off[lane] = si - ci; st_off[lane] = ss - cs; voff[lane] = si - ci + ss - cs; in_cnt_s[lane] = ci;
+                in_base[lane] = P.pool_base + si - ci;
                 const HsBucket B = a.buckets[lane];
                 step_s[lane] = dmul(B.speed, a.dt);                   // speeds * dt
                 r2_s[lane] = dmul(B.radius, B.radius);
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                     bk_s[li] = (unsigned char)b;
                     double x, y, ux, uy;
                     const float* ap;
-                    adv_item(a, P, in_off, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
+                    adv_item(a, P, in_base, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
                     const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
                     const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
                     keep[it] = dadd(dmul(ox, ox), dmul(oy, oy)) <= r2_s[b];   // support disk (:315-320)
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                 const int b = bk_s[li];
                 double x, y, ux, uy;
                 const float* ap;
-                adv_item(a, P, in_off, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
+                adv_item(a, P, in_base, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
                 const float am = *ap;
                 if (kept) {
                     if (rank < P.pool_capacity) {
@@ -514,6 +516,8 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
 // look-back chain -- the scatter kernel sums the per-tile survivor counts of
 // its patch's earlier tiles directly (a few hundred ints, L2-resident).
 struct AdvTables {
+    long long in_base[HS_MAX_BUCKETS];
+    int slack[HS_MAX_BUCKETS];
     int in_off[HS_MAX_BUCKETS + 1], st_off[HS_MAX_BUCKETS + 1], voff[HS_MAX_BUCKETS + 1];
     int in_cnt[HS_MAX_BUCKETS];
     double step[HS_MAX_BUCKETS], r2[HS_MAX_BUCKETS];
@@ -549,6 +553,8 @@ __device__ __forceinline__ bool adv_setup(const HsAdvectArgs& a, AdvTables& T, i
         const int si = warp_incl_scan(ci, lane), ss = warp_incl_scan(cs, lane);
         if (lane < nb) {
             T.in_off[lane] = si - ci; T.st_off[lane] = ss - cs; T.voff[lane] = si - ci + ss - cs; T.in_cnt[lane] = ci;
+            T.in_base[lane] = a.in_seg_base ? (long long)a.in_seg_base[(size_t)p * nb + lane] : P.pool_base + si - ci;
+            T.slack[lane] = a.out_slack_prefix ? a.out_slack_prefix[(size_t)p * nb + lane] : 0;
             const HsBucket B = a.buckets[lane];
             T.step[lane] = dmul(B.speed, a.dt);
             T.r2[lane] = dmul(B.radius, B.radius);
@@ -587,7 +593,7 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_count_kernel(HsAdvectArgs 
             a.out_count[gt] = 0;
             if (a.dropped.x) a.dropped_count[gt] = 0;
         }
-        if (a.splat) {
+        if (a.splat && !a.raw_is_clear) {
             float* r = a.raw_layers;
             const long long n = a.raw_layers_len;
             const long long head = min(n, (long long)((16 - ((size_t)r & 15)) & 15) / 4);
@@ -616,10 +622,10 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_count_kernel(HsAdvectArgs 
             const int b = v < T.seg_end ? T.seg_b : find_seg(T.voff, nb + 1, v);
             double x, y, ux, uy;
             const float* ap;
-            adv_item(a, P, T.in_off, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
+            adv_item(a, P, T.in_base, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
             const double ox = fmax(fmax(dsub(P.x0, x), dsub(x, P.x1)), 0.0);
             const double oy = fmax(fmax(dsub(P.y0, y), dsub(y, P.y1)), 0.0);
-            keep = dadd(dmul(ox, ox), dmul(oy, oy)) <= T.r2[b];       // support disk (:315-320)
+            keep = dadd(dmul(ox, ox), dmul(oy, oy)) <= T.r2[b] && x == x;   // support disk (:315-320); NaN = hole
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) { words[it * (ADV_THREADS / 32) + wid] = bal; mine += __popc(bal); }
@@ -686,17 +692,18 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
         const int rank = tprefix + wpre[w] + __popc(bal & ((1u << lane) - 1u));
         double x, y, ux, uy;
         const float* ap;
-        adv_item(a, P, T.in_off, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
+        adv_item(a, P, T.in_base, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
         const float am = *ap;
         if (kept) {
-            if (rank < P.pool_capacity) {
-                const long long o = P.pool_base + rank;
+            const int slot = rank + T.slack[b];
+            if (slot < P.pool_capacity) {
+                const long long o = P.pool_base + slot;
                 a.out.x[o] = x; a.out.y[o] = y; a.out.ux[o] = ux; a.out.uy[o] = uy; a.out.amp[o] = am;
             } else {
                 atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             }
             if (a.splat) splat_at(raw, T.sl[b], P.x0, P.y0, x, y, am, &clamp_local);
-        } else {
+        } else if (x == x) {                             // a despawn (NaN marks a resident-pool hole)
             if (am > 0.f) {
                 const double amp = (double)am;          // crest despawn energy (particles.py:322-327)
                 atomicAdd(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * T.r2[b]);
@@ -744,6 +751,225 @@ __global__ void __launch_bounds__(256) splat_kernel(HsSplatArgs a) {
     if (cl) atomicAdd(&clamp_s, cl);
     __syncthreads();
     if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
+}
+
+// ====================================================== resident pool ==
+// In-place frame path (HsResidentArgs, include/hybridsea_b200.h).  A tile is
+// 1024 consecutive slots of ONE (patch, bucket) segment, so every CTA works
+// on a single bucket: one step, one support radius, one splat layer, and one
+// atomic per counter at the end.
+constexpr int RES_THREADS = 256;
+constexpr int RES_ITEMS = 4;
+constexpr int RES_TILE = RES_THREADS * RES_ITEMS;
+
+// Persistent CTAs walk the tile list with stride gridDim.x.  A tile-map entry
+// (segment, tile-in-segment, absolute first slot) is prefetched one tile
+// ahead, so each tile costs one memory round trip: the slot loads, the
+// segment length and the bucket/patch/layer constants issue together.
+// Every warp retires its slots independently (no barrier).
+__global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResidentArgs a) {
+    const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
+    double* __restrict__ px = a.pool.x;
+    double* __restrict__ py = a.pool.y;
+    const double* __restrict__ pux = a.pool.ux;
+    const double* __restrict__ puy = a.pool.uy;
+    const float* __restrict__ pam = a.pool.amp;
+    int t = blockIdx.x;
+    int4 m = t < a.max_tiles ? __ldg(tmap + t) : make_int4(-1, 0, 0, 0);
+    while (m.x >= 0) {
+        const int tn = t + gridDim.x;
+        const int4 mn = tn < a.max_tiles ? __ldg(tmap + tn) : make_int4(-1, 0, 0, 0);
+        const int s = m.x;
+        const long long base = (long long)m.z;
+        // slot loads before the length is known: slots past len (up to the
+        // tile end, inside the pool arrays) are read and ignored
+        double x[RES_ITEMS], y[RES_ITEMS], ux[RES_ITEMS], uy[RES_ITEMS];
+        float am[RES_ITEMS];
+#pragma unroll
+        for (int it = 0; it < RES_ITEMS; ++it) {
+            const long long o = base + it * RES_THREADS + threadIdx.x;
+            x[it] = px[o]; y[it] = py[o]; ux[it] = __ldg(pux + o); uy[it] = __ldg(puy + o); am[it] = __ldg(pam + o);
+        }
+        const int n = min(RES_TILE, a.len_in[s] - m.y * RES_TILE);
+        const int p = s / a.nb, b = s - p * a.nb;
+        const HsPatch* P = a.patches + p;
+        const double x0 = __ldg(&P->x0), y0 = __ldg(&P->y0), x1 = __ldg(&P->x1), y1 = __ldg(&P->y1);
+        const HsBucket* Bk = a.buckets + b;
+        const double step = dmul(__ldg(&Bk->speed), a.dt);            // speeds * dt (particles.py:312)
+        const double rad = __ldg(&Bk->radius);
+        const double r2 = dmul(rad, rad);
+        const HsLayer* L = a.layers + __ldg(&P->layer_base) + b;
+        const SplatLayer sl{__ldg(&L->raw_off), 1.0 / (__ldg(&P->texel) * (double)__ldg(&L->f)),
+                            (double)(__ldg(&L->wx) - 1), (double)(__ldg(&L->wy) - 1), __ldg(&L->raw_pitch),
+                            __ldg(&L->pad)};
+        int drops = 0, clamp_local = 0;
+        double e = 0.0;
+#pragma unroll
+        for (int it = 0; it < RES_ITEMS; ++it) {
+            const int k = it * RES_THREADS + threadIdx.x;
+            if (k >= n || x[it] != x[it]) continue;                     // beyond len, or a hole
+            const long long o = base + k;
+            const double nx = dadd(x[it], dmul(ux[it], step));           // pos += dir * (c dt)  (:312-313)
+            const double ny = dadd(y[it], dmul(uy[it], step));
+            const double ox = fmax(fmax(dsub(x0, nx), dsub(nx, x1)), 0.0);
+            const double oy = fmax(fmax(dsub(y0, ny), dsub(ny, y1)), 0.0);
+            if (dadd(dmul(ox, ox), dmul(oy, oy)) <= r2) {                // support disk (:315-320)
+                px[o] = nx;
+                py[o] = ny;
+#ifndef HS_EXP_NOSPLAT
+                splat_at(a.raw_layers, sl, x0, y0, nx, ny, am[it], &clamp_local);
+#endif
+            } else {
+                px[o] = __longlong_as_double(0x7ff8000000000000LL);       // hole: stable compaction is deferred
+                ++drops;
+                if (am[it] > 0.f) {                                       // crest despawn energy (:322-327)
+                    const double amp = (double)am[it];
+                    e += 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2;
+                }
+            }
+        }
+        // per-warp totals (drops and despawns are rare: most warps skip the atomics)
+        if (__any_sync(0xffffffffu, drops != 0 || clamp_local != 0)) {
+            drops = warp_sum(drops);
+            clamp_local = warp_sum(clamp_local);
+            e = warp_sum(e);
+            if ((threadIdx.x & 31) == 0) {
+                if (drops) atomicSub(&a.live[s], drops);
+                if (e != 0.0) atomicAdd(&a.e_out[s], e);
+                if (clamp_local && a.clamped) atomicAdd(&a.clamped[p], clamp_local);
+            }
+        }
+        t = tn;
+        m = mn;
+    }
+}
+
+// One CTA per patch: advect + cull + splat this frame's injected particles
+// (the virtual [new crests b][new troughs b] of particles.py:296-299, advected
+// in their birth frame, harness.py:142-152) and append them at the tails of
+// their bucket segments; culled ones become holes so slots stay in order.
+__global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResidentArgs a) {
+    const int p = blockIdx.x, nb = a.nb;
+    __shared__ int soff[HS_MAX_BUCKETS + 1];
+    __shared__ int kept_s[HS_MAX_BUCKETS];
+    __shared__ double eout_s[HS_MAX_BUCKETS];
+    __shared__ long long dst_s[HS_MAX_BUCKETS];
+    __shared__ int room_s[HS_MAX_BUCKETS];
+    __shared__ double step_s[HS_MAX_BUCKETS], r2_s[HS_MAX_BUCKETS];
+    __shared__ SplatLayer sl_s[HS_MAX_BUCKETS];
+    __shared__ int clamp_s;
+    __shared__ HsPatch P_s;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        const HsPatch P = a.patches[p];
+        if (lane == 0) { P_s = P; clamp_s = 0; }
+        const int s = p * nb + lane;
+        const int c = lane < nb ? a.stage_count[s] : 0;
+        const int inc = warp_incl_scan(c, lane);
+        if (lane < nb) {
+            soff[lane] = inc - c;
+            const int len = a.len_in[s];
+            a.len_out[s] = len + c;
+            dst_s[lane] = (long long)a.seg_base[s] + len;
+            room_s[lane] = a.seg_cap[s] - len;
+            kept_s[lane] = 0;
+            eout_s[lane] = 0.0;
+            const HsBucket Bk = a.buckets[lane];
+            step_s[lane] = dmul(Bk.speed, a.dt);
+            r2_s[lane] = dmul(Bk.radius, Bk.radius);
+            const HsLayer L = a.layers[P.layer_base + lane];
+            sl_s[lane] = SplatLayer{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1),
+                                    (double)(L.wy - 1), L.raw_pitch, L.pad};
+            if (c > a.seg_cap[s] - len) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+        }
+        if (lane == 31) soff[nb] = inc;
+    }
+    __syncthreads();
+    const int N = soff[nb];
+    const HsPatch& P = P_s;
+    int clamp_local = 0;
+    for (int v = threadIdx.x; v < N; v += RES_THREADS) {
+        const int b = find_seg(soff, nb + 1, v);
+        const int j = v - soff[b];
+        const long long src = P.stage_base + v;
+        const double ux = a.stage.ux[src], uy = a.stage.uy[src];
+        const float am = a.stage.amp[src];
+        const double nx = dadd(a.stage.x[src], dmul(ux, step_s[b]));
+        const double ny = dadd(a.stage.y[src], dmul(uy, step_s[b]));
+        const double ox = fmax(fmax(dsub(P.x0, nx), dsub(nx, P.x1)), 0.0);
+        const double oy = fmax(fmax(dsub(P.y0, ny), dsub(ny, P.y1)), 0.0);
+        const bool keep = dadd(dmul(ox, ox), dmul(oy, oy)) <= r2_s[b];
+        if (j < room_s[b]) {
+            const long long o = dst_s[b] + j;
+            a.pool.x[o] = keep ? nx : __longlong_as_double(0x7ff8000000000000LL);
+            a.pool.y[o] = ny; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = am;
+        }
+        if (keep) {
+            atomicAdd(&kept_s[b], 1);
+            splat_at(a.raw_layers, sl_s[b], P.x0, P.y0, nx, ny, am, &clamp_local);
+        } else if (am > 0.f) {
+            const double amp = (double)am;
+            atomicAdd(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2_s[b]);
+        }
+    }
+    if (clamp_local) atomicAdd(&clamp_s, clamp_local);
+    __syncthreads();
+    if (threadIdx.x < nb) {
+        const int s = p * nb + threadIdx.x;
+        if (kept_s[threadIdx.x]) atomicAdd(&a.live[s], kept_s[threadIdx.x]);
+        if (eout_s[threadIdx.x] != 0.0) atomicAdd(&a.e_out[s], eout_s[threadIdx.x]);
+    }
+    if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
+}
+
+// Segment table (HsLayoutArgs).  One CTA: warp w lays out patch w (strided),
+// lane b = bucket b; then a block scan of per-patch tile totals places every
+// segment's tiles in tile_map.
+__global__ void __launch_bounds__(1024) resident_layout_kernel(HsLayoutArgs a) {
+    const int nb = a.nb, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ int ptiles[HS_MAX_PATCHES];
+    __shared__ int pfirst[HS_MAX_PATCHES];
+    __shared__ int scan_sm[33];
+    for (int p = wid; p < a.n_patches; p += nw) {
+        const HsPatch P = a.patches[p];
+        const int s = p * nb + lane;
+        const int c = (lane < nb && a.count) ? a.count[s] : 0;
+        const int inc = warp_incl_scan(c, lane);
+        int nt = 0;
+        if (lane < nb) {
+            const long long base = P.pool_base + (inc - c) + a.slack_prefix[s];
+            const int cap = c + a.slack[s];
+            if (base + cap > P.pool_base + P.pool_capacity) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+            a.seg_base[s] = (int)base;
+            a.seg_cap[s] = cap;
+            a.len[s] = c;
+            a.live[s] = c;
+            nt = (cap + RES_TILE - 1) / RES_TILE;
+        }
+        const int tinc = warp_incl_scan(nt, lane);
+        if (lane == 31) ptiles[p] = tinc;
+    }
+    __syncthreads();
+    // exclusive scan of ptiles over patches (<= HS_MAX_PATCHES <= blockDim.x)
+    {
+        const int v = threadIdx.x < a.n_patches ? ptiles[threadIdx.x] : 0;
+        int tot;
+        const int ex = block_excl_scan(v, scan_sm, &tot);
+        if (threadIdx.x < a.n_patches) pfirst[threadIdx.x] = ex;
+        if (threadIdx.x == 0 && tot > a.max_tiles) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+    }
+    __syncthreads();
+    int4* tmap = reinterpret_cast<int4*>(a.tile_map);
+    for (int t = threadIdx.x; t < a.max_tiles; t += blockDim.x) tmap[t] = make_int4(-1, 0, 0, 0);
+    __syncthreads();
+    for (int p = wid; p < a.n_patches; p += nw) {
+        const int s = p * nb + lane;
+        const int nt = lane < nb ? (a.seg_cap[s] + RES_TILE - 1) / RES_TILE : 0;
+        const int first = pfirst[p] + warp_incl_scan(nt, lane) - nt;
+        if (lane < nb)
+            for (int k = 0; k < nt && first + k < a.max_tiles; ++k)
+                tmap[first + k] = make_int4(s, k, a.seg_base[s] + k * RES_TILE, 0);
+    }
 }
 
 }  // namespace hs
@@ -821,6 +1047,54 @@ extern "C" int hs_splat(const HsSplatArgs* a, void* stream) {
     if (bx > 4096) bx = 4096;
     dim3 grid(bx, a->n_patches);
     splat_kernel<<<grid, 256, 0, st>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+static int check_resident(const HsResidentArgs* a, const char* who) {
+    HS_CHECK_ARG(a != nullptr, "%s: null args", who);
+    HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "%s: nb=%d out of range", who, a->nb);
+    HS_CHECK_ARG(a->n_patches >= 0 && a->n_patches <= HS_MAX_PATCHES, "%s: n_patches out of range", who);
+    HS_CHECK_ARG(a->dt >= 0.0, "%s: dt must be nonnegative", who);
+    HS_CHECK_ARG(a->buckets && a->patches && a->pool.x && a->pool.y && a->pool.ux && a->pool.uy && a->pool.amp &&
+                 a->seg_base && a->seg_cap && a->len_in && a->live && a->e_out && a->raw_layers && a->layers &&
+                 a->status, "%s: missing buffer", who);
+    return 0;
+}
+
+extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
+    if (int rc = check_resident(a, "hs_advect_resident")) return rc;
+    if (a->n_patches == 0) return 0;
+    HS_CHECK_ARG(a->tile_map && a->max_tiles > 0, "hs_advect_resident: missing tile map");
+    HS_CHECK_ARG(((size_t)a->tile_map & 15) == 0, "hs_advect_resident: tile_map must be 16-byte aligned");
+    static int occ = 0;
+    if (!occ) {
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel, RES_THREADS, 0));
+        if (occ < 1) occ = 1;
+    }
+    const int grid = min(a->max_tiles, num_sms() * occ);
+    advect_resident_kernel<<<grid, RES_THREADS, 0, as_stream(stream)>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_append_resident(const HsResidentArgs* a, void* stream) {
+    if (int rc = check_resident(a, "hs_append_resident")) return rc;
+    if (a->n_patches == 0) return 0;
+    HS_CHECK_ARG(a->stage.x && a->stage.amp && a->stage_count && a->len_out, "hs_append_resident: missing stage");
+    append_resident_kernel<<<a->n_patches, RES_THREADS, 0, as_stream(stream)>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_resident_layout(const HsLayoutArgs* a, void* stream) {
+    HS_CHECK_ARG(a != nullptr, "hs_resident_layout: null args");
+    HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "hs_resident_layout: nb out of range");
+    HS_CHECK_ARG(a->n_patches >= 0 && a->n_patches <= HS_MAX_PATCHES, "hs_resident_layout: n_patches out of range");
+    if (a->n_patches == 0) return 0;
+    HS_CHECK_ARG(a->patches && a->slack && a->slack_prefix && a->seg_base && a->seg_cap && a->len && a->live &&
+                 a->tile_map && a->status && a->max_tiles > 0, "hs_resident_layout: missing buffer");
+    resident_layout_kernel<<<1, 1024, 0, as_stream(stream)>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

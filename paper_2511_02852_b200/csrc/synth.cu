@@ -25,7 +25,7 @@ constexpr int SM_RB = 8;                 // outputs per thread along the convolu
 // output rows); the K taps live in registers and each input value is loaded
 // once and feeds up to 8 accumulators.
 template <int H>
-__device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ in, float* __restrict__ mid,
+__device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ in, int IS, float* __restrict__ mid,
                                                      const float* __restrict__ taps_sm, int W, int MS,
                                                      float* __restrict__ out, long long out_base, int ncy,
                                                      int rows_valid, int cols_valid) {
@@ -39,10 +39,10 @@ __device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ i
         float acc[SM_RB];
 #pragma unroll
         for (int k = 0; k < SM_RB; ++k) acc[k] = 0.f;
-        const float* col = in + (rb * SM_RB) * W + c;
+        const float* col = in + (rb * SM_RB) * IS + c;
 #pragma unroll
         for (int u = 0; u < SM_RB + 2 * H; ++u) {
-            const float v = col[u * W];
+            const float v = col[u * IS];
 #pragma unroll
             for (int k = 0; k < SM_RB; ++k) {
                 const int m = u - k;
@@ -77,16 +77,16 @@ __device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ i
     }
 }
 
-__device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in, float* __restrict__ mid,
+__device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in, int IS, float* __restrict__ mid,
                                                     const float* __restrict__ taps, int H, int W, int MS,
                                                     float* __restrict__ out, long long out_base, int ncy,
                                                     int rows_valid, int cols_valid) {
     const int K = 2 * H + 1;
     for (int e = threadIdx.x; e < SM_TILE * W; e += blockDim.x) {
         const int r = e / W, c = e - r * W;
-        const float* col = in + r * W + c;
+        const float* col = in + r * IS + c;
         float s = 0.f;
-        for (int m = 0; m < K; ++m) s = fmaf(taps[m], col[m * W], s);
+        for (int m = 0; m < K; ++m) s = fmaf(taps[m], col[m * IS], s);
         mid[r * MS + c] = s;
     }
     __syncthreads();
@@ -107,33 +107,37 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     const int cx0 = ti[1], cy0 = ti[2];
     const int H = L.H, K = 2 * H + 1, W = SM_TILE + 2 * H;
     const int MS = W | 1;                      // odd row stride: conflict-free column walks
+    // the halo's first column ry0 = cy0 + pad - H = cy0 + 1 (pad = H + 1); loading
+    // from cy0 instead makes every staged row 16-byte aligned in global memory
+    // (raw_off and raw_pitch are multiples of 4 floats), so rows move as float4s
+    const int NV = (W + 1 + 3) >> 2;           // float4s per staged row
+    const int IS = 4 * NV;                     // staged row stride (floats)
     float* taps = smem;                        // K (padded to 4)
-    float* in = taps + ((K + 3) & ~3);         // W x W
-    float* mid = in + W * W;                   // 32 x MS
+    float* in = taps + ((K + 3) & ~3);         // W x IS
+    float* mid = in + W * IS;                  // 32 x MS
     for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
     const float* raw = a.raw_layers + L.raw_off;
-    const int rx0 = cx0 + L.pad - H, ry0 = cy0 + L.pad - H;
-    for (int r = threadIdx.x >> 5; r < W; r += blockDim.x >> 5) {       // warp per row, lanes along it
-        const int gx = rx0 + r;
-        const bool rok = gx >= 0 && gx < L.wx;
-        for (int c = threadIdx.x & 31; c < W; c += 32) {
-            const int gy = ry0 + c;
-            const bool ok = rok && gy >= 0 && gy < L.wy;
-            cp_async4(in + r * W + c, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
-        }
+    const int rx0 = cx0 + L.pad - H;
+    for (int e = threadIdx.x; e < W * NV; e += blockDim.x) {
+        const int r = e / NV, c4 = e - r * NV;
+        const int gx = rx0 + r, gy = cy0 + 4 * c4;
+        // columns in [wy, raw_pitch) are zero; beyond the pitch is the next row
+        const bool ok = gx >= 0 && gx < L.wx && gy < L.raw_pitch;
+        cp_async16z(in + r * IS + 4 * c4, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
     }
     cp_async_wait_all();
     __syncthreads();
+    in += 1;                                   // staged column 1 = halo column 0
     float* out = a.smooth_layers + L.sm_off;
     const long long ob = (long long)cx0 * L.ncy + cy0;
     const int rv = min(SM_TILE, L.ncx - cx0), cv = min(SM_TILE, L.ncy - cy0);
     switch (H) {
-#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(in, mid, taps, W, MS, out, ob, L.ncy, rv, cv); break;
+#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(in, IS, mid, taps, W, MS, out, ob, L.ncy, rv, cv); break;
         HS_SM_CASE(1) HS_SM_CASE(2) HS_SM_CASE(3) HS_SM_CASE(4) HS_SM_CASE(5) HS_SM_CASE(6) HS_SM_CASE(7)
         HS_SM_CASE(8) HS_SM_CASE(9) HS_SM_CASE(10) HS_SM_CASE(11) HS_SM_CASE(12) HS_SM_CASE(13)
         HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16)
 #undef HS_SM_CASE
-        default: smooth_tile_generic(in, mid, taps, H, W, MS, out, ob, L.ncy, rv, cv);
+        default: smooth_tile_generic(in, IS, mid, taps, H, W, MS, out, ob, L.ncy, rv, cv);
     }
 }
 
@@ -325,8 +329,8 @@ extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     cudaStream_t st = as_stream(stream);
     if (a->total_tiles > 0) {
         HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= HS_SMOOTH_FUSED_MAX_H, "hs_smooth: max_H=%d out of range", a->max_H);
-        const int W = SM_TILE + 2 * a->max_H, K = 2 * a->max_H + 1;
-        size_t sm = (size_t)(((K + 3) & ~3) + W * W + SM_TILE * (W | 1)) * sizeof(float);
+        const int W = SM_TILE + 2 * a->max_H, K = 2 * a->max_H + 1, IS = 4 * ((W + 4) >> 2);
+        size_t sm = (size_t)(((K + 3) & ~3) + W * IS + SM_TILE * (W | 1)) * sizeof(float);
         static size_t smooth_attr = 48 * 1024;
         if (sm > smooth_attr) {
             HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

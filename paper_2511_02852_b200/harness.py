@@ -43,6 +43,8 @@ from .spectrum import DirectionalSpectrum, build_buckets, derive_params, log_buc
 
 STAGES = ("fft", "inject", "advect", "interact", "synth", "blend", "output")
 ADV_TILE = 1024
+RES_TILE = 1024          # hs_advect_resident tile (slots of one bucket segment)
+RESIDENT_PERIOD = 32    # frames between resident-pool compactions
 
 
 def build_table(cfg: SimConfig, params):
@@ -123,7 +125,7 @@ class Simulation:
     """Owns all device state of one hybrid scene; `step()` advances a frame."""
 
     def __init__(self, config: SimConfig, device=None, *, pool_capacity: int | None = None,
-                 rng_seed_keys: list | None = None):
+                 rng_seed_keys: list | None = None, compact_period: int | None = None):
         cfg = config.validate()
         if cfg.bodies:
             raise ConfigError("floating bodies are outside the B200 hybrid-step path (SURVEY 8(f))")
@@ -166,19 +168,32 @@ class Simulation:
         self.buckets_dev = structs_to_device(bucket_structs(self.table, self.params), dev)
         self._hr_cache = {}
         self.pool_caps, self.stage_caps, self.member_cap = [], [], 1
+        per_member = 2 if cfg.trough_fraction != 0.0 else 1
+        max_new = []                     # per patch, per bucket: particles one frame can append
+        explicit = pool_capacity is not None or bool(cfg.pool_capacity)
         for k, r in enumerate(self.regions):
+            hr_max = half_rates(r, self.table.omegas, 0.1, cfg.g)       # dt <= 0.1 (config.py validate)
+            mg = max_groups_per_step(hr_max)
+            self.member_cap = max(self.member_cap, mg * self.table.n_theta)
+            max_new.append((np.floor(hr_max) + 1.0).sum(axis=1).astype(np.int64) * self.table.n_theta * per_member)
             if pool_capacity is not None:
                 cap = int(pool_capacity)
             elif cfg.pool_capacity:
                 cap = cfg.pool_capacity
             else:
                 cap = max(4096, int(1.6 * estimate_population(self.table, r, cfg.trough_fraction)))
+                cap += RESIDENT_PERIOD * int(max_new[-1].sum())
                 cap = -(-cap // 1024) * 1024
-            hr_max = half_rates(r, self.table.omegas, 0.1, cfg.g)       # dt <= 0.1 (config.py validate)
-            mg = max_groups_per_step(hr_max)
-            self.member_cap = max(self.member_cap, mg * self.table.n_theta)
             self.pool_caps.append(cap)
             self.stage_caps.append(2 * mg * self.table.n_theta)
+        # resident pool: compaction every K frames; every bucket segment keeps
+        # room for K frames of its largest possible inflow
+        K = RESIDENT_PERIOD if compact_period is None else max(1, int(compact_period))
+        if explicit:
+            while K > 1 and any(K * int(m.sum()) > c // 2 for m, c in zip(max_new, self.pool_caps)):
+                K //= 2
+        self.compact_period = K
+        self._slack_np = (np.stack(max_new) * K).astype(np.int32) if max_new else np.zeros((0, self.nb), np.int32)
         self.pool_base = np.concatenate([[0], np.cumsum(self.pool_caps)]).astype(np.int64)
         self.stage_base = np.concatenate([[0], np.cumsum(self.stage_caps)]).astype(np.int64)
         total_pool = int(self.pool_base[-1])
@@ -196,7 +211,19 @@ class Simulation:
             f32 = lambda n: torch.zeros(max(1, n), dtype=torch.float32, device=dev)  # noqa: E731
             self.pools = [[f64(total_pool), f64(total_pool), f64(total_pool), f64(total_pool), f32(total_pool)]
                           for _ in range(2)]
-            self.counts = [torch.zeros(self.n_patches * self.nb, dtype=torch.int32, device=dev) for _ in range(2)]
+            PB = self.n_patches * self.nb
+            i32 = lambda n: torch.zeros(max(1, n), dtype=torch.int32, device=dev)  # noqa: E731
+            # resident segment table (hs_resident_layout)
+            self.seg_base, self.seg_cap, self.live = i32(PB), i32(PB), i32(PB)
+            self.seg_len = [i32(PB), i32(PB)]
+            self.compact_count = i32(PB)
+            self.slack = torch.from_numpy(self._slack_np.ravel().copy()).to(dev)
+            sp = np.concatenate([np.zeros((self.n_patches, 1), np.int64), np.cumsum(self._slack_np, axis=1)[:, :-1]],
+                                axis=1)
+            self.slack_prefix = torch.from_numpy(sp.astype(np.int32).ravel().copy()).to(dev)
+            self.res_tiles = int(sum(-(-c // RES_TILE) for c in self.pool_caps)) + PB
+            self.tile_map = i32(4 * self.res_tiles)
+            self._buf, self._lp, self._since = 0, 0, 0
             self.stage = [f64(total_stage), f64(total_stage), f64(total_stage), f64(total_stage), f32(total_stage)]
             self.stage_count = torch.zeros(self.n_patches * self.nb, dtype=torch.int32, device=dev)
             self.scratch = f64(2 * self.member_cap * self.n_patches)
@@ -211,18 +238,25 @@ class Simulation:
             self.patch_n = f32(3 * n_grid)
             self.blend_h = f32(n_grid)
             self.blend_n = f32(3 * n_grid)
-            # per-frame accumulators in one block of 4-byte words, zeroed by hs_inject
+            # per-frame accumulators in one block of 4-byte words per frame parity:
+            # frame f accumulates into set f & 1 while its hs_inject zeroes the other
+            # set (frame f + 1's), so no clear sits between concurrent producers
             P = self.n_patches
-            self.stat_words = torch.zeros(5 * P + (P & 1), dtype=torch.int32, device=dev)
-            self.isum = self.stat_words[0:2 * P].view(torch.float64)
-            self.icount = self.stat_words[2 * P:4 * P].view(torch.int64)
-            self.clamped = self.stat_words[4 * P:5 * P]
+            nw = 5 * P + (P & 1)
+            self.stat_words2 = torch.zeros(2 * nw, dtype=torch.int32, device=dev)
+            self._stat_sets = []
+            for q in range(2):
+                w = self.stat_words2[q * nw:(q + 1) * nw]
+                self._stat_sets.append((w, w[0:2 * P].view(torch.float64), w[2 * P:4 * P].view(torch.int64),
+                                        w[4 * P:5 * P]))
             self.max_tiles = int(sum(-(-(pc + sc) // ADV_TILE) for pc, sc in zip(self.pool_caps, self.stage_caps)))
             self.tile_state = torch.zeros(self.max_tiles, dtype=torch.int64, device=dev)
             self.keep_words = torch.zeros(self.max_tiles * 32, dtype=torch.int32, device=dev)
             self.tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
             self._init_boxes()
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        if self.n_patches:
+            self._layout(None, self.seg_len[0])
 
     # ------------------------------------------------------------ helpers --
     def _hr(self, dt: float) -> torch.Tensor:
@@ -252,18 +286,61 @@ class Simulation:
     def _pool(self, k: int) -> N.HsPool:
         return N.pool_struct(*self.pools[k])
 
+    # per-frame stat words of the frame that ran last (see __init__)
+    @property
+    def stat_words(self):
+        return self._stat_sets[self._lp ^ 1][0]
+
+    @property
+    def isum(self):
+        return self._stat_sets[self._lp ^ 1][1]
+
+    @property
+    def icount(self):
+        return self._stat_sets[self._lp ^ 1][2]
+
+    @property
+    def clamped(self):
+        return self._stat_sets[self._lp ^ 1][3]
+
+    def _layout(self, count, len_out) -> None:
+        N.call("hs_resident_layout", N.HsLayoutArgs(
+            n_patches=self.n_patches, nb=self.nb, patches=N.ptr(self.patches_dev), count=N.ptr(count),
+            slack=N.ptr(self.slack), slack_prefix=N.ptr(self.slack_prefix), seg_base=N.ptr(self.seg_base),
+            seg_cap=N.ptr(self.seg_cap), len=N.ptr(len_out), live=N.ptr(self.live), tile_map=N.ptr(self.tile_map),
+            max_tiles=self.res_tiles, status=N.ptr(self.status)), stream_ptr())
+
+    def _resident_args(self, buf: int, lp: int, dt: float, stats) -> N.HsResidentArgs:
+        return N.HsResidentArgs(
+            n_patches=self.n_patches, nb=self.nb, buckets=N.ptr(self.buckets_dev), patches=N.ptr(self.patches_dev),
+            dt=float(dt), rho=float(self.config.rho), g=float(self.config.g), pool=self._pool(buf),
+            seg_base=N.ptr(self.seg_base), seg_cap=N.ptr(self.seg_cap), tile_map=N.ptr(self.tile_map),
+            max_tiles=self.res_tiles, len_in=N.ptr(self.seg_len[lp]), len_out=N.ptr(self.seg_len[lp ^ 1]),
+            live=N.ptr(self.live), stage=N.pool_struct(*self.stage), stage_count=N.ptr(self.stage_count),
+            e_out=N.ptr(self.e_out), raw_layers=N.ptr(self.synth.raw), layers=N.ptr(self.synth.layers),
+            clamped=N.ptr(stats[3]), status=N.ptr(self.status))
+
     # --------------------------------------------------------- the frame --
-    def _enqueue_frame(self, parity: int, dt: float, mark=None) -> None:
-        """Enqueue one frame (graph-capturable).  The background transform
-        only feeds the blend, so it runs on a side stream concurrently with
-        the particle chain inject -> advect -> smooth; the streams join before
-        hs_compose.  `mark(stage)` (optional) is called after each stage's
-        launches on the stream that ran it (CUDA events for stage timing)."""
+    def _enqueue_frame(self, state: tuple, dt: float, mark=None) -> None:
+        """Enqueue one frame (graph-capturable) for resident-pool state
+        `state` = (buffer, length parity, compaction frame?).
+
+        In-place frames (K - 1 of every K):
+            side  : hs_fft_evolve (rows, cols) ..........................┐
+            inj   : hs_inject -> hs_append_resident ──┐                   │
+            main  : hs_advect_resident ──────────────┴► hs_smooth ─► join ─► hs_compose
+            clr   :                                      └► raw-layer clear ─┘ (end of frame)
+        Compaction frames replace the advect pair by hs_inject -> hs_advect
+        (count + scatter into the other buffer, squeezing the holes out) ->
+        hs_resident_layout.  `mark(stage)` (optional) is called after each
+        stage's launches on the stream that ran it (CUDA events for stage
+        timing)."""
+        buf, lp, compact = state
         mark = mark or (lambda _name: None)
         main = torch.cuda.current_stream(self.device)
         fork = self.fft_state is not None and self.n_patches > 0
         if self.fft_state is not None:
-            side = self._side_stream() if fork else main
+            side = self._side_stream("fft") if fork else main
             if fork:
                 side.wait_stream(main)
             with torch.cuda.stream(side):
@@ -275,35 +352,58 @@ class Simulation:
                     fa.frame_advance = N.ptr(self.frame_dev)
                 N.call("hs_fft_evolve", fa, stream_ptr())
                 mark("fft")
-        st = stream_ptr()
         if self.n_patches:
-            mark("particles_start")
-            src, dst = parity, parity ^ 1
-            N.call("hs_inject", N.HsInjectArgs(
+            stats, nxt = self._stat_sets[lp], self._stat_sets[lp ^ 1]
+            cfg = self.config
+            inj_args = N.HsInjectArgs(
                 n_patches=self.n_patches, nb=self.nb, n_theta=self.table.n_theta, buckets=N.ptr(self.buckets_dev),
                 patches=N.ptr(self.patches_dev), half_rate=N.ptr(self._hr(dt)),
-                mean_dir=float(self.config.mean_direction), beta=float(self.config.trough_fraction),
-                rho=float(self.config.rho), g=float(self.config.g), acc=N.ptr(self.acc), groups=N.ptr(self.groups),
+                mean_dir=float(cfg.mean_direction), beta=float(cfg.trough_fraction),
+                rho=float(cfg.rho), g=float(cfg.g), acc=N.ptr(self.acc), groups=N.ptr(self.groups),
                 e_in=N.ptr(self.e_in), rng=N.ptr(self.rng), stage=N.pool_struct(*self.stage),
                 stage_count=N.ptr(self.stage_count), scratch=N.ptr(self.scratch), member_capacity=self.member_cap,
-                status=N.ptr(self.status), zero_words=N.ptr(self.stat_words),
-                n_zero_words=self.stat_words.numel()), st)
-            mark("inject")
-            N.call("hs_advect", N.HsAdvectArgs(
-                n_patches=self.n_patches, nb=self.nb, buckets=N.ptr(self.buckets_dev), patches=N.ptr(self.patches_dev),
-                dt=float(dt), rho=float(self.config.rho), g=float(self.config.g), in_=self._pool(src),
-                in_count=N.ptr(self.counts[src]), stage=N.pool_struct(*self.stage), stage_count=N.ptr(self.stage_count),
-                out=self._pool(dst), out_count=N.ptr(self.counts[dst]), dropped=N.pool_struct(), dropped_count=0,
-                e_out=N.ptr(self.e_out), splat=1, raw_layers=N.ptr(self.synth.raw),
-                raw_layers_len=self.synth.pack.raw_len, layers=N.ptr(self.synth.layers),
-                clamped=N.ptr(self.clamped), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
-                tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status),
-                keep_words=N.ptr(self.keep_words)), st)
-            mark("advect")
-            N.call("hs_smooth", self.synth.smooth_args(), st)
+                status=N.ptr(self.status), zero_words=N.ptr(nxt[0]), n_zero_words=nxt[0].numel())
+            if compact:
+                mark("particles_start")
+                N.call("hs_inject", inj_args, stream_ptr())
+                mark("inject")
+                N.call("hs_advect", N.HsAdvectArgs(
+                    n_patches=self.n_patches, nb=self.nb, buckets=N.ptr(self.buckets_dev),
+                    patches=N.ptr(self.patches_dev), dt=float(dt), rho=float(cfg.rho), g=float(cfg.g),
+                    in_=self._pool(buf), in_count=N.ptr(self.seg_len[lp]), stage=N.pool_struct(*self.stage),
+                    stage_count=N.ptr(self.stage_count), out=self._pool(buf ^ 1),
+                    out_count=N.ptr(self.compact_count), dropped=N.pool_struct(), dropped_count=0,
+                    e_out=N.ptr(self.e_out), splat=1, raw_layers=N.ptr(self.synth.raw),
+                    raw_layers_len=self.synth.pack.raw_len, layers=N.ptr(self.synth.layers),
+                    clamped=N.ptr(stats[3]), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
+                    tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status),
+                    keep_words=N.ptr(self.keep_words), in_seg_base=N.ptr(self.seg_base),
+                    out_slack_prefix=N.ptr(self.slack_prefix), raw_is_clear=1), stream_ptr())
+                self._layout(self.compact_count, self.seg_len[lp ^ 1])
+                mark("advect")
+            else:
+                ra = self._resident_args(buf, lp, dt, stats)
+                inj = self._side_stream("inject")
+                inj.wait_stream(main)
+                with torch.cuda.stream(inj):
+                    mark("inject_start")
+                    N.call("hs_inject", inj_args, stream_ptr())
+                    mark("inject")
+                    N.call("hs_append_resident", ra, stream_ptr())
+                    mark("append")
+                mark("particles_start")
+                N.call("hs_advect_resident", ra, stream_ptr())
+                mark("advect")
+                main.wait_stream(inj)
+                mark("join_inject")
+            N.call("hs_smooth", self.synth.smooth_args(), stream_ptr())
             mark("smooth")
+            clr = self._side_stream("clear")
+            clr.wait_stream(main)
+            with torch.cuda.stream(clr):        # raw layers are consumed: clear them for the next splat
+                self.synth.raw.zero_()
             if fork:
-                main.wait_stream(self._side_stream())
+                main.wait_stream(self._side_stream("fft"))
                 mark("join")
             bg = self.fft_ws
             N.call("hs_compose", N.HsComposeArgs(
@@ -316,21 +416,40 @@ class Simulation:
                 bg_spacing=self.config.fft_domain / self.config.fft_n if bg is not None else 1.0,
                 patch_height=N.ptr(self.patch_h), patch_normal=0,
                 blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
-                interior_sumsq=N.ptr(self.isum), interior_count=N.ptr(self.icount),
-                frame_advance=N.ptr(self.frame_dev)), st)
+                interior_sumsq=N.ptr(stats[1]), interior_count=N.ptr(stats[2]),
+                frame_advance=N.ptr(self.frame_dev)), stream_ptr())
             mark("compose")
+            main.wait_stream(clr)
             self._patch_n_frame = -1          # patch normals are derived lazily (patch_field)
         self._bg_n_frame = -1                 # so are the background normals (background)
         if self.fft_state is None and not self.n_patches:
-            N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(st))
+            N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(stream_ptr()))
 
-    def _side_stream(self):
-        if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=self.device)
-        return self._side
+    def _state(self) -> tuple:
+        if not self.n_patches:
+            return (0, 0, False)
+        return (self._buf, self._lp, self._since == self.compact_period - 1)
 
-    def _graph(self, parity: int):
-        g = self._graphs.get(parity)
+    def _advance_state(self, state: tuple) -> None:
+        if not self.n_patches:
+            return
+        buf, lp, compact = state
+        self._lp = lp ^ 1
+        if compact:
+            self._buf = buf ^ 1
+            self._since = 0
+        else:
+            self._since += 1
+
+    def _side_stream(self, name: str = "fft"):
+        if not hasattr(self, "_sides"):
+            self._sides = {}
+        if name not in self._sides:
+            self._sides[name] = torch.cuda.Stream(device=self.device)
+        return self._sides[name]
+
+    def _graph(self, state: tuple):
+        g = self._graphs.get(state)
         if g is None:
             if self.n_patches:
                 self._hr(self.config.dt)        # host->device uploads must precede capture
@@ -338,32 +457,46 @@ class Simulation:
             s = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.graph(g, stream=s):
-                self._enqueue_frame(parity, self.config.dt)
+                self._enqueue_frame(state, self.config.dt)
             torch.cuda.current_stream(self.device).wait_stream(s)
-            self._graphs[parity] = g
+            self._graphs[state] = g
         return g
 
-    def kernel_launches_per_frame(self) -> int:
-        """Library kernels one frame launches (csrc/*.cu): fft rows + cols
-        (+ periodic normals), inject, advect, smooth (1 or 3), compose,
-        advance_frame."""
-        k = 0
+    def prepare_graphs(self) -> None:
+        """Capture the frame graph of every resident-pool state up front
+        (buffer x length parity x compaction), so no capture happens while
+        stepping (capture enqueues nothing; it only records)."""
+        if not self.config.graph:
+            return
+        states = [(b, l, c) for b in (0, 1) for l in (0, 1) for c in (False, True)] if self.n_patches else [(0, 0, False)]
+        for st in states:
+            self._graph(st)
+
+    def kernel_launches_per_frame(self) -> float:
+        """Library kernels one frame launches on average (csrc/*.cu): fft rows
+        + cols; inject; in-place frames advect_resident + append_resident,
+        compaction frames (1 in K) advect count + scatter + layout; smooth
+        (1 or 3); compose.  (The raw-layer clear is a memset node.)"""
+        k = 0.0
         if self.fft_state is not None:
             k += 2                            # rows + columns (normals are lazy)
         if self.n_patches:
             pk = self.synth.pack
-            # inject, advect count + scatter, compose, smooth (fused + 2 wide passes)
-            k += 4 + (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
-        return max(k, 1)
+            K = self.compact_period
+            k += 1 + 1 + (2.0 * (K - 1) + 3.0) / K
+            k += (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
+        return max(k, 1.0)
 
     def timed_frame(self) -> dict:
         """Replay one frame from a CUDA graph that carries timing-event record
         nodes after every stage; returns {stage: ms} (synchronises).  Each
         stage is timed against the previous event on its own stream, so the
-        concurrently running background transform and particle chain are
-        both per-kernel device times without host launch gaps.  Used by
-        bench.py for the per-kernel roofline."""
-        key = ("timed", self._parity)
+        concurrently running branches are each per-kernel device times
+        without host launch gaps.  Used by bench.py for the per-kernel
+        roofline.  Returns the stages of an in-place frame (the K - 1 in K
+        common case); compaction frames are timed by `timed_compaction`."""
+        state = self._state()
+        key = ("timed",) + state
         if key not in self._graphs:
             if self.n_patches:
                 self._hr(self.config.dt)
@@ -378,23 +511,26 @@ class Simulation:
             s = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.graph(g, stream=s):
-                self._enqueue_frame(self._parity, self.config.dt, mark)
+                self._enqueue_frame(state, self.config.dt, mark)
             torch.cuda.current_stream(self.device).wait_stream(s)
             self._graphs[key] = (g, evs)
         g, evs = self._graphs[key]
         g.replay()
-        self._parity ^= 1
+        self._advance_state(state)
         self.frame += 1
         torch.cuda.synchronize(self.device)
         out, last = {}, {}
         for name, e, sid in evs:
-            if sid in last and not name.endswith("_start") and name != "join":
+            if sid in last and not name.endswith("_start") and not name.startswith("join"):
                 out[name] = out.get(name, 0.0) + last[sid].elapsed_time(e)
             last[sid] = e
-        if "fft_start" in [n for n, _, _ in evs] and "compose" in out:
-            first = next(e for n, e, _ in evs if n in ("fft_start", "particles_start"))
+        names = [n for n, _, _ in evs]
+        if "compose" in out:
+            first = next(e for n, e, _ in evs if n in ("fft_start", "particles_start", "inject_start"))
             end = next(e for n, e, _ in evs if n == "compose")
             out["frame"] = first.elapsed_time(end)
+        out["compaction"] = 1.0 if state[2] else 0.0
+        del names
         return out
 
     def step(self, dt: float | None = None, *, stats: bool = True):
@@ -404,11 +540,12 @@ class Simulation:
         cfg = self.config
         use_dt = cfg.dt if dt is None else float(dt)
         self.t = self.frame * use_dt
+        state = self._state()
         if cfg.graph and use_dt == cfg.dt and self.frame > 0:
-            self._graph(self._parity).replay()
+            self._graph(state).replay()
         else:
-            self._enqueue_frame(self._parity, use_dt)
-        self._parity ^= 1
+            self._enqueue_frame(state, use_dt)
+        self._advance_state(state)
         out = None
         if stats:
             out = self._snapshot()
@@ -423,7 +560,7 @@ class Simulation:
     def _snapshot(self) -> FrameStats:
         snap = {"fsum": self.fft_ws.sumsq.clone() if self.fft_ws is not None else torch.zeros(1, dtype=torch.float64)}
         if self.n_patches:
-            snap.update(counts=self.counts[self._parity].clone(), e_in=self.e_in.clone(), e_out=self.e_out.clone(),
+            snap.update(counts=self.live.clone(), e_in=self.e_in.clone(), e_out=self.e_out.clone(),
                         isum=self.isum.clone(), icount=self.icount.clone())
         return FrameStats(frame=self.frame, t=self.t, stage_ms={s: 0.0 for s in STAGES}, _snap=snap, _nb=self.nb,
                           _n_patches=self.n_patches, _fft_n=self.config.fft_n if self.fft_ws is not None else 0)
@@ -449,20 +586,37 @@ class Simulation:
             self._bg_n_frame = self.frame
         return self.fft_ws.field(self.fft_state)
 
+    @property
+    def counts(self) -> torch.Tensor:
+        """(n_patches * nb) live particles per (patch, bucket), on the device."""
+        return self.live
+
     def counts_host(self) -> np.ndarray:
         """(n_patches, nb) live particles per bucket (synchronises)."""
-        return self.counts[self._parity].cpu().numpy().reshape(self.n_patches, self.nb).astype(np.int64)
+        return self.live.cpu().numpy().reshape(self.n_patches, self.nb).astype(np.int64)
 
     def live_particles(self) -> int:
-        return int(self.counts[self._parity].sum().item()) if self.n_patches else 0
+        return int(self.live.sum().item()) if self.n_patches else 0
 
     def pool(self, k: int) -> ParticleSet:
-        """Patch k's current pool as a ParticleSet (views into device memory)."""
-        c = self.counts_host()[k]
-        lo, n = int(self.pool_base[k]), int(c.sum())
-        x, y, ux, uy, amp = self.pools[self._parity]
-        return ParticleSet.from_segments(x[lo:lo + n], y[lo:lo + n], ux[lo:lo + n], uy[lo:lo + n],
-                                         amp[lo:lo + n], c, self.device)
+        """Patch k's current pool as a ParticleSet, bucket-segmented in the
+        reference's stable order: the live slots of each resident segment,
+        holes dropped (the compaction the device defers, particles.py:167-178)."""
+        nb = self.nb
+        base = self.seg_base.cpu().numpy()[k * nb:(k + 1) * nb]
+        ln = self.seg_len[self._lp].cpu().numpy()[k * nb:(k + 1) * nb]
+        arrs = self.pools[self._buf]
+        parts = [[] for _ in range(5)]
+        counts = np.zeros(nb, np.int64)
+        for b in range(nb):
+            lo, n = int(base[b]), int(ln[b])
+            x = arrs[0][lo:lo + n]
+            keep = ~torch.isnan(x)
+            for q in range(5):
+                parts[q].append(arrs[q][lo:lo + n][keep])
+            counts[b] = int(keep.sum().item())
+        cat = [torch.cat(p_) if p_ else arrs[q][:0] for q, p_ in enumerate(parts)]
+        return ParticleSet.from_segments(*cat, counts, self.device)
 
     def _grid(self, buf: torch.Tensor, k: int, comps: int = 1) -> torch.Tensor:
         res, ny = self.synth.grids[k]

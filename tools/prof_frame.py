@@ -26,9 +26,11 @@ def main() -> int:
     sim.run_frames(3)
     torch.cuda.synchronize()
     sim.config = sim.config.__class__(**{**sim.config.__dict__, "graph": False})
+    torch.cuda.cudart().cudaProfilerStart()      # ncu --profile-from-start off
     for _ in range(args.frames):
         sim.step(stats=False)
     torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
     sim.check()
     print("live", sim.live_particles(), "launches/frame", sim.kernel_launches_per_frame())
     return 0

@@ -9,7 +9,7 @@ for r in rows:
     if not r: continue
     if r[0] == "ID": hdr = r; continue
     if hdr is None or len(r) < len(hdr): continue
-    d = dict(zip(hdr, r)); name = d["Kernel Name"].split("(")[0].replace("void ", "")
+    d = dict(zip(hdr, r)); name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("hs::", "")
     data[name][d["Metric Name"]].append(float(d["Metric Value"].replace(",", "")))
 out = {}
 for k, m in data.items():
