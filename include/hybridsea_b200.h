@@ -80,7 +80,11 @@ typedef struct {
     int stage_capacity;
     int res, ny;         /* node grid: res along x, ny along y */
     int layer_base;      /* first HsLayer of this patch */
-    int pad0;
+    int track;           /* source this patch follows (harness.py:115-123), -1: static */
+    double sx0, sy0;     /* synthesis origin: where this frame's layers, heights and blend
+                            sit.  Equal to (x0, y0) except for a tracking patch, whose region
+                            moves onto its source AFTER injection, advection and emission
+                            (hs_track / hs_emit); x0..y1 is the region those stages use */
 } HsPatch;
 
 /* One per (patch, bucket) synthesis layer (LayerPlan, patch_synthesis.py:227-258). */
@@ -240,6 +244,53 @@ typedef struct {
 } HsResidentArgs;
 HS_API int hs_advect_resident(const HsResidentArgs* a, void* stream);
 HS_API int hs_append_resident(const HsResidentArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Kinematic emitting bodies: the reference's per-frame
+ * buoyancy_step + emit_from_motion + _retrack_patches (interaction.py:140,
+ * 175-231; harness.py:115-123,155-167) for bodies moving at a constant
+ * velocity with a fixed displaced-volume change per frame.  Everything that
+ * is constant per source (energy split, fan directions, amplitudes, buckets)
+ * is formed on the host with the reference's own numpy expressions; the device
+ * moves the sources, finds each one's owning patch, appends the fans to the
+ * resident segments (after this frame's injected particles), splats them,
+ * books the energy and moves tracking patches.                              */
+typedef struct {
+    double vx, vy;            /* horizontal velocity: position += v dt each frame (interaction.py:140) */
+    double hull_extent;       /* fan radius around the source (m) */
+    double e_ring, e_wake;    /* energy booked per frame per branch, 0 = branch silent */
+    double amp_ring, amp_wake;/* signed crest amplitude of each branch (fp64) */
+    int n_ring, n_wake;       /* fan sizes */
+    int ring_bucket, wake_bucket;
+    int dir_off;              /* ring directions, then wake directions, in HsEmitArgs.dirs */
+    int pad;
+} HsSource;
+
+#define HS_MAX_SOURCES 1024
+typedef struct {
+    int n_sources, n_patches, nb;
+    const HsSource* sources;
+    const double* dirs;       /* [total fan size * 2] unit directions (ux, uy) */
+    const double* pos_in;     /* [n_sources*2] positions after the previous frame */
+    double* pos_out;          /* [n_sources*2] positions after this frame (written by hs_emit) */
+    HsPatch* patches;         /* hs_track moves tracking patches */
+    const HsBucket* buckets;
+    double dt, beta, rho, g;
+    HsPool pool; const int* seg_base; const int* seg_cap;
+    int* len;                 /* [n_patches*nb] slots in use; emitted particles are appended */
+    int* live;
+    double* e_in;
+    float* raw_layers; const HsLayer* layers; int* clamped;
+    int* status;
+} HsEmitArgs;
+/* Frame start: tracking patches adopt last frame's synthesis origin as their
+ * region, and take this frame's synthesis origin from their source's new
+ * position, _snap(p - l/2, texel) (harness.py:65-66,115-123).               */
+HS_API int hs_track(const HsEmitArgs* a, void* stream);
+/* After advection and this frame's appends: move every source, emit into its
+ * owning patch (first patch whose region contains it, particles.py:71-74),
+ * splat at the synthesis origin, book e_in (harness.py:155-163).            */
+HS_API int hs_emit(const HsEmitArgs* a, void* stream);
 
 /* Segment table after a compaction (or at start, count = NULL): segment
  * (p, b) gets base = pool_base + sum_{b'<b} count + slack_prefix, cap = count

@@ -20,7 +20,7 @@ import math
 
 import numpy as np
 
-from . import blend_ref, ocean_ref, particles_ref, spectrum_ref, synth_ref
+from . import blend_ref, emit_ref, ocean_ref, particles_ref, spectrum_ref, synth_ref
 
 
 def build_params(sc: dict) -> spectrum_ref.Params:
@@ -61,6 +61,12 @@ class OracleScene:
                 band=sc.get("fft_band"))
         self.background = None
         self.fields = []
+        # kinematic emitting bodies + patch tracking (emit_ref; harness.py:115-123,155-167)
+        self.sources = [emit_ref.Source(np.array(d["position"], dtype=float), np.array(d["velocity"], dtype=float),
+                                        d["hull_extent"], d["volume_rate"], d["submersion"],
+                                        d.get("wake_count", 0), d.get("energy_scale", 1.0))
+                        for d in sc.get("sources", [])]
+        self.track = list(sc.get("patch_track") or [-1] * len(self.patches))
 
     def step(self, dt: float | None = None, synth: bool = True, fft: bool = True) -> dict:
         sc = self.sc
@@ -77,6 +83,21 @@ class OracleScene:
                                              t=t, beta=sc["trough_fraction"]))
         for pc, pool, led in zip(self.patches, self.pools, self.ledgers):
             particles_ref.advect(pool, self.bk, dt, pc, led, self.p.g)
+        # interaction stage (harness.py:155-167): kinematic buoyancy step, emission
+        # into the owning patch (booked like injection), then patch retracking
+        for src in self.sources:
+            src.position = src.position + src.velocity[:2] * dt
+            owner = next((k for k, pc in enumerate(self.patches) if emit_ref.contains(pc, src.position)), None)
+            if owner is None:
+                continue
+            events, emitted = emit_ref.emit(src, self.bk.radius, self.bk.n_theta, sc["rho"], self.p.g,
+                                            sc["trough_fraction"])
+            self.pools[owner].append(emitted)
+            for ev in events:
+                self.ledgers[owner].e_in[ev.bucket] += ev.energy
+        for k, j in enumerate(self.track):
+            if 0 <= j < len(self.sources):
+                self.patches[k] = emit_ref.retrack(self.patches[k], self.res[k], self.sources[j])
         if synth:
             self.fields = []
             for pc, pool, r, pl in zip(self.patches, self.pools, self.res, self.plans):

@@ -132,14 +132,14 @@ def compose_tile_info(grids: list[tuple[int, int]]) -> np.ndarray:
 
 
 def patch_struct(region, res: int, *, pool_base=0, pool_capacity=0, stage_base=0, stage_capacity=0,
-                 grid_base=0, layer_base=0) -> N.HsPatch:
+                 grid_base=0, layer_base=0, track=-1) -> N.HsPatch:
     texel, ny = grid_dims(region, res)
     lo = region.min_corner
     hi = region.max_corner
     return N.HsPatch(float(lo[0]), float(lo[1]), float(hi[0]), float(hi[1]), float(region.l1),
                      float(region.l2), float(region.margin), float(texel), int(pool_base), int(stage_base),
                      int(grid_base), int(pool_capacity), int(stage_capacity), int(res), int(ny),
-                     int(layer_base), 0)
+                     int(layer_base), int(track), float(lo[0]), float(lo[1]))
 
 
 def structs_to_device(items: list, device) -> torch.Tensor:

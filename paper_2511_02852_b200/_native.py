@@ -20,6 +20,7 @@ HS_STATUS_POOL_OVERFLOW = 1
 HS_STATUS_STAGE_OVERFLOW = 2
 HS_MAX_BUCKETS = 32
 HS_MAX_PATCHES = 256
+HS_MAX_SOURCES = 1024
 HS_SMOOTH_FUSED_MAX_H = 40
 
 vp = C.c_void_p
@@ -37,7 +38,7 @@ class HsPatch(C.Structure):
     _fields_ = [("x0", dbl), ("y0", dbl), ("x1", dbl), ("y1", dbl), ("l1", dbl), ("l2", dbl),
                 ("margin", dbl), ("texel", dbl), ("pool_base", i64), ("stage_base", i64),
                 ("grid_base", i64), ("pool_capacity", i32), ("stage_capacity", i32), ("res", i32),
-                ("ny", i32), ("layer_base", i32), ("pad0", i32)]
+                ("ny", i32), ("layer_base", i32), ("track", i32), ("sx0", dbl), ("sy0", dbl)]
 
 
 class HsLayer(C.Structure):
@@ -82,6 +83,19 @@ class HsResidentArgs(C.Structure):
                 ("tile_map", vp), ("max_tiles", i32), ("len_in", vp), ("len_out", vp), ("live", vp),
                 ("stage", HsPool), ("stage_count", vp), ("e_out", vp), ("raw_layers", vp), ("layers", vp),
                 ("clamped", vp), ("status", vp)]
+
+
+class HsSource(C.Structure):
+    _fields_ = [("vx", dbl), ("vy", dbl), ("hull_extent", dbl), ("e_ring", dbl), ("e_wake", dbl),
+                ("amp_ring", dbl), ("amp_wake", dbl), ("n_ring", i32), ("n_wake", i32), ("ring_bucket", i32),
+                ("wake_bucket", i32), ("dir_off", i32), ("pad", i32)]
+
+
+class HsEmitArgs(C.Structure):
+    _fields_ = [("n_sources", i32), ("n_patches", i32), ("nb", i32), ("sources", vp), ("dirs", vp),
+                ("pos_in", vp), ("pos_out", vp), ("patches", vp), ("buckets", vp), ("dt", dbl), ("beta", dbl),
+                ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp), ("len", vp),
+                ("live", vp), ("e_in", vp), ("raw_layers", vp), ("layers", vp), ("clamped", vp), ("status", vp)]
 
 
 class HsLayoutArgs(C.Structure):
@@ -132,15 +146,15 @@ class HsFinishArgs(C.Structure):
 
 ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
-               HsLayoutArgs]
+               HsLayoutArgs, HsSource, HsEmitArgs]
 
-EXPECTED_SIZES = {HsBucket: 64, HsPatch: 112, HsLayer: 64, HsPool: 40}
+EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource: 80}
 
 # every symbol include/hybridsea_b200.h declares
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
-           "hs_resident_layout"]
+           "hs_resident_layout", "hs_track", "hs_emit"]
 
 _lib = None
 

@@ -52,6 +52,8 @@ extern "C" HS_API int hs_struct_size(int which) {
         case 12: return (int)sizeof(HsFinishArgs);
         case 13: return (int)sizeof(HsResidentArgs);
         case 14: return (int)sizeof(HsLayoutArgs);
+        case 15: return (int)sizeof(HsSource);
+        case 16: return (int)sizeof(HsEmitArgs);
         default: return -1;
     }
 }

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
     if (a.frame_advance && tile == 0 && tid == 0) *a.frame_advance += 1;
     const int* ti = a.tile_info + 3 * tile;
     const int p = ti[0], i0 = ti[1], j0 = ti[2];
-    const HsPatch P = a.patches[p];
+    const HsPatch P = synth_view(a.patches[p]);   // the retracked rectangle (tracking patches)
     const bool have_bg = a.bg_height != nullptr && a.blend_mode;
     const int bm = a.bg_n - 1;
     const double inv_sp = have_bg ? 1.0 / a.bg_spacing : 0.0;

@@ -164,6 +164,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// The patch as its synthesised surface sees it: the rectangle at the
+// synthesis origin (HsPatch.sx0/sy0; max corner = min + (l1, l2) as
+// PatchRegion.max_corner, particles.py:63-65)
+__device__ __forceinline__ HsPatch synth_view(HsPatch P) {
+    P.x0 = P.sx0;
+    P.y0 = P.sy0;
+    P.x1 = P.sx0 + P.l1;
+    P.y1 = P.sy0 + P.l2;
+    return P;
+}
+
 __device__ __forceinline__ float smoothstep01(float t) {
     t = fminf(fmaxf(t, 0.f), 1.f);
     return t * t * (3.f - 2.f * t);

@@ -267,7 +267,7 @@ __device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLay
 __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
                                           double x, double y, float amp, int* clamp_acc) {
     SplatLayer S{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1), L.raw_pitch, L.pad};
-    splat_at(raw, S, P.x0, P.y0, x, y, amp, clamp_acc);
+    splat_at(raw, S, P.sx0, P.sy0, x, y, amp, clamp_acc);
 }
 
 // Persistent CTAs take tiles of ADV_TILE virtual items in order from a global
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                         atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
                     }
                     atomicAdd(&keep_hist[b], 1);
-                    if (a.splat) splat_at(raw, sl_s[b], P.x0, P.y0, x, y, am, &clamp_local);
+                    if (a.splat) splat_at(raw, sl_s[b], P.sx0, P.sy0, x, y, am, &clamp_local);
                 } else {
                     if (am > 0.f) {
                         // crest despawn energy rho g A^2 pi r^2 / 8 (particles.py:322-327)
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
             } else {
                 atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             }
-            if (a.splat) splat_at(raw, T.sl[b], P.x0, P.y0, x, y, am, &clamp_local);
+            if (a.splat) splat_at(raw, T.sl[b], P.sx0, P.sy0, x, y, am, &clamp_local);
         } else if (x == x) {                             // a despawn (NaN marks a resident-pool hole)
             if (am > 0.f) {
                 const double amp = (double)am;          // crest despawn energy (particles.py:322-327)
@@ -794,6 +794,7 @@ __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResid
         const int p = s / a.nb, b = s - p * a.nb;
         const HsPatch* P = a.patches + p;
         const double x0 = __ldg(&P->x0), y0 = __ldg(&P->y0), x1 = __ldg(&P->x1), y1 = __ldg(&P->y1);
+        const double sx0 = __ldg(&P->sx0), sy0 = __ldg(&P->sy0);     // synthesis origin (tracking patches)
         const HsBucket* Bk = a.buckets + b;
         const double step = dmul(__ldg(&Bk->speed), a.dt);            // speeds * dt (particles.py:312)
         const double rad = __ldg(&Bk->radius);
@@ -817,7 +818,7 @@ __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResid
                 px[o] = nx;
                 py[o] = ny;
 #ifndef HS_EXP_NOSPLAT
-                splat_at(a.raw_layers, sl, x0, y0, nx, ny, am[it], &clamp_local);
+                splat_at(a.raw_layers, sl, sx0, sy0, nx, ny, am[it], &clamp_local);
 #endif
             } else {
                 px[o] = __longlong_as_double(0x7ff8000000000000LL);       // hole: stable compaction is deferred
@@ -906,7 +907,7 @@ __global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResident
         }
         if (keep) {
             atomicAdd(&kept_s[b], 1);
-            splat_at(a.raw_layers, sl_s[b], P.x0, P.y0, nx, ny, am, &clamp_local);
+            splat_at(a.raw_layers, sl_s[b], P.sx0, P.sy0, nx, ny, am, &clamp_local);
         } else if (am > 0.f) {
             const double amp = (double)am;
             atomicAdd(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2_s[b]);
@@ -969,6 +970,147 @@ __global__ void __launch_bounds__(1024) resident_layout_kernel(HsLayoutArgs a) {
         if (lane < nb)
             for (int k = 0; k < nt && first + k < a.max_tiles; ++k)
                 tmap[first + k] = make_int4(s, k, a.seg_base[s] + k * RES_TILE, 0);
+    }
+}
+
+// ============================================================ emission ==
+// Kinematic emitting bodies (HsEmitArgs).  Positions follow the reference's
+// buoyancy_step update for a constant velocity, position += velocity * dt
+// (interaction.py:140), in fp64 without contraction.
+__device__ __forceinline__ void source_step(const HsEmitArgs& a, int s, double& px, double& py) {
+    const HsSource& S = a.sources[s];
+    px = dadd(a.pos_in[2 * s], dmul(S.vx, a.dt));
+    py = dadd(a.pos_in[2 * s + 1], dmul(S.vy, a.dt));
+}
+
+// owning patch: the first whose region contains the point, inclusive
+// (Simulation.owning_patch, harness.py:125-129; PatchRegion.contains, particles.py:71-74)
+__device__ __forceinline__ int owner_of(const HsEmitArgs& a, double px, double py) {
+    for (int p = 0; p < a.n_patches; ++p) {
+        const HsPatch& P = a.patches[p];
+        if (px >= P.x0 && px <= P.x1 && py >= P.y0 && py <= P.y1) return p;
+    }
+    return -1;
+}
+
+// Frame start (one thread per patch): a tracking patch's region becomes last
+// frame's synthesis origin, and its synthesis origin moves to
+// _snap(p - l/2, texel) of its source's new position (harness.py:65-66,115-123).
+__global__ void track_kernel(HsEmitArgs a) {
+    for (int p = threadIdx.x; p < a.n_patches; p += blockDim.x) {
+        HsPatch* P = a.patches + p;
+        const int s = P->track;
+        if (s < 0 || s >= a.n_sources) continue;
+        const double x0 = P->sx0, y0 = P->sy0;
+        P->x0 = x0;
+        P->y0 = y0;
+        P->x1 = dadd(x0, P->l1);
+        P->y1 = dadd(y0, P->l2);
+        double px, py;
+        source_step(a, s, px, py);
+        P->sx0 = dmul(rint(__ddiv_rn(dsub(px, dmul(P->l1, 0.5)), P->texel)), P->texel);
+        P->sy0 = dmul(rint(__ddiv_rn(dsub(py, dmul(P->l2, 0.5)), P->texel)), P->texel);
+    }
+}
+
+// One CTA per source: find its owner and where its fans go (after the
+// fans of earlier sources with the same owner and bucket, ring before wake,
+// interaction.py:218-230), then write crests and troughs
+// (interaction.py:203-216) and splat them at the synthesis origin.
+__global__ void __launch_bounds__(256) emit_kernel(HsEmitArgs a) {
+    const int s = blockIdx.x, nb = a.nb;
+    __shared__ int before[HS_MAX_BUCKETS];
+    __shared__ int own_s, clamp_s;
+    __shared__ double px_s, py_s;
+    const int m = a.beta != 0.0 ? 2 : 1;
+    if (threadIdx.x < HS_MAX_BUCKETS) before[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        double px, py;
+        source_step(a, s, px, py);
+        px_s = px; py_s = py;
+        own_s = owner_of(a, px, py);
+        clamp_s = 0;
+    }
+    __syncthreads();
+    const int own = own_s;
+    if (own < 0) return;
+    for (int q = threadIdx.x; q < s; q += blockDim.x) {
+        double qx, qy;
+        source_step(a, q, qx, qy);
+        if (owner_of(a, qx, qy) != own) continue;
+        const HsSource& Q = a.sources[q];
+        if (Q.e_ring > 0.0) atomicAdd(&before[Q.ring_bucket], m * Q.n_ring);
+        if (Q.e_wake > 0.0) atomicAdd(&before[Q.wake_bucket], m * Q.n_wake);
+    }
+    __syncthreads();
+    const HsSource S = a.sources[s];
+    const HsPatch& P = a.patches[own];
+    const double px = px_s, py = py_s;
+    int clamp_local = 0;
+#pragma unroll 1
+    for (int branch = 0; branch < 2; ++branch) {
+        const bool ring = branch == 0;
+        if ((ring ? S.e_ring : S.e_wake) <= 0.0) continue;
+        const int b = ring ? S.ring_bucket : S.wake_bucket;
+        const int n = ring ? S.n_ring : S.n_wake;
+        const double amp = ring ? S.amp_ring : S.amp_wake;
+        const int seg = own * nb + b;
+        int off = before[b];
+        if (!ring && S.e_ring > 0.0 && S.ring_bucket == b) off += m * S.n_ring;
+        const long long base = (long long)a.seg_base[seg] + a.len[seg] + off;
+        if (a.len[seg] + off + m * n > a.seg_cap[seg]) {
+            if (threadIdx.x == 0) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+            continue;
+        }
+        const double r = a.buckets[b].radius;
+        const HsLayer L = a.layers[P.layer_base + b];
+        const SplatLayer sl{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1),
+                            L.raw_pitch, L.pad};
+        const double* dirs = a.dirs + 2 * (S.dir_off + (ring ? 0 : S.n_ring));
+        const float ca = (float)amp, ta = (float)dmul(-a.beta, amp);
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+            const double ux = dirs[2 * k], uy = dirs[2 * k + 1];
+            const double cx = dadd(px, dmul(S.hull_extent, ux));      // center + hull * dirs
+            const double cy = dadd(py, dmul(S.hull_extent, uy));
+            long long o = base + k;
+            a.pool.x[o] = cx; a.pool.y[o] = cy; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = ca;
+            splat_at(a.raw_layers, sl, P.sx0, P.sy0, cx, cy, ca, &clamp_local);
+            if (m == 2) {                                              // trailing trough, -beta * amp
+                const double tx = dsub(cx, dmul(r, ux)), ty = dsub(cy, dmul(r, uy));
+                o += n;
+                a.pool.x[o] = tx; a.pool.y[o] = ty; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = ta;
+                splat_at(a.raw_layers, sl, P.sx0, P.sy0, tx, ty, ta, &clamp_local);
+            }
+        }
+    }
+    if (clamp_local) atomicAdd(&clamp_s, clamp_local);
+    __syncthreads();
+    if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[own], clamp_s);
+}
+
+// After every emit CTA: positions, segment lengths, live counts and the
+// energy books, sources in order, ring before wake (harness.py:155-167).
+__global__ void emit_commit_kernel(HsEmitArgs a) {
+    if (threadIdx.x != 0) return;
+    const int m = a.beta != 0.0 ? 2 : 1;
+    for (int s = 0; s < a.n_sources; ++s) {
+        double px, py;
+        source_step(a, s, px, py);
+        a.pos_out[2 * s] = px;
+        a.pos_out[2 * s + 1] = py;
+        const int own = owner_of(a, px, py);
+        if (own < 0) continue;
+        const HsSource& S = a.sources[s];
+        for (int branch = 0; branch < 2; ++branch) {
+            const double e = branch == 0 ? S.e_ring : S.e_wake;
+            if (e <= 0.0) continue;
+            const int seg = own * a.nb + (branch == 0 ? S.ring_bucket : S.wake_bucket);
+            const int cnt = m * (branch == 0 ? S.n_ring : S.n_wake);
+            if (a.len[seg] + cnt > a.seg_cap[seg]) continue;          // overflow flagged by emit_kernel
+            a.len[seg] += cnt;
+            a.live[seg] += cnt;
+            a.e_in[seg] = dadd(a.e_in[seg], e);
+        }
     }
 }
 
@@ -1095,6 +1237,38 @@ extern "C" int hs_resident_layout(const HsLayoutArgs* a, void* stream) {
     HS_CHECK_ARG(a->patches && a->slack && a->slack_prefix && a->seg_base && a->seg_cap && a->len && a->live &&
                  a->tile_map && a->status && a->max_tiles > 0, "hs_resident_layout: missing buffer");
     resident_layout_kernel<<<1, 1024, 0, as_stream(stream)>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+static int check_emit(const HsEmitArgs* a, const char* who) {
+    HS_CHECK_ARG(a != nullptr, "%s: null args", who);
+    HS_CHECK_ARG(a->n_sources >= 0 && a->n_sources <= HS_MAX_SOURCES, "%s: n_sources out of range", who);
+    HS_CHECK_ARG(a->n_patches >= 0 && a->n_patches <= HS_MAX_PATCHES, "%s: n_patches out of range", who);
+    HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "%s: nb out of range", who);
+    HS_CHECK_ARG(a->dt > 0.0, "%s: dt must be positive", who);
+    HS_CHECK_ARG(a->n_sources == 0 || (a->sources && a->pos_in && a->pos_out), "%s: missing source buffers", who);
+    HS_CHECK_ARG(a->n_patches == 0 || a->patches, "%s: missing patches", who);
+    return 0;
+}
+
+extern "C" int hs_track(const HsEmitArgs* a, void* stream) {
+    if (int rc = check_emit(a, "hs_track")) return rc;
+    if (a->n_patches == 0 || a->n_sources == 0) return 0;
+    track_kernel<<<1, 256, 0, as_stream(stream)>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_emit(const HsEmitArgs* a, void* stream) {
+    if (int rc = check_emit(a, "hs_emit")) return rc;
+    if (a->n_sources == 0 || a->n_patches == 0) return 0;
+    HS_CHECK_ARG(a->dirs && a->buckets && a->pool.x && a->pool.amp && a->seg_base && a->seg_cap && a->len &&
+                 a->live && a->e_in && a->raw_layers && a->layers && a->status, "hs_emit: missing buffer");
+    cudaStream_t st = as_stream(stream);
+    emit_kernel<<<a->n_sources, 256, 0, st>>>(*a);
+    HS_LAUNCH_CHECK();
+    emit_commit_kernel<<<1, 32, 0, st>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

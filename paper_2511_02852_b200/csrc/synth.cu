@@ -236,7 +236,7 @@ __device__ void sample_surface(const BgView& bg, int n_patches, const HsPatch* _
                                double x, double y, float& h, float3& nv) {
     sample_bg(bg, x, y, h, nv);
     for (int p = 0; p < n_patches; ++p) {
-        const HsPatch P = patches[p];
+        const HsPatch P = synth_view(patches[p]);
         const double w = blend_w(P, x, y);
         if (!(w > 0.0)) continue;
         float hp; float3 q;
@@ -257,7 +257,7 @@ __global__ void sample_kernel(HsSampleArgs a) {
     BgView bg{a.bg_height, a.bg_normal, a.bg_n, a.bg_spacing, a.bg_x0, a.bg_y0};
     float h; float3 nv;
     if (a.clamped_only) {
-        sample_clamped_at(a.patches[0], a.patch_height, a.patch_normal, a.points[2 * k], a.points[2 * k + 1], h, nv);
+        sample_clamped_at(synth_view(a.patches[0]), a.patch_height, a.patch_normal, a.points[2 * k], a.points[2 * k + 1], h, nv);
     } else {
         sample_surface(bg, a.n_patches, a.patches, a.patch_height, a.patch_normal,
                        a.points[2 * k], a.points[2 * k + 1], h, nv);

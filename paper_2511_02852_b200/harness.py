@@ -23,6 +23,7 @@ path and rejected here.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 import time
 from dataclasses import dataclass, field
@@ -39,6 +40,7 @@ from .errors import CapacityError, ConfigError
 from .fft_background import FftWorkspace, HeightField, fft_args, init_fft
 from .particles import PatchRegion, PhiloxStream, ParticleSet
 from .patch_synthesis import SynthWorkspace, plan_layers
+from .interaction import source_structs
 from .spectrum import DirectionalSpectrum, build_buckets, derive_params, log_buckets
 
 STAGES = ("fft", "inject", "advect", "interact", "synth", "blend", "output")
@@ -171,17 +173,44 @@ class Simulation:
         per_member = 2 if cfg.trough_fraction != 0.0 else 1
         max_new = []                     # per patch, per bucket: particles one frame can append
         explicit = pool_capacity is not None or bool(cfg.pool_capacity)
+        # kinematic emitting sources (interaction.py)
+        self.sources = tuple(cfg.sources) if self.n_patches else ()
+        self.n_sources = len(self.sources)
+        if self.n_sources > N.HS_MAX_SOURCES:
+            raise ConfigError(f"at most {N.HS_MAX_SOURCES} sources per device")
+        src_structs, src_dirs, src_plans = source_structs(self.sources, self.table, cfg.rho, cfg.g)
+        self._tracking = any(pc.track_source >= 0 for pc in pcs)
+        emit_new = np.zeros((self.n_patches, self.nb), np.int64)     # per frame
+        emit_pop = np.zeros(self.n_patches)
+        tracker = {pc.track_source: k for k, pc in enumerate(pcs) if pc.track_source >= 0}
+        for j, (src, pl) in enumerate(zip(self.sources, src_plans)):
+            # a tracked source only ever emits into its patch; others may enter any patch
+            cand = [tracker[j]] if j in tracker else range(self.n_patches)
+            vt = float(np.hypot(*src.velocity[:2])) if j in tracker else 0.0
+            for key_e, key_d, key_b in (("e_ring", "ring_dirs", "ring_bucket"), ("e_wake", "wake_dirs", "wake_bucket")):
+                if pl[key_e] <= 0.0:
+                    continue
+                n, b = per_member * len(pl[key_d]), pl[key_b]
+                bk = self.table.buckets[b]
+                for k in cand:
+                    emit_new[k, b] += n
+                    side = 0.5 * (self.regions[k].l1 + self.regions[k].l2)
+                    stay = (side + 2.0 * bk.radius) / (bk.speed + vt) / cfg.dt
+                    if j not in tracker and np.hypot(*src.velocity[:2]) > 0:
+                        stay = min(stay, 2.0 * side / float(np.hypot(*src.velocity[:2])) / cfg.dt)
+                    emit_pop[k] += n * stay
         for k, r in enumerate(self.regions):
             hr_max = half_rates(r, self.table.omegas, 0.1, cfg.g)       # dt <= 0.1 (config.py validate)
             mg = max_groups_per_step(hr_max)
             self.member_cap = max(self.member_cap, mg * self.table.n_theta)
-            max_new.append((np.floor(hr_max) + 1.0).sum(axis=1).astype(np.int64) * self.table.n_theta * per_member)
+            max_new.append((np.floor(hr_max) + 1.0).sum(axis=1).astype(np.int64) * self.table.n_theta * per_member
+                           + emit_new[k])
             if pool_capacity is not None:
                 cap = int(pool_capacity)
             elif cfg.pool_capacity:
                 cap = cfg.pool_capacity
             else:
-                cap = max(4096, int(1.6 * estimate_population(self.table, r, cfg.trough_fraction)))
+                cap = max(4096, int(1.6 * (estimate_population(self.table, r, cfg.trough_fraction) + emit_pop[k])))
                 cap += RESIDENT_PERIOD * int(max_new[-1].sum())
                 cap = -(-cap // 1024) * 1024
             self.pool_caps.append(cap)
@@ -205,8 +234,16 @@ class Simulation:
             for k, (r, res) in enumerate(zip(self.regions, self.res)):
                 structs.append(patch_struct(r, res, pool_base=self.pool_base[k], pool_capacity=self.pool_caps[k],
                                             stage_base=self.stage_base[k], stage_capacity=self.stage_caps[k],
-                                            grid_base=self.synth.grid_base[k], layer_base=k * self.nb))
+                                            grid_base=self.synth.grid_base[k], layer_base=k * self.nb,
+                                            track=pcs[k].track_source))
             self.patches_dev = structs_to_device(structs, dev)
+            if self.n_sources:
+                self.sources_dev = structs_to_device(src_structs, dev)
+                self.src_dirs = torch.from_numpy(src_dirs.reshape(-1).copy()).to(dev) if src_dirs.size else \
+                    torch.zeros(2, dtype=torch.float64, device=dev)
+                p0 = torch.tensor(np.array([c.position for c in self.sources], dtype=np.float64).reshape(-1),
+                                  device=dev)
+                self.src_pos = [p0, p0.clone()]
             f64 = lambda n: torch.zeros(max(1, n), dtype=torch.float64, device=dev)  # noqa: E731
             f32 = lambda n: torch.zeros(max(1, n), dtype=torch.float32, device=dev)  # noqa: E731
             self.pools = [[f64(total_pool), f64(total_pool), f64(total_pool), f64(total_pool), f32(total_pool)]
@@ -265,6 +302,19 @@ class Simulation:
             self._hr_cache[dt] = torch.from_numpy(hr).to(self.device)
         return self._hr_cache[dt]
 
+    def current_regions(self) -> list:
+        """The patch rectangles the last frame synthesised (tracking patches
+        move with their source: the device-side synthesis origin, synchronises)."""
+        if not (self.n_sources and self._tracking):
+            return self.regions
+        raw = self.patches_dev.cpu().numpy().tobytes()
+        sz = C.sizeof(N.HsPatch)
+        out = []
+        for k, r in enumerate(self.regions):
+            st = N.HsPatch.from_buffer_copy(raw[k * sz:(k + 1) * sz])
+            out.append(PatchRegion((st.sx0, st.sy0), r.l1, r.l2, r.margin))
+        return out
+
     def _init_boxes(self) -> None:
         cfg = self.config
         if self.fft_state is None:
@@ -272,7 +322,7 @@ class Simulation:
             return
         n, spacing = cfg.fft_n, cfg.fft_domain / cfg.fft_n
         boxes, pre = [], [0]
-        for r in self.regions:       # harness.py:230-233
+        for r in self.current_regions():       # harness.py:230-233
             lo = np.clip(np.floor(r.min_corner / spacing).astype(int), 0, n)
             hi = np.clip(np.ceil(r.max_corner / spacing).astype(int) + 1, 0, n)
             boxes += [lo[0], hi[0], lo[1], hi[1]]
@@ -309,6 +359,17 @@ class Simulation:
             slack=N.ptr(self.slack), slack_prefix=N.ptr(self.slack_prefix), seg_base=N.ptr(self.seg_base),
             seg_cap=N.ptr(self.seg_cap), len=N.ptr(len_out), live=N.ptr(self.live), tile_map=N.ptr(self.tile_map),
             max_tiles=self.res_tiles, status=N.ptr(self.status)), stream_ptr())
+
+    def _emit_args(self, buf: int, lp: int, dt: float, stats) -> N.HsEmitArgs:
+        cfg = self.config
+        return N.HsEmitArgs(
+            n_sources=self.n_sources, n_patches=self.n_patches, nb=self.nb, sources=N.ptr(self.sources_dev),
+            dirs=N.ptr(self.src_dirs), pos_in=N.ptr(self.src_pos[lp]), pos_out=N.ptr(self.src_pos[lp ^ 1]),
+            patches=N.ptr(self.patches_dev), buckets=N.ptr(self.buckets_dev), dt=float(dt),
+            beta=float(cfg.trough_fraction), rho=float(cfg.rho), g=float(cfg.g), pool=self._pool(buf),
+            seg_base=N.ptr(self.seg_base), seg_cap=N.ptr(self.seg_cap), len=N.ptr(self.seg_len[lp ^ 1]),
+            live=N.ptr(self.live), e_in=N.ptr(self.e_in), raw_layers=N.ptr(self.synth.raw),
+            layers=N.ptr(self.synth.layers), clamped=N.ptr(stats[3]), status=N.ptr(self.status))
 
     def _resident_args(self, buf: int, lp: int, dt: float, stats) -> N.HsResidentArgs:
         return N.HsResidentArgs(
@@ -355,6 +416,8 @@ class Simulation:
         if self.n_patches:
             stats, nxt = self._stat_sets[lp], self._stat_sets[lp ^ 1]
             cfg = self.config
+            if self.n_sources and self._tracking:       # before every stage that reads the patch rectangles
+                N.call("hs_track", self._emit_args(buf, lp, dt, stats), stream_ptr())
             inj_args = N.HsInjectArgs(
                 n_patches=self.n_patches, nb=self.nb, n_theta=self.table.n_theta, buckets=N.ptr(self.buckets_dev),
                 patches=N.ptr(self.patches_dev), half_rate=N.ptr(self._hr(dt)),
@@ -380,6 +443,8 @@ class Simulation:
                     keep_words=N.ptr(self.keep_words), in_seg_base=N.ptr(self.seg_base),
                     out_slack_prefix=N.ptr(self.slack_prefix), raw_is_clear=1), stream_ptr())
                 self._layout(self.compact_count, self.seg_len[lp ^ 1])
+                if self.n_sources:
+                    N.call("hs_emit", self._emit_args(buf ^ 1, lp, dt, stats), stream_ptr())
                 mark("advect")
             else:
                 ra = self._resident_args(buf, lp, dt, stats)
@@ -390,6 +455,8 @@ class Simulation:
                     N.call("hs_inject", inj_args, stream_ptr())
                     mark("inject")
                     N.call("hs_append_resident", ra, stream_ptr())
+                    if self.n_sources:
+                        N.call("hs_emit", self._emit_args(buf, lp, dt, stats), stream_ptr())
                     mark("append")
                 mark("particles_start")
                 N.call("hs_advect_resident", ra, stream_ptr())
@@ -484,6 +551,8 @@ class Simulation:
             pk = self.synth.pack
             K = self.compact_period
             k += 1 + 1 + (2.0 * (K - 1) + 3.0) / K
+            if self.n_sources:
+                k += 2 + (1 if self._tracking else 0)      # emit + commit (+ track)
             k += (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
         return max(k, 1.0)
 
@@ -632,7 +701,7 @@ class Simulation:
         """Patch k's finished field (finish_field): heights from the last
         frame, clamped-border normals derived on demand (hs_finish)."""
         res, ny = self.synth.grids[k]
-        r = self.regions[k]
+        r = self.current_regions()[k]
         if getattr(self, "_patch_n_frame", -1) != self.frame:
             for q, (rq, nyq) in enumerate(self.synth.grids):
                 N.call("hs_finish", N.HsFinishArgs(nx=rq, ny=nyq, spacing=self.regions[q].l1 / (rq - 1),
@@ -652,7 +721,7 @@ class Simulation:
 
     @property
     def sampler(self) -> SurfaceSampler:
-        surfaces = [PatchSurface(r, self.patch_field(k)) for k, r in enumerate(self.regions)]
+        surfaces = [PatchSurface(r, self.patch_field(k)) for k, r in enumerate(self.current_regions())]
         return SurfaceSampler(self.background, surfaces, self.config.normal_mode)
 
     def stitched_heights(self) -> torch.Tensor:
@@ -661,6 +730,8 @@ class Simulation:
         n = cfg.fft_n
         if self.fft_state is None:
             raise ConfigError("stitched_heights needs the FFT background (mode != wp-only)")
+        if self.n_sources and self._tracking:
+            self._init_boxes()                    # the composited boxes follow the tracking patches
         bg = self.fft_ws
         args = N.HsCompositeArgs(
             n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0,

@@ -24,7 +24,7 @@ import numpy as np
 
 import hybridsea
 from hybridsea import coupling, fft_background, particles, patch_synthesis, spectrum
-from hybridsea.config import PatchConfig, SimConfig
+from hybridsea.config import BodyConfig, PatchConfig, SimConfig
 from hybridsea.harness import Simulation
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -228,6 +228,82 @@ def gen_sim() -> None:
     save("sim.npz", **out)
 
 
+def gen_emit() -> None:
+    """Emission (interaction.py:175-231) and a Simulation with kinematic
+    bodies + a tracking patch (harness.py:115-123,155-167).  Kinematic bodies:
+    `buoyancy_step` is replaced by position += velocity * dt (its own update,
+    interaction.py:140) with a fixed displaced-volume change and submersion
+    per frame, the SURVEY 8(f) form of the BASELINE wake sources."""
+    from hybridsea import harness as H
+    from hybridsea import interaction as I
+    out = {}
+    pb = replace(spectrum.derive_params(15.0, 1e5, G), gamma=3.3)
+    patch = particles.PatchRegion((100.0, 200.0), 128.0, 128.0, 10.0)
+    cases = [  # (count, velocity, d_v, h_c, hull size, trough fraction)
+        (3, (2.0, 0.0, 0.0), 0.02, 0.5, (2.0, 2.0, 1.0), 1.0),
+        (8, (1.2, 0.8, 0.0), 0.01, 0.4, (6.0, 3.0, 1.0), 1.0),
+        (256, (-5.0, 3.0, 0.0), 0.05, 0.5, (12.0, 4.0, 2.0), 1.0),
+        (16, (1.0, 0.0, 1.0), 0.02, 0.5, (2.0, 2.0, 1.0), 0.5),     # ring + wake split
+        (8, (0.0, 0.0, 0.7), -0.02, 0.5, (3.0, 3.0, 1.0), 1.0),     # suction ring only
+        (4, (0.0, 0.0, 0.0), 0.03, 0.2, (2.0, 2.0, 1.0), 1.0),      # static: ring
+    ]
+    for k, (count, vel, dv, hc, size, beta) in enumerate(cases):
+        tbl = log_table(pb, 0.4, 3.0, 12, 2 * count)
+        body = I.box_body([150.0, 260.0, 0.0], size)
+        body.velocity = np.array(vel)
+        body.prev_submerged_volume = 0.0          # d_v = submerged - prev == dv exactly
+        body.submerged_volume = dv
+        body.mean_submersion = hc
+        events, ps = I.emit_from_motion(body, patch, tbl, 1 / 60, 1000.0, G, trough_fraction=beta)
+        out[f"c{k}_params"] = np.array([count, *vel, dv, hc, body.hull_extent, beta, *size])
+        out[f"c{k}_events"] = np.array([[0 if e.mode == "ring" else 1, e.energy, e.bucket] for e in events]).reshape(-1, 3)
+        out.update(pool_arrays(ps, f"c{k}"))
+        out[f"c{k}_radii"] = tbl.radii
+    save("emit.npz", **out)
+
+    # whole Simulation: body 0 (surge) is tracked by the patch, body 1 heaves + drifts
+    cfg = SimConfig(fft_n=64, fft_domain=500.0, dt=0.05, frames=10, n_omega=8, n_theta=8, seed=21,
+                    patches=(PatchConfig(origin=(200.0, 180.0), size=(100.0, 80.0), res=65, margin=10.0,
+                                         track_body=0),),
+                    bodies=(BodyConfig(position=(250.0, 220.0, 0.0), size=(4.0, 2.0, 1.0)),
+                            BodyConfig(position=(230.0, 200.0, 0.0), size=(2.0, 2.0, 1.0))),
+                    write_frames=False)
+    kin = {0: ((3.0, 1.0, 0.0), 0.02, 0.5), 1: ((1.0, -0.5, 0.8), -0.01, 0.3)}
+
+    def kinematic_step(body, query_surface, dt, rho=1000.0, g=9.81):
+        vel, dv, hc = kin[body.body_id]
+        body.velocity = np.array(vel)
+        body.position += body.velocity * dt
+        body.prev_submerged_volume = 0.0         # a fixed d_v per frame (exactly dv)
+        body.submerged_volume = dv
+        body.mean_submersion = hc
+        return body
+
+    orig = H.buoyancy_step
+    H.buoyancy_step = kinematic_step
+    try:
+        sim = Simulation(cfg)
+        sim.rng = np.random.Generator(np.random.Philox(key=[cfg.seed, 0]))
+        stats, origins = [], []
+        for _ in range(cfg.frames):
+            stats.append(sim.step())
+            origins.append(sim.patches[0].region.min_corner.copy())
+    finally:
+        H.buoyancy_step = orig
+    sout = {
+        "counts": np.array([st.particle_counts for st in stats]),
+        "e_in": np.array([st.injected_energy for st in stats]),
+        "e_out": np.array([st.despawned_energy for st in stats]),
+        "origins": np.array(origins),
+        "body_pos": np.array([b.position for b in sim.bodies]),
+        "hulls": np.array([b.hull_extent for b in sim.bodies]),
+        "patch_h": sim.patches[0].surface.field.height,
+        "stitched": sim.stitched_heights(),
+    }
+    sout.update(pool_arrays(sim.patches[0].pool, "pool"))
+    save("emit_sim.npz", **sout)
+
+
 def main() -> int:
     print("reference hybridsea", hybridsea.__version__, "numpy", np.__version__)
     gen_spectrum()
@@ -235,6 +311,7 @@ def main() -> int:
     ctx = gen_particles()
     gen_synth(ctx)
     gen_sim()
+    gen_emit()
     return 0
 
 

@@ -259,3 +259,63 @@ def test_scene_chain_matches_reference_simulation(golden):
     seg = scene.pools[0]
     np.testing.assert_array_equal(seg.pos, gd["pool_pos"])
     np.testing.assert_array_equal(seg.bucket, gd["pool_bucket"])
+
+
+# ---------------------------------------------------------- emission ----
+
+def test_emit_matches_reference_cases(golden):
+    """emit_ref.emit vs the reference's emit_from_motion (interaction.py:175-231)
+    on wake, split ring + wake, suction and static-ring cases (table with
+    n_theta = 2 * count: the SURVEY 8(f) fixed-count wake trick)."""
+    from oracle import emit_ref
+    gd = golden("emit.npz")
+    k = 0
+    while f"c{k}_params" in gd:
+        prm = gd[f"c{k}_params"]
+        count, vel, dv, hc, hull, beta = int(prm[0]), prm[1:4], prm[4], prm[5], prm[6], prm[7]
+        src = emit_ref.Source(np.array([150.0, 260.0]), np.array(vel), hull, dv, hc, wake_count=0)
+        events, pool = emit_ref.emit(src, gd[f"c{k}_radii"], 2 * count, 1000.0, 9.81, beta)
+        ev = gd[f"c{k}_events"]
+        assert len(events) == len(ev)
+        for e, r in zip(events, ev):
+            assert (0 if e.mode == "ring" else 1) == int(r[0]) and e.bucket == int(r[2])
+            assert e.energy == r[1]
+        np.testing.assert_array_equal(pool.pos, gd[f"c{k}_pos"])
+        np.testing.assert_array_equal(pool.dir, gd[f"c{k}_dir"])
+        np.testing.assert_array_equal(pool.amp, gd[f"c{k}_amp"])
+        np.testing.assert_array_equal(pool.bucket, gd[f"c{k}_bucket"])
+        k += 1
+    assert k >= 6
+
+
+def _emit_sim_cfg():
+    import math
+    from paper_2511_02852_b200 import PatchConfig, SimConfig, SourceConfig
+    hull0, hull1 = 0.5 * math.hypot(4.0, 2.0), 0.5 * math.hypot(2.0, 2.0)   # box_body (interaction.py:90)
+    return SimConfig(fft_n=64, fft_domain=500.0, dt=0.05, frames=10, n_omega=8, n_theta=8, seed=21,
+                     patches=(PatchConfig(origin=(200.0, 180.0), size=(100.0, 80.0), res=65, margin=10.0,
+                                          track_source=0),),
+                     sources=(SourceConfig(position=(250.0, 220.0), velocity=(3.0, 1.0, 0.0), hull_extent=hull0,
+                                           volume_rate=0.02, submersion=0.5),
+                              SourceConfig(position=(230.0, 200.0), velocity=(1.0, -0.5, 0.8), hull_extent=hull1,
+                                           volume_rate=-0.01, submersion=0.3)),
+                     write_frames=False)
+
+
+def test_scene_with_sources_matches_reference_simulation(golden):
+    """OracleScene with kinematic sources + a tracking patch vs the reference
+    Simulation (bodies moved kinematically): per-frame counts, injected
+    energy, patch origins, the final pool and the patch heights."""
+    gd = golden("emit_sim.npz")
+    cfg = _emit_sim_cfg()
+    sc = scene_ref.OracleScene(cfg.scene_dict())
+    for k in range(cfg.frames):
+        out = sc.step(synth=(k == cfg.frames - 1))
+        np.testing.assert_array_equal(out["counts"][0], gd["counts"][k], err_msg=f"frame {k}")
+        np.testing.assert_allclose(sc.ledgers[0].e_in, gd["e_in"][k], rtol=1e-13)
+        np.testing.assert_array_equal(sc.patches[0].lo, gd["origins"][k])
+    np.testing.assert_array_equal(sc.sources[0].position, gd["body_pos"][0][:2])
+    np.testing.assert_array_equal(sc.pools[0].pos, gd["pool_pos"])
+    np.testing.assert_array_equal(sc.pools[0].amp, gd["pool_amp"])
+    np.testing.assert_array_equal(sc.pools[0].bucket, gd["pool_bucket"])
+    np.testing.assert_allclose(out["patch_heights"][0], gd["patch_h"], rtol=0, atol=1e-12)
