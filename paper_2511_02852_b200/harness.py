@@ -772,3 +772,78 @@ def benchmark_cell(cfg: SimConfig, warmup: int | None = None, measure: int | Non
     live = sim.live_particles()
     return {"label": label or cfg.mode, "fps": 1e3 / ms if ms > 0 else float("inf"), "median_frame_ms": ms,
             "particles": live, "particle_rate": live * measure / wall if wall > 0 else 0.0}
+
+
+# ---------------------------------------------------------------------------
+# headless run with file outputs (harness.py:248-329)
+# ---------------------------------------------------------------------------
+
+def _format_float(x: float) -> str:
+    return repr(float(x))
+
+
+def stats_header(cfg: SimConfig) -> str:
+    """stats.csv header (harness.py:252-260)."""
+    cols = ["frame", "t", "particles_total"]
+    cols += [f"particles_b{i:02d}" for i in range(cfg.n_omega)]
+    cols += [f"injected_J_b{i:02d}" for i in range(cfg.n_omega)]
+    cols += [f"despawned_J_b{i:02d}" for i in range(cfg.n_omega)]
+    cols += ["patch_variance", "fft_band_variance"]
+    for j in range(len(cfg.bodies)):
+        cols += [f"body{j}_x", f"body{j}_y", f"body{j}_z", f"body{j}_yaw"]
+    return ",".join(cols)
+
+
+def stats_row(cfg: SimConfig, s: FrameStats) -> str:
+    """One stats.csv row (harness.py:263-271); reads the frame's device snapshot."""
+    parts = [str(s.frame), _format_float(s.t), str(int(s.particle_counts.sum()))]
+    parts += [str(int(c)) for c in s.particle_counts]
+    parts += [_format_float(x) for x in s.injected_energy]
+    parts += [_format_float(x) for x in s.despawned_energy]
+    parts += [_format_float(s.patch_variance), _format_float(s.fft_band_variance)]
+    for b in s.body_states:
+        parts += [_format_float(v) for v in b]
+    return ",".join(parts)
+
+
+def run(config: SimConfig, output_dir: str | None = None, progress=None) -> list:
+    """Headless scenario (harness.py:274-329): config.echo, stats.csv,
+    timings.csv and `frame_%06d.raw` (<f4, row-major, x-major) + `.meta`
+    sidecars of the FFT-resolution composite every `output.stride` frames.
+    Frames are stepped as CUDA-graph replays; the device->host copies of the
+    stats snapshots and frames happen after each step, in frame order.
+    timings.csv carries the device time of each frame (CUDA events) in
+    total_ms; per-stage wall times do not exist for a single-graph frame and
+    are written as 0."""
+    import os
+    from .config import dump_config
+
+    cfg = config.validate()
+    out_dir = output_dir if output_dir is not None else cfg.output_dir
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "config.echo"), "w", encoding="utf-8") as fh:
+        fh.write(dump_config(cfg))
+    sim = Simulation(cfg)
+    n = cfg.fft_n
+    spacing = cfg.fft_domain / n
+    with open(os.path.join(out_dir, "stats.csv"), "w", encoding="utf-8") as sfh, \
+            open(os.path.join(out_dir, "timings.csv"), "w", encoding="utf-8") as tfh:
+        sfh.write(stats_header(cfg) + "\n")
+        tfh.write("frame," + ",".join(f"{st}_ms" for st in STAGES) + ",total_ms\n")
+        for k in range(cfg.frames):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s = sim.step()
+            e1.record()
+            if cfg.write_frames and k % cfg.output_stride == 0 and sim.fft_state is not None:
+                grid = sim.stitched_heights().cpu().numpy()
+                path = os.path.join(out_dir, f"frame_{k:06d}.raw")
+                grid.astype("<f4").tofile(path)
+                with open(path[:-4] + ".meta", "w", encoding="utf-8") as mfh:
+                    mfh.write(f"res={n}x{n} spacing={spacing!r} origin=0.0,0.0 t={s.t!r}\n")
+            sfh.write(stats_row(cfg, s) + "\n")
+            e1.synchronize()
+            tfh.write(",".join([str(s.frame)] + ["0.000" for _ in STAGES] + [f"{e0.elapsed_time(e1):.3f}"]) + "\n")
+            if progress is not None:
+                progress(s)
+    return sim._stats
