@@ -347,6 +347,18 @@ typedef struct {
 } HsSmoothArgs;
 HS_API int hs_smooth(const HsSmoothArgs* a, void* stream);
 
+/* One further tile of a summed-cascade background (fft.cascades): periodic,
+ * origin 0, its own spacing.  Samplers add its bilinear height and combine
+ * normals through slopes, n = normalize(sum_c n_c.xy / n_c.z, 1), n_c the
+ * renormalised bilinear of the tile's periodic node normals.               */
+#define HS_MAX_CASCADES 4
+typedef struct {
+    const float* height;      /* [n*n] */
+    int n;                    /* power of two */
+    int pad;
+    double spacing;
+} HsBgTile;
+
 /* ------------------------------------------------------------------------ */
 /* Compose: gain-sum of the bilinearly upsampled layers (synthesize,
  * patch_synthesis.py:301-313), clamped-border normals (finish_field,
@@ -370,6 +382,8 @@ typedef struct {
     double* interior_sumsq;     /* [n_patches] += sum h^2 over the interior inset, or NULL */
     long long* interior_count;  /* [n_patches] matching counts, or NULL */
     long long* frame_advance;   /* optional: device frame counter, += 1 by this launch */
+    int n_extra_bg;             /* further cascades added to the background (0..3) */
+    HsBgTile extra_bg[HS_MAX_CASCADES - 1];
 } HsComposeArgs;
 HS_API int hs_compose(const HsComposeArgs* a, void* stream);
 
@@ -390,6 +404,8 @@ typedef struct {
     float* out_height;
     float* out_normal;          /* [n_points*3] or NULL */
     int clamped_only;           /* 1: sample_clamped of patch 0 only, no weights */
+    int n_extra_bg;             /* further background cascades (bg_* is cascade 0) */
+    HsBgTile extra_bg[HS_MAX_CASCADES - 1];
 } HsSampleArgs;
 HS_API int hs_sample(const HsSampleArgs* a, void* stream);
 
@@ -405,6 +421,8 @@ typedef struct {
     const int* box_prefix;      /* [n_patches+1] cumulative box sizes */
     int total_box;
     float* out;                 /* [n*n] */
+    int n_extra_bg;             /* further background cascades, summed at the grid nodes */
+    HsBgTile extra_bg[HS_MAX_CASCADES - 1];
 } HsCompositeArgs;
 HS_API int hs_composite(const HsCompositeArgs* a, void* stream);
 

@@ -66,13 +66,31 @@ class Field:
     spacing: float
 
 
-def sample(background: Field | None, patches: list[tuple[Patch, Field]], pts: np.ndarray):
+def sample_background(background, pts: np.ndarray):
+    """sample_periodic of the background (fft_background.py:222-249).  A list
+    of Fields is a summed-cascade background: heights add; normals combine
+    through their slopes, n = normalize(sum_c n_c.xy / n_c.z, 1), which for
+    one cascade is the renormalised bilinear normal itself."""
+    if isinstance(background, (list, tuple)):
+        if len(background) == 1:
+            return sample_background(background[0], pts)
+        h = np.zeros(pts.shape[:-1])
+        sl = np.zeros(pts.shape[:-1] + (2,))
+        for f in background:
+            hc, nc = sample_periodic(f.height, f.normal, f.origin, f.spacing, pts)
+            h = h + hc
+            sl = sl + nc[..., :2] / nc[..., 2:3]
+        nrm = np.concatenate([sl, np.ones(pts.shape[:-1] + (1,))], axis=-1)
+        return h, nrm / np.linalg.norm(nrm, axis=-1, keepdims=True)
+    h, nrm = sample_periodic(background.height, background.normal, background.origin, background.spacing, pts)
+    return np.array(h, dtype=float), nrm
+
+
+def sample(background, patches: list[tuple[Patch, Field]], pts: np.ndarray):
     """Blended (height, normal) at world points (coupling.py:120-141)."""
     pts = np.asarray(pts, dtype=float)
     if background is not None:
-        h, nrm = sample_periodic(background.height, background.normal, background.origin,
-                                 background.spacing, pts)
-        h = np.array(h, dtype=float)
+        h, nrm = sample_background(background, pts)
     else:
         h = np.zeros(pts.shape[:-1])
         nrm = np.zeros(pts.shape[:-1] + (3,))
@@ -94,7 +112,17 @@ def stitched(background: Field | None, n: int, domain: float,
              patches: list[tuple[Patch, Field]]) -> np.ndarray:
     """Global FFT-resolution composite with patch boxes resampled (harness.py:219-241)."""
     spacing = domain / n
-    grid = background.height.copy() if background is not None else np.zeros((n, n))
+    if isinstance(background, (list, tuple)) and len(background) > 1:
+        # summed cascades on the largest tile's grid (cascade 0)
+        xs = np.arange(n) * spacing
+        nodes = np.stack(np.meshgrid(xs, xs, indexing="ij"), axis=-1)
+        grid = background[0].height.copy()
+        for f in background[1:]:
+            grid += sample_periodic(f.height, None, f.origin, f.spacing, nodes)[0]
+    elif isinstance(background, (list, tuple)):
+        grid = background[0].height.copy()
+    else:
+        grid = background.height.copy() if background is not None else np.zeros((n, n))
     for patch, _ in patches:
         lo = np.clip(np.floor(patch.lo / spacing).astype(int), 0, n)
         hi = np.clip(np.ceil(patch.hi / spacing).astype(int) + 1, 0, n)

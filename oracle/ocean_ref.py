@@ -23,16 +23,21 @@ def wavenumbers(n: int, domain: float) -> np.ndarray:
 def resolved_band(p: Params, n: int, domain: float, band=None) -> tuple[float, float]:
     """Sampled band clipped to the fundamental and the inscribed Nyquist
     circle (fft_background.py:90-99).  `band` overrides [0.5, 2.5] omega_p."""
-    lo, hi = band if band is not None else (BAND[0] * p.omega_p, BAND[1] * p.omega_p)
+    lo, hi = band if band is not None else (None, None)
+    lo = BAND[0] * p.omega_p if lo is None else lo
+    hi = BAND[1] * p.omega_p if hi is None else hi
     w_min = math.sqrt(p.g * (2.0 * math.pi / domain))
     w_max = math.sqrt(p.g * (math.pi * n / domain))
     return max(lo, w_min), min(hi, w_max)
 
 
 def initial_amplitudes(p: Params, mean_dir: float, n: int, domain: float, seed: int,
-                       band=None) -> np.ndarray:
+                       band=None, kband=None) -> np.ndarray:
     """Complex Gaussian h0 with one-sided variance S (g/2w)/|k| dk^2/2 per bin
-    inside the resolved band, zero elsewhere (fft_background.py:102-146)."""
+    inside the resolved band, zero elsewhere (fft_background.py:102-146).
+    `kband` = (k_lo, k_hi) further keeps k_lo <= |k| < k_hi only: one cascade
+    of a summed-tile background (zero h0 outside the cascade's
+    band; the mirrored conjugate follows from the masked h0)."""
     if n < 2 or n & (n - 1):
         raise ValueError("n must be a power of two")
     kv = wavenumbers(n, domain)
@@ -42,6 +47,8 @@ def initial_amplitudes(p: Params, mean_dir: float, n: int, domain: float, seed: 
     w_lo, w_hi = resolved_band(p, n, domain, band)
     inside = (kmag >= (w_lo ** 2 / p.g) * (1.0 - 1e-12)) & (kmag <= (w_hi ** 2 / p.g) * (1.0 + 1e-12))
     inside[0, 0] = False
+    if kband is not None:
+        inside &= (kmag >= kband[0]) & (kmag < kband[1])
     ks = kmag[inside]
     om = np.sqrt(p.g * ks)
     th = np.arctan2(ky[inside], kx[inside]) - mean_dir

@@ -34,6 +34,19 @@ def build_buckets(sc: dict, p: spectrum_ref.Params) -> spectrum_ref.Buckets:
     return spectrum_ref.equal_energy_buckets(p, sc["n_omega"], sc["n_theta"])
 
 
+def cascade_bands(cascades, n: int) -> list:
+    """[(L, k_lo, k_hi)] largest tile first; boundaries at half the larger
+    tile's Nyquist wavenumber pi n / (2 L) (the scene definition of C4,
+    DESIGN.md; no reference semantics)."""
+    tiles = sorted((float(c) for c in cascades), reverse=True)
+    out, k_lo = [], 0.0
+    for i, L in enumerate(tiles):
+        k_hi = math.pi * n / (2.0 * L) if i + 1 < len(tiles) else math.inf
+        out.append((L, k_lo, k_hi))
+        k_lo = k_hi
+    return out
+
+
 class OracleScene:
     """CPU twin of one hybrid scene."""
 
@@ -59,6 +72,14 @@ class OracleScene:
             self.h0 = h0 if h0 is not None else ocean_ref.initial_amplitudes(
                 self.p, sc["mean_direction"], sc["fft_n"], sc["fft_domain"], sc["seed"],
                 band=sc.get("fft_band"))
+        # summed FFT cascades: tile c of size L_c keeps its
+        # disjoint |k| band and its own seed (seed + c)
+        self.cascades = []
+        if self.fft and sc.get("fft_cascades"):
+            for c, (L, klo, khi) in enumerate(cascade_bands(sc["fft_cascades"], sc["fft_n"])):
+                self.cascades.append((L, ocean_ref.initial_amplitudes(
+                    self.p, sc["mean_direction"], sc["fft_n"], L, sc["seed"] + c, band=sc.get("fft_band"),
+                    kband=(klo, khi))))
         self.background = None
         self.fields = []
         # kinematic emitting bodies + patch tracking (emit_ref; harness.py:115-123,155-167)
@@ -73,7 +94,15 @@ class OracleScene:
         dt = sc["dt"] if dt is None else dt
         t = self.frame * dt
         out = {"t": t}
-        if self.fft and fft:
+        if self.fft and fft and self.cascades:
+            n = sc["fft_n"]
+            self.background = []
+            for L, h0c in self.cascades:
+                h, dx, dy, nrm = ocean_ref.evolve(h0c, L, self.p.g, t, sc["fft_choppiness"])
+                self.background.append(blend_ref.Field(h, nrm, np.zeros(2), L / n))
+                out.setdefault("cascade_heights", []).append(h)
+            out.update(height=self.background[0].height, normal=self.background[0].normal)
+        elif self.fft and fft:
             h, dx, dy, nrm = ocean_ref.evolve(self.h0, sc["fft_domain"], self.p.g, t, sc["fft_choppiness"])
             n = sc["fft_n"]
             self.background = blend_ref.Field(h, nrm, np.zeros(2), sc["fft_domain"] / n)

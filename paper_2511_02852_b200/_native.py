@@ -117,26 +117,36 @@ class HsSmoothArgs(C.Structure):
                 ("total_ytiles", i32), ("max_H_wide", i32)]
 
 
+HS_MAX_CASCADES = 4
+
+
+class HsBgTile(C.Structure):
+    _fields_ = [("height", vp), ("n", i32), ("pad", i32), ("spacing", dbl)]
+
+
 class HsComposeArgs(C.Structure):
     _fields_ = [("n_patches", i32), ("nb", i32), ("patches", vp), ("layers", vp),
                 ("smooth_layers", vp), ("tile_info", vp), ("total_tiles", i32),
                 ("bg_height", vp), ("bg_normal", vp), ("bg_n", i32), ("bg_spacing", dbl),
                 ("patch_height", vp), ("patch_normal", vp), ("blend_height", vp),
                 ("blend_normal", vp), ("blend_mode", i32), ("interior_sumsq", vp),
-                ("interior_count", vp), ("frame_advance", vp)]
+                ("interior_count", vp), ("frame_advance", vp), ("n_extra_bg", i32),
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
 
 
 class HsSampleArgs(C.Structure):
     _fields_ = [("n_points", i32), ("points", vp), ("bg_height", vp), ("bg_normal", vp), ("bg_n", i32),
                 ("bg_spacing", dbl), ("bg_x0", dbl), ("bg_y0", dbl), ("n_patches", i32),
                 ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("out_height", vp),
-                ("out_normal", vp), ("clamped_only", i32)]
+                ("out_normal", vp), ("clamped_only", i32), ("n_extra_bg", i32),
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
 
 
 class HsCompositeArgs(C.Structure):
     _fields_ = [("n", i32), ("spacing", dbl), ("bg_height", vp), ("bg_normal", vp), ("n_patches", i32),
                 ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("box", vp),
-                ("box_prefix", vp), ("total_box", i32), ("out", vp)]
+                ("box_prefix", vp), ("total_box", i32), ("out", vp), ("n_extra_bg", i32),
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
 
 
 class HsFinishArgs(C.Structure):

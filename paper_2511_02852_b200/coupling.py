@@ -99,11 +99,13 @@ class SurfaceSampler:
     Pure reads; the patch fields are packed once into contiguous device
     buffers on construction."""
 
-    def __init__(self, background: HeightField | None, patches: list, normal_mode: str = "blend"):
+    def __init__(self, background: HeightField | None, patches: list, normal_mode: str = "blend",
+                 cascades: list | None = None):
         if normal_mode not in ("blend", "recompute"):
             raise ConfigError(f"unknown normal mode {normal_mode!r}")
         validate_patches([p.patch for p in patches])
         self.background = background
+        self.cascades = list(cascades or [])      # further summed background tiles (HeightField, origin 0)
         self.patches = patches
         self.normal_mode = normal_mode
         self._packed = None
@@ -145,6 +147,10 @@ class SurfaceSampler:
             bg_x0=float(bg.origin[0]) if bg is not None else 0.0, bg_y0=float(bg.origin[1]) if bg is not None else 0.0,
             n_patches=npatch, patches=N.ptr(pst), patch_height=N.ptr(ph), patch_normal=N.ptr(pn),
             out_height=N.ptr(out_h), out_normal=N.ptr(out_n), clamped_only=0)
+        if bg is not None and self.cascades:
+            args.n_extra_bg = len(self.cascades)
+            for c, f in enumerate(self.cascades):
+                args.extra_bg[c] = N.HsBgTile(N.ptr(f.height), f.resolution, 0, float(f.spacing))
         N.call("hs_sample", args, stream_ptr())
         return out_h, out_n
 

@@ -368,6 +368,9 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
                 }
                 const float r2 = rsqrtf(nx * nx + ny * ny + nz * nz);
                 nx *= r2; ny *= r2; nz *= r2;
+                if (a.n_extra_bg > 0)                 // summed cascades (fft.cascades)
+                    add_cascades(a.n_extra_bg, a.extra_bg, P.x0 + (double)ii * P.texel, P.y0 + (double)jj * P.texel,
+                                 hb, nx, ny, nz);
             }
             const float d = fminf(W.row_d[rr], W.col_d[cc]);
             if (d > 0.f) {

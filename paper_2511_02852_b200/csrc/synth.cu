@@ -231,10 +231,12 @@ __device__ __forceinline__ void sample_clamped_at(const HsPatch& P, const float*
     }
 }
 
-__device__ void sample_surface(const BgView& bg, int n_patches, const HsPatch* __restrict__ patches,
+__device__ void sample_surface(const BgView& bg, int n_extra, const HsBgTile* extra, int n_patches,
+                               const HsPatch* __restrict__ patches,
                                const float* __restrict__ ph, const float* __restrict__ pn,
                                double x, double y, float& h, float3& nv) {
     sample_bg(bg, x, y, h, nv);
+    if (bg.h) add_cascades(n_extra, extra, x, y, h, nv.x, nv.y, nv.z);
     for (int p = 0; p < n_patches; ++p) {
         const HsPatch P = synth_view(patches[p]);
         const double w = blend_w(P, x, y);
@@ -259,7 +261,7 @@ __global__ void sample_kernel(HsSampleArgs a) {
     if (a.clamped_only) {
         sample_clamped_at(synth_view(a.patches[0]), a.patch_height, a.patch_normal, a.points[2 * k], a.points[2 * k + 1], h, nv);
     } else {
-        sample_surface(bg, a.n_patches, a.patches, a.patch_height, a.patch_normal,
+        sample_surface(bg, a.n_extra_bg, a.extra_bg, a.n_patches, a.patches, a.patch_height, a.patch_normal,
                        a.points[2 * k], a.points[2 * k + 1], h, nv);
     }
     a.out_height[k] = h;
@@ -277,9 +279,23 @@ __global__ void composite_kernel(HsCompositeArgs a) {
     (void)i1;
     BgView bg{a.bg_height, a.bg_normal, a.n, a.spacing, 0.0, 0.0};
     float h; float3 nv;
-    sample_surface(bg, a.n_patches, a.patches, a.patch_height, nullptr,
+    sample_surface(bg, a.n_extra_bg, a.extra_bg, a.n_patches, a.patches, a.patch_height, nullptr,
                    (double)i * a.spacing, (double)j * a.spacing, h, nv);
     a.out[(long long)i * a.n + j] = h;
+}
+
+// the summed-cascade background on cascade 0's grid (before the patch boxes)
+__global__ void bg_sum_kernel(HsCompositeArgs a) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (long long)a.n * a.n) return;
+    const int i = (int)(k / a.n), j = (int)(k - (long long)i * a.n);
+    float h = a.bg_height[k];
+    for (int c = 0; c < a.n_extra_bg; ++c) {
+        float hc, sx, sy;
+        sample_tile(a.extra_bg[c], (double)i * a.spacing, (double)j * a.spacing, hc, sx, sy);
+        h += hc;
+    }
+    a.out[k] = h;
 }
 
 // =============================================================== finish ==
@@ -374,8 +390,16 @@ extern "C" int hs_composite(const HsCompositeArgs* a, void* stream) {
     HS_CHECK_ARG(a->out, "hs_composite: missing output");
     cudaStream_t st = as_stream(stream);
     const size_t bytes = sizeof(float) * (size_t)a->n * a->n;
-    if (a->bg_height) HS_CUDA(cudaMemcpyAsync(a->out, a->bg_height, bytes, cudaMemcpyDeviceToDevice, st));
-    else HS_CUDA(cudaMemsetAsync(a->out, 0, bytes, st));
+    HS_CHECK_ARG(a->n_extra_bg >= 0 && a->n_extra_bg < HS_MAX_CASCADES, "hs_composite: n_extra_bg out of range");
+    if (a->bg_height && a->n_extra_bg > 0) {
+        const long long nn = (long long)a->n * a->n;
+        bg_sum_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(*a);
+        HS_LAUNCH_CHECK();
+    } else if (a->bg_height) {
+        HS_CUDA(cudaMemcpyAsync(a->out, a->bg_height, bytes, cudaMemcpyDeviceToDevice, st));
+    } else {
+        HS_CUDA(cudaMemsetAsync(a->out, 0, bytes, st));
+    }
     if (a->total_box == 0) return 0;
     composite_kernel<<<(a->total_box + 255) / 256, 256, 0, st>>>(*a);
     HS_LAUNCH_CHECK();

@@ -55,6 +55,55 @@ __device__ __forceinline__ void sample_bg(const BgView& bg, double x, double y, 
     }
 }
 
+// One further cascade of a summed background (HsBgTile): bilinear periodic
+// height and the slope (n.x/n.z, n.y/n.z) of the renormalised bilinear node
+// normal, node normals from periodic central differences of the tile's
+// heights (fft_background.py:162-178, 222-249).
+__device__ __forceinline__ float3 tile_node_normal(const float* __restrict__ H, int n, int i, int j, float inv2s) {
+    const int m = n - 1;
+    const float hx = (__ldg(H + (long long)((i + 1) & m) * n + (j & m)) - __ldg(H + (long long)((i - 1) & m) * n + (j & m))) * inv2s;
+    const float hy = (__ldg(H + (long long)(i & m) * n + ((j + 1) & m)) - __ldg(H + (long long)(i & m) * n + ((j - 1) & m))) * inv2s;
+    const float r = rsqrtf(hx * hx + hy * hy + 1.f);
+    return make_float3(-hx * r, -hy * r, r);
+}
+
+__device__ __forceinline__ void sample_tile(const HsBgTile& T, double x, double y, float& h, float& sx, float& sy) {
+    const double u = x / T.spacing, v = y / T.spacing;
+    const double fi = floor(u), fj = floor(v);
+    const float fu = (float)(u - fi), fv = (float)(v - fj);
+    const int m = T.n - 1;
+    const int i0 = (int)((long long)fi & m), j0 = (int)((long long)fj & m);
+    const int i1 = (i0 + 1) & m, j1 = (j0 + 1) & m;
+    const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
+    const float* H = T.height;
+    h = __ldg(H + (long long)i0 * T.n + j0) * w00 + __ldg(H + (long long)i1 * T.n + j0) * w10
+      + __ldg(H + (long long)i0 * T.n + j1) * w01 + __ldg(H + (long long)i1 * T.n + j1) * w11;
+    const float inv2s = (float)(0.5 / T.spacing);
+    const float3 a = tile_node_normal(H, T.n, i0, j0, inv2s), b = tile_node_normal(H, T.n, i1, j0, inv2s);
+    const float3 c = tile_node_normal(H, T.n, i0, j1, inv2s), d = tile_node_normal(H, T.n, i1, j1, inv2s);
+    const float nx = a.x * w00 + b.x * w10 + c.x * w01 + d.x * w11;
+    const float ny = a.y * w00 + b.y * w10 + c.y * w01 + d.y * w11;
+    const float nz = a.z * w00 + b.z * w10 + c.z * w01 + d.z * w11;
+    sx = nx / nz;                              // renormalisation cancels in the slope
+    sy = ny / nz;
+}
+
+// add the extra cascades at (x, y) to a cascade-0 sample (h, unit normal n)
+__device__ __forceinline__ void add_cascades(int n_extra, const HsBgTile* extra, double x, double y, float& h,
+                                             float& nx, float& ny, float& nz) {
+    if (n_extra <= 0) return;
+    float sx = nx / nz, sy = ny / nz;
+    for (int c = 0; c < n_extra; ++c) {
+        float hc, sxc, syc;
+        sample_tile(extra[c], x, y, hc, sxc, syc);
+        h += hc;
+        sx += sxc;
+        sy += syc;
+    }
+    const float r = rsqrtf(sx * sx + sy * sy + 1.f);
+    nx = sx * r; ny = sy * r; nz = r;
+}
+
 // smoothstep weight from inward boundary depth (coupling.py:27-40)
 __device__ __forceinline__ double blend_w(const HsPatch& P, double x, double y) {
     double d = fmin(fmin(x - P.x0, P.x1 - x), fmin(y - P.y0, P.y1 - y));

@@ -131,10 +131,13 @@ def resolved_band(spectrum: DirectionalSpectrum, n: int, domain_size: float,
 
 
 def init_fft(spectrum: DirectionalSpectrum, n: int, domain_size: float, seed: int,
-             choppiness: float = 1.0, *, band: tuple | None = None, device=None) -> FftState:
+             choppiness: float = 1.0, *, band: tuple | None = None, kband: tuple | None = None,
+             device=None) -> FftState:
     """Initial complex amplitudes, variance-matched to the directional
     spectrum (fft_background.py:102-146).  Host fp64 with numpy's
-    default_rng(seed) so h0 equals the reference's; uploaded once."""
+    default_rng(seed) so h0 equals the reference's; uploaded once.
+    `kband` = (k_lo, k_hi) keeps k_lo <= |k| < k_hi only (one tile of a
+    summed-cascade background, config.cascade_bands)."""
     if n < 2 or (n & (n - 1)) != 0:
         raise ConfigError(f"fft grid size must be a power of two >= 2, got {n}")
     if domain_size <= 0:
@@ -148,6 +151,8 @@ def init_fft(spectrum: DirectionalSpectrum, n: int, domain_size: float, seed: in
     w_lo, w_hi = resolved_band(spectrum, n, domain_size, band)
     live = (kmag >= (w_lo ** 2 / g) * (1.0 - 1e-12)) & (kmag <= (w_hi ** 2 / g) * (1.0 + 1e-12))
     live[0, 0] = False
+    if kband is not None:
+        live &= (kmag >= kband[0]) & (kmag < kband[1])
     kl = kmag[live]
     om = np.sqrt(g * kl)
     theta = np.arctan2(ky[live], kx[live]) - spectrum.mean_direction

@@ -34,7 +34,7 @@ import torch
 from . import _native as N
 from ._layout import (bucket_structs, half_rates, max_groups_per_step, patch_struct, stream_ptr,
                       structs_to_device)
-from .config import SimConfig
+from .config import SimConfig, cascade_bands
 from .coupling import PatchSurface, SurfaceSampler, validate_patches
 from .errors import CapacityError, ConfigError
 from .fft_background import FftWorkspace, HeightField, fft_args, init_fft
@@ -157,13 +157,18 @@ class Simulation:
         # ---- background ------------------------------------------------
         self.fft_state = None
         self.fft_ws = None
+        self.cascades = []                # [(FftState, FftWorkspace)], cascade 0 = fft_state / fft_ws
         if cfg.mode != "wp-only":
             band = None
             if cfg.fft_band_lo is not None or cfg.fft_band_hi is not None:
                 band = (cfg.fft_band_lo, cfg.fft_band_hi)
-            self.fft_state = init_fft(self.spectrum, cfg.fft_n, cfg.fft_domain, cfg.seed,
-                                      choppiness=cfg.fft_choppiness, band=band, device=dev)
-            self.fft_ws = FftWorkspace(cfg.fft_n, dev, normals=cfg.fft_normals or self.n_patches > 0)
+            # one tile, or summed tiles with disjoint |k| bands, seeds seed + c (config.cascade_bands)
+            tiles = cascade_bands(cfg.fft_cascades, cfg.fft_n) if cfg.fft_cascades else [(cfg.fft_domain, None, None)]
+            for c, (L, klo, khi) in enumerate(tiles):
+                st = init_fft(self.spectrum, cfg.fft_n, L, cfg.seed + c, choppiness=cfg.fft_choppiness, band=band,
+                              kband=None if klo is None else (klo, khi), device=dev)
+                self.cascades.append((st, FftWorkspace(cfg.fft_n, dev, normals=cfg.fft_normals or self.n_patches > 0)))
+            self.fft_state, self.fft_ws = self.cascades[0]
         self.frame_dev = torch.zeros(1, dtype=torch.int64, device=dev)
 
         # ---- constants ---------------------------------------------------
@@ -406,12 +411,13 @@ class Simulation:
                 side.wait_stream(main)
             with torch.cuda.stream(side):
                 mark("fft_start")
-                fa = fft_args(self.fft_state, self.fft_ws, frame_ptr=self.frame_dev, dt=dt)
-                fa.emit_normals = 0          # normals are derived lazily (background) / in hs_compose
-                fa.normal = 0
-                if not self.n_patches:
-                    fa.frame_advance = N.ptr(self.frame_dev)
-                N.call("hs_fft_evolve", fa, stream_ptr())
+                for c, (st_c, ws_c) in enumerate(self.cascades):
+                    fa = fft_args(st_c, ws_c, frame_ptr=self.frame_dev, dt=dt)
+                    fa.emit_normals = 0      # normals are derived lazily (background) / in hs_compose
+                    fa.normal = 0
+                    if not self.n_patches and c == len(self.cascades) - 1:
+                        fa.frame_advance = N.ptr(self.frame_dev)
+                    N.call("hs_fft_evolve", fa, stream_ptr())
                 mark("fft")
         if self.n_patches:
             stats, nxt = self._stat_sets[lp], self._stat_sets[lp ^ 1]
@@ -484,13 +490,26 @@ class Simulation:
                 patch_height=N.ptr(self.patch_h), patch_normal=0,
                 blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
                 interior_sumsq=N.ptr(stats[1]), interior_count=N.ptr(stats[2]),
-                frame_advance=N.ptr(self.frame_dev)), stream_ptr())
+                frame_advance=N.ptr(self.frame_dev), **self._extra_bg()), stream_ptr())
             mark("compose")
             main.wait_stream(clr)
             self._patch_n_frame = -1          # patch normals are derived lazily (patch_field)
         self._bg_n_frame = -1                 # so are the background normals (background)
         if self.fft_state is None and not self.n_patches:
             N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(stream_ptr()))
+
+    def _extra_bg(self) -> dict:
+        """n_extra_bg / extra_bg args for cascades 1.. (HsBgTile)."""
+        if len(self.cascades) < 2:
+            return {}
+        arr = (N.HsBgTile * (N.HS_MAX_CASCADES - 1))()
+        for c, (st_c, ws_c) in enumerate(self.cascades[1:]):
+            arr[c] = N.HsBgTile(N.ptr(ws_c.height), st_c.n, 0, float(st_c.spacing))
+        return {"n_extra_bg": len(self.cascades) - 1, "extra_bg": arr}
+
+    def cascade_fields(self) -> list:
+        """HeightFields of every background cascade (cascade 0 = `background`)."""
+        return [ws.field(st) for st, ws in self.cascades]
 
     def _state(self) -> tuple:
         if not self.n_patches:
@@ -627,7 +646,9 @@ class Simulation:
             self.step(dt, stats=False)
 
     def _snapshot(self) -> FrameStats:
-        snap = {"fsum": self.fft_ws.sumsq.clone() if self.fft_ws is not None else torch.zeros(1, dtype=torch.float64)}
+        # summed cascades: band variances add (disjoint |k| bands)
+        snap = {"fsum": sum(ws.sumsq for _, ws in self.cascades).clone() if self.cascades
+                else torch.zeros(1, dtype=torch.float64)}
         if self.n_patches:
             snap.update(counts=self.live.clone(), e_in=self.e_in.clone(), e_out=self.e_out.clone(),
                         isum=self.isum.clone(), icount=self.icount.clone())
@@ -722,7 +743,8 @@ class Simulation:
     @property
     def sampler(self) -> SurfaceSampler:
         surfaces = [PatchSurface(r, self.patch_field(k)) for k, r in enumerate(self.current_regions())]
-        return SurfaceSampler(self.background, surfaces, self.config.normal_mode)
+        return SurfaceSampler(self.background, surfaces, self.config.normal_mode,
+                              cascades=self.cascade_fields()[1:])
 
     def stitched_heights(self) -> torch.Tensor:
         """FFT-resolution composite with patch boxes resampled (harness.py:219-241)."""
@@ -739,7 +761,8 @@ class Simulation:
             patch_height=N.ptr(self.patch_h) if self.n_patches else 0, patch_normal=0,
             box=N.ptr(self.box_dev) if self.n_patches else 0,
             box_prefix=N.ptr(self.box_prefix_dev) if self.n_patches else 0,
-            total_box=int(self.box_prefix_np[-1]), out=N.ptr(self.composite_out if self.n_patches else None))
+            total_box=int(self.box_prefix_np[-1]), out=N.ptr(self.composite_out if self.n_patches else None),
+            **self._extra_bg())
         if not self.n_patches:
             out = torch.empty((n, n), dtype=torch.float32, device=self.device)
             args.out = N.ptr(out)

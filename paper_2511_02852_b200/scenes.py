@@ -13,8 +13,9 @@ patch layouts.
        particles per frame (128-direction Kelvin fan + troughs)
   C3   1024^2 / 4000 m, lambda 1.2; one 256 m patch on a 1024 grid; 16 log
        buckets 0.3-6 rad/s; n_theta 2 (~0.86M live at steady state)
-  C4   512^2 / 4000 m (single cascade until cascades land), U10 20,
-       gamma 5, s 4; 8 x 128 m patches on 512 grids; 16 buckets
+  C4   3 summed 512^2 cascades over 4000 / 1000 / 250 m with disjoint |k|
+       bands (FFT band widened to 6 rad/s), U10 20, gamma 5, s 4; 8 x 128 m
+       patches on 512 grids; 16 buckets
   C5   2048^2 / 8000 m; 64 x 192 m patches on 768 grids; 16 buckets;
        n_theta 16; one ship per patch on a seeded heading at 5-15 m/s, 1024
        Kelvin-wedge particles per frame, the patch tracking its ship
@@ -87,9 +88,12 @@ def c3(**kw) -> SimConfig:
 
 
 def c4(**kw) -> SimConfig:
+    """3 summed cascades 4000 / 1000 / 250 m (disjoint |k| bands, config.cascade_bands)
+    over a band widened to 6 rad/s so every tile carries energy."""
     org = seeded_layout(8, 128.0, 4000.0, seed=4)
     cfg = SimConfig(u10=20.0, fetch=100000.0, gamma=5.0, spread_s=4.0, n_omega=16, n_theta=16, dt=1.0 / 60.0,
                     frames=600, seed=4, fft_n=512, fft_domain=4000.0, fft_choppiness=1.0,
+                    fft_cascades=(4000.0, 1000.0, 250.0), fft_band_hi=6.0,
                     patches=tuple(PatchConfig(origin=o, size=(128.0, 128.0), res=512, margin=10.0) for o in org),
                     write_frames=False)
     return replace(cfg, **kw).validate()

@@ -137,3 +137,33 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+
+
+def test_cascade_bands_partition_k():
+    """fft.cascades: disjoint, contiguous |k| bands, largest tile first,
+    boundaries at half the larger tile's Nyquist (config.cascade_bands),
+    identical to the oracle's scene definition."""
+    import math
+    from oracle.scene_ref import cascade_bands as ref_bands
+    from paper_2511_02852_b200.config import cascade_bands
+    b = cascade_bands((250.0, 4000.0, 1000.0), 512)
+    assert [t[0] for t in b] == [4000.0, 1000.0, 250.0]
+    assert b[0][1] == 0.0 and math.isinf(b[-1][2])
+    for (_, _, hi), (_, lo, _) in zip(b, b[1:]):
+        assert hi == lo
+    assert b[0][2] == math.pi * 512 / (2 * 4000.0)
+    assert b == ref_bands((250.0, 4000.0, 1000.0), 512)
+
+
+def test_single_cascade_scene_equals_plain_scene():
+    """A one-tile cascade list is the plain background (oracle)."""
+    import numpy as np
+    from dataclasses import replace
+    from oracle import scene_ref
+    from paper_2511_02852_b200 import scenes
+    cfg = scenes.pr1(fft_n=64)
+    a = scene_ref.OracleScene(cfg.scene_dict())
+    b = scene_ref.OracleScene(replace(cfg, fft_cascades=(cfg.fft_domain,)).scene_dict())
+    oa, ob = a.step(), b.step()
+    np.testing.assert_array_equal(oa["height"], ob["height"])
+    np.testing.assert_array_equal(oa["blend_heights"][0], ob["blend_heights"][0])
