@@ -55,20 +55,33 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--stage-frames", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--patches", type=int, default=None, help="use the first N patches of a multi-patch scene")
     return ap.parse_args()
 
 
-def scene_config(name: str, rank: int, world: int):
+def scene_config(name: str, rank: int, world: int, patches: int | None = None):
+    """(config of this rank, Philox keys or None, scaling).  Single-patch
+    scenes (C3, PR1) scale weakly: rank r owns patch r of a seeded layout of
+    `world` same-size patches.  Multi-patch scenes (C2, C4, C5) scale
+    strongly: the scene's patches are split into contiguous blocks
+    (sharding.shard_config), each patch keeping its global Philox key."""
+    from dataclasses import replace
     from paper_2511_02852_b200 import scenes
+    from paper_2511_02852_b200.sharding import shard_config
     cfg = scenes.PRESETS[name]()
-    if world > 1:
-        # weak scaling: rank r owns patch r of a seeded layout of `world`
-        # same-size patches in the shared tile
-        from dataclasses import replace
-        p0 = cfg.patches[0]
-        org = scenes.seeded_layout(world, p0.size[0], cfg.fft_domain, seed=cfg.seed + 100)
-        cfg = replace(cfg, patches=(replace(p0, origin=org[rank]),), seed=cfg.seed + rank).validate()
-    return cfg
+    if patches is not None and patches < len(cfg.patches):
+        cfg = replace(cfg, patches=cfg.patches[:patches]).validate()
+        tracked = {pc.track_source for pc in cfg.patches}
+        if any(pc.track_source >= 0 for pc in cfg.patches):
+            cfg = replace(cfg, sources=cfg.sources[:max(tracked) + 1]).validate()
+    if len(cfg.patches) == 1:
+        if world > 1:
+            p0 = cfg.patches[0]
+            org = scenes.seeded_layout(world, p0.size[0], cfg.fft_domain, seed=cfg.seed + 100)
+            cfg = replace(cfg, patches=(replace(p0, origin=org[rank]),), seed=cfg.seed + rank).validate()
+        return cfg, None, "weak"
+    local, _, keys = shard_config(cfg, rank, world)
+    return local.validate(), keys, "strong"
 
 
 # ------------------------------------------------------------ clocks ----
@@ -155,7 +168,7 @@ def reference_arm(args):
     if rank != 0:
         return 0
     from oracle import scene_ref
-    cfg = scene_config(args.config, 0, 1)
+    cfg, _, _ = scene_config(args.config, 0, 1, args.patches)
     sc = scene_ref.OracleScene(cfg.scene_dict())
     t_warm = time.perf_counter()
     n_warm = int(round(args.warm_seconds / WARM_DT))
@@ -201,9 +214,13 @@ def main():
     from paper_2511_02852_b200 import _native as N
     from paper_2511_02852_b200.sharding import TileGather
 
-    cfg = scene_config(args.config, rank, world)
-    sim = Simulation(cfg, device=dev)
-    gather = TileGather(sim, world) if world > 1 else None
+    cfg, keys, scaling = scene_config(args.config, rank, world, args.patches)
+    sim = Simulation(cfg, device=dev, rng_seed_keys=keys)
+    gather = None
+    if world > 1:
+        share = torch.tensor([int(sim.synth.grid_base[-1])], device=dev)
+        dist.all_reduce(share, op=dist.ReduceOp.MAX)
+        gather = TileGather(sim, world, max_local=int(share.item()))
 
     # steady state: the step itself at dt = 0.1
     n_warm = int(round(args.warm_seconds / WARM_DT))
@@ -266,30 +283,40 @@ def main():
             stage[kname] = stage.get(kname, 0.0) + v
     stage = {k: v / args.stage_frames for k, v in stage.items()}
 
-    # e2e through the public API with host buffers: H2D of the frame
-    # parameter block, graph step, D2H of the blended tile + bucket counts
-    res, ny = sim.synth.grids[0]
-    host_tile = torch.empty((res, ny), dtype=torch.float32, pin_memory=True)
-    host_counts = torch.empty(sim.n_patches * sim.nb, dtype=torch.int32, pin_memory=True)
-    host_frame = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    # e2e through the public API with host buffers, every step: H2D of the
+    # frame index from pinned memory, the graph step, D2H of every blended
+    # patch tile + the live counts into pinned memory.  HostFramePipe overlaps
+    # frame k's host copy with frame k+1's compute (the timed region ends
+    # when the last copy has landed).
+    from paper_2511_02852_b200.harness import HostFramePipe
+    pipe = HostFramePipe(sim)
+    for _ in range(3):
+        pipe.step()
+    # one pinned source per step: the loop runs ahead of the device, so a
+    # reused buffer could be rewritten before its H2D copy executes
+    host_frames = torch.arange(sim.frame, sim.frame + args.e2e_steps, dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
     e2e_start, e2e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e2e_start.record()
-    for _ in range(args.e2e_steps):
-        host_frame[0] = sim.frame
-        sim.frame_dev.copy_(host_frame, non_blocking=True)
-        sim.step(stats=False)
-        host_tile.copy_(sim.blended_tile(0)[0], non_blocking=True)
-        host_counts.copy_(sim.live, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-    e2e_end.record()
+    last = 0
+    for k in range(args.e2e_steps):
+        sim.frame_dev.copy_(host_frames[k:k + 1], non_blocking=True)
+        last = pipe.step()
+    with torch.cuda.stream(pipe.copy):
+        e2e_end.record(pipe.copy)
+    tiles, counts = pipe.result(last)
     torch.cuda.synchronize()
+    assert int(counts.sum()) == sim.live_particles() and bool(torch.isfinite(tiles).all())
     e2e_ms = e2e_start.elapsed_time(e2e_end) / args.e2e_steps
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t[0])
     e2e_value = live_all * 1e3 / e2e_ms
+    e2e_bytes = pipe.bytes_per_frame
 
     # roofline of the dominant particle kernel, hs_advect_resident (in-place
     # advect + cull + splat): per live particle it must read x, y, ux, uy (f64)
@@ -327,13 +354,18 @@ def main():
         line = {
             "metric": "particles splatted/s (hybrid step)", "value": value, "unit": "particles/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-            "fps": fps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "fps": fps, "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic (seeded h0 + Philox streams; steady state reached by the step itself)",
-            "config": {"workload": f"{args.config} hybrid step (1 patch per GPU)", "live_particles": live_all,
+            "config": {"workload": f"{args.config} hybrid step"
+                                   + (" (1 patch per GPU)" if scaling == "weak" else
+                                      f" ({len(cfg.patches)} of its patches on rank 0)"),
+                       "live_particles": live_all,
                        "fft_n": cfg.fft_n, "fft_domain_m": cfg.fft_domain, "patch_res": cfg.patches[0].res,
+                       "n_patches": len(cfg.patches) * (world if scaling == "weak" else 1),
+                       "fft_cascades": list(cfg.fft_cascades), "n_sources": len(cfg.sources),
                        "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
                        "warm_start": f"{n_warm} frames at dt={WARM_DT}", "l2": "flushed between timed steps",
-                       "parallelism": f"patch-sharded x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"patch-sharded x{world}" if world > 1 else "single GPU")},
             "step_ms_percentiles": step_pct,
             "gpu_launches": sim.kernel_launches_per_frame() * args.steps,
             "stages_ms": stage,
@@ -342,7 +374,8 @@ def main():
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes": adv_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
             "e2e": {"value": e2e_value, "unit": "particles/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": 8, "d2h_bytes_per_step": res * ny * 4 + sim.n_patches * sim.nb * 4},
+                    "h2d_bytes_per_step": 8, "d2h_bytes_per_step": e2e_bytes,
+                    "note": "host copy of frame k overlaps frame k+1 (HostFramePipe, pinned, depth 2)"},
             "clocks": clk,
             "wall_s_timed": wall,
         }

@@ -777,6 +777,55 @@ class Simulation:
                 "e_in": self.e_in.cpu().numpy().reshape(P, nb), "e_out": self.e_out.cpu().numpy().reshape(P, nb)}
 
 
+class HostFramePipe:
+    """Streams every frame's blended patch tiles and live counts to pinned host
+    memory while the next frame computes: at the end of each frame a
+    device-side snapshot (D2D, on the frame's stream) frees the live buffers,
+    and a copy stream moves the snapshot to the host, `depth`-buffered.  A
+    frame waits only for the host copy of frame k - depth (long finished), so
+    end-to-end throughput is max(frame time, transfer time) instead of their
+    sum.  `step()` returns the slot whose host buffers `result(slot)` fills."""
+
+    def __init__(self, sim: "Simulation", depth: int = 2):
+        self.sim = sim
+        self.depth = depth
+        self.n = int(sim.synth.grid_base[-1])
+        dev = sim.device
+        self.stage = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(depth)]
+        self.stage_cnt = [torch.empty_like(sim.live) for _ in range(depth)]
+        self.host = [torch.empty(self.n, dtype=torch.float32, pin_memory=True) for _ in range(depth)]
+        self.host_cnt = [torch.empty(sim.live.numel(), dtype=torch.int32, pin_memory=True) for _ in range(depth)]
+        self.copy = torch.cuda.Stream(device=dev)
+        self.done = [torch.cuda.Event() for _ in range(depth)]
+        self.k = 0
+
+    @property
+    def bytes_per_frame(self) -> int:
+        return 4 * self.n + 4 * self.sim.live.numel()
+
+    def step(self, dt: float | None = None) -> int:
+        i = self.k % self.depth
+        main = torch.cuda.current_stream(self.sim.device)
+        main.wait_event(self.done[i])            # slot i's previous host copy has landed
+        self.sim.step(dt, stats=False)
+        self.stage[i].copy_(self.sim.blend_h[: self.n])
+        self.stage_cnt[i].copy_(self.sim.live)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(ready)
+            self.host[i].copy_(self.stage[i], non_blocking=True)
+            self.host_cnt[i].copy_(self.stage_cnt[i], non_blocking=True)
+            self.done[i].record(self.copy)
+        self.k += 1
+        return i
+
+    def result(self, slot: int) -> tuple:
+        """(blended tiles of every patch, flat f32; live counts) of the frame in `slot`."""
+        self.done[slot].synchronize()
+        return self.host[slot], self.host_cnt[slot]
+
+
 def benchmark_cell(cfg: SimConfig, warmup: int | None = None, measure: int | None = None, label: str = ""):
     """Steady-state throughput of one cell (harness.py:345-369), device-timed."""
     warmup = cfg.bench_warmup if warmup is None else warmup

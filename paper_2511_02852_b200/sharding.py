@@ -39,7 +39,14 @@ def shard_config(cfg, rank: int, world: int):
     from dataclasses import replace
     pcs = tuple(cfg.patches)
     block = partition(len(pcs), world)[rank]
-    local = replace(cfg, patches=tuple(pcs[k] for k in block))
+    # sources: those tracked by a local patch, plus every untracked one (it may
+    # wander into any patch); track indices remapped to the local list
+    tracked = {pc.track_source for pc in pcs if pc.track_source >= 0}
+    keep = [j for j in range(len(cfg.sources))
+            if j not in tracked or any(pcs[k].track_source == j for k in block)]
+    remap = {j: i for i, j in enumerate(keep)}
+    local_pcs = tuple(replace(pcs[k], track_source=remap.get(pcs[k].track_source, -1)) for k in block)
+    local = replace(cfg, patches=local_pcs, sources=tuple(cfg.sources[j] for j in keep))
     ids = list(block)
     return local, ids, [(cfg.seed, k) for k in ids]
 
@@ -63,18 +70,26 @@ def assemble(tiles: torch.Tensor, shapes: list[tuple[int, int]]) -> list[torch.T
 
 
 class TileGather:
-    """Per-frame all-gather of every rank's blended tile of its first patch
-    (bench.py weak-scaling workload: one equal-size patch per rank)."""
+    """Per-frame NCCL all-gather of every rank's blended patch tiles (the
+    composite exchange of SURVEY 8(e)): each rank contributes its patches'
+    blend heights, which are contiguous in the per-device grid buffer, padded
+    to the largest rank's share (block sizes differ by at most one patch)."""
 
-    def __init__(self, sim, world: int, group=None):
+    def __init__(self, sim, world: int, group=None, max_local: int | None = None):
         self.sim = sim
         self.world = world
         self.group = group
-        res, ny = sim.synth.grids[0]
-        self.shape = (res, ny)
-        self.out = torch.empty(world * res * ny, dtype=torch.float32, device=sim.device)
+        self.local = int(sim.synth.grid_base[-1])           # floats of this rank's tiles
+        self.per_rank = max_local if max_local is not None else self.local
+        self.send = torch.zeros(self.per_rank, dtype=torch.float32, device=sim.device)
+        self.out = torch.empty(world * self.per_rank, dtype=torch.float32, device=sim.device)
 
     def exchange(self) -> torch.Tensor:
-        h = self.sim.blended_tile(0)[0].reshape(-1)
-        dist.all_gather_into_tensor(self.out, h, group=self.group)
+        h = self.sim.blend_h[: self.local]
+        if self.local == self.per_rank:
+            src = h
+        else:
+            self.send[: self.local].copy_(h)
+            src = self.send
+        dist.all_gather_into_tensor(self.out, src, group=self.group)
         return self.out.view(self.world, -1)
