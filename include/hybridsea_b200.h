@@ -144,6 +144,30 @@ typedef struct {
 HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Resident pool (the Simulation frame path), see hs_advect_resident below.  */
+typedef struct {
+    int n_patches, nb;
+    const HsBucket* buckets;
+    const HsPatch* patches;
+    double dt, rho, g;
+    HsPool pool;                   /* the current buffer */
+    const int* seg_base;           /* [n_patches*nb] absolute element offset */
+    const int* seg_cap;            /* [n_patches*nb] */
+    const int* tile_map;           /* [max_tiles*4], 16-byte aligned: (segment, tile within
+                                      segment, absolute first slot, 0); unused tiles (-1, 0, 0, 0) */
+    int max_tiles;                 /* tile-map entries */
+    const int* len_in;             /* [n_patches*nb] slots in use at frame start */
+    int* len_out;                  /* [n_patches*nb] written by hs_append_resident */
+    int* live;                     /* [n_patches*nb] live particles (atomic updates) */
+    HsPool stage; const int* stage_count;   /* hs_append_resident: this frame's injected set */
+    double* e_out;                 /* [n_patches*nb] despawn ledger */
+    float* raw_layers;             /* must be zero at frame start (not cleared here) */
+    const HsLayer* layers;
+    int* clamped;                  /* [n_patches] */
+    int* status;
+} HsResidentArgs;
+
+/* ------------------------------------------------------------------------ */
 /* Boundary injection for all patches (one CTA per patch).  Replaces inject
  * (particles.py:219-300).  Random draws follow numpy's Philox4x64-10 stream:
  * rng[8*p + 0..1] = key, [2..5] = counter0 (256-bit LE), [6] = draw index.   */
@@ -164,6 +188,10 @@ typedef struct {
     int* status;
     int* zero_words;               /* optional: 4-byte words zeroed by this launch (per-frame */
     int n_zero_words;              /*   stat accumulators read by later kernels)             */
+    int append;                    /* 1: the new particles skip the stage -- they are advected,
+                                      culled and splatted here and appended to the resident
+                                      segments (what hs_append_resident does with a stage) */
+    HsResidentArgs res;            /* resident pool for append (its stage fields are unused) */
 } HsInjectArgs;
 HS_API int hs_inject(const HsInjectArgs* a, void* stream);
 
@@ -221,27 +249,7 @@ HS_API int hs_advect(const HsAdvectArgs* a, void* stream);
  * Every K frames hs_advect (count + scatter, in_seg_base/out_slack_prefix)
  * squeezes the holes out into the other buffer and hs_resident_layout
  * re-derives the segment table.                                             */
-typedef struct {
-    int n_patches, nb;
-    const HsBucket* buckets;
-    const HsPatch* patches;
-    double dt, rho, g;
-    HsPool pool;                   /* the current buffer */
-    const int* seg_base;           /* [n_patches*nb] absolute element offset */
-    const int* seg_cap;            /* [n_patches*nb] */
-    const int* tile_map;           /* [max_tiles*4], 16-byte aligned: (segment, tile within
-                                      segment, absolute first slot, 0); unused tiles (-1, 0, 0, 0) */
-    int max_tiles;                 /* tile-map entries */
-    const int* len_in;             /* [n_patches*nb] slots in use at frame start */
-    int* len_out;                  /* [n_patches*nb] written by hs_append_resident */
-    int* live;                     /* [n_patches*nb] live particles (atomic updates) */
-    HsPool stage; const int* stage_count;   /* hs_append_resident: this frame's injected set */
-    double* e_out;                 /* [n_patches*nb] despawn ledger */
-    float* raw_layers;             /* must be zero at frame start (not cleared here) */
-    const HsLayer* layers;
-    int* clamped;                  /* [n_patches] */
-    int* status;
-} HsResidentArgs;
+
 HS_API int hs_advect_resident(const HsResidentArgs* a, void* stream);
 HS_API int hs_append_resident(const HsResidentArgs* a, void* stream);
 

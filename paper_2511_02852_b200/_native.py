@@ -59,12 +59,20 @@ class HsFftArgs(C.Structure):
                 ("omega", vp)]
 
 
+class HsResidentArgs(C.Structure):
+    _fields_ = [("n_patches", i32), ("nb", i32), ("buckets", vp), ("patches", vp), ("dt", dbl),
+                ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp),
+                ("tile_map", vp), ("max_tiles", i32), ("len_in", vp), ("len_out", vp), ("live", vp),
+                ("stage", HsPool), ("stage_count", vp), ("e_out", vp), ("raw_layers", vp), ("layers", vp),
+                ("clamped", vp), ("status", vp)]
+
+
 class HsInjectArgs(C.Structure):
     _fields_ = [("n_patches", i32), ("nb", i32), ("n_theta", i32), ("buckets", vp), ("patches", vp),
                 ("half_rate", vp), ("mean_dir", dbl), ("beta", dbl), ("rho", dbl), ("g", dbl),
                 ("acc", vp), ("groups", vp), ("e_in", vp), ("rng", vp), ("stage", HsPool),
                 ("stage_count", vp), ("scratch", vp), ("member_capacity", i32), ("status", vp),
-                ("zero_words", vp), ("n_zero_words", i32)]
+                ("zero_words", vp), ("n_zero_words", i32), ("append", i32), ("res", HsResidentArgs)]
 
 
 class HsAdvectArgs(C.Structure):
@@ -75,14 +83,6 @@ class HsAdvectArgs(C.Structure):
                 ("raw_layers_len", i64), ("layers", vp), ("clamped", vp), ("tile_state", vp),
                 ("max_tiles", i32), ("tile_counter", vp), ("status", vp), ("keep_words", vp),
                 ("in_seg_base", vp), ("out_slack_prefix", vp), ("raw_is_clear", i32)]
-
-
-class HsResidentArgs(C.Structure):
-    _fields_ = [("n_patches", i32), ("nb", i32), ("buckets", vp), ("patches", vp), ("dt", dbl),
-                ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp),
-                ("tile_map", vp), ("max_tiles", i32), ("len_in", vp), ("len_out", vp), ("live", vp),
-                ("stage", HsPool), ("stage_count", vp), ("e_out", vp), ("raw_layers", vp), ("layers", vp),
-                ("clamped", vp), ("status", vp)]
 
 
 class HsSource(C.Structure):

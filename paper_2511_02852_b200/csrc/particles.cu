@@ -19,6 +19,49 @@
 
 namespace hs {
 
+// Bilinear scatter-add of one particle into its bucket layer
+// (patch_synthesis.py:165-186 at gx/f, 298-310).  u = (x - x0)/(texel f) + pad
+// in fp64 (index and clamp decision), weights in fp32.
+struct SplatLayer {
+    long long raw_off;
+    double inv_tf;          // 1 / (texel * f)
+    double umax, vmax;      // wx - 1, wy - 1
+    int pitch, pad;         // raw row pitch (multiple of 4 floats), grid pad
+};
+
+__device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void red2(float* p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(a), "f"(b) : "memory");
+}
+// add (v0, v1) at row[c], row[c + 1]; row is 16-byte aligned: one 16-byte
+// reduction when the pair sits in one aligned float4, else two 8-byte ones
+// (zero lanes leave their neighbours unchanged)
+__device__ __forceinline__ void red_pair(float* row, int c, float v0, float v1) {
+    const int s = c & 3;
+    float* b = row + (c - s);
+    if (s == 0) red4(b, v0, v1, 0.f, 0.f);
+    else if (s == 1) red4(b, 0.f, v0, v1, 0.f);
+    else if (s == 2) red2(b + 2, v0, v1);
+    else { red2(b + 2, 0.f, v0); red2(b + 4, v1, 0.f); }
+}
+
+__device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLayer& L, double x0, double y0,
+                                         double x, double y, float amp, int* clamp_acc) {
+    double u = (x - x0) * L.inv_tf + (double)L.pad;
+    double v = (y - y0) * L.inv_tf + (double)L.pad;
+    if (u < 0.0 || u > L.umax || v < 0.0 || v > L.vmax) ++(*clamp_acc);
+    u = fmin(fmax(u, 0.0), L.umax - 1e-9);
+    v = fmin(fmax(v, 0.0), L.vmax - 1e-9);
+    const int i0 = (int)u, j0 = (int)v;
+    const float fu = (float)(u - i0), fv = (float)(v - j0);
+    float* row = raw + L.raw_off + (long long)i0 * L.pitch;
+    const float a1 = amp * fu, a0 = amp - a1;          // amp (1 - fu), amp fu
+    red_pair(row, j0, a0 * (1.f - fv), a0 * fv);
+    red_pair(row + L.pitch, j0, a1 * (1.f - fv), a1 * fv);
+}
+
 // ============================================================== inject ==
 struct InjectDev {
     HsInjectArgs a;
@@ -47,6 +90,26 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     __shared__ int scan_sm[33];
     __shared__ int abort_s;
     const HsPatch P = a.patches[p];
+    // resident append (a.append): per-bucket advection constants and segment tails
+    __shared__ double ap_step[HS_MAX_BUCKETS], ap_r2[HS_MAX_BUCKETS], ap_eout[HS_MAX_BUCKETS];
+    __shared__ long long ap_dst[HS_MAX_BUCKETS];
+    __shared__ int ap_room[HS_MAX_BUCKETS], ap_kept[HS_MAX_BUCKETS], ap_clamp;
+    __shared__ SplatLayer ap_sl[HS_MAX_BUCKETS];
+    if (a.append && threadIdx.x >= 32 && threadIdx.x < 32 + nb) {
+        const int b = threadIdx.x - 32, s = p * nb + b;
+        const HsBucket Bk = a.buckets[b];
+        ap_step[b] = dmul(Bk.speed, a.res.dt);            // speeds * dt (particles.py:312)
+        ap_r2[b] = dmul(Bk.radius, Bk.radius);
+        const int len = a.res.len_in[s];
+        ap_dst[b] = (long long)a.res.seg_base[s] + len;
+        ap_room[b] = a.res.seg_cap[s] - len;
+        ap_kept[b] = 0;
+        ap_eout[b] = 0.0;
+        const HsLayer L = a.res.layers[P.layer_base + b];
+        ap_sl[b] = SplatLayer{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1),
+                              L.raw_pitch, L.pad};
+        if (b == 0) ap_clamp = 0;
+    }
     double* acc = a.acc + (size_t)p * ncell;
     const double* hr = a.half_rate + (size_t)p * ncell;
     unsigned long long* rng = a.rng + (size_t)p * 8;
@@ -87,7 +150,10 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     const int g_tot = gstart[ncell];
     int* scount = a.stage_count + (size_t)p * nb;
     if (g_tot == 0 || abort_s) {     // no groups: no RNG draws (particles.py:248-249)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = 0;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            scount[b] = 0;
+            if (a.append) a.res.len_out[p * nb + b] = a.res.len_in[p * nb + b];
+        }
         return;
     }
     const int M = g_tot * nth;
@@ -156,7 +222,10 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     }
     __syncthreads();
     if (abort_s) {
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = 0;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            scount[b] = 0;
+            if (a.append) a.res.len_out[p * nb + b] = a.res.len_in[p * nb + b];
+        }
         if (threadIdx.x == 0) rng[6] = D + (unsigned long long)g_tot * (1 + nth);
         return;
     }
@@ -188,21 +257,64 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
             else if (side == 2) { px = dadd(P.x0, dmul(u, P.l1)); py = P.y0; }
             else                { px = dadd(P.x0, dmul(u, P.l1)); py = dadd(P.y0, P.l2); }
             const int rank = ex - live_before[b];
-            long long o = sb + soff[b] + rank;
-            a.stage.x[o] = px; a.stage.y[o] = py; a.stage.ux[o] = dx; a.stage.uy[o] = dy;
-            a.stage.amp[o] = (float)amp;
-            if (per_live == 2) {
-                o += live_cnt[b];
-                a.stage.x[o] = dsub(px, dmul(B.radius, dx));
-                a.stage.y[o] = dsub(py, dmul(B.radius, dy));
-                a.stage.ux[o] = dx; a.stage.uy[o] = dy;
-                a.stage.amp[o] = (float)(-a.beta * amp);
+            if (a.append) {
+                // advected in their birth frame (harness.py:142-152), culled, appended
+                // in the stage's slot order [crests b][troughs b]; culled ones leave holes
+                const double ph = dsub(px, dmul(B.radius, dx)), qh = dsub(py, dmul(B.radius, dy));
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    if (m == 1 && per_live != 2) break;
+                    const int j = rank + m * live_cnt[b];
+                    const double x0 = m ? ph : px, y0 = m ? qh : py;
+                    const float am = m ? (float)(-a.beta * amp) : (float)amp;
+                    const double nx = dadd(x0, dmul(dx, ap_step[b]));      // pos += dir * (c dt) (:312-313)
+                    const double ny = dadd(y0, dmul(dy, ap_step[b]));
+                    const double ox = fmax(fmax(dsub(P.x0, nx), dsub(nx, P.x1)), 0.0);
+                    const double oy = fmax(fmax(dsub(P.y0, ny), dsub(ny, P.y1)), 0.0);
+                    const bool keep = dadd(dmul(ox, ox), dmul(oy, oy)) <= ap_r2[b];  // (:315-320)
+                    if (j < ap_room[b]) {
+                        const long long o = ap_dst[b] + j;
+                        a.res.pool.x[o] = keep ? nx : __longlong_as_double(0x7ff8000000000000LL);
+                        a.res.pool.y[o] = ny; a.res.pool.ux[o] = dx; a.res.pool.uy[o] = dy; a.res.pool.amp[o] = am;
+                    }
+                    if (keep) {
+                        atomicAdd(&ap_kept[b], 1);
+                        int cl = 0;
+                        splat_at(a.res.raw_layers, ap_sl[b], P.sx0, P.sy0, nx, ny, am, &cl);
+                        if (cl) atomicAdd(&ap_clamp, cl);
+                    } else if (am > 0.f) {
+                        const double e2 = (double)am;                  // crest despawn energy (:322-327)
+                        atomicAdd(&ap_eout[b], 0.125 * a.rho * a.g * (e2 * e2) * 3.141592653589793 * ap_r2[b]);
+                    }
+                }
+            } else {
+                long long o = sb + soff[b] + rank;
+                a.stage.x[o] = px; a.stage.y[o] = py; a.stage.ux[o] = dx; a.stage.uy[o] = dy;
+                a.stage.amp[o] = (float)amp;
+                if (per_live == 2) {
+                    o += live_cnt[b];
+                    a.stage.x[o] = dsub(px, dmul(B.radius, dx));
+                    a.stage.y[o] = dsub(py, dmul(B.radius, dy));
+                    a.stage.ux[o] = dx; a.stage.uy[o] = dy;
+                    a.stage.amp[o] = (float)(-a.beta * amp);
+                }
             }
         }
         carry += tot;
     }
     for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = per_live * live_cnt[b];
     if (threadIdx.x == 0) rng[6] = D + (unsigned long long)g_tot * (1 + nth);
+    if (a.append) {
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            const int s = p * nb + b, n = per_live * live_cnt[b];
+            a.res.len_out[s] = a.res.len_in[s] + n;
+            if (n > ap_room[b]) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
+            if (ap_kept[b]) atomicAdd(&a.res.live[s], ap_kept[b]);
+            if (ap_eout[b] != 0.0) atomicAdd(&a.res.e_out[s], ap_eout[b]);
+        }
+        if (threadIdx.x == 0 && ap_clamp && a.res.clamped) atomicAdd(&a.res.clamped[p], ap_clamp);
+    }
 }
 
 // ============================================================== advect ==
@@ -219,49 +331,6 @@ __device__ __forceinline__ int find_seg(const int* off, int nseg, int v) {
         if (off[mid] <= v) lo = mid; else hi = mid - 1;
     }
     return lo;
-}
-
-// Bilinear scatter-add of one particle into its bucket layer
-// (patch_synthesis.py:165-186 at gx/f, 298-310).  u = (x - x0)/(texel f) + pad
-// in fp64 (index and clamp decision), weights in fp32.
-struct SplatLayer {
-    long long raw_off;
-    double inv_tf;          // 1 / (texel * f)
-    double umax, vmax;      // wx - 1, wy - 1
-    int pitch, pad;         // raw row pitch (multiple of 4 floats), grid pad
-};
-
-__device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
-__device__ __forceinline__ void red2(float* p, float a, float b) {
-    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(a), "f"(b) : "memory");
-}
-// add (v0, v1) at row[c], row[c + 1]; row is 16-byte aligned: one 16-byte
-// reduction when the pair sits in one aligned float4, else two 8-byte ones
-// (zero lanes leave their neighbours unchanged)
-__device__ __forceinline__ void red_pair(float* row, int c, float v0, float v1) {
-    const int s = c & 3;
-    float* b = row + (c - s);
-    if (s == 0) red4(b, v0, v1, 0.f, 0.f);
-    else if (s == 1) red4(b, 0.f, v0, v1, 0.f);
-    else if (s == 2) red2(b + 2, v0, v1);
-    else { red2(b + 2, 0.f, v0); red2(b + 4, v1, 0.f); }
-}
-
-__device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLayer& L, double x0, double y0,
-                                         double x, double y, float amp, int* clamp_acc) {
-    double u = (x - x0) * L.inv_tf + (double)L.pad;
-    double v = (y - y0) * L.inv_tf + (double)L.pad;
-    if (u < 0.0 || u > L.umax || v < 0.0 || v > L.vmax) ++(*clamp_acc);
-    u = fmin(fmax(u, 0.0), L.umax - 1e-9);
-    v = fmin(fmax(v, 0.0), L.vmax - 1e-9);
-    const int i0 = (int)u, j0 = (int)v;
-    const float fu = (float)(u - i0), fv = (float)(v - j0);
-    float* row = raw + L.raw_off + (long long)i0 * L.pitch;
-    const float a1 = amp * fu, a0 = amp - a1;          // amp (1 - fu), amp fu
-    red_pair(row, j0, a0 * (1.f - fv), a0 * fv);
-    red_pair(row + L.pitch, j0, a1 * (1.f - fv), a1 * fv);
 }
 
 __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
@@ -1127,6 +1196,10 @@ extern "C" int hs_inject(const HsInjectArgs* a, void* stream) {
     HS_CHECK_ARG(a->buckets && a->patches && a->half_rate && a->acc && a->groups && a->e_in && a->rng &&
                  a->stage_count && a->scratch && a->status && a->stage.x && a->stage.amp,
                  "hs_inject: missing buffer");
+    if (a->append)
+        HS_CHECK_ARG(a->res.pool.x && a->res.pool.amp && a->res.seg_base && a->res.seg_cap && a->res.len_in &&
+                     a->res.len_out && a->res.live && a->res.e_out && a->res.raw_layers && a->res.layers,
+                     "hs_inject: append needs the resident pool");
     inject_kernel<<<a->n_patches, 512, 0, as_stream(stream)>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;

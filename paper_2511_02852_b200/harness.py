@@ -454,16 +454,17 @@ class Simulation:
                 mark("advect")
             else:
                 ra = self._resident_args(buf, lp, dt, stats)
+                inj_args.append = 1                 # new particles go straight to the segment tails
+                inj_args.res = ra
                 inj = self._side_stream("inject")
                 inj.wait_stream(main)
                 with torch.cuda.stream(inj):
                     mark("inject_start")
                     N.call("hs_inject", inj_args, stream_ptr())
                     mark("inject")
-                    N.call("hs_append_resident", ra, stream_ptr())
                     if self.n_sources:
                         N.call("hs_emit", self._emit_args(buf, lp, dt, stats), stream_ptr())
-                    mark("append")
+                        mark("emit")
                 mark("particles_start")
                 N.call("hs_advect_resident", ra, stream_ptr())
                 mark("advect")
@@ -569,7 +570,7 @@ class Simulation:
         if self.n_patches:
             pk = self.synth.pack
             K = self.compact_period
-            k += 1 + 1 + (2.0 * (K - 1) + 3.0) / K
+            k += 1 + (1.0 * (K - 1) + 3.0) / K       # inject (+append fused); advect or count+scatter+layout
             if self.n_sources:
                 k += 2 + (1 if self._tracking else 0)      # emit + commit (+ track)
             k += (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
