@@ -253,6 +253,18 @@ HS_API int hs_advect(const HsAdvectArgs* a, void* stream);
 HS_API int hs_advect_resident(const HsResidentArgs* a, void* stream);
 HS_API int hs_append_resident(const HsResidentArgs* a, void* stream);
 
+/* One further tile of a summed-cascade background (fft.cascades): periodic,
+ * origin 0, its own spacing.  Samplers add its bilinear height and combine
+ * normals through slopes, n = normalize(sum_c n_c.xy / n_c.z, 1), n_c the
+ * renormalised bilinear of the tile's periodic node normals.               */
+#define HS_MAX_CASCADES 4
+typedef struct {
+    const float* height;      /* [n*n] */
+    int n;                    /* power of two */
+    int pad;
+    double spacing;
+} HsBgTile;
+
 /* ------------------------------------------------------------------------ */
 /* Kinematic emitting bodies: the reference's per-frame
  * buoyancy_step + emit_from_motion + _retrack_patches (interaction.py:140,
@@ -271,8 +283,46 @@ typedef struct {
     int n_ring, n_wake;       /* fan sizes */
     int ring_bucket, wake_bucket;
     int dir_off;              /* ring directions, then wake directions, in HsEmitArgs.dirs */
-    int pad;
+    int body;                 /* >= 0: a floating body (HsEmitArgs.bodies[body]): position, energy
+                                 split, amplitudes and the wake's direction come from its state every
+                                 frame; the wake entries at dir_off + n_ring hold the fan's angle
+                                 offsets (np.linspace(-h, h, n_wake), x component) */
 } HsSource;
+
+/* A floating body (FloatingBody / box_body, interaction.py:36-102), state
+ * updated in place by hs_bodies.                                            */
+#define HS_MAX_PROBES 8
+typedef struct {
+    double pos[3], vel[3];
+    double yaw, yaw_rate;
+    double submerged, prev_submerged, mean_submersion;
+    double mass, hull_extent, draft, drag_linear, drag_yaw;
+    double thrust_force;      /* thrust * max_thrust (N) */
+    double yaw_torque;        /* rudder * max_yaw_torque (N m) */
+    double displaced;         /* sum of probe volumes, in probe order */
+    double probe_off[HS_MAX_PROBES][3];
+    double probe_vol[HS_MAX_PROBES];
+    int n_probes, pad;
+} HsBody;
+
+/* buoyancy_step (interaction.py:105-149) of every body against the blended
+ * surface of the previous frame (SurfaceSampler._raw, coupling.py:120-141):
+ * the periodic background (+ cascades) and the patch heights at their
+ * synthesis rectangles, normals from their finite differences.  Call before
+ * the frame's transform and hs_track overwrite them; `flat` = 1 before the
+ * first synthesised frame (the reference's initial SurfaceSampler(None, [])). */
+typedef struct {
+    int n_bodies;
+    HsBody* bodies;
+    double dt, rho, g;
+    int flat;
+    const float* bg_height; int bg_n; double bg_spacing;
+    int n_extra_bg; HsBgTile extra_bg[HS_MAX_CASCADES - 1];
+    int n_patches;
+    const HsPatch* patches;
+    const float* patch_height;
+} HsBodyArgs;
+HS_API int hs_bodies(const HsBodyArgs* a, void* stream);
 
 #define HS_MAX_SOURCES 1024
 typedef struct {
@@ -290,6 +340,8 @@ typedef struct {
     double* e_in;
     float* raw_layers; const HsLayer* layers; int* clamped;
     int* status;
+    const HsBody* bodies;     /* for sources with body >= 0 */
+    int n_theta;              /* ring fan of bodies (interaction.py:220-222) */
 } HsEmitArgs;
 /* Frame start: tracking patches adopt last frame's synthesis origin as their
  * region, and take this frame's synthesis origin from their source's new
@@ -355,17 +407,7 @@ typedef struct {
 } HsSmoothArgs;
 HS_API int hs_smooth(const HsSmoothArgs* a, void* stream);
 
-/* One further tile of a summed-cascade background (fft.cascades): periodic,
- * origin 0, its own spacing.  Samplers add its bilinear height and combine
- * normals through slopes, n = normalize(sum_c n_c.xy / n_c.z, 1), n_c the
- * renormalised bilinear of the tile's periodic node normals.               */
-#define HS_MAX_CASCADES 4
-typedef struct {
-    const float* height;      /* [n*n] */
-    int n;                    /* power of two */
-    int pad;
-    double spacing;
-} HsBgTile;
+
 
 /* ------------------------------------------------------------------------ */
 /* Compose: gain-sum of the bilinearly upsampled layers (synthesize,
@@ -414,6 +456,10 @@ typedef struct {
     int clamped_only;           /* 1: sample_clamped of patch 0 only, no weights */
     int n_extra_bg;             /* further background cascades (bg_* is cascade 0) */
     HsBgTile extra_bg[HS_MAX_CASCADES - 1];
+    int from_heights;           /* 1: normals from finite differences of the height grids (periodic
+                                   background, clamped patches), bg_normal / patch_normal unused;
+                                   patches at their synthesis rectangles, bg origin 0 -- the
+                                   sampler hs_bodies uses */
 } HsSampleArgs;
 HS_API int hs_sample(const HsSampleArgs* a, void* stream);
 

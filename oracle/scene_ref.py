@@ -20,7 +20,7 @@ import math
 
 import numpy as np
 
-from . import blend_ref, emit_ref, ocean_ref, particles_ref, spectrum_ref, synth_ref
+from . import blend_ref, body_ref, emit_ref, ocean_ref, particles_ref, spectrum_ref, synth_ref
 
 
 def build_params(sc: dict) -> spectrum_ref.Params:
@@ -88,6 +88,14 @@ class OracleScene:
                                         d.get("wake_count", 0), d.get("energy_scale", 1.0))
                         for d in sc.get("sources", [])]
         self.track = list(sc.get("patch_track") or [-1] * len(self.patches))
+        # floating bodies (interaction.py:79-149; harness.py:102-107,155-167): buoyancy
+        # against the previous frame's blended surface, then emission; patches
+        # with track_body follow them
+        self.bodies = [body_ref.box_body(d["position"], d["size"], d.get("density", 500.0), d.get("yaw", 0.0),
+                                         d.get("max_thrust", 0.0), d.get("max_yaw_torque", 0.0))
+                       for d in sc.get("bodies", [])]
+        self.track_body = list(sc.get("patch_track_body") or [-1] * len(self.patches))
+        self.prev_surface = None          # (background, [(patch, field)]) of the last synthesised frame
 
     def step(self, dt: float | None = None, synth: bool = True, fft: bool = True) -> dict:
         sc = self.sc
@@ -112,8 +120,30 @@ class OracleScene:
                                              t=t, beta=sc["trough_fraction"]))
         for pc, pool, led in zip(self.patches, self.pools, self.ledgers):
             particles_ref.advect(pool, self.bk, dt, pc, led, self.p.g)
-        # interaction stage (harness.py:155-167): kinematic buoyancy step, emission
-        # into the owning patch (booked like injection), then patch retracking
+        # interaction stage (harness.py:155-167): bodies first (buoyancy against the
+        # previous frame's sampler -- flat water before the first synthesis -- then
+        # emit_from_motion into the owning patch), then the kinematic sources
+        for body in self.bodies:
+            prev = self.prev_surface
+
+            def query(pts, prev=prev):
+                pts = np.asarray(pts, dtype=float)
+                if prev is None:
+                    n = np.zeros(pts.shape[:-1] + (3,))
+                    n[..., 2] = 1.0
+                    return np.zeros(pts.shape[:-1]), n
+                return blend_ref.sample(prev[0], prev[1], pts)
+            body_ref.buoyancy_step(body, query, dt, sc["rho"], self.p.g)
+            owner = next((k for k, pc in enumerate(self.patches) if emit_ref.contains(pc, body.position[:2])), None)
+            if owner is None:
+                continue
+            src = emit_ref.Source(body.position[:2].copy(), body.velocity.copy(), body.hull_extent,
+                                  body.submerged_volume - body.prev_submerged_volume, body.mean_submersion)
+            events, emitted = emit_ref.emit(src, self.bk.radius, self.bk.n_theta, sc["rho"], self.p.g,
+                                            sc["trough_fraction"])
+            self.pools[owner].append(emitted)
+            for ev in events:
+                self.ledgers[owner].e_in[ev.bucket] += ev.energy
         for src in self.sources:
             src.position = src.position + src.velocity[:2] * dt
             owner = next((k for k, pc in enumerate(self.patches) if emit_ref.contains(pc, src.position)), None)
@@ -127,6 +157,9 @@ class OracleScene:
         for k, j in enumerate(self.track):
             if 0 <= j < len(self.sources):
                 self.patches[k] = emit_ref.retrack(self.patches[k], self.res[k], self.sources[j])
+        for k, j in enumerate(self.track_body):
+            if 0 <= j < len(self.bodies):
+                self.patches[k] = emit_ref.retrack(self.patches[k], self.res[k], self.bodies[j])
         if synth:
             self.fields = []
             for pc, pool, r, pl in zip(self.patches, self.pools, self.res, self.plans):
@@ -140,6 +173,8 @@ class OracleScene:
                      for pc, r in zip(self.patches, self.res)]
             out["blend_heights"] = [tl[0] for tl in tiles]
             out["blend_normals"] = [tl[1] for tl in tiles]
+            self.prev_surface = (self.background, pairs)
+        out["bodies"] = [(b.position.copy(), b.yaw, b.velocity.copy(), b.submerged_volume) for b in self.bodies]
         out["counts"] = np.stack([pool.counts(self.bk.n) for pool in self.pools]) if self.pools else None
         self.frame += 1
         return out

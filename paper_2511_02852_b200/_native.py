@@ -51,6 +51,13 @@ class HsPool(C.Structure):
     _fields_ = [("x", vp), ("y", vp), ("ux", vp), ("uy", vp), ("amp", vp)]
 
 
+HS_MAX_CASCADES = 4
+
+
+class HsBgTile(C.Structure):
+    _fields_ = [("height", vp), ("n", i32), ("pad", i32), ("spacing", dbl)]
+
+
 class HsFftArgs(C.Structure):
     _fields_ = [("n", i32), ("emit_normals", i32), ("g", dbl), ("t", dbl), ("choppiness", dbl),
                 ("frame_ptr", vp), ("dt", dbl), ("spacing", dbl), ("kf", vp), ("h0", vp),
@@ -88,14 +95,33 @@ class HsAdvectArgs(C.Structure):
 class HsSource(C.Structure):
     _fields_ = [("vx", dbl), ("vy", dbl), ("hull_extent", dbl), ("e_ring", dbl), ("e_wake", dbl),
                 ("amp_ring", dbl), ("amp_wake", dbl), ("n_ring", i32), ("n_wake", i32), ("ring_bucket", i32),
-                ("wake_bucket", i32), ("dir_off", i32), ("pad", i32)]
+                ("wake_bucket", i32), ("dir_off", i32), ("body", i32)]
+
+
+HS_MAX_PROBES = 8
+
+
+class HsBody(C.Structure):
+    _fields_ = [("pos", dbl * 3), ("vel", dbl * 3), ("yaw", dbl), ("yaw_rate", dbl), ("submerged", dbl),
+                ("prev_submerged", dbl), ("mean_submersion", dbl), ("mass", dbl), ("hull_extent", dbl),
+                ("draft", dbl), ("drag_linear", dbl), ("drag_yaw", dbl), ("thrust_force", dbl),
+                ("yaw_torque", dbl), ("displaced", dbl), ("probe_off", (dbl * 3) * HS_MAX_PROBES),
+                ("probe_vol", dbl * HS_MAX_PROBES), ("n_probes", i32), ("pad", i32)]
+
+
+class HsBodyArgs(C.Structure):
+    _fields_ = [("n_bodies", i32), ("bodies", vp), ("dt", dbl), ("rho", dbl), ("g", dbl), ("flat", i32),
+                ("bg_height", vp), ("bg_n", i32), ("bg_spacing", dbl), ("n_extra_bg", i32),
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("n_patches", i32), ("patches", vp),
+                ("patch_height", vp)]
 
 
 class HsEmitArgs(C.Structure):
     _fields_ = [("n_sources", i32), ("n_patches", i32), ("nb", i32), ("sources", vp), ("dirs", vp),
                 ("pos_in", vp), ("pos_out", vp), ("patches", vp), ("buckets", vp), ("dt", dbl), ("beta", dbl),
                 ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp), ("len", vp),
-                ("live", vp), ("e_in", vp), ("raw_layers", vp), ("layers", vp), ("clamped", vp), ("status", vp)]
+                ("live", vp), ("e_in", vp), ("raw_layers", vp), ("layers", vp), ("clamped", vp), ("status", vp),
+                ("bodies", vp), ("n_theta", i32)]
 
 
 class HsLayoutArgs(C.Structure):
@@ -117,13 +143,6 @@ class HsSmoothArgs(C.Structure):
                 ("total_ytiles", i32), ("max_H_wide", i32)]
 
 
-HS_MAX_CASCADES = 4
-
-
-class HsBgTile(C.Structure):
-    _fields_ = [("height", vp), ("n", i32), ("pad", i32), ("spacing", dbl)]
-
-
 class HsComposeArgs(C.Structure):
     _fields_ = [("n_patches", i32), ("nb", i32), ("patches", vp), ("layers", vp),
                 ("smooth_layers", vp), ("tile_info", vp), ("total_tiles", i32),
@@ -139,7 +158,7 @@ class HsSampleArgs(C.Structure):
                 ("bg_spacing", dbl), ("bg_x0", dbl), ("bg_y0", dbl), ("n_patches", i32),
                 ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("out_height", vp),
                 ("out_normal", vp), ("clamped_only", i32), ("n_extra_bg", i32),
-                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("from_heights", i32)]
 
 
 class HsCompositeArgs(C.Structure):
@@ -156,7 +175,7 @@ class HsFinishArgs(C.Structure):
 
 ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
-               HsLayoutArgs, HsSource, HsEmitArgs]
+               HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs]
 
 EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource: 80}
 
@@ -164,7 +183,7 @@ EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource:
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
-           "hs_resident_layout", "hs_track", "hs_emit"]
+           "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies"]
 
 _lib = None
 

@@ -54,6 +54,8 @@ extern "C" HS_API int hs_struct_size(int which) {
         case 14: return (int)sizeof(HsLayoutArgs);
         case 15: return (int)sizeof(HsSource);
         case 16: return (int)sizeof(HsEmitArgs);
+        case 17: return (int)sizeof(HsBody);
+        case 18: return (int)sizeof(HsBodyArgs);
         default: return -1;
     }
 }

@@ -15,7 +15,7 @@
 // decoupled-look-back scan, so buckets stay contiguous and in order.
 #include <stdlib.h>
 
-#include "hs_common.cuh"
+#include "synth_common.cuh"
 
 namespace hs {
 
@@ -1048,8 +1048,51 @@ __global__ void __launch_bounds__(1024) resident_layout_kernel(HsLayoutArgs a) {
 // (interaction.py:140), in fp64 without contraction.
 __device__ __forceinline__ void source_step(const HsEmitArgs& a, int s, double& px, double& py) {
     const HsSource& S = a.sources[s];
+    if (S.body >= 0) {                              // a floating body: hs_bodies moved it
+        px = a.bodies[S.body].pos[0];
+        py = a.bodies[S.body].pos[1];
+        return;
+    }
     px = dadd(a.pos_in[2 * s], dmul(S.vx, a.dt));
     py = dadd(a.pos_in[2 * s + 1], dmul(S.vy, a.dt));
+}
+
+// This frame's emission plan of source s (emit_from_motion, interaction.py:
+// 185-230): kinematic sources carry it precomputed; a body's comes from its
+// state after hs_bodies (energy split by |v_z| : |v_h|, signed amplitudes,
+// the wake fan turned to -v_h).
+struct SrcPlan {
+    double e_ring, e_wake, amp_ring, amp_wake, back;
+    int n_ring, n_wake;
+};
+
+__device__ __forceinline__ SrcPlan source_plan(const HsEmitArgs& a, int s) {
+    const HsSource& S = a.sources[s];
+    SrcPlan q{S.e_ring, S.e_wake, S.amp_ring, S.amp_wake, 0.0, S.n_ring, S.n_wake};
+    if (S.body < 0) return q;
+    const HsBody& B = a.bodies[S.body];
+    const double d_v = dsub(B.submerged, B.prev_submerged);
+    const double budget = dmul(dmul(dmul(dmul(1.0, a.rho), a.g), fabs(d_v)), B.mean_submersion);
+    q.e_ring = q.e_wake = 0.0;
+    if (!(budget > 0.0)) return q;
+    const double v_z = fabs(B.vel[2]), v_h = hypot(B.vel[0], B.vel[1]);
+    const double rw = dadd(v_z, v_h) == 0.0 ? 1.0 : __ddiv_rn(v_z, dadd(v_z, v_h));
+    const double sign = d_v >= 0.0 ? 1.0 : -1.0;
+    const double rgp = dmul(dmul(a.rho, a.g), 3.141592653589793);
+    const double er = dmul(rw, budget);
+    if (er > 0.0) {
+        const double r = a.buckets[S.ring_bucket].radius;
+        q.e_ring = er;
+        q.amp_ring = dmul(sign, sqrt(__ddiv_rn(dmul(8.0, __ddiv_rn(er, (double)S.n_ring)), dmul(rgp, dmul(r, r)))));
+    }
+    const double ew = dmul(dsub(1.0, rw), budget);
+    if (ew > 0.0 && v_h > 0.0) {
+        const double r = a.buckets[S.wake_bucket].radius;
+        q.e_wake = ew;
+        q.amp_wake = dmul(sign, sqrt(__ddiv_rn(dmul(8.0, __ddiv_rn(ew, (double)S.n_wake)), dmul(rgp, dmul(r, r)))));
+        q.back = atan2(-B.vel[1], -B.vel[0]);
+    }
+    return q;
 }
 
 // owning patch: the first whose region contains the point, inclusive
@@ -1082,6 +1125,79 @@ __global__ void track_kernel(HsEmitArgs a) {
     }
 }
 
+// buoyancy_step (interaction.py:105-149) for every body, one warp each: lane
+// p samples the previous frame's blended surface at probe p, lane 0 then
+// integrates in the reference's operation order (fp64, no contraction).
+__global__ void __launch_bounds__(128) bodies_kernel(HsBodyArgs a) {
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (w >= a.n_bodies) return;
+    HsBody& B = a.bodies[w];
+    const int np = B.n_probes;
+    const double c = cos(B.yaw), sn = sin(B.yaw);
+    double wx = 0.0, wy = 0.0, wz = 0.0, hgt = 0.0, nx = 0.0, ny = 0.0, nz = 1.0;
+    if (lane < np) {
+        const double* o = B.probe_off[lane];
+        wx = dsub(dadd(B.pos[0], dmul(c, o[0])), dmul(sn, o[1]));     // interaction.py:72-76
+        wy = dadd(dadd(B.pos[1], dmul(sn, o[0])), dmul(c, o[1]));
+        wz = dadd(B.pos[2], o[2]);
+        if (!a.flat) {
+            float h; float3 n;
+            sample_surface_heights(a.bg_height, a.bg_n, a.bg_spacing, a.n_extra_bg, a.extra_bg, a.n_patches,
+                                   a.patches, a.patch_height, wx, wy, h, n);
+            hgt = (double)h; nx = (double)n.x; ny = (double)n.y; nz = (double)n.z;
+        }
+    }
+    if (lane != 0) {
+        // lane 0 gathers every probe below
+    }
+    double Wx[HS_MAX_PROBES], Wy[HS_MAX_PROBES], D[HS_MAX_PROBES], Nx[HS_MAX_PROBES], Ny[HS_MAX_PROBES], Nz[HS_MAX_PROBES];
+#pragma unroll
+    for (int q = 0; q < HS_MAX_PROBES; ++q) {
+        Wx[q] = __shfl_sync(0xffffffffu, wx, q);
+        Wy[q] = __shfl_sync(0xffffffffu, wy, q);
+        D[q] = __shfl_sync(0xffffffffu, dsub(hgt, wz), q);            // depth = h - z
+        Nx[q] = __shfl_sync(0xffffffffu, nx, q);
+        Ny[q] = __shfl_sync(0xffffffffu, ny, q);
+        Nz[q] = __shfl_sync(0xffffffffu, nz, q);
+    }
+    if (lane != 0) return;
+    double frac[HS_MAX_PROBES];
+    double submerged = 0.0;
+    for (int q = 0; q < np; ++q) {
+        frac[q] = fmin(fmax(__ddiv_rn(D[q], B.draft), 0.0), 1.0);
+        submerged = dadd(submerged, dmul(B.probe_vol[q], frac[q]));
+    }
+    double F[3] = {0.0, 0.0, 0.0}, torque_z = 0.0;
+    const double rg = dmul(a.rho, a.g);
+    for (int q = 0; q < np; ++q) {
+        const double sc = dmul(dmul(rg, B.probe_vol[q]), frac[q]);   // rho g vol frac (:126)
+        const double f0 = dmul(sc, Nx[q]), f1 = dmul(sc, Ny[q]), f2 = dmul(sc, Nz[q]);
+        F[0] = dadd(F[0], f0); F[1] = dadd(F[1], f1); F[2] = dadd(F[2], f2);
+        const double r0 = dsub(Wx[q], B.pos[0]), r1 = dsub(Wy[q], B.pos[1]);
+        torque_z = dadd(torque_z, dsub(dmul(r0, f1), dmul(r1, f0)));
+    }
+    const double wet = B.displaced > 0.0 ? __ddiv_rn(submerged, B.displaced) : 0.0;
+    const double dl = dmul(B.drag_linear, wet);
+    for (int k = 0; k < 3; ++k) F[k] = dsub(F[k], dmul(dl, B.vel[k]));
+    F[0] = dadd(F[0], dmul(B.thrust_force, cos(B.yaw)));
+    F[1] = dadd(F[1], dmul(B.thrust_force, sin(B.yaw)));
+    F[2] = dadd(F[2], dmul(B.thrust_force, 0.0));
+    torque_z = dadd(torque_z, dsub(B.yaw_torque, dmul(dmul(B.drag_yaw, wet), B.yaw_rate)));
+    const double inertia = dmul(dmul(0.5, B.mass), dmul(B.hull_extent, B.hull_extent));
+    const double gz[3] = {0.0, 0.0, -a.g};
+    for (int k = 0; k < 3; ++k) B.vel[k] = dadd(B.vel[k], dmul(dadd(__ddiv_rn(F[k], B.mass), gz[k]), a.dt));
+    for (int k = 0; k < 3; ++k) B.pos[k] = dadd(B.pos[k], dmul(B.vel[k], a.dt));
+    B.yaw_rate = dadd(B.yaw_rate, dmul(__ddiv_rn(torque_z, inertia), a.dt));
+    B.yaw = dadd(B.yaw, dmul(B.yaw_rate, a.dt));
+    B.prev_submerged = B.submerged;
+    B.submerged = submerged;
+    double ws = 0.0;
+    int nw = 0;
+    for (int q = 0; q < np; ++q)
+        if (D[q] > 0.0) { ws = dadd(ws, fmin(D[q], B.draft)); ++nw; }
+    B.mean_submersion = nw ? __ddiv_rn(ws, (double)nw) : 0.0;
+}
+
 // One CTA per source: find its owner and where its fans go (after the
 // fans of earlier sources with the same owner and bucket, ring before wake,
 // interaction.py:218-230), then write crests and troughs
@@ -1108,24 +1224,26 @@ __global__ void __launch_bounds__(256) emit_kernel(HsEmitArgs a) {
         source_step(a, q, qx, qy);
         if (owner_of(a, qx, qy) != own) continue;
         const HsSource& Q = a.sources[q];
-        if (Q.e_ring > 0.0) atomicAdd(&before[Q.ring_bucket], m * Q.n_ring);
-        if (Q.e_wake > 0.0) atomicAdd(&before[Q.wake_bucket], m * Q.n_wake);
+        const SrcPlan qp = source_plan(a, q);
+        if (qp.e_ring > 0.0) atomicAdd(&before[Q.ring_bucket], m * qp.n_ring);
+        if (qp.e_wake > 0.0) atomicAdd(&before[Q.wake_bucket], m * qp.n_wake);
     }
     __syncthreads();
     const HsSource S = a.sources[s];
+    const SrcPlan pl = source_plan(a, s);
     const HsPatch& P = a.patches[own];
     const double px = px_s, py = py_s;
     int clamp_local = 0;
 #pragma unroll 1
     for (int branch = 0; branch < 2; ++branch) {
         const bool ring = branch == 0;
-        if ((ring ? S.e_ring : S.e_wake) <= 0.0) continue;
+        if ((ring ? pl.e_ring : pl.e_wake) <= 0.0) continue;
         const int b = ring ? S.ring_bucket : S.wake_bucket;
-        const int n = ring ? S.n_ring : S.n_wake;
-        const double amp = ring ? S.amp_ring : S.amp_wake;
+        const int n = ring ? pl.n_ring : pl.n_wake;
+        const double amp = ring ? pl.amp_ring : pl.amp_wake;
         const int seg = own * nb + b;
         int off = before[b];
-        if (!ring && S.e_ring > 0.0 && S.ring_bucket == b) off += m * S.n_ring;
+        if (!ring && pl.e_ring > 0.0 && S.ring_bucket == b) off += m * pl.n_ring;
         const long long base = (long long)a.seg_base[seg] + a.len[seg] + off;
         if (a.len[seg] + off + m * n > a.seg_cap[seg]) {
             if (threadIdx.x == 0) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
@@ -1137,8 +1255,17 @@ __global__ void __launch_bounds__(256) emit_kernel(HsEmitArgs a) {
                             L.raw_pitch, L.pad};
         const double* dirs = a.dirs + 2 * (S.dir_off + (ring ? 0 : S.n_ring));
         const float ca = (float)amp, ta = (float)dmul(-a.beta, amp);
+        const bool turn = !ring && S.body >= 0;         // a body's wake: back + linspace offset
         for (int k = threadIdx.x; k < n; k += blockDim.x) {
-            const double ux = dirs[2 * k], uy = dirs[2 * k + 1];
+            double ux, uy;
+            if (turn) {
+                const double ang = dadd(pl.back, dirs[2 * k]);
+                ux = cos(ang);
+                uy = sin(ang);
+            } else {
+                ux = dirs[2 * k];
+                uy = dirs[2 * k + 1];
+            }
             const double cx = dadd(px, dmul(S.hull_extent, ux));      // center + hull * dirs
             const double cy = dadd(py, dmul(S.hull_extent, uy));
             long long o = base + k;
@@ -1170,11 +1297,12 @@ __global__ void emit_commit_kernel(HsEmitArgs a) {
         const int own = owner_of(a, px, py);
         if (own < 0) continue;
         const HsSource& S = a.sources[s];
+        const SrcPlan pl = source_plan(a, s);
         for (int branch = 0; branch < 2; ++branch) {
-            const double e = branch == 0 ? S.e_ring : S.e_wake;
+            const double e = branch == 0 ? pl.e_ring : pl.e_wake;
             if (e <= 0.0) continue;
             const int seg = own * a.nb + (branch == 0 ? S.ring_bucket : S.wake_bucket);
-            const int cnt = m * (branch == 0 ? S.n_ring : S.n_wake);
+            const int cnt = m * (branch == 0 ? pl.n_ring : pl.n_wake);
             if (a.len[seg] + cnt > a.seg_cap[seg]) continue;          // overflow flagged by emit_kernel
             a.len[seg] += cnt;
             a.live[seg] += cnt;
@@ -1342,6 +1470,17 @@ extern "C" int hs_emit(const HsEmitArgs* a, void* stream) {
     emit_kernel<<<a->n_sources, 256, 0, st>>>(*a);
     HS_LAUNCH_CHECK();
     emit_commit_kernel<<<1, 32, 0, st>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_bodies(const HsBodyArgs* a, void* stream) {
+    HS_CHECK_ARG(a != nullptr, "hs_bodies: null args");
+    if (a->n_bodies == 0) return 0;
+    HS_CHECK_ARG(a->bodies && a->dt > 0.0, "hs_bodies: missing bodies or dt <= 0");
+    HS_CHECK_ARG(a->n_extra_bg >= 0 && a->n_extra_bg < HS_MAX_CASCADES, "hs_bodies: n_extra_bg out of range");
+    HS_CHECK_ARG(a->flat || a->n_patches == 0 || (a->patches && a->patch_height), "hs_bodies: missing patch surfaces");
+    bodies_kernel<<<(a->n_bodies + 3) / 4, 128, 0, as_stream(stream)>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

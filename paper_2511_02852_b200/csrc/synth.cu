@@ -258,7 +258,10 @@ __global__ void sample_kernel(HsSampleArgs a) {
     if (k >= a.n_points) return;
     BgView bg{a.bg_height, a.bg_normal, a.bg_n, a.bg_spacing, a.bg_x0, a.bg_y0};
     float h; float3 nv;
-    if (a.clamped_only) {
+    if (a.from_heights) {
+        sample_surface_heights(a.bg_height, a.bg_n, a.bg_spacing, a.n_extra_bg, a.extra_bg, a.n_patches, a.patches,
+                               a.patch_height, a.points[2 * k], a.points[2 * k + 1], h, nv);
+    } else if (a.clamped_only) {
         sample_clamped_at(synth_view(a.patches[0]), a.patch_height, a.patch_normal, a.points[2 * k], a.points[2 * k + 1], h, nv);
     } else {
         sample_surface(bg, a.n_extra_bg, a.extra_bg, a.n_patches, a.patches, a.patch_height, a.patch_normal,

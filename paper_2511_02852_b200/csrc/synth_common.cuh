@@ -104,6 +104,70 @@ __device__ __forceinline__ void add_cascades(int n_extra, const HsBgTile* extra,
     nx = sx * r; ny = sy * r; nz = r;
 }
 
+// SurfaceSampler._raw (coupling.py:120-141, normal_mode "blend") from height
+// grids only, as the frame leaves them: the periodic background (cascade 0
+// at origin 0, + further cascades) with central-difference node normals, then
+// every patch (synthesis rectangle) by clamped bilinear heights and
+// clamped-border finite-difference node normals (finish_field, :323-340)
+// under its smoothstep weight.
+__device__ __forceinline__ float3 patch_node_normal(const float* __restrict__ H, int nx, int ny, int i, int j, float s) {
+    float hx, hy;
+    if (i == 0) hx = (H[(long long)ny + j] - H[j]) / s;
+    else if (i == nx - 1) hx = (H[(long long)i * ny + j] - H[(long long)(i - 1) * ny + j]) / s;
+    else hx = (H[(long long)(i + 1) * ny + j] - H[(long long)(i - 1) * ny + j]) / (2.f * s);
+    const long long r = (long long)i * ny;
+    if (j == 0) hy = (H[r + 1] - H[r]) / s;
+    else if (j == ny - 1) hy = (H[r + j] - H[r + j - 1]) / s;
+    else hy = (H[r + j + 1] - H[r + j - 1]) / (2.f * s);
+    const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
+    return make_float3(-hx * rn, -hy * rn, rn);
+}
+
+__device__ __forceinline__ void sample_surface_heights(const float* bg_h, int bg_n, double bg_sp, int n_extra,
+                                                       const HsBgTile* extra, int n_patches,
+                                                       const HsPatch* __restrict__ patches,
+                                                       const float* __restrict__ patch_h, double x, double y,
+                                                       float& h, float3& nv) {
+    h = 0.f;
+    nv = make_float3(0.f, 0.f, 1.f);
+    if (bg_h) {
+        const HsBgTile T0{bg_h, bg_n, 0, bg_sp};
+        float sx, sy;
+        sample_tile(T0, x, y, h, sx, sy);            // renormalised bilinear normal as a slope
+        float nx = sx, ny = sy, nz = 1.f;            // the normal's direction
+        add_cascades(n_extra, extra, x, y, h, nx, ny, nz);
+        const float r = rsqrtf(nx * nx + ny * ny + nz * nz);
+        nv = make_float3(nx * r, ny * r, nz * r);
+    }
+    for (int p = 0; p < n_patches; ++p) {
+        const HsPatch P = synth_view(patches[p]);
+        double d = fmin(fmin(x - P.x0, P.x1 - x), fmin(y - P.y0, P.y1 - y));
+        if (!(d > 0.0)) continue;
+        double t = fmin(fmax(d / P.margin, 0.0), 1.0);
+        const float w = (float)(t * t * (3.0 - 2.0 * t));
+        const double u = fmin(fmax((x - P.x0) / P.texel, 0.0), (double)(P.res - 1));
+        const double v = fmin(fmax((y - P.y0) / P.texel, 0.0), (double)(P.ny - 1));
+        const int i = min((int)u, P.res - 2), j = min((int)v, P.ny - 2);
+        const float fu = (float)(u - i), fv = (float)(v - j);
+        const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
+        const float* H = patch_h + P.grid_base;
+        const long long a00 = (long long)i * P.ny + j;
+        const float hp = H[a00] * w00 + H[a00 + P.ny] * w10 + H[a00 + 1] * w01 + H[a00 + P.ny + 1] * w11;
+        const float s = (float)P.texel;
+        const float3 n00 = patch_node_normal(H, P.res, P.ny, i, j, s), n10 = patch_node_normal(H, P.res, P.ny, i + 1, j, s);
+        const float3 n01 = patch_node_normal(H, P.res, P.ny, i, j + 1, s), n11 = patch_node_normal(H, P.res, P.ny, i + 1, j + 1, s);
+        float qx = n00.x * w00 + n10.x * w10 + n01.x * w01 + n11.x * w11;
+        float qy = n00.y * w00 + n10.y * w10 + n01.y * w01 + n11.y * w11;
+        float qz = n00.z * w00 + n10.z * w10 + n01.z * w01 + n11.z * w11;
+        const float rq = rsqrtf(qx * qx + qy * qy + qz * qz);
+        qx *= rq; qy *= rq; qz *= rq;
+        h = w * hp + (1.f - w) * h;
+        const float mx = w * qx + (1.f - w) * nv.x, my = w * qy + (1.f - w) * nv.y, mz = w * qz + (1.f - w) * nv.z;
+        const float rm = rsqrtf(mx * mx + my * my + mz * mz);
+        nv = make_float3(mx * rm, my * rm, mz * rm);
+    }
+}
+
 // smoothstep weight from inward boundary depth (coupling.py:27-40)
 __device__ __forceinline__ double blend_w(const HsPatch& P, double x, double y) {
     double d = fmin(fmin(x - P.x0, P.x1 - x), fmin(y - P.y0, P.y1 - y));

@@ -40,7 +40,7 @@ from .errors import CapacityError, ConfigError
 from .fft_background import FftWorkspace, HeightField, fft_args, init_fft
 from .particles import PatchRegion, PhiloxStream, ParticleSet
 from .patch_synthesis import SynthWorkspace, plan_layers
-from .interaction import source_structs
+from .interaction import body_structs, source_structs
 from .spectrum import DirectionalSpectrum, build_buckets, derive_params, log_buckets
 
 STAGES = ("fft", "inject", "advect", "interact", "synth", "blend", "output")
@@ -96,6 +96,10 @@ class FrameStats:
             fv = float(s["fsum"][0]) / float(self._fft_n * self._fft_n) if self._fft_n else 0.0
             self._cache.update(particle_counts=counts.astype(np.int64), injected_energy=e_in,
                                despawned_energy=e_out, patch_variance=pv, fft_band_variance=fv)
+            if "bodies" in s:
+                raw, sz = s["bodies"].tobytes(), C.sizeof(N.HsBody)
+                self.body_states = [(b.pos[0], b.pos[1], b.pos[2], b.yaw) for b in
+                                    (N.HsBody.from_buffer_copy(raw[k * sz:(k + 1) * sz]) for k in range(len(raw) // sz))]
         return self._cache
 
     @property
@@ -129,8 +133,6 @@ class Simulation:
     def __init__(self, config: SimConfig, device=None, *, pool_capacity: int | None = None,
                  rng_seed_keys: list | None = None, compact_period: int | None = None):
         cfg = config.validate()
-        if cfg.bodies:
-            raise ConfigError("floating bodies are outside the B200 hybrid-step path (SURVEY 8(f))")
         self.config = cfg
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
@@ -178,20 +180,37 @@ class Simulation:
         per_member = 2 if cfg.trough_fraction != 0.0 else 1
         max_new = []                     # per patch, per bucket: particles one frame can append
         explicit = pool_capacity is not None or bool(cfg.pool_capacity)
-        # kinematic emitting sources (interaction.py)
+        # emitting bodies (interaction.py): floating bodies first
+        # (the reference's order), then kinematic sources; patch track indices
+        # point into that combined list
+        self.bodies = tuple(cfg.bodies) if self.n_patches else ()
+        self.n_bodies = len(self.bodies)
         self.sources = tuple(cfg.sources) if self.n_patches else ()
-        self.n_sources = len(self.sources)
+        body_st, body_dirs, self._body_init = body_structs(self.bodies, self.table, 0)
+        src_structs, src_dirs, src_plans = source_structs(self.sources, self.table, cfg.rho, cfg.g,
+                                                          offset=len(body_dirs))
+        self.n_sources = self.n_bodies + len(self.sources)
         if self.n_sources > N.HS_MAX_SOURCES:
-            raise ConfigError(f"at most {N.HS_MAX_SOURCES} sources per device")
-        src_structs, src_dirs, src_plans = source_structs(self.sources, self.table, cfg.rho, cfg.g)
-        self._tracking = any(pc.track_source >= 0 for pc in pcs)
+            raise ConfigError(f"at most {N.HS_MAX_SOURCES} sources and bodies per device")
+        src_structs = body_st + src_structs
+        src_dirs = np.concatenate([body_dirs.reshape(-1, 2), src_dirs.reshape(-1, 2)])
+        self._track_idx = [pc.track_body if pc.track_body >= 0 else
+                           (self.n_bodies + pc.track_source if pc.track_source >= 0 else -1) for pc in pcs]
+        self._tracking = any(t >= 0 for t in self._track_idx)
         emit_new = np.zeros((self.n_patches, self.nb), np.int64)     # per frame
         emit_pop = np.zeros(self.n_patches)
-        tracker = {pc.track_source: k for k, pc in enumerate(pcs) if pc.track_source >= 0}
-        for j, (src, pl) in enumerate(zip(self.sources, src_plans)):
+        tracker = {t: k for k, t in enumerate(self._track_idx) if t >= 0}
+        plans = []
+        for j, b in enumerate(self.bodies):       # a body may fire both fans every frame
+            st_ = body_st[j]
+            plans.append(({"e_ring": 1.0, "ring_dirs": np.zeros((st_.n_ring, 2)), "ring_bucket": st_.ring_bucket,
+                           "e_wake": 1.0, "wake_dirs": np.zeros((st_.n_wake, 2)), "wake_bucket": st_.wake_bucket},
+                          0.0))
+        plans += [(pl, float(np.hypot(*src.velocity[:2]))) for src, pl in zip(self.sources, src_plans)]
+        for j, (pl, speed) in enumerate(plans):
             # a tracked source only ever emits into its patch; others may enter any patch
             cand = [tracker[j]] if j in tracker else range(self.n_patches)
-            vt = float(np.hypot(*src.velocity[:2])) if j in tracker else 0.0
+            vt = speed if j in tracker else 0.0
             for key_e, key_d, key_b in (("e_ring", "ring_dirs", "ring_bucket"), ("e_wake", "wake_dirs", "wake_bucket")):
                 if pl[key_e] <= 0.0:
                     continue
@@ -201,8 +220,8 @@ class Simulation:
                     emit_new[k, b] += n
                     side = 0.5 * (self.regions[k].l1 + self.regions[k].l2)
                     stay = (side + 2.0 * bk.radius) / (bk.speed + vt) / cfg.dt
-                    if j not in tracker and np.hypot(*src.velocity[:2]) > 0:
-                        stay = min(stay, 2.0 * side / float(np.hypot(*src.velocity[:2])) / cfg.dt)
+                    if j not in tracker and speed > 0:
+                        stay = min(stay, 2.0 * side / speed / cfg.dt)
                     emit_pop[k] += n * stay
         for k, r in enumerate(self.regions):
             hr_max = half_rates(r, self.table.omegas, 0.1, cfg.g)       # dt <= 0.1 (config.py validate)
@@ -240,15 +259,16 @@ class Simulation:
                 structs.append(patch_struct(r, res, pool_base=self.pool_base[k], pool_capacity=self.pool_caps[k],
                                             stage_base=self.stage_base[k], stage_capacity=self.stage_caps[k],
                                             grid_base=self.synth.grid_base[k], layer_base=k * self.nb,
-                                            track=pcs[k].track_source))
+                                            track=self._track_idx[k]))
             self.patches_dev = structs_to_device(structs, dev)
             if self.n_sources:
                 self.sources_dev = structs_to_device(src_structs, dev)
                 self.src_dirs = torch.from_numpy(src_dirs.reshape(-1).copy()).to(dev) if src_dirs.size else \
                     torch.zeros(2, dtype=torch.float64, device=dev)
-                p0 = torch.tensor(np.array([c.position for c in self.sources], dtype=np.float64).reshape(-1),
-                                  device=dev)
+                pos = [(b.position[0], b.position[1]) for b in self.bodies] + [tuple(c.position) for c in self.sources]
+                p0 = torch.tensor(np.array(pos, dtype=np.float64).reshape(-1), device=dev)
                 self.src_pos = [p0, p0.clone()]
+                self.bodies_dev = structs_to_device(self._body_init, dev) if self.n_bodies else None
             f64 = lambda n: torch.zeros(max(1, n), dtype=torch.float64, device=dev)  # noqa: E731
             f32 = lambda n: torch.zeros(max(1, n), dtype=torch.float32, device=dev)  # noqa: E731
             self.pools = [[f64(total_pool), f64(total_pool), f64(total_pool), f64(total_pool), f32(total_pool)]
@@ -374,7 +394,23 @@ class Simulation:
             beta=float(cfg.trough_fraction), rho=float(cfg.rho), g=float(cfg.g), pool=self._pool(buf),
             seg_base=N.ptr(self.seg_base), seg_cap=N.ptr(self.seg_cap), len=N.ptr(self.seg_len[lp ^ 1]),
             live=N.ptr(self.live), e_in=N.ptr(self.e_in), raw_layers=N.ptr(self.synth.raw),
-            layers=N.ptr(self.synth.layers), clamped=N.ptr(stats[3]), status=N.ptr(self.status))
+            layers=N.ptr(self.synth.layers), clamped=N.ptr(stats[3]), status=N.ptr(self.status),
+            bodies=N.ptr(self.bodies_dev), n_theta=self.table.n_theta)
+
+    def _bodies_args(self, dt: float) -> N.HsBodyArgs:
+        cfg = self.config
+        bg = self.fft_ws
+        a = N.HsBodyArgs(n_bodies=self.n_bodies, bodies=N.ptr(self.bodies_dev), dt=float(dt), rho=float(cfg.rho),
+                         g=float(cfg.g), flat=1 if self.frame == 0 else 0,
+                         bg_height=N.ptr(bg.height) if bg is not None else 0,
+                         bg_n=cfg.fft_n if bg is not None else 0,
+                         bg_spacing=self.fft_state.spacing if bg is not None else 1.0,
+                         n_patches=self.n_patches, patches=N.ptr(self.patches_dev), patch_height=N.ptr(self.patch_h))
+        ex = self._extra_bg()
+        if ex:
+            a.n_extra_bg = ex["n_extra_bg"]
+            a.extra_bg = ex["extra_bg"]
+        return a
 
     def _resident_args(self, buf: int, lp: int, dt: float, stats) -> N.HsResidentArgs:
         return N.HsResidentArgs(
@@ -404,6 +440,10 @@ class Simulation:
         buf, lp, compact = state
         mark = mark or (lambda _name: None)
         main = torch.cuda.current_stream(self.device)
+        if self.n_patches and self.n_bodies:
+            # buoyancy against the previous frame's surface, before this frame's
+            # transform and compose overwrite it (harness.py:155-157)
+            N.call("hs_bodies", self._bodies_args(dt), stream_ptr())
         fork = self.fft_state is not None and self.n_patches > 0
         if self.fft_state is not None:
             side = self._side_stream("fft") if fork else main
@@ -653,6 +693,8 @@ class Simulation:
         if self.n_patches:
             snap.update(counts=self.live.clone(), e_in=self.e_in.clone(), e_out=self.e_out.clone(),
                         isum=self.isum.clone(), icount=self.icount.clone())
+            if self.n_bodies:
+                snap["bodies"] = self.bodies_dev.clone()
         return FrameStats(frame=self.frame, t=self.t, stage_ms={s: 0.0 for s in STAGES}, _snap=snap, _nb=self.nb,
                           _n_patches=self.n_patches, _fft_n=self.config.fft_n if self.fft_ws is not None else 0)
 
@@ -746,6 +788,29 @@ class Simulation:
         surfaces = [PatchSurface(r, self.patch_field(k)) for k, r in enumerate(self.current_regions())]
         return SurfaceSampler(self.background, surfaces, self.config.normal_mode,
                               cascades=self.cascade_fields()[1:])
+
+    def surface_from_heights(self, points) -> tuple:
+        """(heights, normals) of the last frame's blended surface at world
+        points, normals from finite differences of the height grids -- the
+        sampler the bodies step against (hs_sample, from_heights)."""
+        cfg = self.config
+        pts = torch.as_tensor(np.asarray(points, dtype=np.float64).reshape(-1, 2), device=self.device).contiguous()
+        n = pts.shape[0]
+        out_h = torch.empty(n, dtype=torch.float32, device=self.device)
+        out_n = torch.empty((n, 3), dtype=torch.float32, device=self.device)
+        bg = self.fft_ws
+        a = N.HsSampleArgs(n_points=n, points=N.ptr(pts), bg_height=N.ptr(bg.height) if bg is not None else 0,
+                           bg_normal=0, bg_n=cfg.fft_n if bg is not None else 0,
+                           bg_spacing=self.fft_state.spacing if bg is not None else 1.0, bg_x0=0.0, bg_y0=0.0,
+                           n_patches=self.n_patches, patches=N.ptr(self.patches_dev) if self.n_patches else 0,
+                           patch_height=N.ptr(self.patch_h) if self.n_patches else 0, patch_normal=0,
+                           out_height=N.ptr(out_h), out_normal=N.ptr(out_n), clamped_only=0, from_heights=1)
+        ex = self._extra_bg()
+        if ex:
+            a.n_extra_bg = ex["n_extra_bg"]
+            a.extra_bg = ex["extra_bg"]
+        N.call("hs_sample", a, stream_ptr())
+        return out_h, out_n
 
     def stitched_heights(self) -> torch.Tensor:
         """FFT-resolution composite with patch boxes resampled (harness.py:219-241)."""

@@ -74,16 +74,70 @@ def source_plan(src, table, rho: float, g: float) -> dict:
     return plan
 
 
-def source_structs(sources, table, rho: float, g: float) -> tuple[list, np.ndarray, list]:
+def box_body(cfg) -> N.HsBody:
+    """HsBody of a BodyConfig: box_body's mass, four bottom probes, hull extent
+    and drags (interaction.py:79-102), at rest."""
+    sx, sy, sz = cfg.size
+    volume = sx * sy * sz
+    mass = cfg.density * volume
+    extent = 0.5 * math.hypot(sx, sy)
+    b = N.HsBody()
+    for k in range(3):
+        b.pos[k] = float(cfg.position[k])
+        b.vel[k] = 0.0
+    b.yaw, b.yaw_rate = float(cfg.yaw), 0.0
+    b.submerged = b.prev_submerged = b.mean_submersion = 0.0
+    b.mass, b.hull_extent, b.draft = mass, extent, float(sz)
+    b.drag_linear, b.drag_yaw = 2.0 * mass, 0.2 * mass * extent ** 2
+    b.thrust_force = 0.0 * cfg.max_thrust          # thrust / rudder commands start at 0 (interaction.py:50-51)
+    b.yaw_torque = 0.0 * cfg.max_yaw_torque
+    half = (sx / 2.0, sy / 2.0)
+    q = 0
+    vols = []
+    for dx in (-1.0, 1.0):
+        for dy in (-1.0, 1.0):
+            b.probe_off[q][0], b.probe_off[q][1], b.probe_off[q][2] = dx * half[0], dy * half[1], -sz / 2.0
+            b.probe_vol[q] = volume / 4.0
+            vols.append(volume / 4.0)
+            q += 1
+    b.displaced = sum(vols)                          # FloatingBody.displaced_volume (:66-67)
+    b.n_probes = 4
+    return b
+
+
+def body_structs(bodies, table, offset: int) -> tuple[list, np.ndarray, list]:
+    """HsSource records of floating bodies (body >= 0): ring fan directions
+    fan(0, pi (1 - 1/n_theta), n_theta) and the wake fan's angle offsets
+    linspace(-K, K, max(n_theta // 2, 3)) (interaction.py:218-230); bucket by
+    nearest radius to the hull extent (ring) and half of it (wake)."""
+    structs, dirs, hb = [], [], []
+    n_th = table.n_theta
+    for j, cfg in enumerate(bodies):
+        b = box_body(cfg)
+        ring = _fan(0.0, math.pi * (1.0 - 1.0 / n_th), n_th)
+        n_w = max(n_th // 2, 3)
+        lin = np.linspace(-KELVIN_HALF_ANGLE, KELVIN_HALF_ANGLE, n_w) if n_w > 1 else np.zeros(1)
+        wake = np.stack([lin, np.zeros_like(lin)], axis=1)
+        structs.append(N.HsSource(0.0, 0.0, b.hull_extent, 0.0, 0.0, 0.0, 0.0, n_th, n_w,
+                                  nearest_bucket(table, b.hull_extent), nearest_bucket(table, b.hull_extent / 2.0),
+                                  offset, j))
+        dirs += [ring, wake]
+        offset += n_th + n_w
+        hb.append(b)
+    d = np.concatenate(dirs) if dirs else np.zeros((0, 2))
+    return structs, d, hb
+
+
+def source_structs(sources, table, rho: float, g: float, offset: int = 0) -> tuple[list, np.ndarray, list]:
     """(HsSource records, concatenated fan directions [n, 2] f64, plans)."""
     structs, dirs, plans = [], [], []
-    off = 0
+    off = offset
     for src in sources:
         pl = source_plan(src, table, rho, g)
         nr, nw = len(pl["ring_dirs"]), len(pl["wake_dirs"])
         structs.append(N.HsSource(float(src.velocity[0]), float(src.velocity[1]), float(src.hull_extent),
                                   float(pl["e_ring"]), float(pl["e_wake"]), float(pl["amp_ring"]),
-                                  float(pl["amp_wake"]), nr, nw, pl["ring_bucket"], pl["wake_bucket"], off, 0))
+                                  float(pl["amp_wake"]), nr, nw, pl["ring_bucket"], pl["wake_bucket"], off, -1))
         dirs += [pl["ring_dirs"], pl["wake_dirs"]]
         off += nr + nw
         plans.append(pl)
@@ -91,4 +145,5 @@ def source_structs(sources, table, rho: float, g: float) -> tuple[list, np.ndarr
     return structs, np.ascontiguousarray(d, dtype=np.float64), plans
 
 
-__all__ = ["KELVIN_HALF_ANGLE", "nearest_bucket", "_fan", "source_plan", "source_structs"]
+__all__ = ["KELVIN_HALF_ANGLE", "nearest_bucket", "_fan", "source_plan", "source_structs", "box_body",
+           "body_structs"]

@@ -304,6 +304,38 @@ def gen_emit() -> None:
     save("emit_sim.npz", **sout)
 
 
+def gen_bodies() -> None:
+    """A reference Simulation with two floating bodies (buoyancy against the
+    previous frame's blended surface, interaction.py:105-149, and emission,
+    :175-231) and a patch tracking body 0 (harness.py:115-123)."""
+    cfg = SimConfig(u10=8.0, fetch=5e4, fft_n=64, fft_domain=400.0, dt=0.05, frames=16, n_omega=8, n_theta=8,
+                    seed=31, patches=(PatchConfig(origin=(150.0, 150.0), size=(80.0, 80.0), res=81, margin=8.0,
+                                                  track_body=0),),
+                    bodies=(BodyConfig(position=(190.0, 188.0, 0.4), size=(4.0, 2.0, 1.0), density=450.0,
+                                       yaw=0.3),
+                            BodyConfig(position=(175.0, 200.0, -0.2), size=(2.0, 2.0, 1.0), density=600.0)),
+                    write_frames=False)
+    sim = Simulation(cfg)
+    sim.rng = np.random.Generator(np.random.Philox(key=[cfg.seed, 0]))
+    stats, origins, bstate = [], [], []
+    for _ in range(cfg.frames):
+        stats.append(sim.step())
+        origins.append(sim.patches[0].region.min_corner.copy())
+        bstate.append([np.concatenate([b.position, [b.yaw], b.velocity, [b.yaw_rate, b.submerged_volume,
+                                                                       b.prev_submerged_volume, b.mean_submersion]])
+                       for b in sim.bodies])
+    out = {
+        "counts": np.array([s.particle_counts for s in stats]),
+        "e_in": np.array([s.injected_energy for s in stats]),
+        "e_out": np.array([s.despawned_energy for s in stats]),
+        "origins": np.array(origins),
+        "bodies": np.array(bstate),
+        "patch_h": sim.patches[0].surface.field.height,
+    }
+    out.update(pool_arrays(sim.patches[0].pool, "pool"))
+    save("bodies_sim.npz", **out)
+
+
 def main() -> int:
     print("reference hybridsea", hybridsea.__version__, "numpy", np.__version__)
     gen_spectrum()
@@ -312,6 +344,7 @@ def main() -> int:
     gen_synth(ctx)
     gen_sim()
     gen_emit()
+    gen_bodies()
     return 0
 
 
