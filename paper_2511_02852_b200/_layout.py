@@ -15,7 +15,8 @@ import torch
 from . import _native as N
 from .errors import ConfigError
 
-TILE = 32          # smooth tile edge (csrc/synth.cu)
+TILE = 32          # smooth wide-kernel tile edge (csrc/synth.cu SM_TILE)
+TILE_X, TILE_Y = 32, 64   # fused smooth tile (csrc/synth.cu SM_TX, SM_TY)
 COMPOSE_TILE = 30  # compose output tile edge (csrc/compose.cu: 32 x 32 haloed heights)
 
 
@@ -111,11 +112,11 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
                 max_hw = max(max_hw, k.half_width)
             else:
                 max_h = max(max_h, k.half_width)
-            prefix.append(prefix[-1] + (0 if wide else _tiles(ncx, ncy)))
+            prefix.append(prefix[-1] + (0 if wide else (-(-ncx // TILE_X)) * (-(-ncy // TILE_Y))))
             xpre.append(xpre[-1] + (_tiles(ncx, wy) if wide else 0))
             ypre.append(ypre[-1] + (_tiles(ncx, ncy) if wide else 0))
-    info = [(l, tx * TILE, ty * TILE) for l, L in enumerate(layers) if L.mid_off < 0
-            for tx in range(-(-L.ncx // TILE)) for ty in range(-(-L.ncy // TILE))]
+    info = [(l, tx * TILE_X, ty * TILE_Y) for l, L in enumerate(layers) if L.mid_off < 0
+            for tx in range(-(-L.ncx // TILE_X)) for ty in range(-(-L.ncy // TILE_Y))]
     # largest kernels first: the long-tap tiles start earliest
     info.sort(key=lambda t: -layers[t[0]].H)
     return LayerPack(layers, np.concatenate(taps) if taps else np.zeros(0, np.float32), raw_off, sm_off,

@@ -17,7 +17,10 @@
 namespace hs {
 
 // =============================================================== smooth ==
-constexpr int SM_TILE = 32;
+constexpr int SM_TILE = 32;             // wide-kernel tiles
+constexpr int SM_TX = 32;               // fused tile: rows (x, axis 0)
+constexpr int SM_TY = 64;               // fused tile: columns (y, axis 1) -- wider tiles: less halo
+                                        // recomputed in the x pass, less staging per output
 
 constexpr int SM_RB = 8;                 // outputs per thread along the convolution axis
 
@@ -28,13 +31,13 @@ template <int H>
 __device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ in, int IS, float* __restrict__ mid,
                                                      const float* __restrict__ taps_sm, int W, int MS,
                                                      float* __restrict__ out, long long out_base, int ncy,
-                                                     int rows_valid, int cols_valid) {
+                                                     int rows_valid, int cols_valid, float* __restrict__ ot) {
     constexpr int K = 2 * H + 1;
     float t[K];
 #pragma unroll
     for (int m = 0; m < K; ++m) t[m] = taps_sm[m];
     // x pass (axis 0): mid[r][c] = sum_m t[m] in[r + m][c]
-    for (int item = threadIdx.x; item < W * (SM_TILE / SM_RB); item += blockDim.x) {
+    for (int item = threadIdx.x; item < W * (SM_TX / SM_RB); item += blockDim.x) {
         const int c = item % W, rb = item / W;
         float acc[SM_RB];
 #pragma unroll
@@ -54,8 +57,8 @@ __device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ i
     }
     __syncthreads();
     // y pass (axis 1): thread item = (row r, block of 8 output columns)
-    for (int item = threadIdx.x; item < SM_TILE * (SM_TILE / SM_RB); item += blockDim.x) {
-        const int r = item % SM_TILE, cb = item / SM_TILE;
+    for (int item = threadIdx.x; item < SM_TX * (SM_TY / SM_RB); item += blockDim.x) {
+        const int r = item % SM_TX, cb = item / SM_TX;
         float acc[SM_RB];
 #pragma unroll
         for (int k = 0; k < SM_RB; ++k) acc[k] = 0.f;
@@ -69,11 +72,15 @@ __device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ i
                 if (m >= 0 && m < K) acc[k] = fmaf(t[m], v, acc[k]);
             }
         }
-        if (r < rows_valid) {
+        // through shared memory (row stride SM_TY + 1: conflict-free) so the
+        // global stores below are whole coalesced row segments
 #pragma unroll
-            for (int k = 0; k < SM_RB; ++k)
-                if (cb * SM_RB + k < cols_valid) out[out_base + (long long)r * ncy + cb * SM_RB + k] = acc[k];
-        }
+        for (int k = 0; k < SM_RB; ++k) ot[r * (SM_TY + 1) + cb * SM_RB + k] = acc[k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < SM_TX * SM_TY; e += blockDim.x) {
+        const int r = e / SM_TY, c = e - r * SM_TY;
+        if (r < rows_valid && c < cols_valid) out[out_base + (long long)r * ncy + c] = ot[r * (SM_TY + 1) + c];
     }
 }
 
@@ -82,7 +89,7 @@ __device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in
                                                     float* __restrict__ out, long long out_base, int ncy,
                                                     int rows_valid, int cols_valid) {
     const int K = 2 * H + 1;
-    for (int e = threadIdx.x; e < SM_TILE * W; e += blockDim.x) {
+    for (int e = threadIdx.x; e < SM_TX * W; e += blockDim.x) {
         const int r = e / W, c = e - r * W;
         const float* col = in + r * IS + c;
         float s = 0.f;
@@ -90,8 +97,8 @@ __device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in
         mid[r * MS + c] = s;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < SM_TILE * SM_TILE; e += blockDim.x) {
-        const int r = e / SM_TILE, c = e - r * SM_TILE;
+    for (int e = threadIdx.x; e < SM_TX * SM_TY; e += blockDim.x) {
+        const int r = e / SM_TY, c = e - r * SM_TY;
         if (r >= rows_valid || c >= cols_valid) continue;
         const float* row = mid + r * MS + c;
         float s = 0.f;
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     const int* ti = a.tile_info + 3 * blockIdx.x;
     const HsLayer L = a.layers[ti[0]];
     const int cx0 = ti[1], cy0 = ti[2];
-    const int H = L.H, K = 2 * H + 1, W = SM_TILE + 2 * H;
+    const int H = L.H, K = 2 * H + 1, W = SM_TY + 2 * H;   // W: staged columns (y halo)
     const int MS = W | 1;                      // odd row stride: conflict-free column walks
     // the halo's first column ry0 = cy0 + pad - H = cy0 + 1 (pad = H + 1); loading
     // from cy0 instead makes every staged row 16-byte aligned in global memory
@@ -113,12 +120,12 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     const int NV = (W + 1 + 3) >> 2;           // float4s per staged row
     const int IS = 4 * NV;                     // staged row stride (floats)
     float* taps = smem;                        // K (padded to 4)
-    float* in = taps + ((K + 3) & ~3);         // W x IS
-    float* mid = in + W * IS;                  // 32 x MS
+    float* in = taps + ((K + 3) & ~3);         // (SM_TX + 2H) x IS
+    float* mid = in + (SM_TX + 2 * H) * IS;    // SM_TX x MS
     for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
     const float* raw = a.raw_layers + L.raw_off;
     const int rx0 = cx0 + L.pad - H;
-    for (int e = threadIdx.x; e < W * NV; e += blockDim.x) {
+    for (int e = threadIdx.x; e < (SM_TX + 2 * H) * NV; e += blockDim.x) {
         const int r = e / NV, c4 = e - r * NV;
         const int gx = rx0 + r, gy = cy0 + 4 * c4;
         // columns in [wy, raw_pitch) are zero; beyond the pitch is the next row
@@ -130,9 +137,9 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     in += 1;                                   // staged column 1 = halo column 0
     float* out = a.smooth_layers + L.sm_off;
     const long long ob = (long long)cx0 * L.ncy + cy0;
-    const int rv = min(SM_TILE, L.ncx - cx0), cv = min(SM_TILE, L.ncy - cy0);
+    const int rv = min(SM_TX, L.ncx - cx0), cv = min(SM_TY, L.ncy - cy0);
     switch (H) {
-#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(in, IS, mid, taps, W, MS, out, ob, L.ncy, rv, cv); break;
+#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(in, IS, mid, taps, W, MS, out, ob, L.ncy, rv, cv, in - 1); break;
         HS_SM_CASE(1) HS_SM_CASE(2) HS_SM_CASE(3) HS_SM_CASE(4) HS_SM_CASE(5) HS_SM_CASE(6) HS_SM_CASE(7)
         HS_SM_CASE(8) HS_SM_CASE(9) HS_SM_CASE(10) HS_SM_CASE(11) HS_SM_CASE(12) HS_SM_CASE(13)
         HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16)
@@ -348,8 +355,8 @@ extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     cudaStream_t st = as_stream(stream);
     if (a->total_tiles > 0) {
         HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= HS_SMOOTH_FUSED_MAX_H, "hs_smooth: max_H=%d out of range", a->max_H);
-        const int W = SM_TILE + 2 * a->max_H, K = 2 * a->max_H + 1, IS = 4 * ((W + 4) >> 2);
-        size_t sm = (size_t)(((K + 3) & ~3) + W * IS + SM_TILE * (W | 1)) * sizeof(float);
+        const int W = SM_TY + 2 * a->max_H, K = 2 * a->max_H + 1, IS = 4 * ((W + 4) >> 2);
+        size_t sm = (size_t)(((K + 3) & ~3) + (SM_TX + 2 * a->max_H) * IS + SM_TX * (W | 1)) * sizeof(float);
         static size_t smooth_attr = 48 * 1024;
         if (sm > smooth_attr) {
             HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
