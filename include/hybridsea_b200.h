@@ -144,6 +144,43 @@ typedef struct {
 HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Device init of the background tile's spectral amplitudes: replaces
+ * init_fft (fft_background.py:102-146) -- band mask, directional variance
+ * (fft_background.py:77-87, spectrum.py:108-121,124-132) and the Gaussian
+ * pairs of np.random.default_rng(seed).standard_normal((n, n, 2))
+ * (fft_background.py:136-137), drawn on the device from the same PCG64
+ * stream through the 256-strip ziggurat (tables from the host,
+ * normal_draws.py).  Draws are parsed from the raw stream in parallel: every
+ * raw position is classified as an attempt, chunks of HS_ZIG_CHUNK positions
+ * summarise "entry offset -> (exit offset, draws)" and a warp scan stitches
+ * the chain from position 0.                                                */
+#define HS_ZIG_CHUNK 128      /* raw positions per chunk */
+#define HS_ZIG_ENTRIES 32     /* entry offsets tracked per chunk */
+#define HS_ZIG_GROUP 64       /* chunks per composition group */
+typedef struct {
+    int n;                    /* power of two, 4..4096 */
+    int spread_const;         /* 1: cos-2s exponent = spread_s; 0: Mitsuyasu s(omega) */
+    double g, dk;             /* dk = 2 pi / domain */
+    const double* kf;         /* [n] 2*pi*fftfreq(n, d=domain/n) (HsFftArgs.kf) */
+    double alpha, omega_p, gamma, sigma_low, sigma_high, spread_s, mean_direction;
+    double k_lo, k_hi;        /* live iff k_lo <= |k| <= k_hi (host applies the 1e-12 slack) */
+    double kb_lo, kb_hi;      /* and, if kb_hi > 0, kb_lo <= |k| < kb_hi (cascade band) */
+    unsigned long long pcg_state[2], pcg_inc[2]; /* (hi, lo) before the first draw */
+    const unsigned long long* zig_k;  /* [256] */
+    const double* zig_w;      /* [256] */
+    const double* zig_f;      /* [256] */
+    double zig_r;
+    void* work;               /* hs_init_workspace_bytes(n) */
+    double* xi;               /* [n*n*2] the draws, or NULL (kept in `work`) */
+    double* h0;               /* [n*n] complex128 (re, im), or NULL */
+    float* h0_f32;            /* [n*n] complex64 (HsFftArgs.h0), or NULL */
+    int* status;              /* device int: 0 ok, 1 attempt ran past the chunk window,
+                                 2 raw stream too short for 2 n^2 draws */
+} HsInitArgs;
+HS_API long long hs_init_workspace_bytes(int n);
+HS_API int hs_init_h0(const HsInitArgs* a, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Resident pool (the Simulation frame path), see hs_advect_resident below.  */
 typedef struct {
     int n_patches, nb;

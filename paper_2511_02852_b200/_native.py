@@ -173,9 +173,18 @@ class HsFinishArgs(C.Structure):
                 ("normal", vp), ("disp", vp)]
 
 
+class HsInitArgs(C.Structure):
+    _fields_ = [("n", i32), ("spread_const", i32), ("g", dbl), ("dk", dbl), ("kf", vp), ("alpha", dbl),
+                ("omega_p", dbl), ("gamma", dbl), ("sigma_low", dbl), ("sigma_high", dbl), ("spread_s", dbl),
+                ("mean_direction", dbl), ("k_lo", dbl), ("k_hi", dbl), ("kb_lo", dbl), ("kb_hi", dbl),
+                ("pcg_state", C.c_uint64 * 2), ("pcg_inc", C.c_uint64 * 2), ("zig_k", vp), ("zig_w", vp),
+                ("zig_f", vp), ("zig_r", dbl), ("work", vp), ("xi", vp), ("h0", vp), ("h0_f32", vp),
+                ("status", vp)]
+
+
 ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
-               HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs]
+               HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs, HsInitArgs]
 
 EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource: 80}
 
@@ -183,7 +192,8 @@ EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource:
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
-           "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies"]
+           "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies", "hs_init_h0",
+           "hs_init_workspace_bytes"]
 
 _lib = None
 
@@ -217,6 +227,8 @@ def lib() -> C.CDLL:
     L.hs_sumsq.argtypes = [vp, i64, vp, vp]
     L.hs_advance_frame.argtypes = [vp, vp]
     L.hs_periodic_normals.argtypes = [vp, vp, i32, dbl, vp]
+    L.hs_init_workspace_bytes.restype = i64
+    L.hs_init_workspace_bytes.argtypes = [C.c_int]
     if L.hs_abi_version() != 1:
         raise RuntimeError("hybridsea_b200 ABI version mismatch")
     _lib = L

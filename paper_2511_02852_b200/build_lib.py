@@ -16,13 +16,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libhybridsea_b200.so")
-SOURCES = ["capi.cu", "fft.cu", "particles.cu", "synth.cu", "compose.cu"]
+SOURCES = ["capi.cu", "fft.cu", "particles.cu", "synth.cu", "compose.cu", "init.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-cudart", "static"]
 # particle arithmetic must round like numpy (separate IEEE mul / add); the
 # kernels spell it out with __dmul_rn/__dadd_rn and this flag backs that up
-PER_FILE_FLAGS = {"particles.cu": ["-fmad=false"]}
+PER_FILE_FLAGS = {"particles.cu": ["-fmad=false"], "init.cu": ["-fmad=false"]}
 
 
 def nvcc() -> str:

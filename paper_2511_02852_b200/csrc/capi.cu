@@ -56,6 +56,7 @@ extern "C" HS_API int hs_struct_size(int which) {
         case 16: return (int)sizeof(HsEmitArgs);
         case 17: return (int)sizeof(HsBody);
         case 18: return (int)sizeof(HsBodyArgs);
+        case 19: return (int)sizeof(HsInitArgs);
         default: return -1;
     }
 }

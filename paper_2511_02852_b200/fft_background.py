@@ -1,9 +1,10 @@
 """Global periodic FFT height field on the B200.
 
 Mirror of `hybridsea.fft_background` (`pkg/src/hybridsea/fft_background.py`).
-`init_fft` stays a host fp64 computation (it runs once and draws the same
-numpy Gaussian stream as the reference, so h0 matches it); every per-frame
-operation -- `evolve_and_synthesize`, `sample_periodic` -- is a CUDA kernel
+`init_fft` forms h0 on the GPU (`hs_init_h0`, csrc/init.cu) from the same
+PCG64 stream numpy's default_rng(seed) draws, so h0 matches the reference's
+to ~1e-14 relative (host numpy formation with `on_device=False`); every
+per-frame operation -- `evolve_and_synthesize`, `sample_periodic` -- is a CUDA kernel
 from libhybridsea_b200 (csrc/fft.cu, csrc/synth.cu).  Outputs are fp32
 device tensors.
 """
@@ -17,7 +18,8 @@ import torch
 
 from . import _native as N
 from ._layout import stream_ptr
-from .errors import ConfigError
+from .errors import ConfigError, NumericError
+from .normal_draws import pcg64_seed_state, ziggurat_r, ziggurat_tables
 from .spectrum import DirectionalSpectrum, directional_density
 
 
@@ -71,15 +73,34 @@ class FftState:
         return np.conj(self.h0[np.ix_(idx, idx)])
 
 
-def _upload(state: FftState, device) -> FftState:
+def _h0_get(self) -> np.ndarray:
+    """Host complex128 h0; a device-initialised state downloads it on first use."""
+    h = self.__dict__.get("_h0")
+    if h is None and self.__dict__.get("_h0_dev64") is not None:
+        h = self.__dict__["_h0_dev64"].cpu().numpy().view(np.complex128)[..., 0]
+        self.__dict__["_h0"] = h
+        self.__dict__["_h0_dev64"] = None
+    return h
+
+
+def _h0_set(self, value) -> None:
+    self.__dict__["_h0"] = value
+
+
+FftState.h0 = property(_h0_get, _h0_set)   # the dataclass __init__ / replace() go through the setter
+
+
+def _upload(state: FftState, device, h0_dev=None, kf_dev=None) -> FftState:
     dev = _device(device)
     n = state.n
-    h0 = np.stack([state.h0.real, state.h0.imag], axis=-1).astype(np.float32)
+    if h0_dev is None:
+        h0 = np.stack([state.h0.real, state.h0.imag], axis=-1).astype(np.float32)
+        h0_dev = torch.from_numpy(np.ascontiguousarray(h0)).to(dev)
     k = np.arange(n)
     tw = np.stack([np.cos(2.0 * math.pi * k / n), np.sin(2.0 * math.pi * k / n)], -1).astype(np.float32)
     object.__setattr__(state, "device", dev)
-    object.__setattr__(state, "h0_dev", torch.from_numpy(np.ascontiguousarray(h0)).to(dev))
-    object.__setattr__(state, "kf_dev", torch.from_numpy(state.kf.copy()).to(dev))
+    object.__setattr__(state, "h0_dev", h0_dev)
+    object.__setattr__(state, "kf_dev", kf_dev if kf_dev is not None else torch.from_numpy(state.kf.copy()).to(dev))
     object.__setattr__(state, "twiddle_dev", torch.from_numpy(np.ascontiguousarray(tw)).to(dev))
     # dispersion on the (|i|, |j|) quarter grid, the reference's own expression
     # (fft_background.py:40-47); the kernel mirrors it over the four quadrants
@@ -132,24 +153,36 @@ def resolved_band(spectrum: DirectionalSpectrum, n: int, domain_size: float,
 
 def init_fft(spectrum: DirectionalSpectrum, n: int, domain_size: float, seed: int,
              choppiness: float = 1.0, *, band: tuple | None = None, kband: tuple | None = None,
-             device=None) -> FftState:
+             device=None, on_device: bool | None = None) -> FftState:
     """Initial complex amplitudes, variance-matched to the directional
-    spectrum (fft_background.py:102-146).  Host fp64 with numpy's
-    default_rng(seed) so h0 equals the reference's; uploaded once.
-    `kband` = (k_lo, k_hi) keeps k_lo <= |k| < k_hi only (one tile of a
-    summed-cascade background, config.cascade_bands)."""
+    spectrum (fft_background.py:102-146).  `kband` = (k_lo, k_hi) keeps
+    k_lo <= |k| < k_hi only (one tile of a summed-cascade background,
+    config.cascade_bands).
+
+    On a CUDA device (the default there) `hs_init_h0` forms h0 on the GPU from
+    default_rng(seed)'s own PCG64 stream (normal_draws.py): the draws equal
+    the reference's to ~1e-14 relative.  `on_device=False` keeps the host
+    fp64 numpy formation (the reference's exact arithmetic)."""
     if n < 2 or (n & (n - 1)) != 0:
         raise ConfigError(f"fft grid size must be a power of two >= 2, got {n}")
     if domain_size <= 0:
         raise ConfigError(f"fft domain_size must be positive, got {domain_size}")
+    if n < 4:
+        raise ConfigError("the B200 FFT path needs fft.n >= 4")
     p = spectrum.params
     g = p.g
+    dev = _device(device)
+    if on_device is None:
+        on_device = dev.type == "cuda"
+    w_lo, w_hi = resolved_band(spectrum, n, domain_size, band)
+    k_lo, k_hi = w_lo ** 2 / g * (1.0 - 1e-12), w_hi ** 2 / g * (1.0 + 1e-12)
+    if on_device:
+        return _init_on_device(spectrum, n, domain_size, seed, choppiness, k_lo, k_hi, kband, dev)
     kf = 2.0 * math.pi * np.fft.fftfreq(n, d=domain_size / n)
     kx, ky = np.meshgrid(kf, kf, indexing="ij")
     kmag = np.hypot(kx, ky)
     dk = 2.0 * math.pi / domain_size
-    w_lo, w_hi = resolved_band(spectrum, n, domain_size, band)
-    live = (kmag >= (w_lo ** 2 / g) * (1.0 - 1e-12)) & (kmag <= (w_hi ** 2 / g) * (1.0 + 1e-12))
+    live = (kmag >= k_lo) & (kmag <= k_hi)
     live[0, 0] = False
     if kband is not None:
         live &= (kmag >= kband[0]) & (kmag < kband[1])
@@ -162,9 +195,66 @@ def init_fft(spectrum: DirectionalSpectrum, n: int, domain_size: float, seed: in
     h0 = np.sqrt(var / 2.0) * (xi[..., 0] + 1j * xi[..., 1])
     h0[~live] = 0.0
     st = FftState(n=n, domain_size=domain_size, g=g, rng_seed=seed, choppiness=choppiness, h0=h0)
-    if n < 4:
-        raise ConfigError("the B200 FFT path needs fft.n >= 4")
-    return _upload(st, device)
+    return _upload(st, dev)
+
+
+_ZIG_DEV: dict = {}
+
+
+def _zig_tables(dev: torch.device):
+    key = str(dev)
+    if key not in _ZIG_DEV:
+        k, w, f = ziggurat_tables()
+        _ZIG_DEV[key] = (torch.from_numpy(k.view(np.int64).copy()).to(dev), torch.from_numpy(w.copy()).to(dev),
+                         torch.from_numpy(f.copy()).to(dev))
+    return _ZIG_DEV[key]
+
+
+def _init_on_device(spectrum, n, domain_size, seed, choppiness, k_lo, k_hi, kband, dev,
+                    xi_out: torch.Tensor | None = None) -> FftState:
+    """hs_init_h0: draws, band mask and variance on the GPU (fp64); the host
+    keeps a complex128 mirror of the result for the reference API.
+    `xi_out` (float64, n*n*2, test hook) receives the Gaussian draws."""
+    p = spectrum.params
+    st = FftState(n=n, domain_size=domain_size, g=p.g, rng_seed=seed, choppiness=choppiness, h0=None)
+    kf = torch.from_numpy(st.kf.copy()).to(dev)
+    zk, zw, zf = _zig_tables(dev)
+    L = N.lib()
+    work = torch.empty(int(L.hs_init_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    h0 = torch.empty((n, n, 2), dtype=torch.float64, device=dev)
+    h0_f32 = torch.empty((n, n, 2), dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    s, inc = pcg64_seed_state(seed)
+    m64 = (1 << 64) - 1
+    a = N.HsInitArgs(n=n, spread_const=int(p.spread_s is not None), g=p.g, dk=2.0 * math.pi / domain_size,
+                     kf=N.ptr(kf), alpha=p.alpha, omega_p=p.omega_p, gamma=p.gamma, sigma_low=p.sigma_low,
+                     sigma_high=p.sigma_high, spread_s=float(p.spread_s or 0.0),
+                     mean_direction=float(spectrum.mean_direction), k_lo=k_lo, k_hi=k_hi,
+                     kb_lo=float(kband[0]) if kband is not None else 0.0,
+                     kb_hi=float(kband[1]) if kband is not None else 0.0,
+                     zig_k=N.ptr(zk), zig_w=N.ptr(zw), zig_f=N.ptr(zf), zig_r=ziggurat_r(), work=N.ptr(work),
+                     xi=N.ptr(xi_out), h0=N.ptr(h0), h0_f32=N.ptr(h0_f32), status=N.ptr(status))
+    a.pcg_state[0], a.pcg_state[1] = s >> 64, s & m64
+    a.pcg_inc[0], a.pcg_inc[1] = inc >> 64, inc & m64
+    with torch.cuda.device(dev):
+        N.call("hs_init_h0", a, torch.cuda.current_stream(dev).cuda_stream)
+        code = int(status.item())
+    if code:
+        raise NumericError(f"hs_init_h0: status {code} (1: ziggurat run past the chunk window, "
+                           "2: raw stream shorter than 2 n^2 draws)")
+    st.__dict__["_h0_dev64"] = h0                # host mirror formed lazily (FftState.h0)
+    return _upload(st, dev, h0_dev=h0_f32.view(n * n * 2).view(n, n, 2), kf_dev=kf)
+
+
+def device_draws(spectrum: DirectionalSpectrum, n: int, domain_size: float, seed: int, device=None) -> torch.Tensor:
+    """The (n, n, 2) Gaussian draws `hs_init_h0` forms for `seed` (test hook:
+    equals default_rng(seed).standard_normal((n, n, 2)) to ~1e-14)."""
+    dev = _device(device)
+    xi = torch.empty((n, n, 2), dtype=torch.float64, device=dev)
+    w_lo, w_hi = resolved_band(spectrum, n, domain_size)
+    _init_on_device(spectrum, n, domain_size, seed, 1.0, w_lo ** 2 / spectrum.params.g * (1.0 - 1e-12),
+                    w_hi ** 2 / spectrum.params.g * (1.0 + 1e-12), None, dev, xi_out=xi)
+    return xi
 
 
 def with_h0(state: FftState, h0: np.ndarray) -> FftState:
