@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--stage-frames", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--patches", type=int, default=None, help="use the first N patches of a multi-patch scene")
+    ap.add_argument("--deterministic", action="store_true", help="device.deterministic (fixed-point sums)")
     return ap.parse_args()
 
 
@@ -216,6 +217,9 @@ def main():
     from paper_2511_02852_b200.sharding import TileGather
 
     cfg, keys, scaling = scene_config(args.config, rank, world, args.patches)
+    if args.deterministic:
+        from dataclasses import replace
+        cfg = replace(cfg, deterministic=True).validate()
     sim = Simulation(cfg, device=dev, rng_seed_keys=keys)
     gather = None
     if world > 1:
@@ -375,7 +379,8 @@ def main():
                        "fft_cascades": list(cfg.fft_cascades), "n_sources": len(cfg.sources),
                        "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
                        "warm_start": f"{n_warm} frames at dt={WARM_DT}", "l2": "flushed between timed steps (256 MiB written, then read back)",
-                       "parallelism": (f"patch-sharded x{world}" if world > 1 else "single GPU")},
+                       "parallelism": (f"patch-sharded x{world}" if world > 1 else "single GPU"),
+                       "deterministic": bool(cfg.deterministic)},
             "step_ms_percentiles": step_pct,
             "gpu_launches": sim.kernel_launches_per_frame() * args.steps,
             "stages_ms": stage,

@@ -45,6 +45,20 @@ extern "C" {
 #define HS_STATUS_STAGE_OVERFLOW 2
 #define HS_STATUS_NONFINITE      4
 
+/* Deterministic mode (fixed_point = 1 in the args below).  Every float sum
+ * whose order depends on scheduling is taken in int64 fixed point, whose
+ * addition is associative, so reruns are byte-identical (the reference's
+ * determinism contract, test_acceptance.py:293-311):
+ *   raw layers   value * 2^HS_FIXED_SPLAT_BITS, one int64 per raw float slot
+ *                (same element offsets); hs_fixed_to_float turns them into the
+ *                float raw layers hs_smooth reads;
+ *   e_out        J * 2^HS_FIXED_ENERGY_BITS (the double slots hold int64);
+ *   sumsq        m^2 * 2^HS_FIXED_SUMSQ_BITS (hs_fft_evolve.sumsq,
+ *                hs_compose.interior_sumsq).                                 */
+#define HS_FIXED_SPLAT_BITS 32
+#define HS_FIXED_ENERGY_BITS 24
+#define HS_FIXED_SUMSQ_BITS 32
+
 HS_API int hs_abi_version(void);
 HS_API const char* hs_last_error(void);
 /* sizeof of ABI struct `which` (0 HsBucket, 1 HsPatch, 2 HsLayer, 3 HsPool,
@@ -140,6 +154,8 @@ typedef struct {
     long long* frame_advance; /* optional: device frame counter, += 1 after the transform */
     const double* omega;      /* optional [(n/2+1)^2] dispersion sqrt(g |k|) at (|i|, |j|) =
                                  (min(i, n-i), min(j, n-j)); NULL: formed per bin each call */
+    int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
+                                 int64 fixed point, see hs_fixed_to_float */
 } HsFftArgs;
 HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
 
@@ -202,6 +218,8 @@ typedef struct {
     const HsLayer* layers;
     int* clamped;                  /* [n_patches] */
     int* status;
+    int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
+                                 int64 fixed point, see hs_fixed_to_float */
 } HsResidentArgs;
 
 /* ------------------------------------------------------------------------ */
@@ -267,6 +285,8 @@ typedef struct {
                                               goes to pool_base + r + out_slack_prefix (gaps between
                                               segments for later in-place appends) */
     int raw_is_clear;                      /* 1: raw layers are already zero (skip the clear) */
+    int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
+                                 int64 fixed point, see hs_fixed_to_float */
 } HsAdvectArgs;
 HS_API int hs_advect(const HsAdvectArgs* a, void* stream);
 
@@ -379,6 +399,8 @@ typedef struct {
     int* status;
     const HsBody* bodies;     /* for sources with body >= 0 */
     int n_theta;              /* ring fan of bodies (interaction.py:220-222) */
+    int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
+                                 int64 fixed point, see hs_fixed_to_float */
 } HsEmitArgs;
 /* Frame start: tracking patches adopt last frame's synthesis origin as their
  * region, and take this frame's synthesis origin from their source's new
@@ -471,6 +493,8 @@ typedef struct {
     long long* frame_advance;   /* optional: device frame counter, += 1 by this launch */
     int n_extra_bg;             /* further cascades added to the background (0..3) */
     HsBgTile extra_bg[HS_MAX_CASCADES - 1];
+    int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
+                                 int64 fixed point, see hs_fixed_to_float */
 } HsComposeArgs;
 HS_API int hs_compose(const HsComposeArgs* a, void* stream);
 
@@ -523,6 +547,9 @@ typedef struct {
     int nx, ny; double spacing; double chop_scale;  /* -chi*displacement_scale */
     const float* height; float* normal; float* disp; /* disp may be NULL */
 } HsFinishArgs;
+/* dst[i] = (float)(src[i] * 2^-bits) for i < n (deterministic-mode raw layers). */
+HS_API int hs_fixed_to_float(const long long* src, float* dst, long long n, int bits, void* stream);
+
 HS_API int hs_finish(const HsFinishArgs* a, void* stream);
 
 /* Reductions used by FrameStats (harness.py:171-206). */

@@ -51,6 +51,9 @@ class HsPool(C.Structure):
     _fields_ = [("x", vp), ("y", vp), ("ux", vp), ("uy", vp), ("amp", vp)]
 
 
+HS_FIXED_SPLAT_BITS = 32
+HS_FIXED_ENERGY_BITS = 24
+HS_FIXED_SUMSQ_BITS = 32
 HS_MAX_CASCADES = 4
 
 
@@ -63,7 +66,7 @@ class HsFftArgs(C.Structure):
                 ("frame_ptr", vp), ("dt", dbl), ("spacing", dbl), ("kf", vp), ("h0", vp),
                 ("twiddle", vp), ("work_a", vp), ("work_b", vp), ("height", vp), ("dx", vp),
                 ("dy", vp), ("normal", vp), ("sumsq", vp), ("frame_advance", vp),
-                ("omega", vp)]
+                ("omega", vp), ("fixed_point", i32)]
 
 
 class HsResidentArgs(C.Structure):
@@ -71,7 +74,7 @@ class HsResidentArgs(C.Structure):
                 ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp),
                 ("tile_map", vp), ("max_tiles", i32), ("len_in", vp), ("len_out", vp), ("live", vp),
                 ("stage", HsPool), ("stage_count", vp), ("e_out", vp), ("raw_layers", vp), ("layers", vp),
-                ("clamped", vp), ("status", vp)]
+                ("clamped", vp), ("status", vp), ("fixed_point", i32)]
 
 
 class HsInjectArgs(C.Structure):
@@ -89,7 +92,7 @@ class HsAdvectArgs(C.Structure):
                 ("dropped_count", vp), ("e_out", vp), ("splat", i32), ("raw_layers", vp),
                 ("raw_layers_len", i64), ("layers", vp), ("clamped", vp), ("tile_state", vp),
                 ("max_tiles", i32), ("tile_counter", vp), ("status", vp), ("keep_words", vp),
-                ("in_seg_base", vp), ("out_slack_prefix", vp), ("raw_is_clear", i32)]
+                ("in_seg_base", vp), ("out_slack_prefix", vp), ("raw_is_clear", i32), ("fixed_point", i32)]
 
 
 class HsSource(C.Structure):
@@ -121,7 +124,7 @@ class HsEmitArgs(C.Structure):
                 ("pos_in", vp), ("pos_out", vp), ("patches", vp), ("buckets", vp), ("dt", dbl), ("beta", dbl),
                 ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp), ("len", vp),
                 ("live", vp), ("e_in", vp), ("raw_layers", vp), ("layers", vp), ("clamped", vp), ("status", vp),
-                ("bodies", vp), ("n_theta", i32)]
+                ("bodies", vp), ("n_theta", i32), ("fixed_point", i32)]
 
 
 class HsLayoutArgs(C.Structure):
@@ -150,7 +153,7 @@ class HsComposeArgs(C.Structure):
                 ("patch_height", vp), ("patch_normal", vp), ("blend_height", vp),
                 ("blend_normal", vp), ("blend_mode", i32), ("interior_sumsq", vp),
                 ("interior_count", vp), ("frame_advance", vp), ("n_extra_bg", i32),
-                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("fixed_point", i32)]
 
 
 class HsSampleArgs(C.Structure):
@@ -193,7 +196,7 @@ EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
            "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies", "hs_init_h0",
-           "hs_init_workspace_bytes"]
+           "hs_init_workspace_bytes", "hs_fixed_to_float"]
 
 _lib = None
 
@@ -227,6 +230,7 @@ def lib() -> C.CDLL:
     L.hs_sumsq.argtypes = [vp, i64, vp, vp]
     L.hs_advance_frame.argtypes = [vp, vp]
     L.hs_periodic_normals.argtypes = [vp, vp, i32, dbl, vp]
+    L.hs_fixed_to_float.argtypes = [vp, vp, i64, i32, vp]
     L.hs_init_workspace_bytes.restype = i64
     L.hs_init_workspace_bytes.argtypes = [C.c_int]
     if L.hs_abi_version() != 1:

@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
 #pragma unroll
             for (int w = 0; w < NW; ++w) { s += W.red[w]; n += W.redc[w]; }
             if (n) {
-                atomicAdd(&a.interior_sumsq[p], s);
+                sumsq_add(&a.interior_sumsq[p], s, a.fixed_point);
                 if (a.interior_count) atomicAdd((unsigned long long*)&a.interior_count[p], (unsigned long long)n);
             }
         }

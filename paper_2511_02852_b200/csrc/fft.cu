@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(FftDev d) {
 
 // ---------------------------------------------------------------- pass 2 --
 struct ColOut {
-    float* h; float* dx; float* dy; double* sumsq; long long* frame_advance;
+    float* h; float* dx; float* dy; double* sumsq; long long* frame_advance; int fixed_point;
 };
 
 template <int CA, int CBP>
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftDev d, ColOut o, int n
         if (threadIdx.x == 0) {
             double t = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-            if (t != 0.0) atomicAdd(o.sumsq, t);
+            if (t != 0.0) sumsq_add(o.sumsq, t, o.fixed_point);
         }
     }
 }
@@ -395,7 +395,7 @@ __global__ void fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
         if (threadIdx.x == 0) {
             double tsum = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tsum += red[w];
-            if (tsum != 0.0) atomicAdd(o.sumsq, tsum);
+            if (tsum != 0.0) sumsq_add(o.sumsq, tsum, o.fixed_point);
         }
     }
 }
@@ -460,7 +460,7 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     d.wa = reinterpret_cast<float2*>(a->work_a);
     d.wb = reinterpret_cast<float2*>(a->work_b);
 
-    ColOut oreg{a->height, a->dx, a->dy, a->sumsq, a->frame_advance};
+    ColOut oreg{a->height, a->dx, a->dy, a->sumsq, a->frame_advance, a->fixed_point};
     int rc_reg = -1;
     switch (n) {
         case 64: rc_reg = launch_fft_reg<64>(d, oreg, st); break;
@@ -491,7 +491,7 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     fft_rows_kernel<<<n / 2 + 1, 256, sm_rows, st>>>(d);
     HS_LAUNCH_CHECK();
 
-    ColOut o{a->height, a->dx, a->dy, a->sumsq, a->frame_advance};
+    ColOut o{a->height, a->dx, a->dy, a->sumsq, a->frame_advance, a->fixed_point};
     // columns per CTA: keep a tile <= 64 KiB of complex64
     auto launch_cols = [&](auto kern, int ca, int cbp) -> int {
         int n_a = n / ca;

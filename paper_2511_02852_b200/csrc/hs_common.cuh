@@ -40,6 +40,15 @@ void set_error(const char* fmt, ...);
         }                                                                          \
     } while (0)
 
+// deterministic-mode sum of squares: fp64 partial -> int64 fixed point
+__device__ __forceinline__ void sumsq_add(double* dst, double v, int fixed_point) {
+    if (fixed_point)
+        atomicAdd(reinterpret_cast<unsigned long long*>(dst),
+                  (unsigned long long)__double2ll_rn(v * (double)(1ull << HS_FIXED_SUMSQ_BITS)));
+    else
+        atomicAdd(dst, v);
+}
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int num_sms();

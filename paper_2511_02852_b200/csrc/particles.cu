@@ -47,6 +47,13 @@ __device__ __forceinline__ void red_pair(float* row, int c, float v0, float v1) 
     else { red2(b + 2, 0.f, v0); red2(b + 4, v1, 0.f); }
 }
 
+// deterministic mode: one int64 fixed-point slot per raw float slot
+__device__ __forceinline__ void red_fixed(float* raw, long long e, float v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(raw) + e,
+              (unsigned long long)__float2ll_rn(v * (float)(1ull << HS_FIXED_SPLAT_BITS)));
+}
+
+template <bool FX>
 __device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLayer& L, double x0, double y0,
                                          double x, double y, float amp, int* clamp_acc) {
     double u = (x - x0) * L.inv_tf + (double)L.pad;
@@ -56,10 +63,40 @@ __device__ __forceinline__ void splat_at(float* __restrict__ raw, const SplatLay
     v = fmin(fmax(v, 0.0), L.vmax - 1e-9);
     const int i0 = (int)u, j0 = (int)v;
     const float fu = (float)(u - i0), fv = (float)(v - j0);
-    float* row = raw + L.raw_off + (long long)i0 * L.pitch;
     const float a1 = amp * fu, a0 = amp - a1;          // amp (1 - fu), amp fu
-    red_pair(row, j0, a0 * (1.f - fv), a0 * fv);
-    red_pair(row + L.pitch, j0, a1 * (1.f - fv), a1 * fv);
+    if constexpr (FX) {
+        const long long e = L.raw_off + (long long)i0 * L.pitch + j0;
+        red_fixed(raw, e, a0 * (1.f - fv));
+        red_fixed(raw, e + 1, a0 * fv);
+        red_fixed(raw, e + L.pitch, a1 * (1.f - fv));
+        red_fixed(raw, e + L.pitch + 1, a1 * fv);
+    } else {
+        float* row = raw + L.raw_off + (long long)i0 * L.pitch;
+        red_pair(row, j0, a0 * (1.f - fv), a0 * fv);
+        red_pair(row + L.pitch, j0, a1 * (1.f - fv), a1 * fv);
+    }
+}
+
+__device__ __forceinline__ void splat_at(bool fx, float* __restrict__ raw, const SplatLayer& L, double x0, double y0,
+                                         double x, double y, float amp, int* clamp_acc) {
+    if (fx) splat_at<true>(raw, L, x0, y0, x, y, amp, clamp_acc);
+    else splat_at<false>(raw, L, x0, y0, x, y, amp, clamp_acc);
+}
+
+// despawn-energy accumulation: fp64, or int64 fixed point (deterministic mode)
+__device__ __forceinline__ long long energy_fixed(double e) {
+    return __double2ll_rn(e * (double)(1ull << HS_FIXED_ENERGY_BITS));
+}
+__device__ __forceinline__ void energy_add(double* dst, double e, bool fx) {
+    if (fx) atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)energy_fixed(e));
+    else atomicAdd(dst, e);
+}
+// add a (shared-memory) accumulator of the same mode into a global one
+__device__ __forceinline__ void energy_flush(double* dst, const double& acc, bool fx) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
+    if (!bits) return;
+    if (fx) atomicAdd(reinterpret_cast<unsigned long long*>(dst), bits);
+    else atomicAdd(dst, acc);
 }
 
 // ============================================================== inject ==
@@ -280,11 +317,12 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
                     if (keep) {
                         atomicAdd(&ap_kept[b], 1);
                         int cl = 0;
-                        splat_at(a.res.raw_layers, ap_sl[b], P.sx0, P.sy0, nx, ny, am, &cl);
+                        splat_at(a.res.fixed_point, a.res.raw_layers, ap_sl[b], P.sx0, P.sy0, nx, ny, am, &cl);
                         if (cl) atomicAdd(&ap_clamp, cl);
                     } else if (am > 0.f) {
                         const double e2 = (double)am;                  // crest despawn energy (:322-327)
-                        atomicAdd(&ap_eout[b], 0.125 * a.rho * a.g * (e2 * e2) * 3.141592653589793 * ap_r2[b]);
+                        energy_add(&ap_eout[b], 0.125 * a.rho * a.g * (e2 * e2) * 3.141592653589793 * ap_r2[b],
+                                   a.res.fixed_point);
                     }
                 }
             } else {
@@ -311,7 +349,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
             a.res.len_out[s] = a.res.len_in[s] + n;
             if (n > ap_room[b]) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             if (ap_kept[b]) atomicAdd(&a.res.live[s], ap_kept[b]);
-            if (ap_eout[b] != 0.0) atomicAdd(&a.res.e_out[s], ap_eout[b]);
+            energy_flush(&a.res.e_out[s], ap_eout[b], a.res.fixed_point);
         }
         if (threadIdx.x == 0 && ap_clamp && a.res.clamped) atomicAdd(&a.res.clamped[p], ap_clamp);
     }
@@ -336,7 +374,7 @@ __device__ __forceinline__ int find_seg(const int* off, int nseg, int v) {
 __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer& L, const HsPatch& P,
                                           double x, double y, float amp, int* clamp_acc) {
     SplatLayer S{L.raw_off, 1.0 / (P.texel * (double)L.f), (double)(L.wx - 1), (double)(L.wy - 1), L.raw_pitch, L.pad};
-    splat_at(raw, S, P.sx0, P.sy0, x, y, amp, clamp_acc);
+    splat_at<false>(raw, S, P.sx0, P.sy0, x, y, amp, clamp_acc);
 }
 
 // Persistent CTAs take tiles of ADV_TILE virtual items in order from a global
@@ -550,7 +588,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                         atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
                     }
                     atomicAdd(&keep_hist[b], 1);
-                    if (a.splat) splat_at(raw, sl_s[b], P.sx0, P.sy0, x, y, am, &clamp_local);
+                    if (a.splat) splat_at(a.fixed_point, raw, sl_s[b], P.sx0, P.sy0, x, y, am, &clamp_local);
                 } else {
                     if (am > 0.f) {
                         // crest despawn energy rho g A^2 pi r^2 / 8 (particles.py:322-327)
@@ -573,7 +611,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
             const int b = threadIdx.x;
             if (keep_hist[b]) atomicAdd(&a.out_count[(size_t)p * nb + b], keep_hist[b]);
             if (drop_hist[b]) atomicAdd(&a.dropped_count[(size_t)p * nb + b], drop_hist[b]);
-            if (eout_s[b] != 0.0) atomicAdd(&a.e_out[(size_t)p * nb + b], eout_s[b]);
+            energy_flush(&a.e_out[(size_t)p * nb + b], eout_s[b], a.fixed_point);
         }
         if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
         __syncthreads();
@@ -771,11 +809,11 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
             } else {
                 atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             }
-            if (a.splat) splat_at(raw, T.sl[b], P.sx0, P.sy0, x, y, am, &clamp_local);
+            if (a.splat) splat_at(a.fixed_point, raw, T.sl[b], P.sx0, P.sy0, x, y, am, &clamp_local);
         } else if (x == x) {                             // a despawn (NaN marks a resident-pool hole)
             if (am > 0.f) {
                 const double amp = (double)am;          // crest despawn energy (particles.py:322-327)
-                atomicAdd(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * T.r2[b]);
+                energy_add(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * T.r2[b], a.fixed_point);
             }
             if (a.dropped.x) {
                 const long long o = P.pool_base + (v - rank);
@@ -791,7 +829,7 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
         const int b = threadIdx.x;
         if (keep_hist[b]) atomicAdd(&a.out_count[(size_t)p * nb + b], keep_hist[b]);
         if (drop_hist[b]) atomicAdd(&a.dropped_count[(size_t)p * nb + b], drop_hist[b]);
-        if (eout_s[b] != 0.0) atomicAdd(&a.e_out[(size_t)p * nb + b], eout_s[b]);
+        energy_flush(&a.e_out[(size_t)p * nb + b], eout_s[b], a.fixed_point);
     }
     if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
 }
@@ -836,6 +874,7 @@ constexpr int RES_TILE = RES_THREADS * RES_ITEMS;
 // ahead, so each tile costs one memory round trip: the slot loads, the
 // segment length and the bucket/patch/layer constants issue together.
 // Every warp retires its slots independently (no barrier).
+template <bool FX>
 __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResidentArgs a) {
     const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
     double* __restrict__ px = a.pool.x;
@@ -874,6 +913,7 @@ __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResid
                             __ldg(&L->pad)};
         int drops = 0, clamp_local = 0;
         double e = 0.0;
+        long long efx = 0;
 #pragma unroll
         for (int it = 0; it < RES_ITEMS; ++it) {
             const int k = it * RES_THREADS + threadIdx.x;
@@ -887,14 +927,15 @@ __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResid
                 px[o] = nx;
                 py[o] = ny;
 #ifndef HS_EXP_NOSPLAT
-                splat_at(a.raw_layers, sl, sx0, sy0, nx, ny, am[it], &clamp_local);
+                splat_at<FX>(a.raw_layers, sl, sx0, sy0, nx, ny, am[it], &clamp_local);
 #endif
             } else {
                 px[o] = __longlong_as_double(0x7ff8000000000000LL);       // hole: stable compaction is deferred
                 ++drops;
                 if (am[it] > 0.f) {                                       // crest despawn energy (:322-327)
                     const double amp = (double)am[it];
-                    e += 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2;
+                    const double ep = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2;
+                    if constexpr (FX) efx += energy_fixed(ep); else e += ep;
                 }
             }
         }
@@ -902,10 +943,14 @@ __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResid
         if (__any_sync(0xffffffffu, drops != 0 || clamp_local != 0)) {
             drops = warp_sum(drops);
             clamp_local = warp_sum(clamp_local);
-            e = warp_sum(e);
+            if constexpr (FX) efx = warp_sum(efx); else e = warp_sum(e);
             if ((threadIdx.x & 31) == 0) {
                 if (drops) atomicSub(&a.live[s], drops);
-                if (e != 0.0) atomicAdd(&a.e_out[s], e);
+                if constexpr (FX) {
+                    if (efx) atomicAdd(reinterpret_cast<unsigned long long*>(&a.e_out[s]), (unsigned long long)efx);
+                } else if (e != 0.0) {
+                    atomicAdd(&a.e_out[s], e);
+                }
                 if (clamp_local && a.clamped) atomicAdd(&a.clamped[p], clamp_local);
             }
         }
@@ -976,10 +1021,10 @@ __global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResident
         }
         if (keep) {
             atomicAdd(&kept_s[b], 1);
-            splat_at(a.raw_layers, sl_s[b], P.sx0, P.sy0, nx, ny, am, &clamp_local);
+            splat_at(a.fixed_point, a.raw_layers, sl_s[b], P.sx0, P.sy0, nx, ny, am, &clamp_local);
         } else if (am > 0.f) {
             const double amp = (double)am;
-            atomicAdd(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2_s[b]);
+            energy_add(&eout_s[b], 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2_s[b], a.fixed_point);
         }
     }
     if (clamp_local) atomicAdd(&clamp_s, clamp_local);
@@ -987,7 +1032,7 @@ __global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResident
     if (threadIdx.x < nb) {
         const int s = p * nb + threadIdx.x;
         if (kept_s[threadIdx.x]) atomicAdd(&a.live[s], kept_s[threadIdx.x]);
-        if (eout_s[threadIdx.x] != 0.0) atomicAdd(&a.e_out[s], eout_s[threadIdx.x]);
+        energy_flush(&a.e_out[s], eout_s[threadIdx.x], a.fixed_point);
     }
     if (threadIdx.x == 0 && clamp_s && a.clamped) atomicAdd(&a.clamped[p], clamp_s);
 }
@@ -1270,12 +1315,12 @@ __global__ void __launch_bounds__(256) emit_kernel(HsEmitArgs a) {
             const double cy = dadd(py, dmul(S.hull_extent, uy));
             long long o = base + k;
             a.pool.x[o] = cx; a.pool.y[o] = cy; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = ca;
-            splat_at(a.raw_layers, sl, P.sx0, P.sy0, cx, cy, ca, &clamp_local);
+            splat_at(a.fixed_point, a.raw_layers, sl, P.sx0, P.sy0, cx, cy, ca, &clamp_local);
             if (m == 2) {                                              // trailing trough, -beta * amp
                 const double tx = dsub(cx, dmul(r, ux)), ty = dsub(cy, dmul(r, uy));
                 o += n;
                 a.pool.x[o] = tx; a.pool.y[o] = ty; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = ta;
-                splat_at(a.raw_layers, sl, P.sx0, P.sy0, tx, ty, ta, &clamp_local);
+                splat_at(a.fixed_point, a.raw_layers, sl, P.sx0, P.sy0, tx, ty, ta, &clamp_local);
             }
         }
     }
@@ -1305,7 +1350,7 @@ __global__ void emit_commit_kernel(HsEmitArgs a) {
             const int cnt = m * (branch == 0 ? pl.n_ring : pl.n_wake);
             if (a.len[seg] + cnt > a.seg_cap[seg]) continue;          // overflow flagged by emit_kernel
             a.len[seg] += cnt;
-            a.live[seg] += cnt;
+            atomicAdd(&a.live[seg], cnt);   // advect_resident decrements live concurrently (other stream)
             a.e_in[seg] = dadd(a.e_in[seg], e);
         }
     }
@@ -1412,11 +1457,12 @@ extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
     HS_CHECK_ARG(((size_t)a->tile_map & 15) == 0, "hs_advect_resident: tile_map must be 16-byte aligned");
     static int occ = 0;
     if (!occ) {
-        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel, RES_THREADS, 0));
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel<false>, RES_THREADS, 0));
         if (occ < 1) occ = 1;
     }
     const int grid = min(a->max_tiles, num_sms() * occ);
-    advect_resident_kernel<<<grid, RES_THREADS, 0, as_stream(stream)>>>(*a);
+    if (a->fixed_point) advect_resident_kernel<true><<<grid, RES_THREADS, 0, as_stream(stream)>>>(*a);
+    else advect_resident_kernel<false><<<grid, RES_THREADS, 0, as_stream(stream)>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

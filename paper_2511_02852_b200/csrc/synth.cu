@@ -416,6 +416,33 @@ extern "C" int hs_composite(const HsCompositeArgs* a, void* stream) {
     return 0;
 }
 
+namespace hs {
+// deterministic-mode raw layers: int64 fixed point -> float, 4 slots per thread
+__global__ void fixed_to_float_kernel(const long long* __restrict__ src, float* __restrict__ dst, long long n,
+                                      double scale) {
+    const long long i = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+    if (i + 3 < n) {
+        const longlong2 a = *reinterpret_cast<const longlong2*>(src + i);
+        const longlong2 b = *reinterpret_cast<const longlong2*>(src + i + 2);
+        *reinterpret_cast<float4*>(dst + i) = make_float4((float)((double)a.x * scale), (float)((double)a.y * scale),
+                                                          (float)((double)b.x * scale), (float)((double)b.y * scale));
+    } else {
+        for (long long k = i; k < n; ++k) dst[k] = (float)((double)src[k] * scale);
+    }
+}
+}  // namespace hs
+
+extern "C" int hs_fixed_to_float(const long long* src, float* dst, long long n, int bits, void* stream) {
+    HS_CHECK_ARG(n >= 0 && (n == 0 || (src && dst)), "hs_fixed_to_float: bad buffers");
+    HS_CHECK_ARG(((size_t)src & 15) == 0 && ((size_t)dst & 15) == 0, "hs_fixed_to_float: buffers must be 16-byte aligned");
+    HS_CHECK_ARG(bits >= 0 && bits < 63, "hs_fixed_to_float: bits=%d", bits);
+    if (n == 0) return 0;
+    const long long threads = (n + 3) / 4;
+    fixed_to_float_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(src, dst, n, ldexp(1.0, -bits));
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
 extern "C" int hs_finish(const HsFinishArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_finish: null args");
     HS_CHECK_ARG(a->nx >= 2 && a->ny >= 2, "hs_finish: grid must be at least 2x2");

@@ -69,6 +69,11 @@ def estimate_population(table, region: PatchRegion, trough_fraction: float) -> f
     return tot
 
 
+def fixed_to_double(a: np.ndarray, bits: int) -> np.ndarray:
+    """Deterministic-mode accumulator (int64 fixed point in fp64 slots) -> fp64."""
+    return np.asarray(a).view(np.int64).astype(np.float64) * (2.0 ** -bits)
+
+
 @dataclass
 class FrameStats:
     """Per-frame statistics (harness.py:32-46).  Device-resident values are
@@ -82,10 +87,16 @@ class FrameStats:
     _fft_n: int = 0
     body_states: list = field(default_factory=list)
     _cache: dict = field(default_factory=dict, repr=False)
+    _fixed: bool = False        # deterministic mode: e_out / isum / fsum hold int64 fixed point
 
     def _get(self):
         if not self._cache:
             s = {k: v.cpu().numpy() for k, v in self._snap.items()}
+            if self._fixed:
+                for k, bits in (("e_out", N.HS_FIXED_ENERGY_BITS), ("isum", N.HS_FIXED_SUMSQ_BITS),
+                                ("fsum", N.HS_FIXED_SUMSQ_BITS)):
+                    if k in s:
+                        s[k] = fixed_to_double(s[k], bits)
             counts = s["counts"].reshape(self._n_patches, self._nb).sum(0) if self._n_patches else np.zeros(self._nb, np.int64)
             e_in = s["e_in"].reshape(self._n_patches, self._nb).sum(0) if self._n_patches else np.zeros(self._nb)
             e_out = s["e_out"].reshape(self._n_patches, self._nb).sum(0) if self._n_patches else np.zeros(self._nb)
@@ -134,6 +145,7 @@ class Simulation:
                  rng_seed_keys: list | None = None, compact_period: int | None = None):
         cfg = config.validate()
         self.config = cfg
+        self.det = bool(cfg.deterministic)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         self.params = derive_params(cfg.u10, cfg.fetch, cfg.g, gamma=cfg.gamma, spread_s=cfg.spread_s)
@@ -254,6 +266,8 @@ class Simulation:
 
         if self.n_patches:
             self.synth = SynthWorkspace(self.regions, self.res, self.plans, dev)
+            if self.det:
+                self.raw_fixed = torch.zeros(self.synth.raw.numel(), dtype=torch.int64, device=dev)
             structs = []
             for k, (r, res) in enumerate(zip(self.regions, self.res)):
                 structs.append(patch_struct(r, res, pool_base=self.pool_base[k], pool_capacity=self.pool_caps[k],
@@ -358,6 +372,11 @@ class Simulation:
         self.box_prefix_dev = torch.from_numpy(self.box_prefix_np).to(self.device)
         self.composite_out = torch.zeros((n, n), dtype=torch.float32, device=self.device)
 
+    def _raw_target(self) -> int:
+        """Where the splats accumulate: the float raw layers, or (deterministic
+        mode) their int64 fixed-point twin."""
+        return N.ptr(self.raw_fixed) if self.det else N.ptr(self.synth.raw)
+
     def _pool(self, k: int) -> N.HsPool:
         return N.pool_struct(*self.pools[k])
 
@@ -393,9 +412,9 @@ class Simulation:
             patches=N.ptr(self.patches_dev), buckets=N.ptr(self.buckets_dev), dt=float(dt),
             beta=float(cfg.trough_fraction), rho=float(cfg.rho), g=float(cfg.g), pool=self._pool(buf),
             seg_base=N.ptr(self.seg_base), seg_cap=N.ptr(self.seg_cap), len=N.ptr(self.seg_len[lp ^ 1]),
-            live=N.ptr(self.live), e_in=N.ptr(self.e_in), raw_layers=N.ptr(self.synth.raw),
+            live=N.ptr(self.live), e_in=N.ptr(self.e_in), raw_layers=self._raw_target(),
             layers=N.ptr(self.synth.layers), clamped=N.ptr(stats[3]), status=N.ptr(self.status),
-            bodies=N.ptr(self.bodies_dev), n_theta=self.table.n_theta)
+            bodies=N.ptr(self.bodies_dev), n_theta=self.table.n_theta, fixed_point=int(self.det))
 
     def _bodies_args(self, dt: float) -> N.HsBodyArgs:
         cfg = self.config
@@ -419,8 +438,8 @@ class Simulation:
             seg_base=N.ptr(self.seg_base), seg_cap=N.ptr(self.seg_cap), tile_map=N.ptr(self.tile_map),
             max_tiles=self.res_tiles, len_in=N.ptr(self.seg_len[lp]), len_out=N.ptr(self.seg_len[lp ^ 1]),
             live=N.ptr(self.live), stage=N.pool_struct(*self.stage), stage_count=N.ptr(self.stage_count),
-            e_out=N.ptr(self.e_out), raw_layers=N.ptr(self.synth.raw), layers=N.ptr(self.synth.layers),
-            clamped=N.ptr(stats[3]), status=N.ptr(self.status))
+            e_out=N.ptr(self.e_out), raw_layers=self._raw_target(), layers=N.ptr(self.synth.layers),
+            clamped=N.ptr(stats[3]), status=N.ptr(self.status), fixed_point=int(self.det))
 
     # --------------------------------------------------------- the frame --
     def _enqueue_frame(self, state: tuple, dt: float, mark=None) -> None:
@@ -455,6 +474,7 @@ class Simulation:
                     fa = fft_args(st_c, ws_c, frame_ptr=self.frame_dev, dt=dt)
                     fa.emit_normals = 0      # normals are derived lazily (background) / in hs_compose
                     fa.normal = 0
+                    fa.fixed_point = int(self.det)
                     if not self.n_patches and c == len(self.cascades) - 1:
                         fa.frame_advance = N.ptr(self.frame_dev)
                     N.call("hs_fft_evolve", fa, stream_ptr())
@@ -482,12 +502,12 @@ class Simulation:
                     in_=self._pool(buf), in_count=N.ptr(self.seg_len[lp]), stage=N.pool_struct(*self.stage),
                     stage_count=N.ptr(self.stage_count), out=self._pool(buf ^ 1),
                     out_count=N.ptr(self.compact_count), dropped=N.pool_struct(), dropped_count=0,
-                    e_out=N.ptr(self.e_out), splat=1, raw_layers=N.ptr(self.synth.raw),
-                    raw_layers_len=self.synth.pack.raw_len, layers=N.ptr(self.synth.layers),
+                    e_out=N.ptr(self.e_out), splat=1, raw_layers=self._raw_target(),
+                    raw_layers_len=self.synth.pack.raw_len * (2 if self.det else 1), layers=N.ptr(self.synth.layers),
                     clamped=N.ptr(stats[3]), tile_state=N.ptr(self.tile_state), max_tiles=self.max_tiles,
                     tile_counter=N.ptr(self.tile_counter), status=N.ptr(self.status),
                     keep_words=N.ptr(self.keep_words), in_seg_base=N.ptr(self.seg_base),
-                    out_slack_prefix=N.ptr(self.slack_prefix), raw_is_clear=1), stream_ptr())
+                    out_slack_prefix=N.ptr(self.slack_prefix), raw_is_clear=1, fixed_point=int(self.det)), stream_ptr())
                 self._layout(self.compact_count, self.seg_len[lp ^ 1])
                 if self.n_sources:
                     N.call("hs_emit", self._emit_args(buf ^ 1, lp, dt, stats), stream_ptr())
@@ -510,12 +530,15 @@ class Simulation:
                 mark("advect")
                 main.wait_stream(inj)
                 mark("join_inject")
+            if self.det:                        # fixed-point raw layers -> the float ones hs_smooth reads
+                N.call_raw("hs_fixed_to_float", N.vp(N.ptr(self.raw_fixed)), N.vp(N.ptr(self.synth.raw)),
+                           N.i64(self.raw_fixed.numel()), N.i32(N.HS_FIXED_SPLAT_BITS), N.vp(stream_ptr()))
             N.call("hs_smooth", self.synth.smooth_args(), stream_ptr())
             mark("smooth")
             clr = self._side_stream("clear")
             clr.wait_stream(main)
             with torch.cuda.stream(clr):        # raw layers are consumed: clear them for the next splat
-                self.synth.raw.zero_()
+                (self.raw_fixed if self.det else self.synth.raw).zero_()
             if fork:
                 main.wait_stream(self._side_stream("fft"))
                 mark("join")
@@ -531,7 +554,7 @@ class Simulation:
                 patch_height=N.ptr(self.patch_h), patch_normal=0,
                 blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
                 interior_sumsq=N.ptr(stats[1]), interior_count=N.ptr(stats[2]),
-                frame_advance=N.ptr(self.frame_dev), **self._extra_bg()), stream_ptr())
+                frame_advance=N.ptr(self.frame_dev), fixed_point=int(self.det), **self._extra_bg()), stream_ptr())
             mark("compose")
             main.wait_stream(clr)
             self._patch_n_frame = -1          # patch normals are derived lazily (patch_field)
@@ -614,6 +637,7 @@ class Simulation:
             if self.n_sources:
                 k += 2 + (1 if self._tracking else 0)      # emit + commit (+ track)
             k += (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
+            k += 1 if self.det else 0                 # fixed-point raw layers -> float
         return max(k, 1.0)
 
     def timed_frame(self) -> dict:
@@ -696,7 +720,8 @@ class Simulation:
             if self.n_bodies:
                 snap["bodies"] = self.bodies_dev.clone()
         return FrameStats(frame=self.frame, t=self.t, stage_ms={s: 0.0 for s in STAGES}, _snap=snap, _nb=self.nb,
-                          _n_patches=self.n_patches, _fft_n=self.config.fft_n if self.fft_ws is not None else 0)
+                          _n_patches=self.n_patches, _fft_n=self.config.fft_n if self.fft_ws is not None else 0,
+                          _fixed=self.det)
 
     def check(self) -> None:
         """Raise if a device capacity flag was set (synchronises)."""
@@ -839,8 +864,11 @@ class Simulation:
 
     def ledger_host(self) -> dict:
         P, nb = self.n_patches, self.nb
+        e_out = self.e_out.cpu().numpy()
+        if self.det:
+            e_out = fixed_to_double(e_out, N.HS_FIXED_ENERGY_BITS)
         return {"acc": self.acc.cpu().numpy().reshape(P, nb, 4), "groups": self.groups.cpu().numpy().reshape(P, nb),
-                "e_in": self.e_in.cpu().numpy().reshape(P, nb), "e_out": self.e_out.cpu().numpy().reshape(P, nb)}
+                "e_in": self.e_in.cpu().numpy().reshape(P, nb), "e_out": e_out.reshape(P, nb)}
 
 
 class HostFramePipe:
