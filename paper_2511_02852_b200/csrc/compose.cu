@@ -110,7 +110,21 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
     const int* ti = a.tile_info + 3 * tile;
     const int p = ti[0], i0 = ti[1], j0 = ti[2];
     const HsPatch P = synth_view(a.patches[p]);   // the retracked rectangle (tracking patches)
-    const bool have_bg = a.bg_height != nullptr && a.blend_mode;
+    // the background only enters texels inside the blend band (w < 1): a tile
+    // whose every output texel sits deeper than the margin skips it.  The
+    // depth min(x - x0, x1 - x) is concave along a row / column, so its
+    // minimum over the tile is at the first or last row / column.
+    bool in_band = false;
+    {
+        const float inv_m = (float)(1.0 / P.margin);
+        const int rl = min(CT, P.res - i0) - 1, cl = min(CT, P.ny - j0) - 1;
+        const double xa = P.x0 + (double)i0 * P.texel, xb = P.x0 + (double)(i0 + rl) * P.texel;
+        const double ya = P.y0 + (double)j0 * P.texel, yb = P.y0 + (double)(j0 + cl) * P.texel;
+        const float dx = fminf((float)fmin(xa - P.x0, P.x1 - xa), (float)fmin(xb - P.x0, P.x1 - xb));
+        const float dy = fminf((float)fmin(ya - P.y0, P.y1 - ya), (float)fmin(yb - P.y0, P.y1 - yb));
+        in_band = fminf(dx, dy) * inv_m < 1.f;
+    }
+    const bool have_bg = a.bg_height != nullptr && a.blend_mode && in_band;
     const int bm = a.bg_n - 1;
     const double inv_sp = have_bg ? 1.0 / a.bg_spacing : 0.0;
     const int4 bq = have_bg ? bg_footprint(P, i0, j0, inv_sp, bm) : make_int4(0, 0, 0, 0);
@@ -334,7 +348,11 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
             ++cnt;
         }
         if (a.blend_mode) {
-            float hb = 0.f, nx = 0.f, ny = 0.f, nz = 1.f;
+            const float d = fminf(W.row_d[rr], W.col_d[cc]);
+            const float w = d > 0.f ? smoothstep01(d * inv_margin) : 0.f;
+            float hb = h, nx = pnx, ny = pny, nz = pnz;    // w == 1: the patch alone (coupling.py:37-40)
+            if (w < 1.f) {
+            hb = 0.f; nx = 0.f; ny = 0.f; nz = 1.f;
             if (have_bg) {
                 const float fv = W.col_fv[cc];
                 if (bg_staged) {
@@ -372,13 +390,12 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
                     add_cascades(a.n_extra_bg, a.extra_bg, P.x0 + (double)ii * P.texel, P.y0 + (double)jj * P.texel,
                                  hb, nx, ny, nz);
             }
-            const float d = fminf(W.row_d[rr], W.col_d[cc]);
             if (d > 0.f) {
-                const float w = smoothstep01(d * inv_margin);
                 hb = lerpf(hb, h, w);
                 const float mx = lerpf(nx, pnx, w), my = lerpf(ny, pny, w), mz = lerpf(nz, pnz, w);
                 const float r2 = rsqrtf(mx * mx + my * my + mz * mz);
                 nx = mx * r2; ny = my * r2; nz = mz * r2;
+            }
             }
             if (a.blend_height) a.blend_height[o] = hb;
             if (a.blend_normal) { a.blend_normal[3 * o] = nx; a.blend_normal[3 * o + 1] = ny; a.blend_normal[3 * o + 2] = nz; }

@@ -869,93 +869,120 @@ constexpr int RES_THREADS = 256;
 constexpr int RES_ITEMS = 4;
 constexpr int RES_TILE = RES_THREADS * RES_ITEMS;
 
-// Persistent CTAs walk the tile list with stride gridDim.x.  A tile-map entry
-// (segment, tile-in-segment, absolute first slot) is prefetched one tile
-// ahead, so each tile costs one memory round trip: the slot loads, the
-// segment length and the bucket/patch/layer constants issue together.
-// Every warp retires its slots independently (no barrier).
-template <bool FX>
-__global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResidentArgs a) {
-    const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
+// Slots k = k0 + it * STRIDE + lane_k (it < ITEMS) of the resident tile m =
+// (segment, tile in segment, absolute first slot): advect in place, cull to a
+// NaN hole, splat; per-warp totals of drops, clamps and despawn energy.
+// Slot loads issue before the segment length is known: slots past len (up to
+// the tile end, inside the pool arrays) are read and ignored.
+template <bool FX, int ITEMS, int STRIDE>
+__device__ __forceinline__ void resident_slots(const HsResidentArgs& a, int4 m, int k0, int lane_k) {
     double* __restrict__ px = a.pool.x;
     double* __restrict__ py = a.pool.y;
     const double* __restrict__ pux = a.pool.ux;
     const double* __restrict__ puy = a.pool.uy;
     const float* __restrict__ pam = a.pool.amp;
+    const int s = m.x;
+    const long long base = (long long)m.z;
+    double x[ITEMS], y[ITEMS], ux[ITEMS], uy[ITEMS];
+    float am[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        const long long o = base + k0 + it * STRIDE + lane_k;
+        x[it] = px[o]; y[it] = py[o]; ux[it] = __ldg(pux + o); uy[it] = __ldg(puy + o); am[it] = __ldg(pam + o);
+    }
+    const int n = min(RES_TILE, a.len_in[s] - m.y * RES_TILE);
+    const int p = s / a.nb, b = s - p * a.nb;
+    const HsPatch* P = a.patches + p;
+    const double x0 = __ldg(&P->x0), y0 = __ldg(&P->y0), x1 = __ldg(&P->x1), y1 = __ldg(&P->y1);
+    const double sx0 = __ldg(&P->sx0), sy0 = __ldg(&P->sy0);     // synthesis origin (tracking patches)
+    const HsBucket* Bk = a.buckets + b;
+    const double step = dmul(__ldg(&Bk->speed), a.dt);            // speeds * dt (particles.py:312)
+    const double rad = __ldg(&Bk->radius);
+    const double r2 = dmul(rad, rad);
+    const HsLayer* L = a.layers + __ldg(&P->layer_base) + b;
+    const SplatLayer sl{__ldg(&L->raw_off), 1.0 / (__ldg(&P->texel) * (double)__ldg(&L->f)),
+                        (double)(__ldg(&L->wx) - 1), (double)(__ldg(&L->wy) - 1), __ldg(&L->raw_pitch),
+                        __ldg(&L->pad)};
+    int drops = 0, clamp_local = 0;
+    double e = 0.0;
+    long long efx = 0;
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        const int k = k0 + it * STRIDE + lane_k;
+        if (k >= n || x[it] != x[it]) continue;                     // beyond len, or a hole
+        const long long o = base + k;
+        const double nx = dadd(x[it], dmul(ux[it], step));           // pos += dir * (c dt)  (:312-313)
+        const double ny = dadd(y[it], dmul(uy[it], step));
+        const double ox = fmax(fmax(dsub(x0, nx), dsub(nx, x1)), 0.0);
+        const double oy = fmax(fmax(dsub(y0, ny), dsub(ny, y1)), 0.0);
+        if (dadd(dmul(ox, ox), dmul(oy, oy)) <= r2) {                // support disk (:315-320)
+            px[o] = nx;
+            py[o] = ny;
+#ifndef HS_EXP_NOSPLAT
+            splat_at<FX>(a.raw_layers, sl, sx0, sy0, nx, ny, am[it], &clamp_local);
+#endif
+        } else {
+            px[o] = __longlong_as_double(0x7ff8000000000000LL);       // hole: stable compaction is deferred
+            ++drops;
+            if (am[it] > 0.f) {                                       // crest despawn energy (:322-327)
+                const double amp = (double)am[it];
+                const double ep = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2;
+                if constexpr (FX) efx += energy_fixed(ep); else e += ep;
+            }
+        }
+    }
+    // per-warp totals (drops and despawns are rare: most warps skip the atomics)
+    if (__any_sync(0xffffffffu, drops != 0 || clamp_local != 0)) {
+        drops = warp_sum(drops);
+        clamp_local = warp_sum(clamp_local);
+        if constexpr (FX) efx = warp_sum(efx); else e = warp_sum(e);
+        if ((threadIdx.x & 31) == 0) {
+            if (drops) atomicSub(&a.live[s], drops);
+            if constexpr (FX) {
+                if (efx) atomicAdd(reinterpret_cast<unsigned long long*>(&a.e_out[s]), (unsigned long long)efx);
+            } else if (e != 0.0) {
+                atomicAdd(&a.e_out[s], e);
+            }
+            if (clamp_local && a.clamped) atomicAdd(&a.clamped[p], clamp_local);
+        }
+    }
+}
+
+// Static schedule: persistent CTAs walk the tile list with stride gridDim.x;
+// a tile-map entry is prefetched one tile ahead.
+template <bool FX>
+__global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResidentArgs a) {
+    const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
     int t = blockIdx.x;
     int4 m = t < a.max_tiles ? __ldg(tmap + t) : make_int4(-1, 0, 0, 0);
     while (m.x >= 0) {
         const int tn = t + gridDim.x;
         const int4 mn = tn < a.max_tiles ? __ldg(tmap + tn) : make_int4(-1, 0, 0, 0);
-        const int s = m.x;
-        const long long base = (long long)m.z;
-        // slot loads before the length is known: slots past len (up to the
-        // tile end, inside the pool arrays) are read and ignored
-        double x[RES_ITEMS], y[RES_ITEMS], ux[RES_ITEMS], uy[RES_ITEMS];
-        float am[RES_ITEMS];
-#pragma unroll
-        for (int it = 0; it < RES_ITEMS; ++it) {
-            const long long o = base + it * RES_THREADS + threadIdx.x;
-            x[it] = px[o]; y[it] = py[o]; ux[it] = __ldg(pux + o); uy[it] = __ldg(puy + o); am[it] = __ldg(pam + o);
-        }
-        const int n = min(RES_TILE, a.len_in[s] - m.y * RES_TILE);
-        const int p = s / a.nb, b = s - p * a.nb;
-        const HsPatch* P = a.patches + p;
-        const double x0 = __ldg(&P->x0), y0 = __ldg(&P->y0), x1 = __ldg(&P->x1), y1 = __ldg(&P->y1);
-        const double sx0 = __ldg(&P->sx0), sy0 = __ldg(&P->sy0);     // synthesis origin (tracking patches)
-        const HsBucket* Bk = a.buckets + b;
-        const double step = dmul(__ldg(&Bk->speed), a.dt);            // speeds * dt (particles.py:312)
-        const double rad = __ldg(&Bk->radius);
-        const double r2 = dmul(rad, rad);
-        const HsLayer* L = a.layers + __ldg(&P->layer_base) + b;
-        const SplatLayer sl{__ldg(&L->raw_off), 1.0 / (__ldg(&P->texel) * (double)__ldg(&L->f)),
-                            (double)(__ldg(&L->wx) - 1), (double)(__ldg(&L->wy) - 1), __ldg(&L->raw_pitch),
-                            __ldg(&L->pad)};
-        int drops = 0, clamp_local = 0;
-        double e = 0.0;
-        long long efx = 0;
-#pragma unroll
-        for (int it = 0; it < RES_ITEMS; ++it) {
-            const int k = it * RES_THREADS + threadIdx.x;
-            if (k >= n || x[it] != x[it]) continue;                     // beyond len, or a hole
-            const long long o = base + k;
-            const double nx = dadd(x[it], dmul(ux[it], step));           // pos += dir * (c dt)  (:312-313)
-            const double ny = dadd(y[it], dmul(uy[it], step));
-            const double ox = fmax(fmax(dsub(x0, nx), dsub(nx, x1)), 0.0);
-            const double oy = fmax(fmax(dsub(y0, ny), dsub(ny, y1)), 0.0);
-            if (dadd(dmul(ox, ox), dmul(oy, oy)) <= r2) {                // support disk (:315-320)
-                px[o] = nx;
-                py[o] = ny;
-#ifndef HS_EXP_NOSPLAT
-                splat_at<FX>(a.raw_layers, sl, sx0, sy0, nx, ny, am[it], &clamp_local);
-#endif
-            } else {
-                px[o] = __longlong_as_double(0x7ff8000000000000LL);       // hole: stable compaction is deferred
-                ++drops;
-                if (am[it] > 0.f) {                                       // crest despawn energy (:322-327)
-                    const double amp = (double)am[it];
-                    const double ep = 0.125 * a.rho * a.g * (amp * amp) * 3.141592653589793 * r2;
-                    if constexpr (FX) efx += energy_fixed(ep); else e += ep;
-                }
-            }
-        }
-        // per-warp totals (drops and despawns are rare: most warps skip the atomics)
-        if (__any_sync(0xffffffffu, drops != 0 || clamp_local != 0)) {
-            drops = warp_sum(drops);
-            clamp_local = warp_sum(clamp_local);
-            if constexpr (FX) efx = warp_sum(efx); else e = warp_sum(e);
-            if ((threadIdx.x & 31) == 0) {
-                if (drops) atomicSub(&a.live[s], drops);
-                if constexpr (FX) {
-                    if (efx) atomicAdd(reinterpret_cast<unsigned long long*>(&a.e_out[s]), (unsigned long long)efx);
-                } else if (e != 0.0) {
-                    atomicAdd(&a.e_out[s], e);
-                }
-                if (clamp_local && a.clamped) atomicAdd(&a.clamped[p], clamp_local);
-            }
-        }
+        resident_slots<FX, RES_ITEMS, RES_THREADS>(a, m, 0, threadIdx.x);
         t = tn;
         m = mn;
+    }
+}
+
+// Dynamic schedule (a.work_counter): CTAs claim whole tiles from a frame
+// counter (one atomic per 1024 slots), the next claim in flight while the
+// current tile runs.  CTAs that start late -- the FFT branch shares the SMs --
+// simply take fewer tiles.
+template <bool FX>
+__global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_dyn_kernel(HsResidentArgs a) {
+    const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
+    __shared__ int claim[2];
+    if (threadIdx.x == 0) claim[0] = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    int t = claim[0], buf = 0;
+    while (t < a.max_tiles) {
+        const int4 m = __ldg(tmap + t);
+        if (m.x < 0) break;                          // past the last used tile
+        if (threadIdx.x == 0) claim[buf ^ 1] = atomicAdd(a.work_counter, 1);
+        resident_slots<FX, RES_ITEMS, RES_THREADS>(a, m, 0, threadIdx.x);
+        __syncthreads();
+        buf ^= 1;
+        t = claim[buf];
     }
 }
 
@@ -1461,8 +1488,14 @@ extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
         if (occ < 1) occ = 1;
     }
     const int grid = min(a->max_tiles, num_sms() * occ);
-    if (a->fixed_point) advect_resident_kernel<true><<<grid, RES_THREADS, 0, as_stream(stream)>>>(*a);
-    else advect_resident_kernel<false><<<grid, RES_THREADS, 0, as_stream(stream)>>>(*a);
+    cudaStream_t st = as_stream(stream);
+    if (a->work_counter) {
+        if (a->fixed_point) advect_resident_dyn_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);
+        else advect_resident_dyn_kernel<false><<<grid, RES_THREADS, 0, st>>>(*a);
+    } else {
+        if (a->fixed_point) advect_resident_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);
+        else advect_resident_kernel<false><<<grid, RES_THREADS, 0, st>>>(*a);
+    }
     HS_LAUNCH_CHECK();
     return 0;
 }

@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -146,6 +147,9 @@ class Simulation:
         cfg = config.validate()
         self.config = cfg
         self.det = bool(cfg.deterministic)
+        # hs_advect_resident claims work per warp (HsResidentArgs.work_counter);
+        # HS_ADVECT_STATIC=1 selects the static per-CTA tile stride (A/B runs)
+        self.dynamic_advect = os.environ.get("HS_ADVECT_STATIC", "0") != "1"
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         self.params = derive_params(cfg.u10, cfg.fetch, cfg.g, gamma=cfg.gamma, spread_s=cfg.spread_s)
@@ -317,14 +321,15 @@ class Simulation:
             # per-frame accumulators in one block of 4-byte words per frame parity:
             # frame f accumulates into set f & 1 while its hs_inject zeroes the other
             # set (frame f + 1's), so no clear sits between concurrent producers
+            # (word 5P: the resident advect's work counter of that frame)
             P = self.n_patches
-            nw = 5 * P + (P & 1)
+            nw = 5 * P + 2 + (P & 1)
             self.stat_words2 = torch.zeros(2 * nw, dtype=torch.int32, device=dev)
             self._stat_sets = []
             for q in range(2):
                 w = self.stat_words2[q * nw:(q + 1) * nw]
                 self._stat_sets.append((w, w[0:2 * P].view(torch.float64), w[2 * P:4 * P].view(torch.int64),
-                                        w[4 * P:5 * P]))
+                                        w[4 * P:5 * P], w[5 * P:5 * P + 1]))
             self.max_tiles = int(sum(-(-(pc + sc) // ADV_TILE) for pc, sc in zip(self.pool_caps, self.stage_caps)))
             self.tile_state = torch.zeros(self.max_tiles, dtype=torch.int64, device=dev)
             self.keep_words = torch.zeros(self.max_tiles * 32, dtype=torch.int32, device=dev)
@@ -439,7 +444,8 @@ class Simulation:
             max_tiles=self.res_tiles, len_in=N.ptr(self.seg_len[lp]), len_out=N.ptr(self.seg_len[lp ^ 1]),
             live=N.ptr(self.live), stage=N.pool_struct(*self.stage), stage_count=N.ptr(self.stage_count),
             e_out=N.ptr(self.e_out), raw_layers=self._raw_target(), layers=N.ptr(self.synth.layers),
-            clamped=N.ptr(stats[3]), status=N.ptr(self.status), fixed_point=int(self.det))
+            clamped=N.ptr(stats[3]), status=N.ptr(self.status), fixed_point=int(self.det),
+            work_counter=N.ptr(stats[4]) if self.dynamic_advect else 0)
 
     # --------------------------------------------------------- the frame --
     def _enqueue_frame(self, state: tuple, dt: float, mark=None) -> None:
