@@ -18,6 +18,17 @@
 
 namespace hs {
 
+#ifdef HS_COMPOSE_TRACE
+// per-phase globaltimer stamps of thread 0 of each CTA (tools/compose_trace.py)
+__device__ unsigned long long g_trace[4096 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+#define TRACE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_trace[blockIdx.x * 8 + (k)] = gtime(); } while (0)
+#else
+#define TRACE(k) do {} while (0)
+#endif
+
 constexpr int CT = 30;            // output tile edge
 constexpr int CH = CT + 2;        // haloed height tile (32): lane = haloed column
 constexpr int NW = 4;             // warps per tile (CTA)
@@ -106,6 +117,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
     LayerPlan* const Wpl = reinterpret_cast<LayerPlan*>(smem_raw + sizeof(TileSmem));
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int tile = blockIdx.x;
+    TRACE(0);
     if (a.frame_advance && tile == 0 && tid == 0) *a.frame_advance += 1;
     const int* ti = a.tile_info + 3 * tile;
     const int p = ti[0], i0 = ti[1], j0 = ti[2];
@@ -193,6 +205,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         }
     }
     __syncthreads();
+    TRACE(1);
     // every coarse footprint, one batch
     for (int b = 0; b < nb; ++b) {
         const LayerPlan& L = Wpl[b];
@@ -201,7 +214,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         const float inv_nc = 1.f / (float)L.ncol;
         for (int e = tid; e < L.nr * L.ncol; e += NT) {
             const int rr = fdiv(e, inv_nc) , cc = e - rr * L.ncol;
-            cp_async4(W.cs + L.cs_off + e, Sg + (long long)rr * L.ncy + cc, true);
+            cp_async4(W.cs + L.cs_off + e, Sg + (rr * L.ncy + cc), true);
         }
     }
     // f == 1 layers straight into the accumulators (lane = haloed column, coalesced rows)
@@ -217,12 +230,13 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         const float* Sg = a.smooth_layers + L.sm_off;
         float v[RPW];
 #pragma unroll
-        for (int k = 0; k < RPW; ++k) v[k] = Sg[(long long)min(max(ib + qb + k, 0), P.res - 1) * L.ncy + j];
+        for (int k = 0; k < RPW; ++k) v[k] = Sg[min(max(ib + qb + k, 0), P.res - 1) * L.ncy + j];
 #pragma unroll
         for (int k = 0; k < RPW; ++k) acc[k] = fmaf(L.gain, v[k], acc[k]);
     }
     cp_async_wait_all();
     __syncthreads();
+    TRACE(2);
     // f == 1 sum to shared memory; the coarse pass below picks it up transposed
     {
         const int jr = jb + c;
@@ -246,6 +260,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
             W.u2.tc[L.tc_off + r * TCP + (tid & 31)] = lerpf(src[r * L.ncol], src[r * L.ncol + d1], wj);
     }
     __syncthreads();
+    TRACE(3);
     // ---- coarse layers: thread = haloed row q, columns c0 .. c0+7; per layer the
     // row weights are formed once and each texel costs two table reads ----
     {
@@ -286,6 +301,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         }
     }
     __syncthreads();                               // tc dead: trow may overwrite it
+    TRACE(4);
     // background: node normals (given, or from the staged heights), x-lerped per output row
     const float inv2sp = have_bg ? (float)(0.5 / a.bg_spacing) : 0.f;
     if (bg_staged) {
@@ -318,6 +334,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         }
     }
     __syncthreads();
+    TRACE(5);
 
     // ---- normals, blend, outputs ----
     const float inv_s = (float)(1.0 / P.texel), inv_2s = (float)(0.5 / P.texel);
@@ -340,7 +357,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
         const float hy = (hr - hl) * ((jj == 0 || jj == P.ny - 1) ? inv_s : inv_2s);
         const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
         const float pnx = -hx * rn, pny = -hy * rn, pnz = rn;
-        const long long o = gb + (long long)ii * P.ny + jj;
+        const int o = (int)gb + ii * P.ny + jj;         // 32-bit: the harness keeps 3 x texels < 2^31
         if (a.patch_height) a.patch_height[o] = h;
         if (a.patch_normal) { a.patch_normal[3 * o] = pnx; a.patch_normal[3 * o + 1] = pny; a.patch_normal[3 * o + 2] = pnz; }
         if (ii >= inset && ii < P.res - inset && jj >= inset && jj < P.ny - inset) {
@@ -401,6 +418,7 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
             if (a.blend_normal) { a.blend_normal[3 * o] = nx; a.blend_normal[3 * o + 1] = ny; a.blend_normal[3 * o + 2] = nz; }
         }
     }
+    TRACE(6);
     if (a.interior_sumsq) {
         accv = warp_sum(accv);
         cnt = warp_sum(cnt);
@@ -422,6 +440,12 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
 }  // namespace hs
 
 using namespace hs;
+
+#ifdef HS_COMPOSE_TRACE
+extern "C" HS_API int hs_debug_trace(void* dst) {
+    return (int)cudaMemcpyFromSymbol(dst, hs::g_trace, sizeof(hs::g_trace));
+}
+#endif
 
 extern "C" int hs_compose(const HsComposeArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_compose: null args");

@@ -1487,7 +1487,12 @@ extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
         HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel<false>, RES_THREADS, 0));
         if (occ < 1) occ = 1;
     }
-    const int grid = min(a->max_tiles, num_sms() * occ);
+    static int per_sm = -1;
+    if (per_sm < 0) {   // experiment hook: resident CTAs per SM (leave room for the FFT branch)
+        const char* e = getenv("HS_RES_CTAS");
+        per_sm = e ? max(1, min(occ, atoi(e))) : occ;
+    }
+    const int grid = min(a->max_tiles, num_sms() * per_sm);
     cudaStream_t st = as_stream(stream);
     if (a->work_counter) {
         if (a->fixed_point) advect_resident_dyn_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);

@@ -314,6 +314,8 @@ class Simulation:
             keys = rng_seed_keys if rng_seed_keys is not None else [(cfg.seed, k) for k in range(self.n_patches)]
             self.rng = torch.cat([PhiloxStream(keys[k], dev).state for k in range(self.n_patches)])
             n_grid = int(self.synth.grid_base[-1])
+            if 3 * n_grid >= 2 ** 31:            # hs_compose indexes the (texel, 3) normals in 32 bits
+                raise ConfigError(f"patch grids hold {n_grid} texels; at most {(2 ** 31 - 1) // 3} per GPU")
             self.patch_h = f32(n_grid)
             self.patch_n = f32(3 * n_grid)
             self.blend_h = f32(n_grid)
