@@ -220,8 +220,6 @@ typedef struct {
     int* status;
     int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
                                  int64 fixed point, see hs_fixed_to_float */
-    int* work_counter;        /* hs_advect_resident: zero at launch -> warps claim 128-slot pieces
-                                 dynamically; NULL -> static tile stride per CTA */
 } HsResidentArgs;
 
 /* ------------------------------------------------------------------------ */

@@ -74,7 +74,7 @@ class HsResidentArgs(C.Structure):
                 ("rho", dbl), ("g", dbl), ("pool", HsPool), ("seg_base", vp), ("seg_cap", vp),
                 ("tile_map", vp), ("max_tiles", i32), ("len_in", vp), ("len_out", vp), ("live", vp),
                 ("stage", HsPool), ("stage_count", vp), ("e_out", vp), ("raw_layers", vp), ("layers", vp),
-                ("clamped", vp), ("status", vp), ("fixed_point", i32), ("work_counter", vp)]
+                ("clamped", vp), ("status", vp), ("fixed_point", i32)]
 
 
 class HsInjectArgs(C.Structure):

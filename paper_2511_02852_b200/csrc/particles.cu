@@ -948,10 +948,16 @@ __device__ __forceinline__ void resident_slots(const HsResidentArgs& a, int4 m, 
     }
 }
 
-// Static schedule: persistent CTAs walk the tile list with stride gridDim.x;
-// a tile-map entry is prefetched one tile ahead.
+// Persistent CTAs walk the tile list with stride gridDim.x; a tile-map entry
+// is prefetched one tile ahead, so each tile costs one memory round trip.
+// Every warp retires its slots independently (no barrier).  (A dynamic
+// variant -- atomic tile claims plus a shared-memory splat of small layers --
+// measured slower on C3 and C5 once the FFT branch forks after inject.)
+#ifndef HS_RES_MINB
+#define HS_RES_MINB 3          // 3 CTAs/SM: 80 registers, no inner-loop spills
+#endif
 template <bool FX>
-__global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResidentArgs a) {
+__global__ void __launch_bounds__(RES_THREADS, HS_RES_MINB) advect_resident_kernel(HsResidentArgs a) {
     const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
     int t = blockIdx.x;
     int4 m = t < a.max_tiles ? __ldg(tmap + t) : make_int4(-1, 0, 0, 0);
@@ -961,28 +967,6 @@ __global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_kernel(HsResid
         resident_slots<FX, RES_ITEMS, RES_THREADS>(a, m, 0, threadIdx.x);
         t = tn;
         m = mn;
-    }
-}
-
-// Dynamic schedule (a.work_counter): CTAs claim whole tiles from a frame
-// counter (one atomic per 1024 slots), the next claim in flight while the
-// current tile runs.  CTAs that start late -- the FFT branch shares the SMs --
-// simply take fewer tiles.
-template <bool FX>
-__global__ void __launch_bounds__(RES_THREADS, 4) advect_resident_dyn_kernel(HsResidentArgs a) {
-    const int4* __restrict__ tmap = reinterpret_cast<const int4*>(a.tile_map);
-    __shared__ int claim[2];
-    if (threadIdx.x == 0) claim[0] = atomicAdd(a.work_counter, 1);
-    __syncthreads();
-    int t = claim[0], buf = 0;
-    while (t < a.max_tiles) {
-        const int4 m = __ldg(tmap + t);
-        if (m.x < 0) break;                          // past the last used tile
-        if (threadIdx.x == 0) claim[buf ^ 1] = atomicAdd(a.work_counter, 1);
-        resident_slots<FX, RES_ITEMS, RES_THREADS>(a, m, 0, threadIdx.x);
-        __syncthreads();
-        buf ^= 1;
-        t = claim[buf];
     }
 }
 
@@ -1487,20 +1471,10 @@ extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
         HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel<false>, RES_THREADS, 0));
         if (occ < 1) occ = 1;
     }
-    static int per_sm = -1;
-    if (per_sm < 0) {   // experiment hook: resident CTAs per SM (leave room for the FFT branch)
-        const char* e = getenv("HS_RES_CTAS");
-        per_sm = e ? max(1, min(occ, atoi(e))) : occ;
-    }
-    const int grid = min(a->max_tiles, num_sms() * per_sm);
+    const int grid = min(a->max_tiles, num_sms() * occ);
     cudaStream_t st = as_stream(stream);
-    if (a->work_counter) {
-        if (a->fixed_point) advect_resident_dyn_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);
-        else advect_resident_dyn_kernel<false><<<grid, RES_THREADS, 0, st>>>(*a);
-    } else {
-        if (a->fixed_point) advect_resident_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);
-        else advect_resident_kernel<false><<<grid, RES_THREADS, 0, st>>>(*a);
-    }
+    if (a->fixed_point) advect_resident_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);
+    else advect_resident_kernel<false><<<grid, RES_THREADS, 0, st>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

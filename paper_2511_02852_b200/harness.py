@@ -147,9 +147,6 @@ class Simulation:
         cfg = config.validate()
         self.config = cfg
         self.det = bool(cfg.deterministic)
-        # hs_advect_resident claims work per warp (HsResidentArgs.work_counter);
-        # HS_ADVECT_STATIC=1 selects the static per-CTA tile stride (A/B runs)
-        self.dynamic_advect = os.environ.get("HS_ADVECT_STATIC", "0") != "1"
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         self.params = derive_params(cfg.u10, cfg.fetch, cfg.g, gamma=cfg.gamma, spread_s=cfg.spread_s)
@@ -323,15 +320,14 @@ class Simulation:
             # per-frame accumulators in one block of 4-byte words per frame parity:
             # frame f accumulates into set f & 1 while its hs_inject zeroes the other
             # set (frame f + 1's), so no clear sits between concurrent producers
-            # (word 5P: the resident advect's work counter of that frame)
             P = self.n_patches
-            nw = 5 * P + 2 + (P & 1)
+            nw = 5 * P + (P & 1)
             self.stat_words2 = torch.zeros(2 * nw, dtype=torch.int32, device=dev)
             self._stat_sets = []
             for q in range(2):
                 w = self.stat_words2[q * nw:(q + 1) * nw]
                 self._stat_sets.append((w, w[0:2 * P].view(torch.float64), w[2 * P:4 * P].view(torch.int64),
-                                        w[4 * P:5 * P], w[5 * P:5 * P + 1]))
+                                        w[4 * P:5 * P]))
             self.max_tiles = int(sum(-(-(pc + sc) // ADV_TILE) for pc, sc in zip(self.pool_caps, self.stage_caps)))
             self.tile_state = torch.zeros(self.max_tiles, dtype=torch.int64, device=dev)
             self.keep_words = torch.zeros(self.max_tiles * 32, dtype=torch.int32, device=dev)
@@ -446,8 +442,7 @@ class Simulation:
             max_tiles=self.res_tiles, len_in=N.ptr(self.seg_len[lp]), len_out=N.ptr(self.seg_len[lp ^ 1]),
             live=N.ptr(self.live), stage=N.pool_struct(*self.stage), stage_count=N.ptr(self.stage_count),
             e_out=N.ptr(self.e_out), raw_layers=self._raw_target(), layers=N.ptr(self.synth.layers),
-            clamped=N.ptr(stats[3]), status=N.ptr(self.status), fixed_point=int(self.det),
-            work_counter=N.ptr(stats[4]) if self.dynamic_advect else 0)
+            clamped=N.ptr(stats[3]), status=N.ptr(self.status), fixed_point=int(self.det))
 
     # --------------------------------------------------------- the frame --
     def _enqueue_frame(self, state: tuple, dt: float, mark=None) -> None:
@@ -455,13 +450,17 @@ class Simulation:
         `state` = (buffer, length parity, compaction frame?).
 
         In-place frames (K - 1 of every K):
-            side  : hs_fft_evolve (rows, cols) ..........................┐
-            inj   : hs_inject -> hs_append_resident ──┐                   │
+            side  :               └► hs_fft_evolve (rows, cols) ........┐
+            inj   : hs_inject (+append) ─┴► hs_emit ──┐                 │
             main  : hs_advect_resident ──────────────┴► hs_smooth ─► join ─► hs_compose
             clr   :                                      └► raw-layer clear ─┘ (end of frame)
-        Compaction frames replace the advect pair by hs_inject -> hs_advect
-        (count + scatter into the other buffer, squeezing the holes out) ->
-        hs_resident_layout.  `mark(stage)` (optional) is called after each
+        The FFT branch forks after the (one CTA per patch) inject kernel, so
+        the resident advect -- the head of the critical chain -- takes the SMs
+        first and the transforms fill in behind it (every kernel here fills the
+        register file, so the two do not co-reside; forking at frame start cost
+        ~8 us of C3 frame).  Compaction frames replace the advect pair by
+        hs_inject -> hs_advect (count + scatter into the other buffer,
+        squeezing the holes out) -> hs_resident_layout.  `mark(stage)` (optional) is called after each
         stage's launches on the stream that ran it (CUDA events for stage
         timing)."""
         buf, lp, compact = state
@@ -472,10 +471,10 @@ class Simulation:
             # transform and compose overwrite it (harness.py:155-157)
             N.call("hs_bodies", self._bodies_args(dt), stream_ptr())
         fork = self.fft_state is not None and self.n_patches > 0
-        if self.fft_state is not None:
+        def fft_branch(after):
             side = self._side_stream("fft") if fork else main
             if fork:
-                side.wait_stream(main)
+                side.wait_stream(after)
             with torch.cuda.stream(side):
                 mark("fft_start")
                 for c, (st_c, ws_c) in enumerate(self.cascades):
@@ -487,6 +486,8 @@ class Simulation:
                         fa.frame_advance = N.ptr(self.frame_dev)
                     N.call("hs_fft_evolve", fa, stream_ptr())
                 mark("fft")
+        if self.fft_state is not None and not fork:
+            fft_branch(main)
         if self.n_patches:
             stats, nxt = self._stat_sets[lp], self._stat_sets[lp ^ 1]
             cfg = self.config
@@ -504,6 +505,8 @@ class Simulation:
                 mark("particles_start")
                 N.call("hs_inject", inj_args, stream_ptr())
                 mark("inject")
+                if fork:
+                    fft_branch(main)
                 N.call("hs_advect", N.HsAdvectArgs(
                     n_patches=self.n_patches, nb=self.nb, buckets=N.ptr(self.buckets_dev),
                     patches=N.ptr(self.patches_dev), dt=float(dt), rho=float(cfg.rho), g=float(cfg.g),
@@ -530,6 +533,9 @@ class Simulation:
                     mark("inject_start")
                     N.call("hs_inject", inj_args, stream_ptr())
                     mark("inject")
+                if fork:                            # FFT branch forks after the 1-CTA-per-patch inject:
+                    fft_branch(inj)                 # the resident advect fills the SMs first
+                with torch.cuda.stream(inj):
                     if self.n_sources:
                         N.call("hs_emit", self._emit_args(buf, lp, dt, stats), stream_ptr())
                         mark("emit")

@@ -18,10 +18,13 @@ def main() -> int:
     ap.add_argument("--config", default="C3")
     ap.add_argument("--frames", type=int, default=5)
     ap.add_argument("--warm-frames", type=int, default=2000)
+    ap.add_argument("--patches", type=int, default=None, help="first N patches of a multi-patch scene")
     args = ap.parse_args()
     import torch
-    from paper_2511_02852_b200 import Simulation, scenes
-    sim = Simulation(scenes.PRESETS[args.config](), device="cuda:0")
+    from paper_2511_02852_b200 import Simulation
+    from bench import scene_config
+    cfg, keys, _ = scene_config(args.config, 0, 1, args.patches)
+    sim = Simulation(cfg, device="cuda:0", rng_seed_keys=keys)
     sim.run_frames(args.warm_frames, dt=0.1)
     sim.run_frames(3)
     torch.cuda.synchronize()
