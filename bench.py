@@ -344,16 +344,16 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = adv_bytes / (adv_ms * 1e-3) / 1e9 if adv_ms == adv_ms and adv_ms > 0 else None
-    # DRAM bytes per hs_advect call (count + scatter kernels) from the committed
-    # ncu launch list of this workload (tools/ncu_launches.sh -> tools/traffic_json.py)
+    # DRAM bytes per hs_advect_resident launch from the committed ncu launch list
+    # of this workload (tools/ncu_launches.sh -> tools/traffic_json.py)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tp):
         try:
             ks = json.load(open(tp))["kernels"]
-            traffic = sum(ks[k]["dram_read_bytes"] + ks[k]["dram_write_bytes"]
-                          for k in ("advect_resident_kernel",))
-        except (OSError, KeyError, ValueError):
+            k = next(k for k in ks if k.startswith("advect_resident_kernel"))
+            traffic = ks[k]["dram_read_bytes"] + ks[k]["dram_write_bytes"]
+        except (OSError, KeyError, ValueError, StopIteration):
             traffic = None
 
     cpu = None
