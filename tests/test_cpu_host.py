@@ -167,3 +167,30 @@ def test_single_cascade_scene_equals_plain_scene():
     oa, ob = a.step(), b.step()
     np.testing.assert_array_equal(oa["height"], ob["height"])
     np.testing.assert_array_equal(oa["blend_heights"][0], ob["blend_heights"][0])
+
+
+def test_deterministic_mode_config_and_fixed_point_decoding():
+    """device.deterministic parses / round-trips, and the host decodes the
+    int64 fixed-point accumulators (HS_FIXED_* in the header) exactly."""
+    from paper_2511_02852_b200 import _native as N
+    from paper_2511_02852_b200 import dump_config, parse_config
+    from paper_2511_02852_b200.harness import fixed_to_double
+    cfg = parse_config("device.deterministic = true\nfft.n = 64\n")
+    assert cfg.deterministic and parse_config(dump_config(cfg)) == cfg
+    assert not parse_config("fft.n = 64\n").deterministic
+    header = open(os.path.join(ROOT, "include", "hybridsea_b200.h")).read()
+    for name in ("HS_FIXED_SPLAT_BITS", "HS_FIXED_ENERGY_BITS", "HS_FIXED_SUMSQ_BITS"):
+        assert int(re.search(rf"#define {name} (\d+)", header).group(1)) == getattr(N, name)
+    e = np.array([1234.5, 0.0, 3.0e6])
+    fx = np.rint(e * 2.0 ** N.HS_FIXED_ENERGY_BITS).astype(np.int64)
+    np.testing.assert_array_equal(fixed_to_double(fx.view(np.float64), N.HS_FIXED_ENERGY_BITS), e)
+
+
+def test_device_init_workspace_sizes():
+    """hs_init_workspace_bytes: positive and growing with n for the supported
+    sizes, -1 outside them (no device work)."""
+    from paper_2511_02852_b200 import _native as N
+    L = N.lib()
+    sizes = [L.hs_init_workspace_bytes(n) for n in (4, 64, 1024, 4096)]
+    assert all(b > 0 for b in sizes) and sizes == sorted(sizes)
+    assert L.hs_init_workspace_bytes(100) == -1 and L.hs_init_workspace_bytes(8192) == -1
