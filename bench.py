@@ -23,8 +23,10 @@ cores, on the same config, as a bounded sample.
 
 Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank owns
 one C3-geometry patch (seeded layout in the shared 4000 m tile, own Philox
-stream), runs the replicated background, and the blended patch tiles are
-all-gathered over NCCL every frame (the composite exchange of SURVEY 8(e)).
+stream), runs the replicated background, and every frame the composite is
+exchanged at FFT resolution: each rank resamples its patch boxes of the
+stitched grid, one NCCL all-gather moves them, every rank pastes them over the
+background (sharding.CompositeGather).
 """
 from __future__ import annotations
 
@@ -214,7 +216,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2511_02852_b200 import Simulation
     from paper_2511_02852_b200 import _native as N
-    from paper_2511_02852_b200.sharding import TileGather
+    from paper_2511_02852_b200.sharding import CompositeGather
 
     cfg, keys, scaling = scene_config(args.config, rank, world, args.patches)
     if args.deterministic:
@@ -223,9 +225,14 @@ def main():
     sim = Simulation(cfg, device=dev, rng_seed_keys=keys)
     gather = None
     if world > 1:
-        share = torch.tensor([int(sim.synth.grid_base[-1])], device=dev)
-        dist.all_reduce(share, op=dist.ReduceOp.MAX)
-        gather = TileGather(sim, world, max_local=int(share.item()))
+        # the composite exchange at FFT resolution: every rank's
+        # patch boxes of the stitched grid, all-gathered and pasted on every rank
+        gather = CompositeGather(sim.box_np.reshape(-1, 4), cfg.fft_n, world, device=dev)
+        bg_buf = None if len(sim.cascades) == 1 else torch.empty((cfg.fft_n, cfg.fft_n), device=dev)
+
+    def exchange():
+        sim.composite_boxes(gather.send)
+        gather.exchange(sim.fft_ws.height if bg_buf is None else sim.background_sum(bg_buf))
 
     # steady state: the step itself at dt = 0.1
     n_warm = int(round(args.warm_seconds / WARM_DT))
@@ -236,7 +243,7 @@ def main():
     for _ in range(max(3, args.warmup)):
         sim.step(stats=False)
         if gather:
-            gather.exchange()
+            exchange()
     torch.cuda.synchronize()
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -263,7 +270,7 @@ def main():
         starts[k].record()
         sim.step(stats=False)
         if gather:
-            gather.exchange()
+            exchange()
         ends[k].record()
     torch.cuda.synchronize()
     if world > 1:
@@ -382,7 +389,7 @@ def main():
                        "parallelism": (f"patch-sharded x{world}" if world > 1 else "single GPU"),
                        "deterministic": bool(cfg.deterministic)},
             "step_ms_percentiles": step_pct,
-            "gpu_launches": sim.kernel_launches_per_frame() * args.steps,
+            "gpu_launches": (sim.kernel_launches_per_frame() + (1 if gather else 0)) * args.steps,
             "stages_ms": stage,
             "roofline": {"bound": "hbm", "kernel": "hs_advect_resident (in-place advect+cull+splat)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -538,6 +538,9 @@ typedef struct {
     float* out;                 /* [n*n] */
     int n_extra_bg;             /* further background cascades, summed at the grid nodes */
     HsBgTile extra_bg[HS_MAX_CASCADES - 1];
+    float* box_out;             /* optional [total_box]: write the boxes' values here, compact in
+                                   box_prefix order, instead of the grid (`out` unused): a rank's
+                                   share of the multi-GPU composite exchange (sharding.py) */
 } HsCompositeArgs;
 HS_API int hs_composite(const HsCompositeArgs* a, void* stream);
 

@@ -168,7 +168,7 @@ class HsCompositeArgs(C.Structure):
     _fields_ = [("n", i32), ("spacing", dbl), ("bg_height", vp), ("bg_normal", vp), ("n_patches", i32),
                 ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("box", vp),
                 ("box_prefix", vp), ("total_box", i32), ("out", vp), ("n_extra_bg", i32),
-                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("box_out", vp)]
 
 
 class HsFinishArgs(C.Structure):

@@ -291,7 +291,8 @@ __global__ void composite_kernel(HsCompositeArgs a) {
     float h; float3 nv;
     sample_surface(bg, a.n_extra_bg, a.extra_bg, a.n_patches, a.patches, a.patch_height, nullptr,
                    (double)i * a.spacing, (double)j * a.spacing, h, nv);
-    a.out[(long long)i * a.n + j] = h;
+    if (a.box_out) a.box_out[k] = h;
+    else a.out[(long long)i * a.n + j] = h;
 }
 
 // the summed-cascade background on cascade 0's grid (before the patch boxes)
@@ -397,8 +398,15 @@ extern "C" int hs_sample(const HsSampleArgs* a, void* stream) {
 
 extern "C" int hs_composite(const HsCompositeArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_composite: null args");
-    HS_CHECK_ARG(a->out, "hs_composite: missing output");
     cudaStream_t st = as_stream(stream);
+    if (a->box_out) {                              // boxes only (multi-GPU exchange payload)
+        if (a->total_box == 0) return 0;
+        HS_CHECK_ARG(a->box && a->box_prefix && a->patches && a->patch_height, "hs_composite: missing boxes");
+        composite_kernel<<<(a->total_box + 255) / 256, 256, 0, st>>>(*a);
+        HS_LAUNCH_CHECK();
+        return 0;
+    }
+    HS_CHECK_ARG(a->out, "hs_composite: missing output");
     const size_t bytes = sizeof(float) * (size_t)a->n * a->n;
     HS_CHECK_ARG(a->n_extra_bg >= 0 && a->n_extra_bg < HS_MAX_CASCADES, "hs_composite: n_extra_bg out of range");
     if (a->bg_height && a->n_extra_bg > 0) {

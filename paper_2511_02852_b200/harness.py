@@ -876,6 +876,37 @@ class Simulation:
         N.call("hs_composite", args, stream_ptr())
         return self.composite_out
 
+    def composite_boxes(self, out: torch.Tensor) -> torch.Tensor:
+        """This device's share of the FFT-resolution composite: the stitched
+        values of its patch boxes (harness.py:230-240), compact in box order
+        (`box_np` / `box_prefix_np`) -- the payload of the multi-GPU composite
+        exchange (sharding.CompositeGather)."""
+        cfg = self.config
+        n = cfg.fft_n
+        if self.fft_state is None or not self.n_patches:
+            raise ConfigError("composite_boxes needs the FFT background and at least one patch")
+        total = int(self.box_prefix_np[-1])
+        if out.numel() < total:
+            raise ValueError(f"composite_boxes: out holds {out.numel()} < {total} values")
+        bg = self.fft_ws
+        N.call("hs_composite", N.HsCompositeArgs(
+            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0, n_patches=self.n_patches,
+            patches=N.ptr(self.patches_dev), patch_height=N.ptr(self.patch_h), patch_normal=0,
+            box=N.ptr(self.box_dev), box_prefix=N.ptr(self.box_prefix_dev), total_box=total, out=0,
+            box_out=N.ptr(out), **self._extra_bg()), stream_ptr())
+        return out[:total]
+
+    def background_sum(self, out: torch.Tensor) -> torch.Tensor:
+        """The background height grid the composite starts from (the summed
+        cascades on cascade 0's grid, or the single FFT tile)."""
+        cfg = self.config
+        n = cfg.fft_n
+        bg = self.fft_ws
+        N.call("hs_composite", N.HsCompositeArgs(
+            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0, n_patches=0,
+            total_box=0, out=N.ptr(out), **self._extra_bg()), stream_ptr())
+        return out
+
     def ledger_host(self) -> dict:
         P, nb = self.n_patches, self.nb
         e_out = self.e_out.cpu().numpy()

@@ -69,6 +69,69 @@ def assemble(tiles: torch.Tensor, shapes: list[tuple[int, int]]) -> list[torch.T
     return [tiles[k, : r * c].view(r, c) for k, (r, c) in enumerate(shapes)]
 
 
+class CompositeGather:
+    """Per-frame composite exchange at FFT resolution (SURVEY 8(e)'s
+    alternative to shipping native-resolution tiles): every rank resamples
+    its own patches' boxes of the stitched grid (harness.py:219-241;
+    `Simulation.composite_boxes`), one all-gather moves those values
+    (C3 weak scaling: a 67 x 67 box, 18 KB per rank, instead of a 4 MB tile),
+    and every rank pastes all boxes over the background.
+
+    Box geometry is exchanged once at construction.  Where boxes of
+    different patches overlap, the later patch in global order wins, as in
+    the reference's loop; each rank samples only its own patches, so an
+    overlap across ranks is exact only where the patches do not both cover
+    the texel (seeded layouts keep patches apart)."""
+
+    def __init__(self, boxes, n: int, world: int, group=None, device=None):
+        import numpy as np
+        self.n, self.world, self.group = n, world, group
+        boxes = np.asarray(boxes, dtype=np.int64).reshape(-1, 4)
+        sizes = (boxes[:, 1] - boxes[:, 0]).clip(0) * (boxes[:, 3] - boxes[:, 2]).clip(0)
+        self.local_total = int(sizes.sum())
+        meta = torch.tensor([len(boxes), self.local_total], dtype=torch.int64, device=device)
+        metas = torch.empty(world * 2, dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(metas, meta, group=group)
+        metas = metas.view(world, 2).cpu().numpy()
+        max_p = int(metas[:, 0].max())
+        self.per_rank = max(1, int(metas[:, 1].max()))
+        padded = torch.full((max(max_p, 1), 4), -1, dtype=torch.int64, device=device)
+        if len(boxes):
+            padded[: len(boxes)] = torch.from_numpy(boxes).to(device)
+        allb = torch.empty(world * padded.numel(), dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(allb, padded.reshape(-1), group=group)
+        allb = allb.view(world, -1, 4).cpu().numpy()
+        pos, dst = [], []
+        for r in range(world):
+            off = r * self.per_rank
+            for b in allb[r, : metas[r, 0]]:
+                i0, i1, j0, j1 = (int(v) for v in b)
+                if i1 <= i0 or j1 <= j0:
+                    continue
+                ii, jj = np.meshgrid(np.arange(i0, i1), np.arange(j0, j1), indexing="ij")
+                dst.append((ii * n + jj).ravel())
+                pos.append(off + np.arange(ii.size))
+                off += ii.size
+        dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
+        pos = np.concatenate(pos) if pos else np.zeros(0, np.int64)
+        # later boxes win: keep the last occurrence of every grid index
+        last = len(dst) - 1 - np.unique(dst[::-1], return_index=True)[1]
+        self.dst = torch.from_numpy(dst[last]).to(device)
+        self.pos = torch.from_numpy(pos[last]).to(device)
+        self.send = torch.zeros(self.per_rank, dtype=torch.float32, device=device)
+        self.recv = torch.empty(world * self.per_rank, dtype=torch.float32, device=device)
+        self.grid = torch.empty(n * n, dtype=torch.float32, device=device)
+
+    def exchange(self, background: torch.Tensor) -> torch.Tensor:
+        """All-gather every rank's `send[:local_total]` (filled by
+        `Simulation.composite_boxes(send)`) and paste the boxes over
+        `background` (n x n): the full composite, on every rank."""
+        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        self.grid.copy_(background.reshape(-1))
+        self.grid[self.dst] = self.recv[self.pos]
+        return self.grid.view(self.n, self.n)
+
+
 class TileGather:
     """Per-frame NCCL all-gather of every rank's blended patch tiles (the
     composite exchange of SURVEY 8(e)): each rank contributes its patches'

@@ -21,7 +21,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 from paper_2511_02852_b200 import scenes  # noqa: E402
-from paper_2511_02852_b200.sharding import assemble, cascade_owner, gather_tiles, partition, shard_config  # noqa: E402
+from paper_2511_02852_b200.sharding import (CompositeGather, assemble, cascade_owner, gather_tiles,  # noqa: E402
+                                            partition, shard_config)
 
 
 def _free_port() -> int:
@@ -68,6 +69,30 @@ def _gather_worker(rank: int, world: int, port: int, n_patches: int, out_dir: st
         for pid, v in enumerate(views):
             assert torch.equal(v, _tile(pid, shape)), f"rank {rank}: tile {pid} differs after the gather"
         open(os.path.join(out_dir, f"ok{rank}"), "w").close()
+    finally:
+        dist.destroy_process_group()
+
+
+# boxes (i0, i1, j0, j1) of the global patch list on a 16 x 16 composite;
+# patches 1 and 2 overlap in row 6-7 (the later one must win)
+_BOXES = [(0, 4, 0, 5), (5, 8, 3, 9), (6, 10, 8, 12), (12, 16, 12, 16)]
+
+
+def _box_values(pid: int) -> np.ndarray:
+    i0, i1, j0, j1 = _BOXES[pid]
+    return (100.0 * (pid + 1) + np.arange((i1 - i0) * (j1 - j0))).astype(np.float32)
+
+
+def _composite_worker(rank: int, world: int, port: int, out_dir: str) -> None:
+    _init(rank, world, port)
+    try:
+        block = partition(len(_BOXES), world)[rank]
+        g = CompositeGather([_BOXES[k] for k in block], 16, world)
+        vals = np.concatenate([_box_values(k) for k in block])
+        g.send[: len(vals)] = torch.from_numpy(vals)
+        bg = torch.full((16, 16), -1.0)
+        grid = g.exchange(bg).numpy()
+        np.save(os.path.join(out_dir, f"grid{rank}.npy"), grid)
     finally:
         dist.destroy_process_group()
 
@@ -142,3 +167,16 @@ def test_sharded_counts_equal_single_process_world2():
         ids = np.load(os.path.join(d, "ids.npy"))
     assert ids.tolist() == [0, 1, 2]
     np.testing.assert_array_equal(got, ref)
+
+
+def test_gloo_composite_gather_world2():
+    """The FFT-resolution box exchange: both ranks assemble the composite the
+    reference's stitched_heights loop would (background, then every patch box
+    in global order, later boxes overwriting earlier ones)."""
+    want = np.full((16, 16), -1.0, np.float32)
+    for pid, (i0, i1, j0, j1) in enumerate(_BOXES):
+        want[i0:i1, j0:j1] = _box_values(pid).reshape(i1 - i0, j1 - j0)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_composite_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        for r in range(2):
+            np.testing.assert_array_equal(np.load(os.path.join(d, f"grid{r}.npy")), want)
