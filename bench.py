@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--patches", type=int, default=None, help="use the first N patches of a multi-patch scene")
     ap.add_argument("--deterministic", action="store_true", help="device.deterministic (fixed-point sums)")
+    ap.add_argument("--exchange", action="store_true",
+                    help="run the multi-GPU composite exchange even at N=1 (a 1-rank NCCL group): checks "
+                         "and times that path on one GPU")
     return ap.parse_args()
 
 
@@ -212,7 +215,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.exchange:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2511_02852_b200 import Simulation
     from paper_2511_02852_b200 import _native as N
@@ -224,15 +232,22 @@ def main():
         cfg = replace(cfg, deterministic=True).validate()
     sim = Simulation(cfg, device=dev, rng_seed_keys=keys)
     gather = None
-    if world > 1:
+    if world > 1 or args.exchange:
         # the composite exchange at FFT resolution: every rank's
         # patch boxes of the stitched grid, all-gathered and pasted on every rank
         gather = CompositeGather(sim.box_np.reshape(-1, 4), cfg.fft_n, world, device=dev)
-        bg_buf = None if len(sim.cascades) == 1 else torch.empty((cfg.fft_n, cfg.fft_n), device=dev)
 
-    def exchange():
+    def exchange_ops():
         sim.composite_boxes(gather.send)
-        gather.exchange(sim.fft_ws.height if bg_buf is None else sim.background_sum(bg_buf))
+        gather.gather()
+
+    if gather is not None:
+        # the exchange rides at the end of every frame graph (one graph launch per
+        # step: box resample + NCCL all-gather, no host work in between); the full
+        # composite is pasted on demand (gather.assemble), like stitched_heights
+        exchange_ops()                              # NCCL communicator set up outside capture
+        torch.cuda.synchronize()
+        sim.post_frame = exchange_ops
 
     # steady state: the step itself at dt = 0.1
     n_warm = int(round(args.warm_seconds / WARM_DT))
@@ -242,8 +257,6 @@ def main():
     sim.prepare_graphs()
     for _ in range(max(3, args.warmup)):
         sim.step(stats=False)
-        if gather:
-            exchange()
     torch.cuda.synchronize()
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -269,8 +282,6 @@ def main():
         flush_l2()                                 # L2 flush between timed steps (outside the events)
         starts[k].record()
         sim.step(stats=False)
-        if gather:
-            exchange()
         ends[k].record()
     torch.cuda.synchronize()
     if world > 1:
@@ -283,6 +294,10 @@ def main():
                 "max": float(np.max(step_ms))}
     live_after = sim.live_particles()
     sim.check()
+    if gather is not None:                         # the assembled composite of the last frame
+        bg = sim.fft_ws.height if len(sim.cascades) == 1 else \
+            sim.background_sum(torch.empty((cfg.fft_n, cfg.fft_n), device=dev))
+        assert bool(torch.isfinite(gather.assemble(bg)).all())
     live = 0.5 * (live_before + live_after)
     if world > 1:
         t = torch.tensor([total_ms, live], dtype=torch.float64, device=dev)
@@ -404,7 +419,7 @@ def main():
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 

@@ -147,6 +147,9 @@ class Simulation:
         cfg = config.validate()
         self.config = cfg
         self.det = bool(cfg.deterministic)
+        # optional callable enqueued at the end of every frame (captured into the
+        # frame graphs): the multi-GPU composite exchange (bench.py, sharding.py)
+        self.post_frame = None
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         self.params = derive_params(cfg.u10, cfg.fetch, cfg.g, gamma=cfg.gamma, spread_s=cfg.spread_s)
@@ -575,6 +578,9 @@ class Simulation:
         self._bg_n_frame = -1                 # so are the background normals (background)
         if self.fft_state is None and not self.n_patches:
             N.call_raw("hs_advance_frame", N.vp(N.ptr(self.frame_dev)), N.vp(stream_ptr()))
+        if self.post_frame is not None:
+            self.post_frame()
+            mark("post_frame")
 
     def _extra_bg(self) -> dict:
         """n_extra_bg / extra_bg args for cascades 1.. (HsBgTile)."""

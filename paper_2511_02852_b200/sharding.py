@@ -114,22 +114,38 @@ class CompositeGather:
                 off += ii.size
         dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
         pos = np.concatenate(pos) if pos else np.zeros(0, np.int64)
-        # later boxes win: keep the last occurrence of every grid index
-        last = len(dst) - 1 - np.unique(dst[::-1], return_index=True)[1]
-        self.dst = torch.from_numpy(dst[last]).to(device)
-        self.pos = torch.from_numpy(pos[last]).to(device)
+        # per composite texel: the payload slot that covers it (later boxes win,
+        # as in the reference loop), or none -> background
+        src = np.full(n * n, -1, np.int64)
+        last = len(dst) - 1 - np.unique(dst[::-1], return_index=True)[1]   # last occurrence per texel
+        src[dst[last]] = pos[last]
+        self.covered = torch.from_numpy(src >= 0).to(device)
+        self.src = torch.from_numpy(np.maximum(src, 0)).to(device)
         self.send = torch.zeros(self.per_rank, dtype=torch.float32, device=device)
         self.recv = torch.empty(world * self.per_rank, dtype=torch.float32, device=device)
         self.grid = torch.empty(n * n, dtype=torch.float32, device=device)
+        self._picked = torch.empty(n * n, dtype=torch.float32, device=device)
+
+    def gather(self) -> torch.Tensor:
+        """All-gather every rank's `send[:local_total]` (filled by
+        `Simulation.composite_boxes(send)`): afterwards every rank holds every
+        patch box of the stitched grid.  Fixed buffers and no host
+        synchronisation, so it is captured into the frame's CUDA graph
+        (`Simulation.post_frame`)."""
+        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        return self.recv
+
+    def assemble(self, background: torch.Tensor) -> torch.Tensor:
+        """Paste the gathered boxes over `background` (n x n): the full
+        composite (on demand, like the reference's stitched_heights)."""
+        torch.index_select(self.recv, 0, self.src, out=self._picked)
+        torch.where(self.covered, self._picked, background.reshape(-1), out=self.grid)
+        return self.grid.view(self.n, self.n)
 
     def exchange(self, background: torch.Tensor) -> torch.Tensor:
-        """All-gather every rank's `send[:local_total]` (filled by
-        `Simulation.composite_boxes(send)`) and paste the boxes over
-        `background` (n x n): the full composite, on every rank."""
-        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
-        self.grid.copy_(background.reshape(-1))
-        self.grid[self.dst] = self.recv[self.pos]
-        return self.grid.view(self.n, self.n)
+        """gather() + assemble()."""
+        self.gather()
+        return self.assemble(background)
 
 
 class TileGather:
