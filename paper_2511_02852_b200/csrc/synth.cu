@@ -107,8 +107,19 @@ __device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in
     }
 }
 
+#ifdef HS_SMOOTH_TRACE
+__device__ unsigned long long g_strace[4096 * 4];
+__device__ __forceinline__ unsigned long long sgtime() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+#define STRACE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_strace[blockIdx.x * 4 + (k)] = sgtime(); } while (0)
+#else
+#define STRACE(k) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     extern __shared__ float smem[];
+    STRACE(0);
     const int* ti = a.tile_info + 3 * blockIdx.x;
     const HsLayer L = a.layers[ti[0]];
     const int cx0 = ti[1], cy0 = ti[2];
@@ -134,6 +145,7 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
     }
     cp_async_wait_all();
     __syncthreads();
+    STRACE(1);
     in += 1;                                   // staged column 1 = halo column 0
     float* out = a.smooth_layers + L.sm_off;
     const long long ob = (long long)cx0 * L.ncy + cy0;
@@ -146,6 +158,7 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
 #undef HS_SM_CASE
         default: smooth_tile_generic(in, IS, mid, taps, H, W, MS, out, ob, L.ncy, rv, cv);
     }
+    STRACE(2);
 }
 
 // Wide kernels (H > HS_SMOOTH_FUSED_MAX_H): two 1-D passes through `mid`.
@@ -349,6 +362,12 @@ __global__ void sumsq_kernel(const float* __restrict__ x, long long n, double* o
 }  // namespace hs
 
 using namespace hs;
+
+#ifdef HS_SMOOTH_TRACE
+extern "C" HS_API int hs_debug_strace(void* dst) {
+    return (int)cudaMemcpyFromSymbol(dst, hs::g_strace, sizeof(hs::g_strace));
+}
+#endif
 
 extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_smooth: null args");
