@@ -344,6 +344,47 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
     int cnt = 0;
     const long long gb = P.grid_base;
     const int bn = a.bg_n;
+    if (!have_bg && a.blend_mode) {
+        // interior tile (every texel deeper than the margin, or no background):
+        // the blend is the patch itself -- a light loop without the background
+        // state, so the common case carries no spilled registers
+        const bool bg_any = a.bg_height != nullptr;
+        for (int e = tid; e < CT * CT; e += NT) {
+            const int rr = e / CT, cc = e - rr * CT;
+            const int ii = i0 + rr, jj = j0 + cc;
+            if (ii >= P.res || jj >= P.ny) continue;
+            const float h = W.hs[rr + 1][cc + 1];
+            const float hu = ii == P.res - 1 ? h : W.hs[rr + 2][cc + 1];
+            const float hd = ii == 0 ? h : W.hs[rr][cc + 1];
+            const float hr = jj == P.ny - 1 ? h : W.hs[rr + 1][cc + 2];
+            const float hl = jj == 0 ? h : W.hs[rr + 1][cc];
+            const float hx = (hu - hd) * ((ii == 0 || ii == P.res - 1) ? inv_s : inv_2s);
+            const float hy = (hr - hl) * ((jj == 0 || jj == P.ny - 1) ? inv_s : inv_2s);
+            const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
+            const float pnx = -hx * rn, pny = -hy * rn, pnz = rn;
+            const int o = (int)gb + ii * P.ny + jj;
+            if (a.patch_height) a.patch_height[o] = h;
+            if (a.patch_normal) { a.patch_normal[3 * o] = pnx; a.patch_normal[3 * o + 1] = pny; a.patch_normal[3 * o + 2] = pnz; }
+            if (ii >= inset && ii < P.res - inset && jj >= inset && jj < P.ny - inset) {
+                accv = fma((double)h, (double)h, accv);
+                ++cnt;
+            }
+            float hb = h, nx = pnx, ny = pny, nz = pnz;
+            const float d = fminf(W.row_d[rr], W.col_d[cc]);
+            if (!bg_any || d * inv_margin < 1.f) {     // no background at all: blend with the flat sea
+                const float w = d > 0.f ? smoothstep01(d * inv_margin) : 0.f;
+                if (w < 1.f) {
+                    hb = lerpf(0.f, h, w);
+                    const float mx = lerpf(0.f, pnx, w), my = lerpf(0.f, pny, w), mz = lerpf(1.f, pnz, w);
+                    const float r2 = rsqrtf(mx * mx + my * my + mz * mz);
+                    nx = mx * r2; ny = my * r2; nz = mz * r2;
+                    if (d <= 0.f) { hb = 0.f; nx = 0.f; ny = 0.f; nz = 1.f; }
+                }
+            }
+            if (a.blend_height) a.blend_height[o] = hb;
+            if (a.blend_normal) { a.blend_normal[3 * o] = nx; a.blend_normal[3 * o + 1] = ny; a.blend_normal[3 * o + 2] = nz; }
+        }
+    } else
     for (int e = tid; e < CT * CT; e += NT) {
         const int rr = e / CT, cc = e - rr * CT;
         const int ii = i0 + rr, jj = j0 + cc;
