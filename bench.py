@@ -238,13 +238,14 @@ def main():
         gather = CompositeGather(sim.box_np.reshape(-1, 4), cfg.fft_n, world, device=dev)
 
     def exchange_ops():
-        sim.composite_boxes(gather.send)
+        gather.pack(sim.composite_frame)            # this rank's patch boxes of its frame composite
         gather.gather()
+        gather.paste_others(sim.composite_frame)    # the other ranks' boxes into this frame composite
 
     if gather is not None:
-        # the exchange rides at the end of every frame graph (one graph launch per
-        # step: box resample + NCCL all-gather, no host work in between); the full
-        # composite is pasted on demand (gather.assemble), like stitched_heights
+        # the frame's composite (stitched_heights, part of the step) goes through
+        # the exchange: pack + NCCL all-gather + paste at the end of every frame
+        # graph (one graph launch per step, no host work in between)
         exchange_ops()                              # NCCL communicator set up outside capture
         torch.cuda.synchronize()
         sim.post_frame = exchange_ops
@@ -295,9 +296,7 @@ def main():
     live_after = sim.live_particles()
     sim.check()
     if gather is not None:                         # the assembled composite of the last frame
-        bg = sim.fft_ws.height if len(sim.cascades) == 1 else \
-            sim.background_sum(torch.empty((cfg.fft_n, cfg.fft_n), device=dev))
-        assert bool(torch.isfinite(gather.assemble(bg)).all())
+        assert bool(torch.isfinite(sim.composite_frame).all())
     live = 0.5 * (live_before + live_after)
     if world > 1:
         t = torch.tensor([total_ms, live], dtype=torch.float64, device=dev)

@@ -495,6 +495,10 @@ typedef struct {
     HsBgTile extra_bg[HS_MAX_CASCADES - 1];
     int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
                                  int64 fixed point, see hs_fixed_to_float */
+    float* composite;           /* optional [bg_n*bg_n] FFT-resolution composite (stitched_heights,
+                                   harness.py:219-241) that already holds the background: every
+                                   composite node strictly inside a patch is blended in place from
+                                   the tile that covers it (needs bg_height) */
 } HsComposeArgs;
 HS_API int hs_compose(const HsComposeArgs* a, void* stream);
 

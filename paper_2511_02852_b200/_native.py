@@ -153,7 +153,7 @@ class HsComposeArgs(C.Structure):
                 ("patch_height", vp), ("patch_normal", vp), ("blend_height", vp),
                 ("blend_normal", vp), ("blend_mode", i32), ("interior_sumsq", vp),
                 ("interior_count", vp), ("frame_advance", vp), ("n_extra_bg", i32),
-                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("fixed_point", i32)]
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("fixed_point", i32), ("composite", vp)]
 
 
 class HsSampleArgs(C.Structure):

@@ -459,6 +459,38 @@ __global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
             if (a.blend_normal) { a.blend_normal[3 * o] = nx; a.blend_normal[3 * o + 1] = ny; a.blend_normal[3 * o + 2] = nz; }
         }
     }
+    // FFT-resolution composite (stitched_heights, harness.py:219-241): the
+    // composite nodes whose patch-grid row/column falls in this tile, strictly
+    // inside the patch, get w h_patch + (1 - w) h_bg (the patch step of
+    // sample_surface_heights / SurfaceSampler._raw) from the staged tile; the
+    // grid already holds the background (every other node keeps it)
+    if (a.composite && a.bg_height) {
+        const double sp = a.bg_spacing;
+        const int n = a.bg_n;
+        const double xa = P.x0 + (double)i0 * P.texel, xb = P.x0 + (double)(i0 + CT) * P.texel;
+        const double ya = P.y0 + (double)j0 * P.texel, yb = P.y0 + (double)(j0 + CT) * P.texel;
+        const int ga0 = max((int)ceil(xa / sp), 0), ga1 = min((int)ceil(xb / sp), n);
+        const int gb0 = max((int)ceil(ya / sp), 0), gb1 = min((int)ceil(yb / sp), n);
+        const int cols = gb1 - gb0, tot = max(ga1 - ga0, 0) * max(cols, 0);
+        for (int e = tid; e < tot; e += NT) {
+            const int gi = ga0 + e / cols, gj = gb0 + e % cols;
+            const double x = gi * sp, y = gj * sp;
+            const double d = fmin(fmin(x - P.x0, P.x1 - x), fmin(y - P.y0, P.y1 - y));
+            if (!(d > 0.0)) continue;
+            const double t = fmin(fmax(d / P.margin, 0.0), 1.0);
+            const float w = (float)(t * t * (3.0 - 2.0 * t));
+            const double u = fmin(fmax((x - P.x0) / P.texel, 0.0), (double)(P.res - 1));
+            const double v = fmin(fmax((y - P.y0) / P.texel, 0.0), (double)(P.ny - 1));
+            const int i = min(max(min((int)u, P.res - 2), ib), ib + CH - 2);
+            const int j = min(max(min((int)v, P.ny - 2), jb), jb + CH - 2);
+            const float fu = (float)(u - i), fv = (float)(v - j);
+            const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv, w11 = fu * fv;
+            const int r = i - ib, q = j - jb;
+            const float hp = W.hs[r][q] * w00 + W.hs[r + 1][q] * w10 + W.hs[r][q + 1] * w01 + W.hs[r + 1][q + 1] * w11;
+            float* c = a.composite + (long long)gi * n + gj;
+            *c = w * hp + (1.f - w) * *c;
+        }
+    }
     TRACE(6);
     if (a.interior_sumsq) {
         accv = warp_sum(accv);

@@ -147,8 +147,12 @@ class Simulation:
         cfg = config.validate()
         self.config = cfg
         self.det = bool(cfg.deterministic)
-        # optional callable enqueued at the end of every frame (captured into the
-        # frame graphs): the multi-GPU composite exchange (bench.py, sharding.py)
+        # The frame ends with the FFT-resolution composite (stitched_heights,
+        # harness.py:219-241, part of the north_star step) written to
+        # composite_out.  `post_frame`, if set, replaces it: an optional callable
+        # enqueued at the end of every frame (captured into the frame graphs),
+        # e.g. the multi-GPU composite exchange (bench.py, sharding.py).
+        self.composite_each_frame = True
         self.post_frame = None
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
@@ -376,7 +380,13 @@ class Simulation:
         self.box_prefix_np = np.array(pre, np.int32)
         self.box_dev = torch.from_numpy(self.box_np).to(self.device)
         self.box_prefix_dev = torch.from_numpy(self.box_prefix_np).to(self.device)
-        self.composite_out = torch.zeros((n, n), dtype=torch.float32, device=self.device)
+        if not hasattr(self, "composite_out"):
+            self.composite_out = torch.zeros((n, n), dtype=torch.float32, device=self.device)
+        if not hasattr(self, "composite_frame"):
+            # every frame's composite (written inside the captured graphs: the
+            # background copy on the FFT branch, the patch nodes by hs_compose,
+            # which follows tracking patches on the device)
+            self.composite_frame = torch.zeros((n, n), dtype=torch.float32, device=self.device)
 
     def _raw_target(self) -> int:
         """Where the splats accumulate: the float raw layers, or (deterministic
@@ -474,6 +484,7 @@ class Simulation:
             # transform and compose overwrite it (harness.py:155-157)
             N.call("hs_bodies", self._bodies_args(dt), stream_ptr())
         fork = self.fft_state is not None and self.n_patches > 0
+        frame_composite = fork and (self.composite_each_frame or self.post_frame is not None)
         def fft_branch(after):
             side = self._side_stream("fft") if fork else main
             if fork:
@@ -488,6 +499,8 @@ class Simulation:
                     if not self.n_patches and c == len(self.cascades) - 1:
                         fa.frame_advance = N.ptr(self.frame_dev)
                     N.call("hs_fft_evolve", fa, stream_ptr())
+                if frame_composite:             # the composite starts as the background; hs_compose
+                    self._composite(self.composite_frame, (None, None, 0))   # blends the patch nodes in
                 mark("fft")
         if self.fft_state is not None and not fork:
             fft_branch(main)
@@ -571,7 +584,8 @@ class Simulation:
                 patch_height=N.ptr(self.patch_h), patch_normal=0,
                 blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
                 interior_sumsq=N.ptr(stats[1]), interior_count=N.ptr(stats[2]),
-                frame_advance=N.ptr(self.frame_dev), fixed_point=int(self.det), **self._extra_bg()), stream_ptr())
+                frame_advance=N.ptr(self.frame_dev), fixed_point=int(self.det),
+                composite=N.ptr(self.composite_frame) if frame_composite else 0, **self._extra_bg()), stream_ptr())
             mark("compose")
             main.wait_stream(clr)
             self._patch_n_frame = -1          # patch normals are derived lazily (patch_field)
@@ -658,6 +672,8 @@ class Simulation:
                 k += 2 + (1 if self._tracking else 0)      # emit + commit (+ track)
             k += (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
             k += 1 if self.det else 0                 # fixed-point raw layers -> float
+            if self.fft_state is not None and (self.composite_each_frame or self.post_frame is not None):
+                k += 1 if len(self.cascades) > 1 else 0   # composite background (cascade sum; else a copy)
         return max(k, 1.0)
 
     def timed_frame(self) -> dict:
@@ -857,29 +873,36 @@ class Simulation:
         N.call("hs_sample", a, stream_ptr())
         return out_h, out_n
 
+    def _composite(self, out: torch.Tensor, boxes=None) -> None:
+        """Enqueue the FFT-resolution composite into `out` (graph-capturable);
+        boxes = (box, box_prefix, total) device geometry, default the current."""
+        cfg = self.config
+        n = cfg.fft_n
+        bg = self.fft_ws
+        if boxes is None:
+            boxes = (self.box_dev, self.box_prefix_dev, int(self.box_prefix_np[-1])) if self.n_patches else (None, None, 0)
+        N.call("hs_composite", N.HsCompositeArgs(
+            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0,
+            n_patches=self.n_patches, patches=N.ptr(self.patches_dev) if self.n_patches else 0,
+            patch_height=N.ptr(self.patch_h) if self.n_patches else 0, patch_normal=0,
+            box=N.ptr(boxes[0]), box_prefix=N.ptr(boxes[1]), total_box=boxes[2], out=N.ptr(out),
+            **self._extra_bg()), stream_ptr())
+
     def stitched_heights(self) -> torch.Tensor:
-        """FFT-resolution composite with patch boxes resampled (harness.py:219-241)."""
+        """FFT-resolution composite with patch boxes resampled (harness.py:219-241).
+        Every frame already ends with it (composite_out); this re-forms it on
+        demand (tracking patches: with the boxes moved to their current rectangles)."""
         cfg = self.config
         n = cfg.fft_n
         if self.fft_state is None:
             raise ConfigError("stitched_heights needs the FFT background (mode != wp-only)")
         if self.n_sources and self._tracking:
             self._init_boxes()                    # the composited boxes follow the tracking patches
-        bg = self.fft_ws
-        args = N.HsCompositeArgs(
-            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0,
-            n_patches=self.n_patches, patches=N.ptr(self.patches_dev) if self.n_patches else 0,
-            patch_height=N.ptr(self.patch_h) if self.n_patches else 0, patch_normal=0,
-            box=N.ptr(self.box_dev) if self.n_patches else 0,
-            box_prefix=N.ptr(self.box_prefix_dev) if self.n_patches else 0,
-            total_box=int(self.box_prefix_np[-1]), out=N.ptr(self.composite_out if self.n_patches else None),
-            **self._extra_bg())
         if not self.n_patches:
             out = torch.empty((n, n), dtype=torch.float32, device=self.device)
-            args.out = N.ptr(out)
-            N.call("hs_composite", args, stream_ptr())
+            self._composite(out)
             return out
-        N.call("hs_composite", args, stream_ptr())
+        self._composite(self.composite_out)
         return self.composite_out
 
     def composite_boxes(self, out: torch.Tensor) -> torch.Tensor:

@@ -89,6 +89,9 @@ class CompositeGather:
         boxes = np.asarray(boxes, dtype=np.int64).reshape(-1, 4)
         sizes = (boxes[:, 1] - boxes[:, 0]).clip(0) * (boxes[:, 3] - boxes[:, 2]).clip(0)
         self.local_total = int(sizes.sum())
+        loc = [(np.arange(b[0], b[1])[:, None] * n + np.arange(b[2], b[3])[None, :]).ravel()
+               for b in boxes if b[1] > b[0] and b[3] > b[2]]
+        self.local_index = torch.from_numpy(np.concatenate(loc) if loc else np.zeros(0, np.int64)).to(device)
         meta = torch.tensor([len(boxes), self.local_total], dtype=torch.int64, device=device)
         metas = torch.empty(world * 2, dtype=torch.int64, device=device)
         dist.all_gather_into_tensor(metas, meta, group=group)
@@ -101,7 +104,8 @@ class CompositeGather:
         allb = torch.empty(world * padded.numel(), dtype=torch.int64, device=device)
         dist.all_gather_into_tensor(allb, padded.reshape(-1), group=group)
         allb = allb.view(world, -1, 4).cpu().numpy()
-        pos, dst = [], []
+        pos, dst, own = [], [], []
+        me = dist.get_rank(group)
         for r in range(world):
             off = r * self.per_rank
             for b in allb[r, : metas[r, 0]]:
@@ -111,20 +115,33 @@ class CompositeGather:
                 ii, jj = np.meshgrid(np.arange(i0, i1), np.arange(j0, j1), indexing="ij")
                 dst.append((ii * n + jj).ravel())
                 pos.append(off + np.arange(ii.size))
+                own.append(np.full(ii.size, r == me))
                 off += ii.size
         dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
         pos = np.concatenate(pos) if pos else np.zeros(0, np.int64)
+        own = np.concatenate(own) if own else np.zeros(0, bool)
         # per composite texel: the payload slot that covers it (later boxes win,
         # as in the reference loop), or none -> background
         src = np.full(n * n, -1, np.int64)
         last = len(dst) - 1 - np.unique(dst[::-1], return_index=True)[1]   # last occurrence per texel
         src[dst[last]] = pos[last]
+        # the other ranks' winning nodes, for pasting into this rank's own frame composite
+        keep = last[~own[last]]
+        self.other_dst = torch.from_numpy(dst[keep]).to(device)
+        self.other_pos = torch.from_numpy(pos[keep]).to(device)
+        self._other_vals = torch.empty(len(keep), dtype=torch.float32, device=device)
         self.covered = torch.from_numpy(src >= 0).to(device)
         self.src = torch.from_numpy(np.maximum(src, 0)).to(device)
         self.send = torch.zeros(self.per_rank, dtype=torch.float32, device=device)
         self.recv = torch.empty(world * self.per_rank, dtype=torch.float32, device=device)
         self.grid = torch.empty(n * n, dtype=torch.float32, device=device)
         self._picked = torch.empty(n * n, dtype=torch.float32, device=device)
+
+    def pack(self, composite: torch.Tensor) -> None:
+        """Fill `send` with this rank's box nodes of its own frame composite
+        (the grid hs_compose blended its patches into)."""
+        if self.local_total:
+            torch.index_select(composite.reshape(-1), 0, self.local_index, out=self.send[: self.local_total])
 
     def gather(self) -> torch.Tensor:
         """All-gather every rank's `send[:local_total]` (filled by
@@ -141,6 +158,14 @@ class CompositeGather:
         torch.index_select(self.recv, 0, self.src, out=self._picked)
         torch.where(self.covered, self._picked, background.reshape(-1), out=self.grid)
         return self.grid.view(self.n, self.n)
+
+    def paste_others(self, composite: torch.Tensor) -> torch.Tensor:
+        """Paste the other ranks' gathered boxes into this rank's own frame
+        composite (which already holds the background and its own boxes)."""
+        if self.other_dst.numel():
+            torch.index_select(self.recv, 0, self.other_pos, out=self._other_vals)
+            composite.view(-1).index_copy_(0, self.other_dst, self._other_vals)
+        return composite
 
     def exchange(self, background: torch.Tensor) -> torch.Tensor:
         """gather() + assemble()."""

@@ -109,3 +109,21 @@ def test_composite_boxes_are_the_stitched_boxes(cuda):
         grid[i0:i1, j0:j1] = vals[pre[p]:pre[p + 1]].reshape(i1 - i0, j1 - j0)
     np.testing.assert_array_equal(grid, want.cpu().numpy())
     assert boxes.shape[0] == len(cfg.patches) and pre[-1] > 0
+
+
+@pytest.mark.parametrize("scene", ["c2", "c4"])
+def test_frame_composite_equals_stitched_heights(cuda, scene):
+    """Every frame ends with the FFT-resolution composite (the background copy
+    on the FFT branch, the patch nodes blended in by hs_compose from its staged
+    tiles): it equals the on-demand stitched_heights (hs_composite,
+    harness.py:219-241) to fp32 rounding."""
+    from paper_2511_02852_b200 import Simulation, scenes
+    cfg = getattr(scenes, scene)(frames=6)
+    sim = Simulation(cfg, device=cuda)
+    for _ in range(cfg.frames):
+        sim.step(stats=False)
+    got = sim.composite_frame.clone().cpu().numpy()
+    want = sim.stitched_heights().cpu().numpy()
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() <= 1e-6 * scale
+    assert np.mean(got == want) > 0.999

@@ -93,6 +93,12 @@ def _composite_worker(rank: int, world: int, port: int, out_dir: str) -> None:
         bg = torch.full((16, 16), -1.0)
         grid = g.exchange(bg).numpy()
         np.save(os.path.join(out_dir, f"grid{rank}.npy"), grid)
+        # the in-place route: own frame composite (background + own boxes) + others pasted
+        own = torch.full((16, 16), -1.0)
+        for k in block:
+            i0, i1, j0, j1 = _BOXES[k]
+            own[i0:i1, j0:j1] = torch.from_numpy(_box_values(k).reshape(i1 - i0, j1 - j0))
+        np.save(os.path.join(out_dir, f"own{rank}.npy"), g.paste_others(own).numpy())
     finally:
         dist.destroy_process_group()
 
@@ -180,3 +186,4 @@ def test_gloo_composite_gather_world2():
         mp.spawn(_composite_worker, args=(2, _free_port(), d), nprocs=2, join=True)
         for r in range(2):
             np.testing.assert_array_equal(np.load(os.path.join(d, f"grid{r}.npy")), want)
+            np.testing.assert_array_equal(np.load(os.path.join(d, f"own{r}.npy")), want)
