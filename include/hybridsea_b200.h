@@ -569,6 +569,9 @@ HS_API int hs_periodic_normals(const float* height, float* normal, int n, double
 
 /* frame += 1 on the device (end of a captured frame). */
 HS_API int hs_advance_frame(long long* frame, void* stream);
+/* Zero `bytes` bytes at `p` (the consumed raw layers at the end of a frame):
+ * a memset node when captured, cheaper than a fill kernel. */
+HS_API int hs_clear(void* p, long long bytes, void* stream);
 
 #ifdef __cplusplus
 }

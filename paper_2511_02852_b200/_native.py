@@ -196,7 +196,7 @@ EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
            "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies", "hs_init_h0",
-           "hs_init_workspace_bytes", "hs_fixed_to_float"]
+           "hs_init_workspace_bytes", "hs_fixed_to_float", "hs_clear"]
 
 _lib = None
 
@@ -231,6 +231,7 @@ def lib() -> C.CDLL:
     L.hs_advance_frame.argtypes = [vp, vp]
     L.hs_periodic_normals.argtypes = [vp, vp, i32, dbl, vp]
     L.hs_fixed_to_float.argtypes = [vp, vp, i64, i32, vp]
+    L.hs_clear.argtypes = [vp, i64, vp]
     L.hs_init_workspace_bytes.restype = i64
     L.hs_init_workspace_bytes.argtypes = [C.c_int]
     if L.hs_abi_version() != 1:

@@ -483,6 +483,12 @@ namespace hs {
 __global__ void advance_frame_kernel(long long* f) { *f += 1; }
 }  // namespace hs
 
+extern "C" int hs_clear(void* p, long long bytes, void* stream) {
+    HS_CHECK_ARG(bytes >= 0 && (bytes == 0 || p), "hs_clear: bad buffer");
+    if (bytes) HS_CUDA(cudaMemsetAsync(p, 0, (size_t)bytes, as_stream(stream)));
+    return 0;
+}
+
 extern "C" int hs_advance_frame(long long* frame, void* stream) {
     HS_CHECK_ARG(frame != nullptr, "hs_advance_frame: null counter");
     hs::advance_frame_kernel<<<1, 1, 0, as_stream(stream)>>>(frame);

@@ -568,7 +568,8 @@ class Simulation:
             clr = self._side_stream("clear")
             clr.wait_stream(main)
             with torch.cuda.stream(clr):        # raw layers are consumed: clear them for the next splat
-                (self.raw_fixed if self.det else self.synth.raw).zero_()
+                raw = self.raw_fixed if self.det else self.synth.raw
+                N.call_raw("hs_clear", N.vp(N.ptr(raw)), N.i64(raw.numel() * raw.element_size()), N.vp(stream_ptr()))
             if fork:
                 main.wait_stream(self._side_stream("fft"))
                 mark("join")
