@@ -405,7 +405,13 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
     constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
     // transforms per column CTA (B needs 2 CT <= N): 256 threads, so that the
     // 1.5 N column transforms spread evenly over the SMs (all CTAs resident)
-    constexpr int CT = (256 / T) < 1 ? 1 : ((256 / T) < N / 2 ? (256 / T) : N / 2);
+#ifndef HS_FFT_COLS_MIN_CT
+#define HS_FFT_COLS_MIN_CT 4
+#endif
+    // at least HS_FFT_COLS_MIN_CT columns per CTA where the CTA stays <= 512
+    // threads: 4 adjacent float2 columns fill a 32-byte sector per row read
+    constexpr int CT0 = (256 / T) < 1 ? 1 : ((256 / T) < N / 2 ? (256 / T) : N / 2);
+    constexpr int CT = (CT0 < HS_FFT_COLS_MIN_CT && HS_FFT_COLS_MIN_CT * T <= 512) ? HS_FFT_COLS_MIN_CT : CT0;
     const int rows_threads = 3 * T < 32 ? 32 : 3 * T;
     const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2);
     const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
