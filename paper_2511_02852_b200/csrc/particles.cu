@@ -1418,19 +1418,12 @@ extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
     HS_CUDA(cudaMemsetAsync(a->tile_state, 0, sizeof(unsigned long long) * (size_t)a->max_tiles, st));
     HS_CUDA(cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st));
     if (a->splat) HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
-    static int chunks = 0, occ1 = 0, occ4 = 0;
-    if (chunks == 0) {
-        const char* e = getenv("HS_ADVECT_CHUNKS");
-        chunks = (e && atoi(e) == 4) ? 4 : 1;
-        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, advect_kernel<1>, ADV_THREADS, 0));
-        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, advect_kernel<4>, ADV_THREADS, 0));
-        if (occ1 < 1) occ1 = 1;
-        if (occ4 < 1) occ4 = 1;
+    static int occ = 0;
+    if (occ == 0) {
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_kernel<1>, ADV_THREADS, 0));
+        if (occ < 1) occ = 1;
     }
-    const int occ = chunks == 4 ? occ4 : occ1;
-    const int grid = num_sms() * occ;
-    if (chunks == 4) advect_kernel<4><<<grid, ADV_THREADS, 0, st>>>(*a);
-    else advect_kernel<1><<<grid, ADV_THREADS, 0, st>>>(*a);
+    advect_kernel<1><<<num_sms() * occ, ADV_THREADS, 0, st>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }
