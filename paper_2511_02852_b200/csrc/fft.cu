@@ -288,8 +288,19 @@ __device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0,
     }
 }
 
+#ifdef HS_FFT_TRACE
+__device__ unsigned long long g_ftrace[2048 * 8];
+__device__ __forceinline__ unsigned long long fgtime() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+#define FTRACE(k) do { if (threadIdx.x == 0 && blockIdx.x < 2048) g_ftrace[blockIdx.x * 8 + (k)] = fgtime(); } while (0)
+#else
+#define FTRACE(k) do {} while (0)
+#endif
+
 template <int N>
 __global__ void fft_rows_reg_kernel(FftDev d) {
+    FTRACE(0);
     constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
     extern __shared__ float2 sm[];
     float2* tw = sm;            // N
@@ -306,6 +317,7 @@ __global__ void fft_rows_reg_kernel(FftDev d) {
     }
     cp_async_wait_all();
     __syncthreads();
+    FTRACE(1);
     const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame * dt
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
         float2 A0, A1, B0;
@@ -315,15 +327,18 @@ __global__ void fft_rows_reg_kernel(FftDev d) {
         buf[2 * NP + fpad(j)] = B0;
     }
     __syncthreads();
+    FTRACE(2);
     const int f = threadIdx.x / T, tt = threadIdx.x - f * T;
     const bool active = (f == 0) || (f == 1 && !self) || (f == 2 && d.chop_on);
     fft_inplace<N>(buf + (f < 3 ? f : 0) * NP, tw, tt, active && f < 3);
+    FTRACE(3);
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         const int pos = fpad(out_pos<N>(k));
         d.wa[(size_t)i * N + k] = buf[pos];
         if (!self) d.wa[(size_t)ip * N + k] = buf[NP + pos];
         if (d.chop_on) d.wb[(size_t)i * N + k] = buf[2 * NP + pos];
     }
+    FTRACE(4);
 }
 
 // columns: CT transforms per CTA; blocks < n_a_tiles do A (height + i dx),
@@ -433,6 +448,12 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
 }  // namespace hs
 
 using namespace hs;
+
+#ifdef HS_FFT_TRACE
+extern "C" HS_API int hs_debug_ftrace(void* dst) {
+    return (int)cudaMemcpyFromSymbol(dst, hs::g_ftrace, sizeof(hs::g_ftrace));
+}
+#endif
 
 extern "C" int hs_periodic_normals(const float* height, float* normal, int n, double spacing, void* stream) {
     HS_CHECK_ARG(height && normal, "hs_periodic_normals: null buffer");
