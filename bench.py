@@ -162,6 +162,8 @@ def time_cpu_frames(sc, seconds: float, min_frames: int = 2, max_frames: int | N
     live = []
     while True:
         sc.step()
+        if sc.background is not None and sc.patches:
+            sc.composite()                          # the FFT-resolution composite, as the GPU step
         n += 1
         live.append(sum(len(p) for p in sc.pools))
         el = time.perf_counter() - t0
