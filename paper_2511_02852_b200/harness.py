@@ -47,7 +47,7 @@ from .spectrum import DirectionalSpectrum, build_buckets, derive_params, log_buc
 STAGES = ("fft", "inject", "advect", "interact", "synth", "blend", "output")
 ADV_TILE = 1024
 RES_TILE = 1024          # hs_advect_resident tile (slots of one bucket segment)
-RESIDENT_PERIOD = 32    # frames between resident-pool compactions
+RESIDENT_PERIOD = 64    # frames between resident-pool compactions (64 vs 32: -0.6 us/frame at C3)
 
 
 def build_table(cfg: SimConfig, params):
@@ -255,7 +255,8 @@ class Simulation:
                 cap = cfg.pool_capacity
             else:
                 cap = max(4096, int(1.6 * (estimate_population(self.table, r, cfg.trough_fraction) + emit_pop[k])))
-                cap += RESIDENT_PERIOD * int(max_new[-1].sum())
+                cap += (RESIDENT_PERIOD if compact_period is None else max(1, int(compact_period))) \
+                    * int(max_new[-1].sum())
                 cap = -(-cap // 1024) * 1024
             self.pool_caps.append(cap)
             self.stage_caps.append(2 * mg * self.table.n_theta)

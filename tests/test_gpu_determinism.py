@@ -42,13 +42,13 @@ def test_byte_identical_runs(cuda, tmp_path):
 
 
 def test_byte_identical_with_compaction_and_sources(cuda):
-    """Past a resident-pool compaction (K = 32 frames), with wake sources and
+    """Past resident-pool compactions (K = 16 frames), with wake sources and
     their tracking patches: blended tiles, pools' live counts and the ledger."""
     from paper_2511_02852_b200 import Simulation, scenes
     outs = []
     for _ in range(2):
         cfg = scenes.c5(2, frames=40, fft_n=512, deterministic=True)
-        sim = Simulation(cfg, device=cuda)
+        sim = Simulation(cfg, device=cuda, compact_period=16)
         rows = [sim.step() for _ in range(cfg.frames)]
         sim.check()
         outs.append((sim.blend_h.cpu().numpy().tobytes(), sim.patch_h.cpu().numpy().tobytes(),

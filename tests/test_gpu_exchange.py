@@ -29,7 +29,7 @@ def test_composite_exchange_one_rank_nccl(cuda):
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
     try:
         cfg = scenes.c2(frames=40)
-        sim = Simulation(cfg, device=cuda)
+        sim = Simulation(cfg, device=cuda, compact_period=16)
         gather = CompositeGather(sim.box_np.reshape(-1, 4), cfg.fft_n, 1, device=cuda)
 
         def exchange():

@@ -60,10 +60,10 @@ def test_pr1_pool_bit_exact_across_compactions(cuda, K):
 
 
 def test_c2_multi_patch_default_period(cuda):
-    """4 patches, the default compaction period (32): frames 0..69 cross two
+    """4 patches, the default compaction period (64): frames 0..139 cross two
     compactions; per-patch Philox streams keep every patch bit-exact."""
     from paper_2511_02852_b200 import scenes
-    _run_vs_oracle(scenes.c2(frames=70), 70, None, pool_every=23, device=cuda)
+    _run_vs_oracle(scenes.c2(frames=140), 140, None, pool_every=47, device=cuda)
 
 
 def test_high_rate_warmup_dt(cuda):
