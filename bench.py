@@ -184,7 +184,7 @@ def reference_arm(args):
     for _ in range(n_warm):                       # same warm-up as the GPU arm, no synthesis
         sc.step(dt=WARM_DT, synth=False, fft=False)
     warm_s = time.perf_counter() - t_warm
-    n_w = 3                                       # W >= 3 untimed full frames (~1 s each at C3: bounded)
+    n_w = min(max(3, args.warmup), 20)            # W >= 3 untimed full frames (~1 s each at C3: capped at 20)
     for _ in range(n_w):
         sc.step()
     budget = 90.0
