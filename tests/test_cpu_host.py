@@ -194,3 +194,28 @@ def test_device_init_workspace_sizes():
     sizes = [L.hs_init_workspace_bytes(n) for n in (4, 64, 1024, 4096)]
     assert all(b > 0 for b in sizes) and sizes == sorted(sizes)
     assert L.hs_init_workspace_bytes(100) == -1 and L.hs_init_workspace_bytes(8192) == -1
+
+
+def test_abi_rejects_bad_arguments_without_a_device():
+    """Every entry point validates its arguments on the host before touching
+    the device: bad calls return nonzero with a message in hs_last_error()
+    (the ABI's error convention, include/hybridsea_b200.h), here on a CPU-only
+    host."""
+    import ctypes as C
+    from paper_2511_02852_b200 import _native as N
+    L = N.lib()
+
+    def rejected(rc, *words):
+        msg = L.hs_last_error().decode()
+        assert rc != 0, msg
+        assert all(w in msg for w in words), msg
+
+    for name in ("hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat", "hs_smooth", "hs_compose", "hs_sample",
+                 "hs_composite", "hs_finish", "hs_advect_resident", "hs_append_resident", "hs_resident_layout",
+                 "hs_track", "hs_emit", "hs_bodies", "hs_init_h0"):
+        rejected(getattr(L, name)(None, None), name)
+    rejected(L.hs_fft_evolve(C.byref(N.HsFftArgs(n=100)), None), "power of two")
+    rejected(L.hs_init_h0(C.byref(N.HsInitArgs(n=100)), None), "power of two")
+    rejected(L.hs_compose(C.byref(N.HsComposeArgs(nb=0)), None), "nb")
+    rejected(L.hs_clear(None, N.i64(-1), None), "hs_clear")
+    rejected(L.hs_fixed_to_float(None, None, N.i64(16), N.i32(0), None), "hs_fixed_to_float")
