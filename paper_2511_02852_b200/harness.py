@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._layout import (bucket_structs, half_rates, max_groups_per_step, patch_struct, stream_ptr,
+from ._layout import (COMPOSE_TILE, bucket_structs, half_rates, max_groups_per_step, patch_struct, stream_ptr,
                       structs_to_device)
 from .config import SimConfig, cascade_bands
 from .coupling import PatchSurface, SurfaceSampler, validate_patches
@@ -275,6 +275,7 @@ class Simulation:
 
         if self.n_patches:
             self.synth = SynthWorkspace(self.regions, self.res, self.plans, dev)
+            self._order_compose_tiles()
             if self.det:
                 self.raw_fixed = torch.zeros(self.synth.raw.numel(), dtype=torch.int64, device=dev)
             structs = []
@@ -388,6 +389,25 @@ class Simulation:
             # background copy on the FFT branch, the patch nodes by hs_compose,
             # which follows tracking patches on the device)
             self.composite_frame = torch.zeros((n, n), dtype=torch.float32, device=self.device)
+
+    def _order_compose_tiles(self) -> None:
+        """Launch the compose tiles that touch a patch's blend band first: they
+        carry the background work, and in the kernel's single wave the warp
+        schedulers favour the older (lower-index) CTAs, so the heavy tiles no
+        longer finish last.  (Host geometry only; the kernel decides per tile.)"""
+        info = self.synth.compose_info_np
+        T = COMPOSE_TILE
+        band = np.zeros(len(info), bool)
+        for k, (p, i0, j0) in enumerate(info):
+            r = self.regions[p]
+            res, ny = self.synth.grids[p]
+            texel = r.l1 / (res - 1)
+            rl, cl = min(T, res - i0) - 1, min(T, ny - j0) - 1
+            d = min(min(i0, res - 1 - (i0 + rl)), min(j0, ny - 1 - (j0 + cl))) * texel
+            band[k] = d < r.margin + texel
+        order = np.concatenate([np.nonzero(band)[0], np.nonzero(~band)[0]])
+        self.synth.compose_info_np = np.ascontiguousarray(info[order])
+        self.synth.compose_info = torch.from_numpy(self.synth.compose_info_np).to(self.device)
 
     def _raw_target(self) -> int:
         """Where the splats accumulate: the float raw layers, or (deterministic
