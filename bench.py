@@ -403,7 +403,10 @@ def main():
                        "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
                        "warm_start": f"{n_warm} frames at dt={WARM_DT}", "l2": "flushed between timed steps (256 MiB written, then read back)",
                        "parallelism": (f"patch-sharded x{world}" if world > 1 else "single GPU"),
-                       "deterministic": bool(cfg.deterministic)},
+                       "deterministic": bool(cfg.deterministic),
+                       "step": "FFT background + boundary injection + resident advect/cull/splat + per-bucket "
+                               "smoothing + upsample-sum/normals/blend at the patch nodes + FFT-resolution "
+                               "composite (one CUDA graph); pool compaction every %d frames" % sim.compact_period},
             "step_ms_percentiles": step_pct,
             "gpu_launches": (sim.kernel_launches_per_frame() + (1 if gather else 0)) * args.steps,
             "stages_ms": stage,
