@@ -85,7 +85,11 @@ def scene_config(name: str, rank: int, world: int, patches: int | None = None):
         if world > 1:
             p0 = cfg.patches[0]
             org = scenes.seeded_layout(world, p0.size[0], cfg.fft_domain, seed=cfg.seed + 100)
-            cfg = replace(cfg, patches=(replace(p0, origin=org[rank]),), seed=cfg.seed + rank).validate()
+            # one coherent scene: every rank keeps cfg.seed (the replicated
+            # background is identical everywhere) and its patch draws its own
+            # Philox stream, key (seed, rank) -- the patch's global id
+            cfg = replace(cfg, patches=(replace(p0, origin=org[rank]),)).validate()
+            return cfg, [(cfg.seed, rank)], "weak"
         return cfg, None, "weak"
     local, _, keys = shard_config(cfg, rank, world)
     return local.validate(), keys, "strong"

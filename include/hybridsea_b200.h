@@ -378,6 +378,9 @@ typedef struct {
     int n_patches;
     const HsPatch* patches;
     const float* patch_height;
+    const long long* frame;   /* optional device frame counter: if set, the surface is flat
+                                 while *frame == 0 (read on the device, so a captured graph
+                                 replayed from frame 0 on still sees the live value) */
 } HsBodyArgs;
 HS_API int hs_bodies(const HsBodyArgs* a, void* stream);
 

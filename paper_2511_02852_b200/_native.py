@@ -116,7 +116,7 @@ class HsBodyArgs(C.Structure):
     _fields_ = [("n_bodies", i32), ("bodies", vp), ("dt", dbl), ("rho", dbl), ("g", dbl), ("flat", i32),
                 ("bg_height", vp), ("bg_n", i32), ("bg_spacing", dbl), ("n_extra_bg", i32),
                 ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("n_patches", i32), ("patches", vp),
-                ("patch_height", vp)]
+                ("patch_height", vp), ("frame", vp)]
 
 
 class HsEmitArgs(C.Structure):

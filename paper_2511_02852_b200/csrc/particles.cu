@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
                         a.res.pool.x[o] = keep ? nx : __longlong_as_double(0x7ff8000000000000LL);
                         a.res.pool.y[o] = ny; a.res.pool.ux[o] = dx; a.res.pool.uy[o] = dy; a.res.pool.amp[o] = am;
                     }
-                    if (keep) {
+                    if (keep && j < ap_room[b]) {        // overflowed members are lost (status bit)
                         atomicAdd(&ap_kept[b], 1);
                         int cl = 0;
                         splat_at(a.res.fixed_point, a.res.raw_layers, ap_sl[b], P.sx0, P.sy0, nx, ny, am, &cl);
@@ -346,7 +346,9 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         __syncthreads();
         for (int b = threadIdx.x; b < nb; b += blockDim.x) {
             const int s = p * nb + b, n = per_live * live_cnt[b];
-            a.res.len_out[s] = a.res.len_in[s] + n;
+            // an overflowing segment keeps only the members that fit: its length
+            // never runs past seg_cap into the next bucket's segment
+            a.res.len_out[s] = a.res.len_in[s] + min(n, ap_room[b]);
             if (n > ap_room[b]) atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             if (ap_kept[b]) atomicAdd(&a.res.live[s], ap_kept[b]);
             energy_flush(&a.res.e_out[s], ap_eout[b], a.res.fixed_point);
@@ -995,7 +997,7 @@ __global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResident
         if (lane < nb) {
             soff[lane] = inc - c;
             const int len = a.len_in[s];
-            a.len_out[s] = len + c;
+            a.len_out[s] = len + min(c, a.seg_cap[s] - len);      // clamped on overflow (status bit)
             dst_s[lane] = (long long)a.seg_base[s] + len;
             room_s[lane] = a.seg_cap[s] - len;
             kept_s[lane] = 0;
@@ -1030,7 +1032,7 @@ __global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResident
             a.pool.x[o] = keep ? nx : __longlong_as_double(0x7ff8000000000000LL);
             a.pool.y[o] = ny; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = am;
         }
-        if (keep) {
+        if (keep && j < room_s[b]) {
             atomicAdd(&kept_s[b], 1);
             splat_at(a.fixed_point, a.raw_layers, sl_s[b], P.sx0, P.sy0, nx, ny, am, &clamp_local);
         } else if (am > 0.f) {
@@ -1196,7 +1198,8 @@ __global__ void __launch_bounds__(128) bodies_kernel(HsBodyArgs a) {
         wx = dsub(dadd(B.pos[0], dmul(c, o[0])), dmul(sn, o[1]));     // interaction.py:72-76
         wy = dadd(dadd(B.pos[1], dmul(sn, o[0])), dmul(c, o[1]));
         wz = dadd(B.pos[2], o[2]);
-        if (!a.flat) {
+        const bool flat = a.frame ? (*a.frame == 0) : (a.flat != 0);
+        if (!flat) {
             float h; float3 n;
             sample_surface_heights(a.bg_height, a.bg_n, a.bg_spacing, a.n_extra_bg, a.extra_bg, a.n_patches,
                                    a.patches, a.patch_height, wx, wy, h, n);

@@ -295,8 +295,12 @@ class Simulation:
                 self.bodies_dev = structs_to_device(self._body_init, dev) if self.n_bodies else None
             f64 = lambda n: torch.zeros(max(1, n), dtype=torch.float64, device=dev)  # noqa: E731
             f32 = lambda n: torch.zeros(max(1, n), dtype=torch.float32, device=dev)  # noqa: E731
-            self.pools = [[f64(total_pool), f64(total_pool), f64(total_pool), f64(total_pool), f32(total_pool)]
-                          for _ in range(2)]
+            # one tile of padding: hs_advect_resident issues a tile's slot loads
+            # before it knows the segment length, so the last tile of the last
+            # segment may read up to RES_TILE - 1 slots past pool_base[-1]
+            # (explicit capacities are not rounded to the tile)
+            padded = total_pool + RES_TILE
+            self.pools = [[f64(padded), f64(padded), f64(padded), f64(padded), f32(padded)] for _ in range(2)]
             PB = self.n_patches * self.nb
             i32 = lambda n: torch.zeros(max(1, n), dtype=torch.int32, device=dev)  # noqa: E731
             # resident segment table (hs_resident_layout)
@@ -457,7 +461,7 @@ class Simulation:
         cfg = self.config
         bg = self.fft_ws
         a = N.HsBodyArgs(n_bodies=self.n_bodies, bodies=N.ptr(self.bodies_dev), dt=float(dt), rho=float(cfg.rho),
-                         g=float(cfg.g), flat=1 if self.frame == 0 else 0,
+                         g=float(cfg.g), flat=0, frame=N.ptr(self.frame_dev),
                          bg_height=N.ptr(bg.height) if bg is not None else 0,
                          bg_n=cfg.fft_n if bg is not None else 0,
                          bg_spacing=self.fft_state.spacing if bg is not None else 1.0,
@@ -957,6 +961,13 @@ class Simulation:
             n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0, n_patches=0,
             total_box=0, out=N.ptr(out), **self._extra_bg()), stream_ptr())
         return out
+
+    def source_positions(self) -> np.ndarray:
+        """(n_bodies + n_sources, 2) emitter positions after the last frame
+        (bodies first, then kinematic sources; synchronises)."""
+        if not self.n_sources:
+            return np.zeros((0, 2))
+        return self.src_pos[self._lp].cpu().numpy().reshape(-1, 2).copy()
 
     def ledger_host(self) -> dict:
         P, nb = self.n_patches, self.nb

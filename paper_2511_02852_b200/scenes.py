@@ -8,14 +8,16 @@ patch layouts.
   PR1  256^2 / 1000 m, U10 10, F 100 km, gamma 3.3, s 8; one 64 m patch on a
        256 grid; 8 log buckets 0.5-4 rad/s; n_theta 16; dt 1/60, 120 frames
   C2   512^2 / 2000 m, U10 15, s 10; 4 x 128 m patches on 512 grids (seeded
-       layout); 12 equal-energy buckets; n_theta 4; 300 frames; one point wake
+       layout); 12 equal-energy buckets; n_theta 8 (~62k live at steady
+       state, BASELINE's ~65k); 300 frames; one point wake
        source per patch moving straight at 8 m/s on a seeded heading, 256
        particles per frame (128-direction Kelvin fan + troughs)
   C3   1024^2 / 4000 m, lambda 1.2; one 256 m patch on a 1024 grid; 16 log
        buckets 0.3-6 rad/s; n_theta 2 (~0.86M live at steady state)
   C4   3 summed 512^2 cascades over 4000 / 1000 / 250 m with disjoint |k|
        bands (FFT band widened to 6 rad/s), U10 20, gamma 5, s 4; 8 x 128 m
-       patches on 512 grids; 16 buckets
+       patches on 512 grids; 16 log buckets 0.3-6 rad/s (the range is
+       unspecified; C3's), n_theta 5 (~4.3M live, BASELINE's ~4M)
   C5   2048^2 / 8000 m; 64 x 192 m patches on 768 grids; 16 buckets;
        n_theta 16; one ship per patch on a seeded heading at 5-15 m/s, 1024
        Kelvin-wedge particles per frame, the patch tracking its ship
@@ -71,7 +73,7 @@ def wake_sources(origins, size: float, speeds, count: int, hull: float, seed: in
 def c2(**kw) -> SimConfig:
     org = seeded_layout(4, 128.0, 2000.0, seed=2)
     src = wake_sources(org, 128.0, [8.0] * 4, count=128, hull=1.0, seed=22, start_back=20.0)
-    cfg = SimConfig(u10=15.0, fetch=100000.0, spread_s=10.0, n_omega=12, n_theta=4, dt=1.0 / 60.0, frames=300,
+    cfg = SimConfig(u10=15.0, fetch=100000.0, spread_s=10.0, n_omega=12, n_theta=8, dt=1.0 / 60.0, frames=300,
                     seed=2, fft_n=512, fft_domain=2000.0, fft_choppiness=1.0,
                     patches=tuple(PatchConfig(origin=o, size=(128.0, 128.0), res=512, margin=10.0) for o in org),
                     sources=src, write_frames=False)
@@ -91,8 +93,8 @@ def c4(**kw) -> SimConfig:
     """3 summed cascades 4000 / 1000 / 250 m (disjoint |k| bands, config.cascade_bands)
     over a band widened to 6 rad/s so every tile carries energy."""
     org = seeded_layout(8, 128.0, 4000.0, seed=4)
-    cfg = SimConfig(u10=20.0, fetch=100000.0, gamma=5.0, spread_s=4.0, n_omega=16, n_theta=16, dt=1.0 / 60.0,
-                    frames=600, seed=4, fft_n=512, fft_domain=4000.0, fft_choppiness=1.0,
+    cfg = SimConfig(u10=20.0, fetch=100000.0, gamma=5.0, spread_s=4.0, n_omega=16, n_theta=5,
+                    bucket_spacing="log", omega_lo=0.3, omega_hi=6.0, dt=1.0 / 60.0, frames=600, seed=4, fft_n=512, fft_domain=4000.0, fft_choppiness=1.0,
                     fft_cascades=(4000.0, 1000.0, 250.0), fft_band_hi=6.0,
                     patches=tuple(PatchConfig(origin=o, size=(128.0, 128.0), res=512, margin=10.0) for o in org),
                     write_frames=False)
