@@ -154,6 +154,9 @@ class Simulation:
         # e.g. the multi-GPU composite exchange (bench.py, sharding.py).
         self.composite_each_frame = True
         self.post_frame = None
+        # frame schedule knobs (tools/ab_sched.py): FFT branch fork point, stream priorities
+        self.fft_fork_at_start = False
+        self.sched_priorities = False
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         self.params = derive_params(cfg.u10, cfg.fetch, cfg.g, gamma=cfg.gamma, spread_s=cfg.spread_s)
@@ -575,7 +578,7 @@ class Simulation:
                     N.call("hs_inject", inj_args, stream_ptr())
                     mark("inject")
                 if fork:                            # FFT branch forks after the 1-CTA-per-patch inject:
-                    fft_branch(inj)                 # the resident advect fills the SMs first
+                    fft_branch(main if self.fft_fork_at_start else inj)   # the resident advect fills the SMs first
                 with torch.cuda.stream(inj):
                     if self.n_sources:
                         N.call("hs_emit", self._emit_args(buf, lp, dt, stats), stream_ptr())
@@ -651,12 +654,22 @@ class Simulation:
         else:
             self._since += 1
 
+    # stream priorities of the frame's branches (lower = more urgent): the
+    # particle / synthesis chain is the critical path, the FFT fills idle SMs
+    # (tools/ab_sched.py: no measurable effect at C3, off by default)
+    STREAM_PRIORITY = {"fft": 0}
+    CRITICAL_PRIORITY = -5
+
     def _side_stream(self, name: str = "fft"):
         if not hasattr(self, "_sides"):
             self._sides = {}
         if name not in self._sides:
-            self._sides[name] = torch.cuda.Stream(device=self.device)
+            prio = self.STREAM_PRIORITY.get(name, self.CRITICAL_PRIORITY) if self.sched_priorities else 0
+            self._sides[name] = torch.cuda.Stream(device=self.device, priority=prio)
         return self._sides[name]
+
+    def _capture_stream(self):
+        return torch.cuda.Stream(device=self.device, priority=self.CRITICAL_PRIORITY if self.sched_priorities else 0)
 
     def _graph(self, state: tuple):
         g = self._graphs.get(state)
@@ -664,7 +677,7 @@ class Simulation:
             if self.n_patches:
                 self._hr(self.config.dt)        # host->device uploads must precede capture
             g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream(device=self.device)
+            s = self._capture_stream()
             s.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.graph(g, stream=s):
                 self._enqueue_frame(state, self.config.dt)
@@ -723,7 +736,7 @@ class Simulation:
                 e.record(strm)
                 evs.append((name, e, strm.cuda_stream))
             g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream(device=self.device)
+            s = self._capture_stream()
             s.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.graph(g, stream=s):
                 self._enqueue_frame(state, self.config.dt, mark)
