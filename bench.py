@@ -3,36 +3,40 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
 One "step" = one frame of the hybrid step over the configured scene
-(SURVEY 8(d)): FFT background (rotation + IFFT2 + normals), boundary
-injection, advect + cull + compaction + splat, per-bucket smoothing, gain-sum
-+ normals + smoothstep blend at the patch nodes.  Default workload: C3
-(1024^2 FFT / 4000 m, lambda 1.2, one 256 m patch on a 1024^2 grid, 16 log
-buckets 0.3-6 rad/s, n_theta 2), warmed to steady state (~0.86M live
-particles) by running the step itself at dt = 0.1 for 200 s of simulated
+(SURVEY 8(d)): FFT background (rotation + IFFT2), boundary injection,
+advect + cull + compaction + splat, per-bucket smoothing, gain-sum + normals
++ smoothstep blend at the patch nodes, and the FFT-resolution composite
+(reference `Simulation.step` + `stitched_heights`, harness.py:131-241).
+Workload at N = 1: C3 (1024^2 FFT over 4000 m, lambda 1.2; one 256 m patch on
+a 1024^2 grid; 16 log buckets 0.3-6 rad/s, n_theta 2), warmed to steady state
+(~0.86M live particles) by the step itself at dt = 0.1 for 200 s of simulated
 time, then timed at dt = 1/60.  Synthetic seeded inputs (no dataset exists).
 
 metric: particles splatted per second (live particles x frames/s, whole job);
-fps and ms/frame are reported beside it.  L2 is flushed (256 MiB written,
-then read back)
+fps and ms/frame beside it.  L2 is flushed (256 MiB written, then read back)
 between timed steps; steps are timed with CUDA events on the launching
 stream, max over ranks.
 
---impl reference times the CPU oracle port of the reference algorithm
-(oracle/, numpy, the reference's own single-threaded numpy path) on the host
-cores, on the same config, as a bounded sample.
+Multi-GPU (one process per GPU; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run): the default workload becomes C4 --
+strong scaling of its 8 patches over the N ranks (contiguous blocks, global
+Philox keys), its 3 FFT cascades round-robin (sharding.CascadeShard, one
+all-gather of their heights per frame) -- and every frame ends with the
+composite exchange (sharding.BoxExchange: hs_box_pack, one in-place NCCL
+all-gather, hs_box_paste), all inside the frame's CUDA graph.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank owns
-one C3-geometry patch (seeded layout in the shared 4000 m tile, own Philox
-stream), runs the replicated background, and every frame the composite is
-exchanged at FFT resolution: each rank resamples its patch boxes of the
-stitched grid, one NCCL all-gather moves them, every rank pastes them over the
-background (sharding.CompositeGather).
+--impl reference times the reference's own CPU implementation: the
+unmodified reference package (baseline/_ref, pip-installed from
+/root/reference) driven through its Simulation.step + stitched_heights on the
+same scene (baseline/refchain.py), where the reference can express the scene
+(C3); otherwise the numpy oracle port of the reference algorithm (oracle/).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -45,33 +49,58 @@ sys.path.insert(0, ROOT)
 WARM_DT = 0.1
 WARM_SECONDS = 200.0
 
+# SURVEY 8(d) / DESIGN section 6: algorithmic HBM bytes per unit of each stage
+BYTES_PER_UNIT = {
+    "fft": (20.0, "FFT bin per cascade: h0 c64 read + height, dx, dy fp32 written"),
+    "inject": (36.0, "new particle: x, y, ux, uy fp64 + amp fp32 written"),
+    "advect": (52.0, "live particle: x, y, ux, uy fp64 + amp fp32 read, x, y fp64 written"),
+    "smooth": (8.0, "layer texel: raw read + smoothed written (L2-resident intermediates)"),
+    "compose": (20.0, "patch texel: patch height, blended height, blended normal fp32 written"),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default=None, help="scene preset (default: C3 at N = 1, C4 at N > 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--warm-seconds", type=float, default=WARM_SECONDS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--stage-frames", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--patches", type=int, default=None, help="use the first N patches of a multi-patch scene")
     ap.add_argument("--deterministic", action="store_true", help="device.deterministic (fixed-point sums)")
     ap.add_argument("--exchange", action="store_true",
-                    help="run the multi-GPU composite exchange even at N=1 (a 1-rank NCCL group): checks "
-                         "and times that path on one GPU")
-    return ap.parse_args()
+                    help="run the multi-GPU composite exchange even at N=1 (a 1-rank NCCL group)")
+    args = ap.parse_args()
+    if args.config is None:
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        args.config = "C4" if world > 1 else "C3"
+    return args
+
+
+def relaunch_distributed(args) -> int:
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run
+    with N processes (one per GPU, NCCL); rank 0's JSON line is this process's."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def scene_config(name: str, rank: int, world: int, patches: int | None = None):
-    """(config of this rank, Philox keys or None, scaling).  Single-patch
-    scenes (C3, PR1) scale weakly: rank r owns patch r of a seeded layout of
-    `world` same-size patches.  Multi-patch scenes (C2, C4, C5) scale
-    strongly: the scene's patches are split into contiguous blocks
-    (sharding.shard_config), each patch keeping its global Philox key."""
+    """(config of this rank, Philox keys or None, scaling, whole scene).
+    Single-patch scenes (C3, PR1) scale weakly: rank r owns patch r of a
+    seeded layout of `world` same-size patches in one coherent scene (same
+    seed, so the same background everywhere; patch r draws the Philox stream
+    (seed, r)).  Multi-patch scenes (C2, C4, C5) scale strongly: the scene's
+    patches are split into contiguous blocks (sharding.shard_config), each
+    patch keeping its global Philox key."""
     from dataclasses import replace
     from paper_2511_02852_b200 import scenes
     from paper_2511_02852_b200.sharding import shard_config
@@ -85,14 +114,12 @@ def scene_config(name: str, rank: int, world: int, patches: int | None = None):
         if world > 1:
             p0 = cfg.patches[0]
             org = scenes.seeded_layout(world, p0.size[0], cfg.fft_domain, seed=cfg.seed + 100)
-            # one coherent scene: every rank keeps cfg.seed (the replicated
-            # background is identical everywhere) and its patch draws its own
-            # Philox stream, key (seed, rank) -- the patch's global id
-            cfg = replace(cfg, patches=(replace(p0, origin=org[rank]),)).validate()
-            return cfg, [(cfg.seed, rank)], "weak"
-        return cfg, None, "weak"
+            full = replace(cfg, patches=tuple(replace(p0, origin=o) for o in org)).validate()
+            local, _, keys = shard_config(full, rank, world)
+            return local.validate(), keys, "weak", full
+        return cfg, None, "weak", cfg
     local, _, keys = shard_config(cfg, rank, world)
-    return local.validate(), keys, "strong"
+    return local.validate(), keys, "strong", cfg
 
 
 # ------------------------------------------------------------ clocks ----
@@ -135,33 +162,31 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ---------------------------------------------------------- reference ---
-def cpu_scene_from(sim, cfg):
-    """Build the CPU oracle scene in the GPU simulation's current state
-    (pools in bucket-segment order, ledgers, Philox stream positions)."""
-    from oracle import particles_ref, scene_ref
-    sc = scene_ref.OracleScene(cfg.scene_dict(), h0=sim.fft_state.h0 if sim.fft_state is not None else None)
-    sc.frame = sim.frame
-    led = sim.ledger_host()
-    rng_words = sim.rng.cpu().numpy().view(np.uint64)
-    for k in range(sim.n_patches):
-        ps = sim.pool(k)
-        pos, d, a = ps.positions, ps.directions, ps.amplitudes
-        sc.pools[k] = particles_ref.Pool(pos, d, a, ps.buckets.astype(np.int32), np.zeros(len(a)))
-        sc.ledgers[k].acc = led["acc"][k].copy()
-        sc.ledgers[k].groups = led["groups"][k].copy()
-        sc.ledgers[k].e_in = led["e_in"][k].copy()
-        sc.ledgers[k].e_out = led["e_out"][k].copy()
-        w = rng_words[8 * k: 8 * k + 8]
-        c0 = sum(int(w[2 + i]) << (64 * i) for i in range(4))
-        d_idx = int(w[6])
-        gen = np.random.Generator(np.random.Philox(key=[int(w[0]), int(w[1])], counter=(c0 + d_idx // 4) % (1 << 256)))
-        gen.bit_generator.random_raw(d_idx % 4)
-        sc.rngs[k] = gen
-    return sc
+# ------------------------------------------------------------- CPU legs --
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
-def time_cpu_frames(sc, seconds: float, min_frames: int = 2, max_frames: int | None = None):
+def time_reference_frames(sim, seconds: float, min_frames: int = 2, max_frames: int | None = None):
+    """Mean s/frame of the reference's Simulation.step + stitched_heights
+    (baseline/refchain.frame) over a bounded sample."""
+    from baseline import refchain
+    n, t0 = 0, time.perf_counter()
+    live = []
+    while True:
+        refchain.frame(sim)
+        n += 1
+        live.append(sum(len(ps.pool) for ps in sim.patches))
+        el = time.perf_counter() - t0
+        if (el >= seconds and n >= min_frames) or (max_frames is not None and n >= max_frames):
+            break
+    return el / n, float(np.mean(live)), n
+
+
+def time_port_frames(sc, seconds: float, min_frames: int = 2, max_frames: int | None = None):
     n, t0 = 0, time.perf_counter()
     live = []
     while True:
@@ -176,36 +201,123 @@ def time_cpu_frames(sc, seconds: float, min_frames: int = 2, max_frames: int | N
     return el / n, float(np.mean(live)), n
 
 
+def cpu_baselines(sim, cfg, seconds: float, name: str) -> dict:
+    """The reference (where it can express the scene) and the oracle port,
+    both started from the GPU's steady state (cloned pools, ledgers, Philox
+    positions), on one host core each."""
+    from baseline import refchain
+    from oracle.clone import oracle_from_sim
+    out = {}
+    cores = host_cores()
+    why = refchain.expressible(cfg) if refchain.load() is not None else "reference not installed in baseline/_ref"
+    if why is None:
+        rsim = refchain.build(cfg)
+        led = sim.ledger_host()
+        pools = []
+        for k in range(sim.n_patches):
+            ps = sim.pool(k)
+            pools.append((ps.positions, ps.directions, ps.amplitudes, ps.buckets))
+        ledgers = [{q: led[q][k] for q in ("acc", "groups", "e_in", "e_out")} for k in range(sim.n_patches)]
+        refchain.load_state(rsim, pools, ledgers, sim.rng.cpu().numpy()[0:8], sim.frame)
+        frame_s, live, n = time_reference_frames(rsim, seconds * 0.6)
+        out["reference"] = {"value": live / frame_s, "unit": "particles/s", "cores": 1, "host_cores": cores,
+                            "kind": "reference", "ms_per_frame": frame_s * 1e3,
+                            "sample": f"{n} {name} frames of the unmodified reference package (baseline/_ref: "
+                                      f"Simulation.step + stitched_heights) from the GPU's steady state "
+                                      f"({live:.0f} live particles); numpy single-threaded: 1 of {cores} host cores"}
+    sc = oracle_from_sim(sim, cfg)
+    frame_s, live, n = time_port_frames(sc, seconds * (0.4 if why is None else 1.0))
+    out["port"] = {"value": live / frame_s, "unit": "particles/s", "cores": 1, "host_cores": cores, "kind": "port",
+                   "ms_per_frame": frame_s * 1e3,
+                   "sample": f"{n} {name} frames of the numpy oracle port (oracle/) from the GPU's steady state "
+                             f"({live:.0f} live particles); 1 of {cores} host cores"
+                             + ("" if why is None else f"; reference not run: {why}")}
+    return out
+
+
 def reference_arm(args):
+    """`--impl reference`: the reference's own CPU implementation of the step
+    on this arm's workload (rank 0 only), a bounded sample of frames."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import scene_ref
-    cfg, _, _ = scene_config(args.config, 0, 1, args.patches)
-    sc = scene_ref.OracleScene(cfg.scene_dict())
-    t_warm = time.perf_counter()
+    from baseline import refchain
+    cfg = scene_config(args.config, 0, 1, args.patches)[0]
     n_warm = int(round(args.warm_seconds / WARM_DT))
-    for _ in range(n_warm):                       # same warm-up as the GPU arm, no synthesis
-        sc.step(dt=WARM_DT, synth=False, fft=False)
-    warm_s = time.perf_counter() - t_warm
     n_w = min(max(3, args.warmup), 20)            # W >= 3 untimed full frames (~1 s each at C3: capped at 20)
-    for _ in range(n_w):
-        sc.step()
     budget = 90.0
-    frame_s, live, n = time_cpu_frames(sc, seconds=budget, min_frames=1, max_frames=max(1, args.steps))
+    why = refchain.expressible(cfg) if refchain.load() is not None else "reference not installed in baseline/_ref"
+    t_warm = time.perf_counter()
+    if why is None:
+        sim = refchain.build(cfg)
+        refchain.warm(sim, n_warm, WARM_DT)       # the reference's own inject + advect at dt = 0.1
+        warm_s = time.perf_counter() - t_warm
+        for _ in range(n_w):
+            refchain.frame(sim)
+        frame_s, live, n = time_reference_frames(sim, budget, min_frames=1, max_frames=max(1, args.steps))
+        kind = "reference"
+        what = "the unmodified reference package (baseline/_ref): Simulation.step + stitched_heights"
+    else:
+        from oracle import scene_ref
+        sc = scene_ref.OracleScene(cfg.scene_dict())
+        for _ in range(n_warm):                   # same warm-up as the GPU arm, no synthesis
+            sc.step(dt=WARM_DT, synth=False, fft=False)
+        warm_s = time.perf_counter() - t_warm
+        for _ in range(n_w):
+            sc.step()
+        frame_s, live, n = time_port_frames(sc, budget, min_frames=1, max_frames=max(1, args.steps))
+        kind = "port"
+        what = f"the numpy oracle port of the reference algorithm (reference not run: {why})"
     pps = live / frame_s
+    cores = host_cores()
     line = {"impl": "reference", "metric": "particles splatted/s (hybrid step)", "value": pps,
             "unit": "particles/s", "n_gpus": args.gpus, "steps": n, "warmup": n_w,
             "ms_per_step": frame_s * 1e3, "fps": 1.0 / frame_s, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, steady state via the step itself)",
             "config": {"workload": f"{args.config} hybrid step", "live_particles": live, "fft_n": cfg.fft_n,
                        "patch_res": cfg.patches[0].res, "n_omega": cfg.n_omega, "n_theta": cfg.n_theta},
-            "cpu_baseline": {"value": pps, "unit": "particles/s", "cores": 1, "kind": "port",
-                             "sample": f"{n} full {args.config} frames after {n_warm} warm-up frames "
-                                       f"(warm-up {warm_s:.1f}s); numpy single-threaded"},
+            "cpu_baseline": {"value": pps, "unit": "particles/s", "cores": 1, "host_cores": cores, "kind": kind,
+                             "sample": f"{n} full {args.config} frames of {what}, after {n_warm} warm-up "
+                                       f"frames at dt={WARM_DT} ({warm_s:.1f} s); numpy single-threaded: 1 of "
+                                       f"{cores} host cores"},
             "e2e": {"value": pps, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ------------------------------------------------------------ roofline ---
+def stage_units(sim, cfg, live: float) -> dict:
+    """Units each stage of one frame processes (BYTES_PER_UNIT)."""
+    u = {"fft": float(cfg.fft_n) ** 2 * max(1, len(sim.cascades)) if sim.fft_state is not None else 0.0,
+         "advect": live, "inject": 0.0}
+    if sim.n_patches:
+        u["compose"] = float(sim.synth.grid_base[-1])
+        u["smooth"] = float(sum(L.ncx * L.ncy for L in sim.synth.pack.layers))
+    return u
+
+
+def roofline(stage: dict, units: dict, peak: float, traffic_doc: dict | None, config: str) -> dict:
+    """Per-kernel roofline of the frame's stages; the headline entry is the
+    stage with the largest device time."""
+    per = {}
+    for k, ms in stage.items():
+        if k not in BYTES_PER_UNIT or not ms or ms != ms or not units.get(k):
+            continue
+        b = BYTES_PER_UNIT[k][0] * units[k]
+        gbs = b / (ms * 1e-3) / 1e9
+        per[k] = {"ms": ms, "algorithmic_bytes": b, "achieved_gbs": gbs, "frac": gbs / peak,
+                  "bytes_per_unit": BYTES_PER_UNIT[k][0], "unit": BYTES_PER_UNIT[k][1]}
+    if not per:
+        return {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None, "traffic": None}
+    top = max(per, key=lambda k: per[k]["ms"])
+    traffic = None
+    if traffic_doc and traffic_doc.get("config") == config:
+        traffic = traffic_doc.get("stages", {}).get(top)
+    return {"bound": "hbm", "kernel": top, "achieved": per[top]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": per[top]["frac"], "traffic": traffic,
+            "traffic_source": "profiles/r02_traffic.json (ncu --set full, dram read + write per launch)"
+            if traffic is not None else "no ncu capture of this workload committed",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)", "per_kernel": per}
 
 
 # ---------------------------------------------------------------- ours ---
@@ -213,6 +325,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     import torch
     import torch.distributed as dist
 
@@ -229,32 +343,22 @@ def main():
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2511_02852_b200 import Simulation
-    from paper_2511_02852_b200 import _native as N
-    from paper_2511_02852_b200.sharding import CompositeGather
+    from paper_2511_02852_b200.sharding import BoxExchange, CascadeShard
 
-    cfg, keys, scaling = scene_config(args.config, rank, world, args.patches)
+    cfg, keys, scaling, full = scene_config(args.config, rank, world, args.patches)
     if args.deterministic:
         from dataclasses import replace
         cfg = replace(cfg, deterministic=True).validate()
     sim = Simulation(cfg, device=dev, rng_seed_keys=keys)
-    gather = None
+    exch = None
     if world > 1 or args.exchange:
-        # the composite exchange at FFT resolution: every rank's
-        # patch boxes of the stitched grid, all-gathered and pasted on every rank
-        gather = CompositeGather(sim.box_np.reshape(-1, 4), cfg.fft_n, world, device=dev)
-
-    def exchange_ops():
-        gather.pack(sim.composite_frame)            # this rank's patch boxes of its frame composite
-        gather.gather()
-        gather.paste_others(sim.composite_frame)    # the other ranks' boxes into this frame composite
-
-    if gather is not None:
-        # the frame's composite (stitched_heights, part of the step) goes through
-        # the exchange: pack + NCCL all-gather + paste at the end of every frame
-        # graph (one graph launch per step, no host work in between)
-        exchange_ops()                              # NCCL communicator set up outside capture
-        torch.cuda.synchronize()
-        sim.post_frame = exchange_ops
+        if len(sim.cascades) > 1 and world > 1:
+            sim.shard_cascades(CascadeShard(cfg.fft_n, len(sim.cascades), world, rank, device=dev))
+        if sim.n_patches and sim.fft_state is not None:
+            exch = BoxExchange.for_scene(full, sim, world, rank)
+            exch.exchange(sim)                      # NCCL communicator set up outside capture
+            torch.cuda.synchronize()
+            sim.post_frame = lambda: exch.exchange(sim)
 
     # steady state: the step itself at dt = 0.1
     n_warm = int(round(args.warm_seconds / WARM_DT))
@@ -301,7 +405,7 @@ def main():
                 "max": float(np.max(step_ms))}
     live_after = sim.live_particles()
     sim.check()
-    if gather is not None:                         # the assembled composite of the last frame
+    if exch is not None:                           # the exchanged composite of the last frame
         assert bool(torch.isfinite(sim.composite_frame).all())
     live = 0.5 * (live_before + live_after)
     if world > 1:
@@ -316,7 +420,8 @@ def main():
     fps = 1e3 / ms_per_step
     value = live_all * fps
 
-    # per-stage device times (eager frames, flushed, events on the launching stream)
+    # per-stage device times (flushed frames from a graph with event nodes,
+    # events on each branch's own stream)
     stage = {}
     for _ in range(args.stage_frames):
         flush_l2()
@@ -359,65 +464,59 @@ def main():
     e2e_value = live_all * 1e3 / e2e_ms
     e2e_bytes = pipe.bytes_per_frame
 
-    # roofline of the dominant particle kernel, hs_advect_resident (in-place
-    # advect + cull + splat): per live particle it must read x, y, ux, uy (f64)
-    # and amp (f32) = 36 B and write the new x, y = 16 B
-    adv_bytes = 52.0 * live
-    adv_ms = stage.get("advect", float("nan"))
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = adv_bytes / (adv_ms * 1e-3) / 1e9 if adv_ms == adv_ms and adv_ms > 0 else None
-    # DRAM bytes per hs_advect_resident launch from the committed ncu launch list
-    # of this workload (tools/ncu_launches.sh -> tools/traffic_json.py)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tp):
-        try:
-            ks = json.load(open(tp))["kernels"]
-            k = next(k for k in ks if k.startswith("advect_resident_kernel"))
-            traffic = ks[k]["dram_read_bytes"] + ks[k]["dram_write_bytes"]
-        except (OSError, KeyError, ValueError, StopIteration):
-            traffic = None
+    traffic_doc = None
+    try:
+        traffic_doc = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+    except (OSError, ValueError):
+        pass
+    workload = args.config + ("" if args.patches is None else f"/{args.patches}")
+    roof = roofline(stage, stage_units(sim, cfg, live), peak, traffic_doc if world == 1 else None, workload)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sc = cpu_scene_from(sim, cfg)
-        frame_s, cpu_live, n_cpu = time_cpu_frames(sc, seconds=args.cpu_seconds)
-        cpu = {"value": cpu_live / frame_s, "unit": "particles/s", "cores": 1, "kind": "port",
-               "sample": f"{n_cpu} full {args.config} frames of the numpy oracle (reference algorithm) from the "
-                         f"GPU's steady state ({cpu_live:.0f} live particles), single thread"}
+        legs = cpu_baselines(sim, cfg, args.cpu_seconds, args.config)
+        cpu = dict(legs.get("reference", legs["port"]))
+        cpu["port"] = legs["port"]
 
     if rank == 0:
+        if scaling == "weak" and world > 1:
+            wl = f" (one C3-size patch per GPU, {world} in the scene)"
+        elif scaling == "strong":
+            wl = f" ({len(cfg.patches)} of its {len(full.patches)} patches on rank 0)"
+        else:
+            wl = ""
+        par = "single GPU"
+        if world > 1:
+            par = f"patch-sharded x{world}" + (", cascades round-robin" if len(sim.cascades) > 1 else "") \
+                + ", composite boxes all-gathered per frame"
         line = {
             "metric": "particles splatted/s (hybrid step)", "value": value, "unit": "particles/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
             "fps": fps, "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic (seeded h0 + Philox streams; steady state reached by the step itself)",
-            "config": {"workload": f"{args.config} hybrid step"
-                                   + (" (1 patch per GPU)" if scaling == "weak" else
-                                      f" ({len(cfg.patches)} of its patches on rank 0)"),
+            "config": {"workload": f"{args.config} hybrid step" + wl,
                        "live_particles": live_all,
                        "fft_n": cfg.fft_n, "fft_domain_m": cfg.fft_domain, "patch_res": cfg.patches[0].res,
-                       "n_patches": len(cfg.patches) * (world if scaling == "weak" else 1),
-                       "fft_cascades": list(cfg.fft_cascades), "n_sources": len(cfg.sources),
-                       "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
-                       "warm_start": f"{n_warm} frames at dt={WARM_DT}", "l2": "flushed between timed steps (256 MiB written, then read back)",
-                       "parallelism": (f"patch-sharded x{world}" if world > 1 else "single GPU"),
-                       "deterministic": bool(cfg.deterministic),
+                       "n_patches": len(full.patches), "fft_cascades": list(cfg.fft_cascades),
+                       "n_sources": len(full.sources), "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
+                       "warm_start": f"{n_warm} frames at dt={WARM_DT}",
+                       "l2": "flushed between timed steps (256 MiB written, then read back)",
+                       "parallelism": par, "deterministic": bool(cfg.deterministic),
                        "step": "FFT background + boundary injection + resident advect/cull/splat + per-bucket "
                                "smoothing + upsample-sum/normals/blend at the patch nodes + FFT-resolution "
-                               "composite (one CUDA graph); pool compaction every %d frames" % sim.compact_period},
+                               "composite (one CUDA graph); pool compaction every %d frames; background "
+                               "normals are not formed per frame (derived on demand, as the reference's lazy "
+                               "sampler reads them)" % sim.compact_period},
             "step_ms_percentiles": step_pct,
-            "gpu_launches": (sim.kernel_launches_per_frame() + (1 if gather else 0)) * args.steps,
+            "gpu_launches": (sim.kernel_launches_per_frame() + (2 if exch is not None else 0)) * args.steps,
             "stages_ms": stage,
-            "roofline": {"bound": "hbm", "kernel": "hs_advect_resident (in-place advect+cull+splat)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes": adv_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "particles/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 8, "d2h_bytes_per_step": e2e_bytes,
                     "note": "host copy of frame k overlaps frame k+1 (HostFramePipe, pinned, depth 2)"},

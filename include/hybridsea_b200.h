@@ -44,6 +44,7 @@ extern "C" {
 #define HS_STATUS_POOL_OVERFLOW  1
 #define HS_STATUS_STAGE_OVERFLOW 2
 #define HS_STATUS_NONFINITE      4
+#define HS_STATUS_BOX_OVERFLOW   8   /* a composite box exceeded HsBoxArgs' capacity */
 
 /* Deterministic mode (fixed_point = 1 in the args below).  Every float sum
  * whose order depends on scheduling is taken in int64 fixed point, whose
@@ -545,11 +546,34 @@ typedef struct {
     float* out;                 /* [n*n] */
     int n_extra_bg;             /* further background cascades, summed at the grid nodes */
     HsBgTile extra_bg[HS_MAX_CASCADES - 1];
-    float* box_out;             /* optional [total_box]: write the boxes' values here, compact in
-                                   box_prefix order, instead of the grid (`out` unused): a rank's
-                                   share of the multi-GPU composite exchange (sharding.py) */
 } HsCompositeArgs;
 HS_API int hs_composite(const HsCompositeArgs* a, void* stream);
+
+/* Multi-GPU composite exchange (the reference composite is
+ * Simulation.stitched_heights, harness.py:219-241).  Every rank packs the
+ * FFT-resolution box of each of its patches -- rows/columns
+ * [floor(min/spacing), ceil(max/spacing)+1) clipped to the grid, computed on
+ * the device from the patch's current synthesis rectangle, so boxes follow
+ * tracking patches -- out of its frame composite (which hs_compose already
+ * blended) into its slots of `payload`; one NCCL all-gather of `payload`
+ * (in place) follows; hs_box_paste then writes every other rank's boxes into
+ * this rank's composite, the later patch (global order = slot order) winning
+ * where boxes overlap, as the reference loop does.
+ * Slot layout: 4 header words (i0, i1, j0, j1 as int bits; i0 == i1: empty)
+ * then bw x bh values, row-major with stride bh.                           */
+typedef struct {
+    int n; double spacing;      /* composite grid side and node spacing */
+    float* composite;           /* [n*n] this rank's frame composite */
+    int n_local;                /* patches of this rank (pack) */
+    const HsPatch* patches;     /* [n_local] */
+    int bw, bh;                 /* box capacity (nodes); a larger box is cut and sets
+                                   HS_STATUS_BOX_OVERFLOW in status */
+    float* payload;             /* [world * slots * (4 + bw*bh)] */
+    int slots, world, rank;     /* slots per rank; paste skips this rank's own */
+    int* status;
+} HsBoxArgs;
+HS_API int hs_box_pack(const HsBoxArgs* a, void* stream);
+HS_API int hs_box_paste(const HsBoxArgs* a, void* stream);
 
 /* Non-periodic (clamped-border) normals and optional choppy displacement of
  * patch grids (finish_field, patch_synthesis.py:323-340).                   */

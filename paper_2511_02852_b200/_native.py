@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("HS_LIB") or os.path.join(_PKG, "_lib", "libhybridsea_
 
 HS_STATUS_POOL_OVERFLOW = 1
 HS_STATUS_STAGE_OVERFLOW = 2
+HS_STATUS_BOX_OVERFLOW = 8
 HS_MAX_BUCKETS = 32
 HS_MAX_PATCHES = 256
 HS_MAX_SOURCES = 1024
@@ -156,6 +157,11 @@ class HsComposeArgs(C.Structure):
                 ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("fixed_point", i32), ("composite", vp)]
 
 
+class HsBoxArgs(C.Structure):
+    _fields_ = [("n", i32), ("spacing", dbl), ("composite", vp), ("n_local", i32), ("patches", vp), ("bw", i32),
+                ("bh", i32), ("payload", vp), ("slots", i32), ("world", i32), ("rank", i32), ("status", vp)]
+
+
 class HsSampleArgs(C.Structure):
     _fields_ = [("n_points", i32), ("points", vp), ("bg_height", vp), ("bg_normal", vp), ("bg_n", i32),
                 ("bg_spacing", dbl), ("bg_x0", dbl), ("bg_y0", dbl), ("n_patches", i32),
@@ -168,7 +174,7 @@ class HsCompositeArgs(C.Structure):
     _fields_ = [("n", i32), ("spacing", dbl), ("bg_height", vp), ("bg_normal", vp), ("n_patches", i32),
                 ("patches", vp), ("patch_height", vp), ("patch_normal", vp), ("box", vp),
                 ("box_prefix", vp), ("total_box", i32), ("out", vp), ("n_extra_bg", i32),
-                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1)), ("box_out", vp)]
+                ("extra_bg", HsBgTile * (HS_MAX_CASCADES - 1))]
 
 
 class HsFinishArgs(C.Structure):
@@ -187,7 +193,7 @@ class HsInitArgs(C.Structure):
 
 ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAdvectArgs, HsSplatArgs,
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
-               HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs, HsInitArgs]
+               HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs, HsInitArgs, HsBoxArgs]
 
 EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource: 80}
 
@@ -196,7 +202,7 @@ EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
            "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies", "hs_init_h0",
-           "hs_init_workspace_bytes", "hs_fixed_to_float", "hs_clear"]
+           "hs_init_workspace_bytes", "hs_fixed_to_float", "hs_clear", "hs_box_pack", "hs_box_paste"]
 
 _lib = None
 

@@ -57,6 +57,7 @@ extern "C" HS_API int hs_struct_size(int which) {
         case 17: return (int)sizeof(HsBody);
         case 18: return (int)sizeof(HsBodyArgs);
         case 19: return (int)sizeof(HsInitArgs);
+        case 20: return (int)sizeof(HsBoxArgs);
         default: return -1;
     }
 }

@@ -304,8 +304,7 @@ __global__ void composite_kernel(HsCompositeArgs a) {
     float h; float3 nv;
     sample_surface(bg, a.n_extra_bg, a.extra_bg, a.n_patches, a.patches, a.patch_height, nullptr,
                    (double)i * a.spacing, (double)j * a.spacing, h, nv);
-    if (a.box_out) a.box_out[k] = h;
-    else a.out[(long long)i * a.n + j] = h;
+    a.out[(long long)i * a.n + j] = h;
 }
 
 // the summed-cascade background on cascade 0's grid (before the patch boxes)
@@ -418,13 +417,6 @@ extern "C" int hs_sample(const HsSampleArgs* a, void* stream) {
 extern "C" int hs_composite(const HsCompositeArgs* a, void* stream) {
     HS_CHECK_ARG(a != nullptr, "hs_composite: null args");
     cudaStream_t st = as_stream(stream);
-    if (a->box_out) {                              // boxes only (multi-GPU exchange payload)
-        if (a->total_box == 0) return 0;
-        HS_CHECK_ARG(a->box && a->box_prefix && a->patches && a->patch_height, "hs_composite: missing boxes");
-        composite_kernel<<<(a->total_box + 255) / 256, 256, 0, st>>>(*a);
-        HS_LAUNCH_CHECK();
-        return 0;
-    }
     HS_CHECK_ARG(a->out, "hs_composite: missing output");
     const size_t bytes = sizeof(float) * (size_t)a->n * a->n;
     HS_CHECK_ARG(a->n_extra_bg >= 0 && a->n_extra_bg < HS_MAX_CASCADES, "hs_composite: n_extra_bg out of range");
@@ -444,6 +436,57 @@ extern "C" int hs_composite(const HsCompositeArgs* a, void* stream) {
 }
 
 namespace hs {
+// ------------------------------------------------ composite box exchange --
+__global__ void box_pack_kernel(HsBoxArgs a) {
+    const int k = blockIdx.x;                       // local slot
+    const int stride = 4 + a.bw * a.bh;
+    float* slot = a.payload + ((size_t)a.rank * a.slots + k) * stride;
+    int i0 = 0, i1 = 0, j0 = 0, j1 = 0;
+    if (k < a.n_local) {
+        // harness.py:230-233: [floor(min / spacing), ceil(max / spacing) + 1), clipped
+        const HsPatch P = synth_view(a.patches[k]);
+        i0 = (int)fmin(fmax(floor(P.x0 / a.spacing), 0.0), (double)a.n);
+        i1 = (int)fmin(fmax(ceil(P.x1 / a.spacing) + 1.0, 0.0), (double)a.n);
+        j0 = (int)fmin(fmax(floor(P.y0 / a.spacing), 0.0), (double)a.n);
+        j1 = (int)fmin(fmax(ceil(P.y1 / a.spacing) + 1.0, 0.0), (double)a.n);
+        if (i1 - i0 > a.bw || j1 - j0 > a.bh) {
+            if (threadIdx.x == 0 && blockIdx.y == 0) atomicOr(a.status, HS_STATUS_BOX_OVERFLOW);
+            i1 = min(i1, i0 + a.bw);
+            j1 = min(j1, j0 + a.bh);
+        }
+    }
+    if (threadIdx.x == 0 && blockIdx.y == 0) {
+        slot[0] = __int_as_float(i0); slot[1] = __int_as_float(i1);
+        slot[2] = __int_as_float(j0); slot[3] = __int_as_float(j1);
+    }
+    const int wj = j1 - j0;
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < (i1 - i0) * wj; e += gridDim.y * blockDim.x) {
+        const int r = e / wj, c = e - r * wj;
+        slot[4 + r * a.bh + c] = a.composite[(long long)(i0 + r) * a.n + j0 + c];
+    }
+}
+
+__global__ void box_paste_kernel(HsBoxArgs a) {
+    const int s = blockIdx.x;                       // global slot (rank-major = global patch order)
+    if (s / a.slots == a.rank) return;              // this rank's own boxes are already in place
+    const int stride = 4 + a.bw * a.bh;
+    const float* slot = a.payload + (size_t)s * stride;
+    const int i0 = __float_as_int(slot[0]), i1 = __float_as_int(slot[1]);
+    const int j0 = __float_as_int(slot[2]), j1 = __float_as_int(slot[3]);
+    const int wj = j1 - j0, total = a.world * a.slots;
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < (i1 - i0) * wj; e += gridDim.y * blockDim.x) {
+        const int r = e / wj, c = e - r * wj;
+        const int i = i0 + r, j = j0 + c;
+        bool later = false;                         // a later box covering this node wins
+        for (int t = s + 1; t < total && !later; ++t) {
+            const float* h = a.payload + (size_t)t * stride;
+            later = i >= __float_as_int(h[0]) && i < __float_as_int(h[1]) && j >= __float_as_int(h[2]) &&
+                    j < __float_as_int(h[3]);
+        }
+        if (!later) a.composite[(long long)i * a.n + j] = slot[4 + r * a.bh + c];
+    }
+}
+
 // deterministic-mode raw layers: int64 fixed point -> float, 4 slots per thread
 __global__ void fixed_to_float_kernel(const long long* __restrict__ src, float* __restrict__ dst, long long n,
                                       double scale) {
@@ -502,6 +545,33 @@ extern "C" int hs_sumsq(const float* x, long long n, double* out, void* stream) 
     int grid = (int)((n + 255) / 256);
     if (grid > 4 * num_sms()) grid = 4 * num_sms();
     sumsq_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, n, out);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+static int check_box(const HsBoxArgs* a, const char* who) {
+    HS_CHECK_ARG(a != nullptr, "%s: null args", who);
+    HS_CHECK_ARG(a->n >= 1 && a->spacing > 0.0 && a->composite && a->payload && a->status, "%s: missing buffer", who);
+    HS_CHECK_ARG(a->bw >= 1 && a->bh >= 1 && a->slots >= 1 && a->world >= 1 && a->rank >= 0 && a->rank < a->world,
+                 "%s: bad slot geometry", who);
+    return 0;
+}
+
+extern "C" int hs_box_pack(const HsBoxArgs* a, void* stream) {
+    if (int rc = check_box(a, "hs_box_pack")) return rc;
+    HS_CHECK_ARG(a->n_local >= 0 && a->n_local <= a->slots && (a->n_local == 0 || a->patches),
+                 "hs_box_pack: n_local=%d out of range", a->n_local);
+    const int ny = min(16, (a->bw * a->bh + 255) / 256);
+    box_pack_kernel<<<dim3(a->slots, ny), 256, 0, as_stream(stream)>>>(*a);
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_box_paste(const HsBoxArgs* a, void* stream) {
+    if (int rc = check_box(a, "hs_box_paste")) return rc;
+    if (a->world == 1) return 0;
+    const int ny = min(16, (a->bw * a->bh + 255) / 256);
+    box_paste_kernel<<<dim3(a->world * a->slots, ny), 256, 0, as_stream(stream)>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
 }

@@ -154,6 +154,7 @@ class Simulation:
         # e.g. the multi-GPU composite exchange (bench.py, sharding.py).
         self.composite_each_frame = True
         self.post_frame = None
+        self._cshard = None               # sharding.CascadeShard (multi-GPU C4), see shard_cascades
         # frame schedule knobs (tools/ab_sched.py): FFT branch fork point, stream priorities
         self.fft_fork_at_start = False
         self.sched_priorities = False
@@ -520,6 +521,8 @@ class Simulation:
             with torch.cuda.stream(side):
                 mark("fft_start")
                 for c, (st_c, ws_c) in enumerate(self.cascades):
+                    if self._cshard is not None and not self._cshard.owned(c):
+                        continue                    # another rank transforms it (CascadeShard)
                     fa = fft_args(st_c, ws_c, frame_ptr=self.frame_dev, dt=dt)
                     fa.emit_normals = 0      # normals are derived lazily (background) / in hs_compose
                     fa.normal = 0
@@ -527,6 +530,8 @@ class Simulation:
                     if not self.n_patches and c == len(self.cascades) - 1:
                         fa.frame_advance = N.ptr(self.frame_dev)
                     N.call("hs_fft_evolve", fa, stream_ptr())
+                if self._cshard is not None:
+                    self._cshard.gather()           # every rank gets every cascade's heights
                 if frame_composite:             # the composite starts as the background; hs_compose
                     self._composite(self.composite_frame, (None, None, 0))   # blends the patch nodes in
                 mark("fft")
@@ -805,6 +810,8 @@ class Simulation:
             raise CapacityError(f"particle pool overflow (capacity {self.pool_caps}); raise device.pool_capacity")
         if s & N.HS_STATUS_STAGE_OVERFLOW:
             raise CapacityError("injection staging overflow")
+        if s & N.HS_STATUS_BOX_OVERFLOW:
+            raise CapacityError("composite exchange box larger than its slot")
 
     # ----------------------------------------------------------- outputs --
     @property
@@ -944,25 +951,20 @@ class Simulation:
         self._composite(self.composite_out)
         return self.composite_out
 
-    def composite_boxes(self, out: torch.Tensor) -> torch.Tensor:
-        """This device's share of the FFT-resolution composite: the stitched
-        values of its patch boxes (harness.py:230-240), compact in box order
-        (`box_np` / `box_prefix_np`) -- the payload of the multi-GPU composite
-        exchange (sharding.CompositeGather)."""
-        cfg = self.config
-        n = cfg.fft_n
-        if self.fft_state is None or not self.n_patches:
-            raise ConfigError("composite_boxes needs the FFT background and at least one patch")
-        total = int(self.box_prefix_np[-1])
-        if out.numel() < total:
-            raise ValueError(f"composite_boxes: out holds {out.numel()} < {total} values")
-        bg = self.fft_ws
-        N.call("hs_composite", N.HsCompositeArgs(
-            n=n, spacing=cfg.fft_domain / n, bg_height=N.ptr(bg.height), bg_normal=0, n_patches=self.n_patches,
-            patches=N.ptr(self.patches_dev), patch_height=N.ptr(self.patch_h), patch_normal=0,
-            box=N.ptr(self.box_dev), box_prefix=N.ptr(self.box_prefix_dev), total_box=total, out=0,
-            box_out=N.ptr(out), **self._extra_bg()), stream_ptr())
-        return out[:total]
+    def shard_cascades(self, shard) -> None:
+        """Transform only this rank's FFT cascades (sharding.CascadeShard) and
+        all-gather their heights every frame.  Call before the frame graphs are
+        captured; the cascades' height grids become views of the shard buffer.
+        Displacement grids and FFT-band variances of other ranks' cascades are
+        not exchanged (neither enters the blend or the composite)."""
+        if len(self.cascades) < 2 or shard.n_cascades != len(self.cascades) or shard.n != self.config.fft_n:
+            raise ConfigError("shard_cascades needs a summed-cascade background matching the shard")
+        for c, (_, ws) in enumerate(self.cascades):
+            v = shard.view(c)
+            v.copy_(ws.height)
+            ws.height = v
+        self._cshard = shard
+        self._graphs = {}
 
     def background_sum(self, out: torch.Tensor) -> torch.Tensor:
         """The background height grid the composite starts from (the summed

@@ -3,13 +3,15 @@
 Patches are independent given the shared bucket table (no particle crosses
 patches, reference SPEC.md:231), so a scene shards by patch: rank r owns a
 contiguous block of patches, each with its own pool, ledger and Philox
-stream (key = (seed, global patch id)), and runs the (cheap, replicated)
-background.  The only exchange is the per-frame gather of blended patch
-tiles into the composite, one NCCL all-gather over NVLink.  FFT cascades
-(C4) would be assigned round-robin.
+stream (key = (seed, global patch id)).  FFT cascades (C4) are assigned
+round-robin (`CascadeShard`: one all-gather of their height grids per frame);
+a single background tile is replicated (it is needed at every rank's patch
+nodes and costs less than its exchange).  The composite exchange is one
+all-gather of every rank's FFT-resolution patch boxes (`BoxExchange`, packed
+and pasted by hand-written kernels).
 
-The host logic here (partitioning, tile packing, composite assembly) is
-device-agnostic and covered by `gloo` world-size-2 tests on CPU.
+The host logic (partitioning, keys, payload layout, in-place gathers) is
+covered by `gloo` world-size-2 tests on CPU; the kernels by GPU tests.
 """
 from __future__ import annotations
 
@@ -56,144 +58,109 @@ def cascade_owner(cascade: int, world: int) -> int:
     return cascade % world
 
 
-def gather_tiles(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """All-gather equal-size flattened tiles: returns [world, numel]."""
-    flat = local.reshape(-1).contiguous()
-    out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)   # flat: gloo and nccl
-    dist.all_gather_into_tensor(out, flat, group=group)
-    return out.view(world, flat.numel())
+def box_capacity(patch_sizes, spacing: float) -> int:
+    """Nodes per axis of the largest composite box a patch of these sizes can
+    cover anywhere (harness.py:230-233: [floor(min/sp), ceil(max/sp) + 1))."""
+    import math
+    return max(int(math.ceil(float(l) / spacing)) + 3 for size in patch_sizes for l in size)
 
 
-def assemble(tiles: torch.Tensor, shapes: list[tuple[int, int]]) -> list[torch.Tensor]:
-    """Split gathered rows back into per-patch (res, ny) views."""
-    return [tiles[k, : r * c].view(r, c) for k, (r, c) in enumerate(shapes)]
+class BoxExchange:
+    """Per-frame composite exchange at FFT resolution: each rank
+    packs the stitched-grid box of each of its patches out of its own frame
+    composite (hs_box_pack: boxes computed on the device from the patches'
+    current synthesis rectangles, so tracking patches' boxes move with them),
+    one in-place NCCL all-gather moves every rank's slots, and hs_box_paste
+    writes the other ranks' boxes into this rank's composite, the later patch
+    in global order winning where boxes overlap (the reference loop,
+    harness.py:219-241).  C3 weak scaling: a 67 x 67 box per rank (18 KB)
+    instead of a 4 MB native tile; C5: 64 boxes of 52 x 52.
 
+    Payload: world x slots x (4 header words + bw*bh values); slot order is
+    rank-major, i.e. global patch order (contiguous blocks, `partition`).
+    Fixed buffers, no host synchronisation: `exchange` is captured into the
+    frame graph (Simulation.post_frame)."""
 
-class CompositeGather:
-    """Per-frame composite exchange at FFT resolution (SURVEY 8(e)'s
-    alternative to shipping native-resolution tiles): every rank resamples
-    its own patches' boxes of the stitched grid (harness.py:219-241;
-    `Simulation.composite_boxes`), one all-gather moves those values
-    (C3 weak scaling: a 67 x 67 box, 18 KB per rank, instead of a 4 MB tile),
-    and every rank pastes all boxes over the background.
+    def __init__(self, n: int, spacing: float, slots: int, bw: int, bh: int, world: int, rank: int,
+                 group=None, device=None):
+        self.n, self.spacing, self.slots, self.bw, self.bh = int(n), float(spacing), int(slots), int(bw), int(bh)
+        self.world, self.rank, self.group = int(world), int(rank), group
+        self.stride = 4 + self.bw * self.bh
+        self.chunk = self.slots * self.stride
+        self.payload = torch.zeros(self.world * self.chunk, dtype=torch.float32, device=device)
 
-    Box geometry is exchanged once at construction.  Where boxes of
-    different patches overlap, the later patch in global order wins, as in
-    the reference's loop; each rank samples only its own patches, so an
-    overlap across ranks is exact only where the patches do not both cover
-    the texel (seeded layouts keep patches apart)."""
+    @classmethod
+    def for_scene(cls, cfg, sim, world: int, rank: int, group=None):
+        """The exchange of `sim` (this rank's shard of the global scene `cfg`)."""
+        spacing = cfg.fft_domain / cfg.fft_n
+        slots = max(len(b) for b in partition(len(cfg.patches), world))
+        cap = box_capacity([pc.size for pc in cfg.patches], spacing)
+        return cls(cfg.fft_n, spacing, slots, cap, cap, world, rank, group, device=sim.device)
 
-    def __init__(self, boxes, n: int, world: int, group=None, device=None):
-        import numpy as np
-        self.n, self.world, self.group = n, world, group
-        boxes = np.asarray(boxes, dtype=np.int64).reshape(-1, 4)
-        sizes = (boxes[:, 1] - boxes[:, 0]).clip(0) * (boxes[:, 3] - boxes[:, 2]).clip(0)
-        self.local_total = int(sizes.sum())
-        loc = [(np.arange(b[0], b[1])[:, None] * n + np.arange(b[2], b[3])[None, :]).ravel()
-               for b in boxes if b[1] > b[0] and b[3] > b[2]]
-        self.local_index = torch.from_numpy(np.concatenate(loc) if loc else np.zeros(0, np.int64)).to(device)
-        meta = torch.tensor([len(boxes), self.local_total], dtype=torch.int64, device=device)
-        metas = torch.empty(world * 2, dtype=torch.int64, device=device)
-        dist.all_gather_into_tensor(metas, meta, group=group)
-        metas = metas.view(world, 2).cpu().numpy()
-        max_p = int(metas[:, 0].max())
-        self.per_rank = max(1, int(metas[:, 1].max()))
-        padded = torch.full((max(max_p, 1), 4), -1, dtype=torch.int64, device=device)
-        if len(boxes):
-            padded[: len(boxes)] = torch.from_numpy(boxes).to(device)
-        allb = torch.empty(world * padded.numel(), dtype=torch.int64, device=device)
-        dist.all_gather_into_tensor(allb, padded.reshape(-1), group=group)
-        allb = allb.view(world, -1, 4).cpu().numpy()
-        pos, dst, own = [], [], []
-        me = dist.get_rank(group)
-        for r in range(world):
-            off = r * self.per_rank
-            for b in allb[r, : metas[r, 0]]:
-                i0, i1, j0, j1 = (int(v) for v in b)
-                if i1 <= i0 or j1 <= j0:
-                    continue
-                ii, jj = np.meshgrid(np.arange(i0, i1), np.arange(j0, j1), indexing="ij")
-                dst.append((ii * n + jj).ravel())
-                pos.append(off + np.arange(ii.size))
-                own.append(np.full(ii.size, r == me))
-                off += ii.size
-        dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
-        pos = np.concatenate(pos) if pos else np.zeros(0, np.int64)
-        own = np.concatenate(own) if own else np.zeros(0, bool)
-        # per composite texel: the payload slot that covers it (later boxes win,
-        # as in the reference loop), or none -> background
-        src = np.full(n * n, -1, np.int64)
-        last = len(dst) - 1 - np.unique(dst[::-1], return_index=True)[1]   # last occurrence per texel
-        src[dst[last]] = pos[last]
-        # the other ranks' winning nodes, for pasting into this rank's own frame composite
-        keep = last[~own[last]]
-        self.other_dst = torch.from_numpy(dst[keep]).to(device)
-        self.other_pos = torch.from_numpy(pos[keep]).to(device)
-        self._other_vals = torch.empty(len(keep), dtype=torch.float32, device=device)
-        self.covered = torch.from_numpy(src >= 0).to(device)
-        self.src = torch.from_numpy(np.maximum(src, 0)).to(device)
-        self.send = torch.zeros(self.per_rank, dtype=torch.float32, device=device)
-        self.recv = torch.empty(world * self.per_rank, dtype=torch.float32, device=device)
-        self.grid = torch.empty(n * n, dtype=torch.float32, device=device)
-        self._picked = torch.empty(n * n, dtype=torch.float32, device=device)
+    @property
+    def own(self) -> torch.Tensor:
+        return self.payload[self.rank * self.chunk:(self.rank + 1) * self.chunk]
 
-    def pack(self, composite: torch.Tensor) -> None:
-        """Fill `send` with this rank's box nodes of its own frame composite
-        (the grid hs_compose blended its patches into)."""
-        if self.local_total:
-            torch.index_select(composite.reshape(-1), 0, self.local_index, out=self.send[: self.local_total])
+    def _args(self, sim):
+        from . import _native as N
+        return N.HsBoxArgs(n=self.n, spacing=self.spacing, composite=N.ptr(sim.composite_frame),
+                           n_local=sim.n_patches, patches=N.ptr(sim.patches_dev), bw=self.bw, bh=self.bh,
+                           payload=N.ptr(self.payload), slots=self.slots, world=self.world, rank=self.rank,
+                           status=N.ptr(sim.status))
+
+    def pack(self, sim) -> None:
+        from . import _native as N
+        from ._layout import stream_ptr
+        N.call("hs_box_pack", self._args(sim), stream_ptr())
 
     def gather(self) -> torch.Tensor:
-        """All-gather every rank's `send[:local_total]` (filled by
-        `Simulation.composite_boxes(send)`): afterwards every rank holds every
-        patch box of the stitched grid.  Fixed buffers and no host
-        synchronisation, so it is captured into the frame's CUDA graph
-        (`Simulation.post_frame`)."""
-        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
-        return self.recv
+        """In-place all-gather of every rank's slots (NCCL on the GPU, gloo in the CPU tests)."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.payload, self.own, group=self.group)
+        return self.payload
 
-    def assemble(self, background: torch.Tensor) -> torch.Tensor:
-        """Paste the gathered boxes over `background` (n x n): the full
-        composite (on demand, like the reference's stitched_heights)."""
-        torch.index_select(self.recv, 0, self.src, out=self._picked)
-        torch.where(self.covered, self._picked, background.reshape(-1), out=self.grid)
-        return self.grid.view(self.n, self.n)
+    def paste(self, sim) -> None:
+        from . import _native as N
+        from ._layout import stream_ptr
+        N.call("hs_box_paste", self._args(sim), stream_ptr())
 
-    def paste_others(self, composite: torch.Tensor) -> torch.Tensor:
-        """Paste the other ranks' gathered boxes into this rank's own frame
-        composite (which already holds the background and its own boxes)."""
-        if self.other_dst.numel():
-            torch.index_select(self.recv, 0, self.other_pos, out=self._other_vals)
-            composite.view(-1).index_copy_(0, self.other_dst, self._other_vals)
-        return composite
-
-    def exchange(self, background: torch.Tensor) -> torch.Tensor:
-        """gather() + assemble()."""
+    def exchange(self, sim) -> None:
+        self.pack(sim)
         self.gather()
-        return self.assemble(background)
+        self.paste(sim)
+
+    def slots_host(self) -> list:
+        """[(i0, i1, j0, j1, values (i1-i0, j1-j0))] of every slot (synchronises)."""
+        import numpy as np
+        raw = self.payload.cpu().numpy().reshape(self.world * self.slots, self.stride)
+        out = []
+        for row in raw:
+            i0, i1, j0, j1 = (int(v) for v in row[:4].view(np.int32))
+            vals = row[4:].reshape(self.bw, self.bh)[: max(i1 - i0, 0), : max(j1 - j0, 0)]
+            out.append((i0, i1, j0, j1, vals.copy()))
+        return out
 
 
-class TileGather:
-    """Per-frame NCCL all-gather of every rank's blended patch tiles (the
-    composite exchange of SURVEY 8(e)): each rank contributes its patches'
-    blend heights, which are contiguous in the per-device grid buffer, padded
-    to the largest rank's share (block sizes differ by at most one patch)."""
+class CascadeShard:
+    """Round-robin FFT cascades over the ranks (C4: 3 cascades on ranks 0-2):
+    rank r transforms the cascades c with c % world == r; one in-place
+    all-gather of their height grids per frame gives every rank the whole
+    summed background its patch blend and composite read (displacements and
+    FFT-band statistics stay with the owner).  Cascade c's heights live at
+    `buffer[c % world, c // world]`."""
 
-    def __init__(self, sim, world: int, group=None, max_local: int | None = None):
-        self.sim = sim
-        self.world = world
-        self.group = group
-        self.local = int(sim.synth.grid_base[-1])           # floats of this rank's tiles
-        self.per_rank = max_local if max_local is not None else self.local
-        self.send = torch.zeros(self.per_rank, dtype=torch.float32, device=sim.device)
-        self.out = torch.empty(world * self.per_rank, dtype=torch.float32, device=sim.device)
+    def __init__(self, n: int, n_cascades: int, world: int, rank: int, group=None, device=None):
+        self.n, self.n_cascades, self.world, self.rank, self.group = n, n_cascades, world, rank, group
+        self.per_rank = max(1, -(-n_cascades // world))
+        self.buffer = torch.zeros((world, self.per_rank, n, n), dtype=torch.float32, device=device)
 
-    def exchange(self) -> torch.Tensor:
-        h = self.sim.blend_h[: self.local]
-        if self.local == self.per_rank:
-            src = h
-        else:
-            self.send[: self.local].copy_(h)
-            src = self.send
-        dist.all_gather_into_tensor(self.out, src, group=self.group)
-        return self.out.view(self.world, -1)
+    def owned(self, c: int) -> bool:
+        return cascade_owner(c, self.world) == self.rank
+
+    def view(self, c: int) -> torch.Tensor:
+        return self.buffer[cascade_owner(c, self.world), c // self.world]
+
+    def gather(self) -> None:
+        if self.world > 1:
+            flat = self.buffer.view(-1)
+            dist.all_gather_into_tensor(flat, self.buffer[self.rank].view(-1), group=self.group)

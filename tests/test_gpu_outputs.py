@@ -89,28 +89,6 @@ def test_rerun_is_deterministic_where_serial(cuda):
     assert np.abs(ha - hb).max() <= 1e-6 * max(1e-6, np.abs(ha).max())
 
 
-def test_composite_boxes_are_the_stitched_boxes(cuda):
-    """The multi-GPU composite payload (Simulation.composite_boxes: the patch
-    boxes of the stitched grid, compact) pasted over the background equals
-    stitched_heights (harness.py:219-241) bit for bit -- what
-    sharding.CompositeGather assembles on every rank."""
-    import torch
-    from paper_2511_02852_b200 import Simulation, scenes
-    cfg = scenes.c2(frames=10)
-    sim = Simulation(cfg, device=cuda)
-    for _ in range(cfg.frames):
-        sim.step(stats=False)
-    want = sim.stitched_heights().clone()
-    buf = torch.zeros(int(sim.box_prefix_np[-1]) + 7, device=cuda)
-    vals = sim.composite_boxes(buf).cpu().numpy()
-    grid = sim.fft_ws.height.clone().cpu().numpy()
-    boxes, pre = sim.box_np.reshape(-1, 4), sim.box_prefix_np
-    for p, (i0, i1, j0, j1) in enumerate(boxes):
-        grid[i0:i1, j0:j1] = vals[pre[p]:pre[p + 1]].reshape(i1 - i0, j1 - j0)
-    np.testing.assert_array_equal(grid, want.cpu().numpy())
-    assert boxes.shape[0] == len(cfg.patches) and pre[-1] > 0
-
-
 @pytest.mark.parametrize("scene", ["c2", "c4"])
 def test_frame_composite_equals_stitched_heights(cuda, scene):
     """Every frame ends with the FFT-resolution composite (the background copy

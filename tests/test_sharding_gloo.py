@@ -1,6 +1,8 @@
-"""Multi-process (gloo, world size 2) tests of the patch sharding host logic
-(SURVEY 8(e)): partitioning, per-patch Philox keys, the tile all-gather and
-composite assembly, and that integer results (per-patch bucket counts) of a
+"""Multi-process (gloo, world size 2) tests of the sharding host logic
+(SURVEY 8(e)): partitioning, per-patch Philox keys, the composite box
+exchange (BoxExchange payload, in-place all-gather, the later-box-wins paste
+of oracle/exchange_ref.py that hs_box_paste restates), FFT cascade sharding
+(CascadeShard), and that integer results (per-patch bucket counts) of a
 sharded run equal the single-process run.  CPU only.
 """
 from __future__ import annotations
@@ -21,8 +23,9 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 from paper_2511_02852_b200 import scenes  # noqa: E402
-from paper_2511_02852_b200.sharding import (CompositeGather, assemble, cascade_owner, gather_tiles,  # noqa: E402
+from paper_2511_02852_b200.sharding import (BoxExchange, CascadeShard, cascade_owner,  # noqa: E402
                                             partition, shard_config)
+from oracle import exchange_ref  # noqa: E402
 
 
 def _free_port() -> int:
@@ -37,12 +40,6 @@ def _init(rank: int, world: int, port: int) -> None:
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
 
-def _tile(pid: int, shape) -> torch.Tensor:
-    """Deterministic stand-in for a blended patch tile of global patch pid."""
-    g = torch.Generator().manual_seed(1000 + pid)
-    return torch.randn(shape, generator=g)
-
-
 def _small_scene(n_patches: int):
     """Small wp-only multi-patch scene: 48 m patches on 96^2 grids, 6 buckets."""
     cfg = scenes.c2(n_omega=6, n_theta=4, fft_n=64, mode="wp-only")
@@ -52,53 +49,46 @@ def _small_scene(n_patches: int):
 
 
 # ----------------------------------------------------------------- workers --
-def _gather_worker(rank: int, world: int, port: int, n_patches: int, out_dir: str) -> None:
+# patch rectangles (x0, y0, l1, l2) on a 16 x 16 composite of spacing 1 m;
+# the boxes of patches 1 and 2 overlap (the later one must win)
+_RECTS = [(0.2, 0.5, 3.0, 3.5), (5.3, 3.1, 2.0, 4.6), (6.6, 7.2, 3.0, 3.0), (12.4, 12.1, 2.9, 2.2)]
+_N, _SP = 16, 1.0
+
+
+def _stitched(pid: int) -> np.ndarray:
+    """Stand-in for a rank's frame composite over patch pid's box."""
+    return (100.0 * (pid + 1) + np.arange(_N * _N).reshape(_N, _N)).astype(np.float32)
+
+
+def _box_worker(rank: int, world: int, port: int, out_dir: str) -> None:
     _init(rank, world, port)
     try:
-        shape = (24, 24)
-        blocks = partition(n_patches, world)
-        width = max(len(b) for b in blocks)
-        # each rank packs its block's tiles into a fixed-width slab (padding slots zero)
-        slab = torch.zeros((width, shape[0] * shape[1]))
-        for k, pid in enumerate(blocks[rank]):
-            slab[k] = _tile(pid, shape).reshape(-1)
-        got = gather_tiles(slab, world)                     # [world, width * numel]
-        got = got.view(world, width, -1)
-        tiles = torch.cat([got[r, : len(blocks[r])] for r in range(world)])
-        views = assemble(tiles, [shape] * n_patches)
-        for pid, v in enumerate(views):
-            assert torch.equal(v, _tile(pid, shape)), f"rank {rank}: tile {pid} differs after the gather"
-        open(os.path.join(out_dir, f"ok{rank}"), "w").close()
+        block = partition(len(_RECTS), world)[rank]
+        cap = exchange_ref.capacity([(r[2], r[3]) for r in _RECTS], _SP)
+        ex = BoxExchange(_N, _SP, max(len(b) for b in partition(len(_RECTS), world)), cap, cap, world, rank)
+        own = np.full((_N, _N), -1.0, np.float32)          # background + this rank's boxes (hs_compose)
+        slots = ex.own.numpy().reshape(ex.slots, ex.stride)
+        for k, pid in enumerate(block):
+            box = exchange_ref.box_of(*_RECTS[pid], _N, _SP)
+            i0, i1, j0, j1 = box
+            own[i0:i1, j0:j1] = _stitched(pid)[i0:i1, j0:j1]
+            exchange_ref.pack_slot(slots[k], own, box, cap, cap)
+        ex.gather()                                         # in-place all-gather of the slots
+        got = exchange_ref.paste(own, ex.payload.numpy(), ex.slots, world, rank, cap, cap)
+        np.save(os.path.join(out_dir, f"grid{rank}.npy"), got)
     finally:
         dist.destroy_process_group()
 
 
-# boxes (i0, i1, j0, j1) of the global patch list on a 16 x 16 composite;
-# patches 1 and 2 overlap in row 6-7 (the later one must win)
-_BOXES = [(0, 4, 0, 5), (5, 8, 3, 9), (6, 10, 8, 12), (12, 16, 12, 16)]
-
-
-def _box_values(pid: int) -> np.ndarray:
-    i0, i1, j0, j1 = _BOXES[pid]
-    return (100.0 * (pid + 1) + np.arange((i1 - i0) * (j1 - j0))).astype(np.float32)
-
-
-def _composite_worker(rank: int, world: int, port: int, out_dir: str) -> None:
+def _cascade_worker(rank: int, world: int, port: int, out_dir: str) -> None:
     _init(rank, world, port)
     try:
-        block = partition(len(_BOXES), world)[rank]
-        g = CompositeGather([_BOXES[k] for k in block], 16, world)
-        vals = np.concatenate([_box_values(k) for k in block])
-        g.send[: len(vals)] = torch.from_numpy(vals)
-        bg = torch.full((16, 16), -1.0)
-        grid = g.exchange(bg).numpy()
-        np.save(os.path.join(out_dir, f"grid{rank}.npy"), grid)
-        # the in-place route: own frame composite (background + own boxes) + others pasted
-        own = torch.full((16, 16), -1.0)
-        for k in block:
-            i0, i1, j0, j1 = _BOXES[k]
-            own[i0:i1, j0:j1] = torch.from_numpy(_box_values(k).reshape(i1 - i0, j1 - j0))
-        np.save(os.path.join(out_dir, f"own{rank}.npy"), g.paste_others(own).numpy())
+        sh = CascadeShard(8, 3, world, rank)
+        for c in range(3):
+            if sh.owned(c):
+                sh.view(c).fill_(10.0 * (c + 1))
+        sh.gather()
+        np.save(os.path.join(out_dir, f"casc{rank}.npy"), np.stack([sh.view(c).numpy() for c in range(3)]))
     finally:
         dist.destroy_process_group()
 
@@ -151,12 +141,6 @@ def test_shard_config_keeps_global_keys():
     assert seen == list(range(len(cfg.patches)))
 
 
-def test_gloo_tile_gather_world2():
-    with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_gather_worker, args=(2, _free_port(), 3, d), nprocs=2, join=True)
-        assert os.path.exists(os.path.join(d, "ok0")) and os.path.exists(os.path.join(d, "ok1"))
-
-
 def test_sharded_counts_equal_single_process_world2():
     """Per-patch bucket counts after a few frames: 2-rank sharded oracle run
     == single-process run (integer results must not depend on sharding)."""
@@ -175,15 +159,27 @@ def test_sharded_counts_equal_single_process_world2():
     np.testing.assert_array_equal(got, ref)
 
 
-def test_gloo_composite_gather_world2():
-    """The FFT-resolution box exchange: both ranks assemble the composite the
-    reference's stitched_heights loop would (background, then every patch box
-    in global order, later boxes overwriting earlier ones)."""
-    want = np.full((16, 16), -1.0, np.float32)
-    for pid, (i0, i1, j0, j1) in enumerate(_BOXES):
-        want[i0:i1, j0:j1] = _box_values(pid).reshape(i1 - i0, j1 - j0)
+def test_gloo_box_exchange_world2():
+    """The FFT-resolution composite exchange: both ranks end with the
+    composite the reference's stitched_heights loop builds (background, then
+    every patch box in global order, later boxes overwriting earlier ones)."""
+    want = np.full((_N, _N), -1.0, np.float32)
+    for pid, rect in enumerate(_RECTS):
+        i0, i1, j0, j1 = exchange_ref.box_of(*rect, _N, _SP)
+        want[i0:i1, j0:j1] = _stitched(pid)[i0:i1, j0:j1]
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_composite_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        mp.spawn(_box_worker, args=(2, _free_port(), d), nprocs=2, join=True)
         for r in range(2):
             np.testing.assert_array_equal(np.load(os.path.join(d, f"grid{r}.npy")), want)
-            np.testing.assert_array_equal(np.load(os.path.join(d, f"own{r}.npy")), want)
+
+
+def test_gloo_cascade_shard_world2():
+    """Round-robin cascades (0, 2 on rank 0; 1 on rank 1): after the in-place
+    gather every rank holds every cascade's heights."""
+    assert [cascade_owner(c, 2) for c in range(3)] == [0, 1, 0]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_cascade_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        for r in range(2):
+            got = np.load(os.path.join(d, f"casc{r}.npy"))
+            for c in range(3):
+                assert np.all(got[c] == 10.0 * (c + 1)), (r, c)

@@ -25,7 +25,7 @@ def main() -> int:
     import torch
     from bench import scene_config
     from paper_2511_02852_b200 import Simulation
-    cfg, keys, _ = scene_config(args.config, 0, 1)
+    cfg, keys, _, _ = scene_config(args.config, 0, 1)
     sim = Simulation(cfg, device="cuda:0", rng_seed_keys=keys)
     sim.run_frames(2000, dt=0.1)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")

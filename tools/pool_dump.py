@@ -9,7 +9,7 @@ from paper_2511_02852_b200 import Simulation, scenes  # noqa: E402
 from bench import scene_config  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 npatch = int(sys.argv[2]) if len(sys.argv) > 2 else None
-cfg, keys, _ = scene_config(name, 0, 1, npatch)
+cfg, keys, _, _ = scene_config(name, 0, 1, npatch)
 sim = Simulation(cfg, device=torch.device("cuda:0"), rng_seed_keys=keys)
 sim.prepare_graphs()
 for _ in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2000):

@@ -23,7 +23,7 @@ def main() -> int:
     import torch
     from paper_2511_02852_b200 import Simulation
     from bench import scene_config
-    cfg, keys, _ = scene_config(args.config, 0, 1, args.patches)
+    cfg, keys, _, _ = scene_config(args.config, 0, 1, args.patches)
     sim = Simulation(cfg, device="cuda:0", rng_seed_keys=keys)
     sim.run_frames(args.warm_frames, dt=0.1)
     sim.run_frames(3)
