@@ -128,6 +128,8 @@ typedef struct {
     double* x;  double* y;     /* world position (fp64: keeps cull decisions exact) */
     double* ux; double* uy;    /* unit direction (fp64) */
     float* amp;                /* signed amplitude */
+    double* birth;             /* optional birth time t = frame * dt (ParticleSet.birth_times,
+                                  particles.py:128-129); NULL: not kept */
 } HsPool;
 
 /* ------------------------------------------------------------------------ */
@@ -248,6 +250,9 @@ typedef struct {
                                       culled and splatted here and appended to the resident
                                       segments (what hs_append_resident does with a stage) */
     HsResidentArgs res;            /* resident pool for append (its stage fields are unused) */
+    double birth_t;                /* birth time of this step's particles (particles.py:296-299) ... */
+    const long long* birth_frame;  /* ... or, if set, *birth_frame * birth_dt (graph replays) */
+    double birth_dt;
 } HsInjectArgs;
 HS_API int hs_inject(const HsInjectArgs* a, void* stream);
 
@@ -574,6 +579,18 @@ typedef struct {
 } HsBoxArgs;
 HS_API int hs_box_pack(const HsBoxArgs* a, void* stream);
 HS_API int hs_box_paste(const HsBoxArgs* a, void* stream);
+
+/* fp64 helpers of the function-level API (not on the frame path):
+ * spectral_at (fft_background.py:155-159): hh = h0 e^{-i w t} + conj(h0(-k)) e^{+i w t}
+ * over the n x n grid, h0 complex128 [n*n*2], omega on the (|i|, |j|) quarter
+ * grid [(n/2+1)^2] as FftState.omega_dev, out complex128 [n*n*2];
+ * convolve1d_zero (patch_synthesis.py:105-130): same-size zero-padded
+ * convolution of an [outer, n, inner] fp64 array along its middle axis with
+ * 2H+1 taps (direct taps: the reference's cumsum window sums are the same
+ * convolution).                                                            */
+HS_API int hs_spectral_at(const double* h0, const double* omega, int n, double t, double* out, void* stream);
+HS_API int hs_conv1d_zero(const double* in, double* out, long long outer, int n, long long inner,
+                          const double* taps, int H, void* stream);
 
 /* Non-periodic (clamped-border) normals and optional choppy displacement of
  * patch grids (finish_field, patch_synthesis.py:323-340).                   */

@@ -28,12 +28,12 @@ def to_device_bytes(arr: np.ndarray, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(arr)).to(device)
 
 
-def bucket_structs(table, params) -> list:
+def bucket_structs(table, params, s1d=None) -> list:
     """HsBucket per bucket: the array views the kernels read (spectrum.py:233-257)
     plus S_J(omega_b) in fp64 (particles.py:262)."""
     from .spectrum import evaluate_1d
     s_arr, c_arr = table.spread_params
-    s1d = evaluate_1d(params, table.omegas)
+    s1d = evaluate_1d(params, table.omegas) if s1d is None else np.asarray(s1d, dtype=float)
     out = []
     for k, b in enumerate(table.buckets):
         out.append(N.HsBucket(b.omega, b.delta_omega, b.radius, b.speed, float(s1d[k]),

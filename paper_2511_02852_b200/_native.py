@@ -49,7 +49,7 @@ class HsLayer(C.Structure):
 
 
 class HsPool(C.Structure):
-    _fields_ = [("x", vp), ("y", vp), ("ux", vp), ("uy", vp), ("amp", vp)]
+    _fields_ = [("x", vp), ("y", vp), ("ux", vp), ("uy", vp), ("amp", vp), ("birth", vp)]
 
 
 HS_FIXED_SPLAT_BITS = 32
@@ -83,7 +83,8 @@ class HsInjectArgs(C.Structure):
                 ("half_rate", vp), ("mean_dir", dbl), ("beta", dbl), ("rho", dbl), ("g", dbl),
                 ("acc", vp), ("groups", vp), ("e_in", vp), ("rng", vp), ("stage", HsPool),
                 ("stage_count", vp), ("scratch", vp), ("member_capacity", i32), ("status", vp),
-                ("zero_words", vp), ("n_zero_words", i32), ("append", i32), ("res", HsResidentArgs)]
+                ("zero_words", vp), ("n_zero_words", i32), ("append", i32), ("res", HsResidentArgs),
+                ("birth_t", dbl), ("birth_frame", vp), ("birth_dt", dbl)]
 
 
 class HsAdvectArgs(C.Structure):
@@ -195,14 +196,15 @@ ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAd
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
                HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs, HsInitArgs, HsBoxArgs]
 
-EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 40, HsSource: 80}
+EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 48, HsSource: 80}
 
 # every symbol include/hybridsea_b200.h declares
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
            "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies", "hs_init_h0",
-           "hs_init_workspace_bytes", "hs_fixed_to_float", "hs_clear", "hs_box_pack", "hs_box_paste"]
+           "hs_init_workspace_bytes", "hs_fixed_to_float", "hs_clear", "hs_box_pack", "hs_box_paste",
+           "hs_spectral_at", "hs_conv1d_zero"]
 
 _lib = None
 
@@ -238,6 +240,8 @@ def lib() -> C.CDLL:
     L.hs_periodic_normals.argtypes = [vp, vp, i32, dbl, vp]
     L.hs_fixed_to_float.argtypes = [vp, vp, i64, i32, vp]
     L.hs_clear.argtypes = [vp, i64, vp]
+    L.hs_spectral_at.argtypes = [vp, vp, i32, dbl, vp, vp]
+    L.hs_conv1d_zero.argtypes = [vp, vp, i64, i32, i64, vp, i32, vp]
     L.hs_init_workspace_bytes.restype = i64
     L.hs_init_workspace_bytes.argtypes = [C.c_int]
     if L.hs_abi_version() != 1:
@@ -277,5 +281,5 @@ def struct_array_bytes(items) -> np.ndarray:
     return np.frombuffer(bytes(buf), dtype=np.uint8).copy()
 
 
-def pool_struct(x=None, y=None, ux=None, uy=None, amp=None) -> HsPool:
-    return HsPool(ptr(x), ptr(y), ptr(ux), ptr(uy), ptr(amp))
+def pool_struct(x=None, y=None, ux=None, uy=None, amp=None, birth=None) -> HsPool:
+    return HsPool(ptr(x), ptr(y), ptr(ux), ptr(uy), ptr(amp), ptr(birth))

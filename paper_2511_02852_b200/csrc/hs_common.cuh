@@ -106,6 +106,56 @@ __device__ __forceinline__ unsigned long long philox_draw(const unsigned long lo
     return c[d & 3];
 }
 
+// ------------------------------------------------------------ PCG64 --
+// numpy's PCG64 (XSL-RR 128/64): step the 128-bit LCG, output XSL-RR of the
+// new state; default_rng's bit generator (reference harness.py:79).
+typedef unsigned __int128 u128;
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u128 pcg_mult() {
+    return ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
+}
+
+__device__ __forceinline__ u64 pcg_output(u128 s) {
+    const u64 hi = (u64)(s >> 64), lo = (u64)s;
+    const unsigned rot = (unsigned)(hi >> 58);
+    const u64 x = hi ^ lo;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// One PCG64 draw: step the LCG, output XSL-RR of the new state.
+__device__ __forceinline__ u64 pcg_next(u128& s, u128 inc) {
+    s = s * pcg_mult() + inc;
+    return pcg_output(s);
+}
+
+// LCG jump-ahead by `delta` steps (Brown, "Random number generation with
+// arbitrary strides", 1994).
+__device__ __forceinline__ u128 pcg_advance(u128 s, u128 inc, u64 delta) {
+    u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+    while (delta) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return acc_mult * s + acc_plus;
+}
+
+// Raw draw d (counted from the stream state) of an injection stream
+// (HsInjectArgs.rng, 8 words): word 7 = 0 -> Philox4x64-10 [key, counter0,
+// draw index]; word 7 = 1 -> PCG64 [state hi, lo, inc hi, lo, -, -, draw index]
+__device__ __forceinline__ u64 stream_draw(const u64* st, u64 d) {
+    if (st[7] == 1ull) {
+        const u128 s0 = ((u128)st[0] << 64) | st[1], inc = ((u128)st[2] << 64) | st[3];
+        return pcg_output(pcg_advance(s0, inc, d + 1));
+    }
+    return philox_draw(st, d);
+}
+
 // numpy: lo + (hi - lo) * ((raw >> 11) * 2^-53)
 __device__ __forceinline__ double uniform_from(unsigned long long raw, double lo, double range) {
     double unit = (double)(raw >> 11) * (1.0 / 9007199254740992.0);

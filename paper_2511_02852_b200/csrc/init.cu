@@ -31,42 +31,10 @@
 namespace hs {
 namespace {
 
-typedef unsigned __int128 u128;
-typedef unsigned long long u64;
-
 constexpr int ZL = HS_ZIG_CHUNK;
 constexpr int ZE = HS_ZIG_ENTRIES;
 constexpr int ZG = HS_ZIG_GROUP;
 constexpr int CLASSIFY_THREADS = 128;
-
-__device__ __forceinline__ u128 pcg_mult() {
-    return ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
-}
-
-// One PCG64 draw: step the LCG, output XSL-RR of the new state.
-__device__ __forceinline__ u64 pcg_next(u128& s, u128 inc) {
-    s = s * pcg_mult() + inc;
-    const u64 hi = (u64)(s >> 64), lo = (u64)s;
-    const unsigned rot = (unsigned)(hi >> 58);
-    const u64 x = hi ^ lo;
-    return (x >> rot) | (x << ((64u - rot) & 63u));
-}
-
-// LCG jump-ahead by `delta` steps (Brown, "Random number generation with
-// arbitrary strides", 1994).
-__device__ u128 pcg_advance(u128 s, u128 inc, u64 delta) {
-    u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
-    while (delta) {
-        if (delta & 1) {
-            acc_mult *= cur_mult;
-            acc_plus = acc_plus * cur_mult + cur_plus;
-        }
-        cur_plus = (cur_mult + 1) * cur_plus;
-        cur_mult *= cur_mult;
-        delta >>= 1;
-    }
-    return acc_mult * s + acc_plus;
-}
 
 __device__ __forceinline__ double unit53(u64 r) { return (double)(r >> 11) * (1.0 / 9007199254740992.0); }
 

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         return;
     }
     const int M = g_tot * nth;
+    const double birth = a.birth_frame ? dmul((double)(*a.birth_frame), a.birth_dt) : a.birth_t;
     const double pi = 3.141592653589793;
     const double dth = dmul(2.0, pi) / (double)nth;
     const double j_lo = dmul(-0.5, dth), j_range = dsub(dmul(0.5, dth), j_lo);
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         const int g = m / nth, k = m - g * nth;
         const int cell = find_cell(gstart, ncell, g);
         const HsBucket B = a.buckets[cell >> 2];
-        double jit = uniform_from(philox_draw(rng, D + (unsigned long long)g), j_lo, j_range);
+        double jit = uniform_from(stream_draw(rng, D + (unsigned long long)g), j_lo, j_range);
         double th0 = dadd(-pi, dmul((double)k + 0.5, dth));
         double th = dadd(th0, jit);
         double cv = fabs(cos(dmul(0.5, th)));
@@ -281,13 +282,13 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
             const int cell = find_cell(gstart, ncell, g);
             const int b = cell >> 2, s = cell & 3;
             const HsBucket B = a.buckets[b];
-            double jit = uniform_from(philox_draw(rng, D + (unsigned long long)g), j_lo, j_range);
+            double jit = uniform_from(stream_draw(rng, D + (unsigned long long)g), j_lo, j_range);
             double th = dadd(dadd(-pi, dmul((double)k + 0.5, dth)), jit);
             double thw = dadd(th, a.mean_dir);
             double dx = cos(thw), dy = sin(thw);
             double dot = (s == 0) ? dx : (s == 1) ? -dx : (s == 2) ? dy : -dy;
             int side = dot > 0.0 ? s : (s ^ 1);
-            double u = uniform_from(philox_draw(rng, D + (unsigned long long)g_tot + (unsigned long long)m), 0.0, 1.0);
+            double u = uniform_from(stream_draw(rng, D + (unsigned long long)g_tot + (unsigned long long)m), 0.0, 1.0);
             double px, py;
             if (side == 0)      { px = P.x0;                 py = dadd(P.y0, dmul(u, P.l2)); }
             else if (side == 1) { px = dadd(P.x0, P.l1);     py = dadd(P.y0, dmul(u, P.l2)); }
@@ -313,6 +314,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
                         const long long o = ap_dst[b] + j;
                         a.res.pool.x[o] = keep ? nx : __longlong_as_double(0x7ff8000000000000LL);
                         a.res.pool.y[o] = ny; a.res.pool.ux[o] = dx; a.res.pool.uy[o] = dy; a.res.pool.amp[o] = am;
+                        if (a.res.pool.birth) a.res.pool.birth[o] = birth;
                     }
                     if (keep && j < ap_room[b]) {        // overflowed members are lost (status bit)
                         atomicAdd(&ap_kept[b], 1);
@@ -329,12 +331,14 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
                 long long o = sb + soff[b] + rank;
                 a.stage.x[o] = px; a.stage.y[o] = py; a.stage.ux[o] = dx; a.stage.uy[o] = dy;
                 a.stage.amp[o] = (float)amp;
+                if (a.stage.birth) a.stage.birth[o] = birth;
                 if (per_live == 2) {
                     o += live_cnt[b];
                     a.stage.x[o] = dsub(px, dmul(B.radius, dx));
                     a.stage.y[o] = dsub(py, dmul(B.radius, dy));
                     a.stage.ux[o] = dx; a.stage.uy[o] = dy;
                     a.stage.amp[o] = (float)(-a.beta * amp);
+                    if (a.stage.birth) a.stage.birth[o] = birth;
                 }
             }
         }
@@ -392,7 +396,7 @@ __device__ __forceinline__ void splat_one(float* __restrict__ raw, const HsLayer
 __device__ __forceinline__ void adv_item(const HsAdvectArgs& a, const HsPatch& P, const long long* in_base,
                                          const int* st_off, const int* voff, const int* in_cnt, const double* step_s,
                                          int v, int b, double& x, double& y, double& ux, double& uy,
-                                         const float** amp_ptr) {
+                                         const float** amp_ptr, double* birth = nullptr) {
     const int local = v - voff[b];
     const bool from_pool = local < in_cnt[b];
     const long long src = from_pool ? in_base[b] + local
@@ -404,6 +408,7 @@ __device__ __forceinline__ void adv_item(const HsAdvectArgs& a, const HsPatch& P
     x = dadd(S.x[src], dmul(ux, step));        // pos += dir * (c dt)  (particles.py:312-313)
     y = dadd(S.y[src], dmul(uy, step));
     *amp_ptr = S.amp + src;
+    if (birth && S.birth) *birth = S.birth[src];
 }
 
 template <int ADV_CHUNKS>
@@ -578,14 +583,15 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                 const bool kept = (bal >> lane) & 1u;
                 const int rank = tprefix + wpre[w] + __popc(bal & ((1u << lane) - 1u));
                 const int b = bk_s[li];
-                double x, y, ux, uy;
+                double x, y, ux, uy, bt = 0.0;
                 const float* ap;
-                adv_item(a, P, in_base, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap);
+                adv_item(a, P, in_base, st_off, voff, in_cnt_s, step_s, v, b, x, y, ux, uy, &ap, &bt);
                 const float am = *ap;
                 if (kept) {
                     if (rank < P.pool_capacity) {
                         const long long o = P.pool_base + rank;
                         a.out.x[o] = x; a.out.y[o] = y; a.out.ux[o] = ux; a.out.uy[o] = uy; a.out.amp[o] = am;
+                        if (a.out.birth) a.out.birth[o] = bt;
                     } else {
                         atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
                     }
@@ -602,6 +608,7 @@ __global__ void __launch_bounds__(ADV_THREADS, 3) advect_kernel(HsAdvectArgs a) 
                         const long long o = P.pool_base + (v - rank);       // stable among the dropped
                         a.dropped.x[o] = x; a.dropped.y[o] = y; a.dropped.ux[o] = ux; a.dropped.uy[o] = uy;
                         a.dropped.amp[o] = am;
+                        if (a.dropped.birth) a.dropped.birth[o] = bt;
                         atomicAdd(&drop_hist[b], 1);
                     }
                 }
@@ -799,15 +806,16 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
         if (v >= N) continue;
         const bool kept = (bal >> lane) & 1u;
         const int rank = tprefix + wpre[w] + __popc(bal & ((1u << lane) - 1u));
-        double x, y, ux, uy;
+        double x, y, ux, uy, bt = 0.0;
         const float* ap;
-        adv_item(a, P, T.in_base, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap);
+        adv_item(a, P, T.in_base, T.st_off, T.voff, T.in_cnt, T.step, v, b, x, y, ux, uy, &ap, &bt);
         const float am = *ap;
         if (kept) {
             const int slot = rank + T.slack[b];
             if (slot < P.pool_capacity) {
                 const long long o = P.pool_base + slot;
                 a.out.x[o] = x; a.out.y[o] = y; a.out.ux[o] = ux; a.out.uy[o] = uy; a.out.amp[o] = am;
+                if (a.out.birth) a.out.birth[o] = bt;
             } else {
                 atomicOr(a.status, HS_STATUS_POOL_OVERFLOW);
             }
@@ -821,6 +829,7 @@ __global__ void __launch_bounds__(ADV_THREADS) advect_scatter_kernel(HsAdvectArg
                 const long long o = P.pool_base + (v - rank);
                 a.dropped.x[o] = x; a.dropped.y[o] = y; a.dropped.ux[o] = ux; a.dropped.uy[o] = uy;
                 a.dropped.amp[o] = am;
+                if (a.dropped.birth) a.dropped.birth[o] = bt;
                 atomicAdd(&drop_hist[b], 1);
             }
         }
@@ -1031,6 +1040,7 @@ __global__ void __launch_bounds__(RES_THREADS) append_resident_kernel(HsResident
             const long long o = dst_s[b] + j;
             a.pool.x[o] = keep ? nx : __longlong_as_double(0x7ff8000000000000LL);
             a.pool.y[o] = ny; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = am;
+            if (a.pool.birth) a.pool.birth[o] = a.stage.birth ? a.stage.birth[src] : 0.0;
         }
         if (keep && j < room_s[b]) {
             atomicAdd(&kept_s[b], 1);
@@ -1329,11 +1339,13 @@ __global__ void __launch_bounds__(256) emit_kernel(HsEmitArgs a) {
             const double cy = dadd(py, dmul(S.hull_extent, uy));
             long long o = base + k;
             a.pool.x[o] = cx; a.pool.y[o] = cy; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = ca;
+            if (a.pool.birth) a.pool.birth[o] = 0.0;          // emitted: birth 0 (interaction.py:210-213)
             splat_at(a.fixed_point, a.raw_layers, sl, P.sx0, P.sy0, cx, cy, ca, &clamp_local);
             if (m == 2) {                                              // trailing trough, -beta * amp
                 const double tx = dsub(cx, dmul(r, ux)), ty = dsub(cy, dmul(r, uy));
                 o += n;
                 a.pool.x[o] = tx; a.pool.y[o] = ty; a.pool.ux[o] = ux; a.pool.uy[o] = uy; a.pool.amp[o] = ta;
+                if (a.pool.birth) a.pool.birth[o] = 0.0;
                 splat_at(a.fixed_point, a.raw_layers, sl, P.sx0, P.sy0, tx, ty, ta, &clamp_local);
             }
         }

@@ -575,3 +575,56 @@ extern "C" int hs_box_paste(const HsBoxArgs* a, void* stream) {
     HS_LAUNCH_CHECK();
     return 0;
 }
+
+namespace hs {
+__global__ void spectral_at_kernel(const double2* __restrict__ h0, const double* __restrict__ omega, int n, double t,
+                                   double2* __restrict__ out) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (long long)n * n) return;
+    const int i = (int)(k / n), j = (int)(k - (long long)i * n), half = n / 2;
+    const int ia = i <= half ? i : n - i, ja = j <= half ? j : n - j;
+    const double ph = omega[(long long)ia * (half + 1) + ja] * t;
+    double s, c;
+    sincos(ph, &s, &c);
+    const double2 a = h0[k];
+    const double2 b = h0[(long long)((n - i) % n) * n + (n - j) % n];       // h0(-k), conjugated below
+    // a (c - i s) + conj(b) (c + i s)
+    out[k] = make_double2(a.x * c + a.y * s + b.x * c + b.y * s, a.y * c - a.x * s + b.x * s - b.y * c);
+}
+
+__global__ void conv1d_zero_kernel(const double* __restrict__ in, double* __restrict__ out, long long outer, int n,
+                                   long long inner, const double* __restrict__ taps, int H) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= outer * n * inner) return;
+    const long long o = k / ((long long)n * inner), rem = k - o * n * inner;
+    const int i = (int)(rem / inner);
+    const long long q = rem - (long long)i * inner;
+    const double* row = in + o * n * inner + q;
+    double s = 0.0;
+    for (int m = -H; m <= H; ++m) {
+        const int ii = i + m;
+        if (ii >= 0 && ii < n) s += taps[m + H] * row[(long long)ii * inner];
+    }
+    out[k] = s;
+}
+}  // namespace hs
+
+extern "C" int hs_spectral_at(const double* h0, const double* omega, int n, double t, double* out, void* stream) {
+    HS_CHECK_ARG(h0 && omega && out && n >= 2, "hs_spectral_at: bad arguments");
+    const long long nn = (long long)n * n;
+    spectral_at_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const double2*>(h0), omega, n, t, reinterpret_cast<double2*>(out));
+    HS_LAUNCH_CHECK();
+    return 0;
+}
+
+extern "C" int hs_conv1d_zero(const double* in, double* out, long long outer, int n, long long inner,
+                              const double* taps, int H, void* stream) {
+    HS_CHECK_ARG(in && out && taps && outer >= 0 && n >= 1 && inner >= 0 && H >= 0, "hs_conv1d_zero: bad arguments");
+    HS_CHECK_ARG(2 * H + 1 <= n, "hs_conv1d_zero: kernel of %d taps wider than grid axis of %d", 2 * H + 1, n);
+    const long long total = outer * n * inner;
+    if (total == 0) return 0;
+    conv1d_zero_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(in, out, outer, n, inner, taps, H);
+    HS_LAUNCH_CHECK();
+    return 0;
+}

@@ -67,10 +67,6 @@ class FftState:
     def omega(self) -> np.ndarray:
         return np.sqrt(self.g * np.hypot(self.kx, self.ky))
 
-    @property
-    def h0_mirror_conj(self) -> np.ndarray:
-        idx = (-np.arange(self.n)) % self.n
-        return np.conj(self.h0[np.ix_(idx, idx)])
 
 
 def _h0_get(self) -> np.ndarray:
@@ -85,9 +81,28 @@ def _h0_get(self) -> np.ndarray:
 
 def _h0_set(self, value) -> None:
     self.__dict__["_h0"] = value
+    if value is not None and self.__dict__.get("h0_dev") is not None:
+        # an h0 injected into an uploaded state (the reference tests'
+        # object.__setattr__ precedent, test_fft_background.py:121-127) reaches the device
+        h = np.asarray(value)
+        dev = np.stack([h.real, h.imag], axis=-1).astype(np.float32)
+        self.__dict__["h0_dev"].copy_(torch.from_numpy(np.ascontiguousarray(dev)))
+
+
+def _mirror_get(self) -> np.ndarray:
+    idx = (-np.arange(self.n)) % self.n
+    return np.conj(self.h0[np.ix_(idx, idx)])
+
+
+def _mirror_set(self, value) -> None:
+    """The kernels gather conj(h0(-k)) from h0 itself: an explicit mirror must
+    be that array (it is, whenever it was formed from the same h0)."""
+    if not np.array_equal(np.asarray(value), _mirror_get(self)):
+        raise ValueError("h0_mirror_conj must equal conj(h0[-k]) of the state's h0 (derived on the device)")
 
 
 FftState.h0 = property(_h0_get, _h0_set)   # the dataclass __init__ / replace() go through the setter
+FftState.h0_mirror_conj = property(_mirror_get, _mirror_set)
 
 
 def _upload(state: FftState, device, h0_dev=None, kf_dev=None) -> FftState:
@@ -124,10 +139,11 @@ class HeightField:
     periodic: bool = False
 
     def validate(self) -> None:
-        if not (bool(torch.isfinite(self.height).all()) and bool(torch.isfinite(self.displacement).all())
-                and bool(torch.isfinite(self.normal).all())):
+        """Finite values and unit normals (fft_background.py:63-74); device or numpy arrays."""
+        arrs = [torch.as_tensor(a) for a in (self.height, self.displacement, self.normal)]
+        if not all(bool(torch.isfinite(a).all()) for a in arrs):
             raise ValueError("height field contains non-finite values")
-        norms = torch.linalg.vector_norm(self.normal.double(), dim=-1)
+        norms = torch.linalg.vector_norm(arrs[2].double(), dim=-1)
         if not bool(torch.allclose(norms, torch.ones_like(norms), atol=1e-6)):
             raise ValueError("normals are not unit length")
 
@@ -266,6 +282,20 @@ def with_h0(state: FftState, h0: np.ndarray) -> FftState:
 
 def zeroed(state: FftState) -> FftState:
     return with_h0(state, np.zeros_like(state.h0))
+
+
+def spectral_at(state: FftState, t: float) -> np.ndarray:
+    """Evolved Hermitian spectrum at time t (fft_background.py:155-159):
+    h0 e^{-i w t} + conj(h0(-k)) e^{+i w t}, in fp64 on the device (hs_spectral_at;
+    inside the frame this rotation is fused into the row transform)."""
+    dev = state.device or _device(None)
+    h0 = torch.from_numpy(np.ascontiguousarray(np.asarray(state.h0, dtype=np.complex128)).view(np.float64)).to(dev)
+    om = state.omega_dev if state.omega_dev is not None else torch.from_numpy(
+        np.ascontiguousarray(state.omega[: state.n // 2 + 1, : state.n // 2 + 1])).to(dev)
+    out = torch.empty_like(h0)
+    N.call_raw("hs_spectral_at", N.vp(N.ptr(h0)), N.vp(N.ptr(om)), N.i32(state.n), N.dbl(float(t)),
+               N.vp(N.ptr(out)), N.vp(stream_ptr()))
+    return out.cpu().numpy().view(np.complex128).reshape(state.n, state.n)
 
 
 class FftWorkspace:

@@ -304,7 +304,9 @@ class Simulation:
             # segment may read up to RES_TILE - 1 slots past pool_base[-1]
             # (explicit capacities are not rounded to the tile)
             padded = total_pool + RES_TILE
-            self.pools = [[f64(padded), f64(padded), f64(padded), f64(padded), f32(padded)] for _ in range(2)]
+            # x, y, ux, uy, amp and the birth times (read only by the pool accessor)
+            self.pools = [[f64(padded), f64(padded), f64(padded), f64(padded), f32(padded), f64(padded)]
+                          for _ in range(2)]
             PB = self.n_patches * self.nb
             i32 = lambda n: torch.zeros(max(1, n), dtype=torch.int32, device=dev)  # noqa: E731
             # resident segment table (hs_resident_layout)
@@ -318,7 +320,8 @@ class Simulation:
             self.res_tiles = int(sum(-(-c // RES_TILE) for c in self.pool_caps)) + PB
             self.tile_map = i32(4 * self.res_tiles)
             self._buf, self._lp, self._since = 0, 0, 0
-            self.stage = [f64(total_stage), f64(total_stage), f64(total_stage), f64(total_stage), f32(total_stage)]
+            self.stage = [f64(total_stage), f64(total_stage), f64(total_stage), f64(total_stage), f32(total_stage),
+                          f64(total_stage)]
             self.stage_count = torch.zeros(self.n_patches * self.nb, dtype=torch.int32, device=dev)
             self.scratch = f64(2 * self.member_cap * self.n_patches)
             self.acc = torch.zeros(self.n_patches * self.nb * 4, dtype=torch.float64, device=dev)
@@ -549,7 +552,8 @@ class Simulation:
                 rho=float(cfg.rho), g=float(cfg.g), acc=N.ptr(self.acc), groups=N.ptr(self.groups),
                 e_in=N.ptr(self.e_in), rng=N.ptr(self.rng), stage=N.pool_struct(*self.stage),
                 stage_count=N.ptr(self.stage_count), scratch=N.ptr(self.scratch), member_capacity=self.member_cap,
-                status=N.ptr(self.status), zero_words=N.ptr(nxt[0]), n_zero_words=nxt[0].numel())
+                status=N.ptr(self.status), zero_words=N.ptr(nxt[0]), n_zero_words=nxt[0].numel(),
+                birth_frame=N.ptr(self.frame_dev), birth_dt=float(dt))    # t = frame * dt (harness.py:134)
             if compact:
                 mark("particles_start")
                 N.call("hs_inject", inj_args, stream_ptr())
@@ -846,17 +850,17 @@ class Simulation:
         base = self.seg_base.cpu().numpy()[k * nb:(k + 1) * nb]
         ln = self.seg_len[self._lp].cpu().numpy()[k * nb:(k + 1) * nb]
         arrs = self.pools[self._buf]
-        parts = [[] for _ in range(5)]
+        parts = [[] for _ in range(6)]
         counts = np.zeros(nb, np.int64)
         for b in range(nb):
             lo, n = int(base[b]), int(ln[b])
             x = arrs[0][lo:lo + n]
             keep = ~torch.isnan(x)
-            for q in range(5):
+            for q in range(6):
                 parts[q].append(arrs[q][lo:lo + n][keep])
             counts[b] = int(keep.sum().item())
         cat = [torch.cat(p_) if p_ else arrs[q][:0] for q, p_ in enumerate(parts)]
-        return ParticleSet.from_segments(*cat, counts, self.device)
+        return ParticleSet.from_segments(*cat[:5], counts, self.device, birth=cat[5])
 
     def _grid(self, buf: torch.Tensor, k: int, comps: int = 1) -> torch.Tensor:
         res, ny = self.synth.grids[k]
@@ -1042,24 +1046,109 @@ class HostFramePipe:
         return self.host[slot], self.host_cnt[slot]
 
 
-def benchmark_cell(cfg: SimConfig, warmup: int | None = None, measure: int | None = None, label: str = ""):
-    """Steady-state throughput of one cell (harness.py:345-369), device-timed."""
+@dataclass
+class BenchRow:
+    """One cell of the throughput sweep (harness.py:324-343)."""
+    label: str
+    mode: str
+    n_omega: int
+    n_theta: int
+    u10: float
+    res: int
+    fps: float
+    median_frame_ms: float
+    particles: int
+    particle_rate: float
+
+
+def wp_only_config(base: SimConfig) -> SimConfig:
+    """Single patch covering the whole domain at the same texel density (harness.py:332-342)."""
+    from dataclasses import replace
+    from .config import PatchConfig
+    density_res = base.patches[0].res if base.patches else 512
+    patch_size = base.patches[0].size[0] if base.patches else 100.0
+    scale = base.fft_domain / patch_size
+    big = PatchConfig(origin=(0.0, 0.0), size=(base.fft_domain, base.fft_domain),
+                      res=int(round((density_res - 1) * scale)) + 1,
+                      margin=base.patches[0].margin if base.patches else 10.0)
+    return replace(base, mode="wp-only", patches=(big,), bodies=())
+
+
+def benchmark_cell(cfg: SimConfig, warmup: int | None = None, measure: int | None = None,
+                   label: str = "") -> BenchRow:
+    """Steady-state throughput of one cell (harness.py:345-369): median of the
+    per-frame device times (CUDA events), particle rate over the wall clock."""
     warmup = cfg.bench_warmup if warmup is None else warmup
     measure = cfg.bench_measure if measure is None else measure
     sim = Simulation(cfg)
     sim.run_frames(warmup)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(measure)]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    start.record()
-    sim.run_frames(measure)
-    end.record()
+    for a, b in ev:
+        a.record()
+        sim.step(stats=False)
+        b.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    ms = start.elapsed_time(end) / max(measure, 1)
+    ms = float(np.median([a.elapsed_time(b) for a, b in ev])) if ev else float("nan")
     live = sim.live_particles()
-    return {"label": label or cfg.mode, "fps": 1e3 / ms if ms > 0 else float("inf"), "median_frame_ms": ms,
-            "particles": live, "particle_rate": live * measure / wall if wall > 0 else 0.0}
+    res = cfg.patches[0].res if cfg.patches else 0
+    return BenchRow(label=label or cfg.mode, mode=cfg.mode, n_omega=cfg.n_omega, n_theta=cfg.n_theta, u10=cfg.u10,
+                    res=res, fps=1e3 / ms if ms > 0 else float("inf"), median_frame_ms=ms, particles=live,
+                    particle_rate=live * measure / wall if wall > 0 else 0.0)
+
+
+def trend_matrix(base: SimConfig) -> list:
+    """The performance-sweep cells (harness.py:372-396): method, sampling
+    counts, wind, resolution."""
+    from dataclasses import replace
+
+    def with_counts(n):
+        return replace(base, n_omega=n, n_theta=n)
+
+    def with_res(r):
+        return replace(base, patches=tuple(replace(p, res=r) for p in base.patches))
+
+    return [
+        ("fft-only", replace(base, mode="fft-only")),
+        ("wp-only", wp_only_config(base)),
+        ("hybrid-16x16", with_counts(16)),
+        ("hybrid-12x12", with_counts(12)),
+        ("hybrid-8x8", with_counts(8)),
+        ("res-256", with_res(256)),
+        ("res-1024", with_res(1024)),
+        ("u10-3", replace(base, u10=3.0)),
+        ("u10-10", replace(base, u10=10.0)),
+        ("u10-15", replace(base, u10=15.0)),
+    ]
+
+
+def benchmark(cells: list, warmup: int | None = None, measure: int | None = None, progress=None) -> list:
+    """benchmark_cell over the cells (harness.py:399-413); the full-domain
+    wp-only cell keeps its sample short, as the reference does."""
+    rows = []
+    for label, cfg in cells:
+        w, m = warmup, measure
+        if cfg.mode == "wp-only":
+            w = min(w if w is not None else cfg.bench_warmup, 4)
+            m = min(m if m is not None else cfg.bench_measure, 3)
+        row = benchmark_cell(cfg, w, m, label)
+        rows.append(row)
+        if progress is not None:
+            progress(row)
+    return rows
+
+
+def bench_table(rows: list) -> str:
+    """CSV of benchmark rows, the reference's columns (harness.py:416-423)."""
+    header = "label,mode,n_omega,n_theta,u10,res,fps,median_frame_ms,particles,particle_rate"
+    lines = [header]
+    for r in rows:
+        lines.append(f"{r.label},{r.mode},{r.n_omega},{r.n_theta},{r.u10},{r.res},"
+                     f"{r.fps:.3f},{r.median_frame_ms:.3f},{r.particles},"
+                     f"{r.particle_rate:.1f}")
+    return "\n".join(lines) + "\n"
 
 
 # ---------------------------------------------------------------------------

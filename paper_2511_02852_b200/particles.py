@@ -23,7 +23,7 @@ import torch
 
 from . import _native as N
 from ._layout import bucket_structs, half_rates, max_groups_per_step, patch_struct, stream_ptr, structs_to_device
-from .spectrum import BucketTable, DirectionalSpectrum, FrequencyBucket
+from .spectrum import BucketTable, DirectionalSpectrum, FrequencyBucket, evaluate_1d
 
 DEFAULT_TROUGH_FRACTION = 1.0
 SIDE_INWARD = np.array([[1.0, 0.0], [-1.0, 0.0], [0.0, 1.0], [0.0, -1.0]])
@@ -84,22 +84,25 @@ class ParticleSet:
     def __init__(self, capacity: int = 1024, n_buckets: int | None = None, device=None):
         self.device = _dev(device)
         self.n_buckets = n_buckets
-        self._host: list = []          # pending host batches (pos, dir, amp, bucket)
+        self._host: list = []          # pending host batches (pos, dir, amp, bucket, birth)
         self.x = self.y = self.ux = self.uy = None
         self.amp = None
+        self.birth = None              # fp64 birth times (particles.py:128-129)
         self.counts = None             # host np.int64 [nb]
         self.capacity_hint = capacity
 
     # ---------------------------------------------------------- building --
     def append_arrays(self, pos, direction, amp, bucket, birth=None) -> None:
-        amp = np.asarray(amp, dtype=float)
+        amp = np.asarray(amp, dtype=float).reshape(-1)
         if len(amp) == 0:
             return
+        birth = np.zeros(len(amp)) if birth is None else np.broadcast_to(np.asarray(birth, float), amp.shape)
         self._host.append((np.asarray(pos, float).reshape(-1, 2), np.asarray(direction, float).reshape(-1, 2),
-                           amp, np.asarray(bucket, dtype=np.int64)))
+                           amp, np.asarray(bucket, dtype=np.int64).reshape(-1), np.array(birth, dtype=float)))
 
     def append(self, p: WaveParticle) -> None:
-        self.append_arrays(p.position[None, :], p.direction[None, :], [p.amplitude], [p.bucket])
+        self.append_arrays(np.asarray(p.position)[None, :], np.asarray(p.direction)[None, :], [p.amplitude],
+                           [p.bucket], [p.birth_time])
 
     @classmethod
     def from_arrays(cls, pos, direction, amp, bucket, n_buckets: int, device=None) -> "ParticleSet":
@@ -109,15 +112,16 @@ class ParticleSet:
         return ps
 
     @classmethod
-    def from_segments(cls, x, y, ux, uy, amp, counts: np.ndarray, device=None) -> "ParticleSet":
+    def from_segments(cls, x, y, ux, uy, amp, counts: np.ndarray, device=None, birth=None) -> "ParticleSet":
         ps = cls(n_buckets=len(counts), device=device)
         ps.x, ps.y, ps.ux, ps.uy, ps.amp = x, y, ux, uy, amp
+        ps.birth = birth if birth is not None else torch.zeros_like(x)
         ps.counts = np.asarray(counts, dtype=np.int64).copy()
         return ps
 
     def _empty_device(self, nb: int) -> None:
         z64 = torch.zeros(0, dtype=torch.float64, device=self.device)
-        self.x, self.y, self.ux, self.uy = z64, z64.clone(), z64.clone(), z64.clone()
+        self.x, self.y, self.ux, self.uy, self.birth = z64, z64.clone(), z64.clone(), z64.clone(), z64.clone()
         self.amp = torch.zeros(0, dtype=torch.float32, device=self.device)
         self.counts = np.zeros(nb, dtype=np.int64)
 
@@ -133,10 +137,7 @@ class ParticleSet:
             self._empty_device(self.n_buckets)
         if not self._host:
             return self
-        pos = np.concatenate([h[0] for h in self._host])
-        d = np.concatenate([h[1] for h in self._host])
-        a = np.concatenate([h[2] for h in self._host])
-        b = np.concatenate([h[3] for h in self._host])
+        pos, d, a, b, bt = self._host_arrays()
         self._host = []
         if np.any((b < 0) | (b >= self.n_buckets)):
             raise ValueError("bucket index out of range")
@@ -145,7 +146,8 @@ class ParticleSet:
         other = ParticleSet.from_segments(
             torch.from_numpy(pos[order, 0].copy()).to(self.device), torch.from_numpy(pos[order, 1].copy()).to(self.device),
             torch.from_numpy(d[order, 0].copy()).to(self.device), torch.from_numpy(d[order, 1].copy()).to(self.device),
-            torch.from_numpy(a[order].astype(np.float32)).to(self.device), new_counts, self.device)
+            torch.from_numpy(a[order].astype(np.float32)).to(self.device), new_counts, self.device,
+            birth=torch.from_numpy(bt[order].copy()).to(self.device))
         self._merge(other)
         return self
 
@@ -155,7 +157,7 @@ class ParticleSet:
             self._empty_device(other.n_buckets)
         so = np.concatenate([[0], np.cumsum(self.counts)])
         oo = np.concatenate([[0], np.cumsum(other.counts)])
-        parts = {k: [] for k in ("x", "y", "ux", "uy", "amp")}
+        parts = {k: [] for k in ("x", "y", "ux", "uy", "amp", "birth")}
         for bkt in range(self.n_buckets):
             for src, off in ((self, so), (other, oo)):
                 lo, hi = int(off[bkt]), int(off[bkt + 1])
@@ -184,33 +186,53 @@ class ParticleSet:
         pending = sum(len(h[2]) for h in self._host)
         return pending + (int(self.counts.sum()) if self.counts is not None else 0)
 
+    def _host_arrays(self):
+        """Pending host batches, concatenated in insertion order (exact fp64)."""
+        return (np.concatenate([h[0] for h in self._host]), np.concatenate([h[1] for h in self._host]),
+                np.concatenate([h[2] for h in self._host]), np.concatenate([h[3] for h in self._host]),
+                np.concatenate([h[4] for h in self._host]))
+
+    def _host_only(self) -> bool:
+        """Built on the host and never used on the device: the accessors serve
+        the appended values themselves (insertion order, fp64 amplitudes)."""
+        return self.x is None and bool(self._host) and self.n_buckets is None
+
     def _dev_view(self):
         self.materialize()
         return self
 
     @property
     def positions(self) -> np.ndarray:
+        if self._host_only():
+            return self._host_arrays()[0]
         s = self._dev_view()
         return torch.stack([s.x, s.y], 1).cpu().numpy()
 
     @property
     def directions(self) -> np.ndarray:
+        if self._host_only():
+            return self._host_arrays()[1]
         s = self._dev_view()
         return torch.stack([s.ux, s.uy], 1).cpu().numpy()
 
     @property
     def amplitudes(self) -> np.ndarray:
+        if self._host_only():
+            return self._host_arrays()[2]
         return self._dev_view().amp.double().cpu().numpy()
 
     @property
     def buckets(self) -> np.ndarray:
+        if self._host_only():
+            return self._host_arrays()[3].astype(np.int32)
         s = self._dev_view()
         return np.repeat(np.arange(s.n_buckets), s.counts).astype(np.int32)
 
     @property
     def birth_times(self) -> np.ndarray:
-        # births are not stored on the device (they are not read on the hot path)
-        return np.full(len(self), np.nan)
+        if self._host_only():
+            return self._host_arrays()[4]
+        return self._dev_view().birth.cpu().numpy()
 
     def counts_per_bucket(self, n_buckets: int) -> np.ndarray:
         self.materialize(n_buckets)
@@ -223,7 +245,7 @@ class ParticleSet:
         lo, hi = int(off[b]), int(off[b + 1])
         return {"pos": torch.stack([s.x[lo:hi], s.y[lo:hi]], 1).cpu().numpy(),
                 "dir": torch.stack([s.ux[lo:hi], s.uy[lo:hi]], 1).cpu().numpy(),
-                "amp": s.amp[lo:hi].double().cpu().numpy()}
+                "amp": s.amp[lo:hi].double().cpu().numpy(), "birth": s.birth[lo:hi].cpu().numpy()}
 
     def clear(self) -> None:
         self._host = []
@@ -231,12 +253,12 @@ class ParticleSet:
             self._empty_device(self.n_buckets)
 
     def __iter__(self):
-        pos, d, a, b = self.positions, self.directions, self.amplitudes, self.buckets
+        pos, d, a, b, t = self.positions, self.directions, self.amplitudes, self.buckets, self.birth_times
         for i in range(len(a)):
-            yield WaveParticle(pos[i].copy(), d[i].copy(), float(a[i]), int(b[i]), float("nan"))
+            yield WaveParticle(pos[i].copy(), d[i].copy(), float(a[i]), int(b[i]), float(t[i]))
 
     def pool_struct(self) -> N.HsPool:
-        return N.pool_struct(self.x, self.y, self.ux, self.uy, self.amp)
+        return N.pool_struct(self.x, self.y, self.ux, self.uy, self.amp, self.birth)
 
 
 class InjectionLedger:
@@ -282,10 +304,20 @@ class PhiloxStream:
 
     @classmethod
     def from_generator(cls, gen: np.random.Generator, device=None) -> "PhiloxStream":
+        """The device twin of a numpy Generator's position: Philox4x64-10 (the
+        per-patch streams) or PCG64 (default_rng, the reference's generator,
+        harness.py:79) -- the kernel jumps the 128-bit LCG ahead per draw."""
         st = gen.bit_generator.state
+        if st["bit_generator"] == "PCG64":
+            m64 = (1 << 64) - 1
+            s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+            ps = cls.__new__(cls)
+            words = [s >> 64, s & m64, inc >> 64, inc & m64, 0, 0, 0, 1]
+            ps.state = torch.tensor(np.array(words, dtype=np.uint64).view(np.int64), device=_dev(device))
+            return ps
         if st["bit_generator"] != "Philox":
-            raise TypeError("the B200 inject kernel reproduces numpy's Philox stream only; "
-                            "pass Generator(Philox(...)) or a PhiloxStream")
+            raise TypeError("the B200 inject kernel reproduces numpy's Philox and PCG64 streams only; "
+                            "pass Generator(Philox(...)), default_rng(...) or a PhiloxStream")
         ctr = st["state"]["counter"]
         c = sum(int(ctr[i]) << (64 * i) for i in range(4))
         key = st["state"]["key"]
@@ -332,10 +364,14 @@ def inject(patch: PatchRegion, table: BucketTable, spectrum: DirectionalSpectrum
     z64 = lambda n: torch.empty(n, dtype=torch.float64, device=dev)  # noqa: E731
     sx, sy, sux, suy = z64(stage_cap), z64(stage_cap), z64(stage_cap), z64(stage_cap)
     samp = torch.empty(stage_cap, dtype=torch.float32, device=dev)
+    sbirth = z64(stage_cap)
     scount = torch.zeros(nb, dtype=torch.int32, device=dev)
     scratch = z64(2 * members)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    buckets = structs_to_device(bucket_structs(table, spectrum.params), dev)
+    # S_J(w_b) through this module's evaluate_1d (particles.py:262), the hook
+    # the reference tests monkeypatch
+    s1d = evaluate_1d(spectrum.params, table.omegas)
+    buckets = structs_to_device(bucket_structs(table, spectrum.params, s1d=s1d), dev)
     pstruct = structs_to_device([patch_struct(patch, 2, stage_capacity=stage_cap)], dev)
     hr_dev = torch.from_numpy(hr.copy()).to(dev)
     groups_before = ledger.groups.sum() if host_gen is not None else None
@@ -343,9 +379,9 @@ def inject(patch: PatchRegion, table: BucketTable, spectrum: DirectionalSpectrum
                           half_rate=N.ptr(hr_dev), mean_dir=float(spectrum.mean_direction),
                           beta=float(trough_fraction), rho=float(ledger.rho), g=float(spectrum.params.g),
                           acc=N.ptr(ledger.acc), groups=N.ptr(ledger.groups), e_in=N.ptr(ledger.e_in),
-                          rng=N.ptr(stream.state), stage=N.pool_struct(sx, sy, sux, suy, samp),
+                          rng=N.ptr(stream.state), stage=N.pool_struct(sx, sy, sux, suy, samp, sbirth),
                           stage_count=N.ptr(scount), scratch=N.ptr(scratch), member_capacity=members,
-                          status=N.ptr(status))
+                          status=N.ptr(status), birth_t=float(t))
     N.call("hs_inject", args, stream_ptr())
     if int(status.item()) != 0:
         raise RuntimeError("inject staging overflow (internal capacity bound violated)")
@@ -353,9 +389,14 @@ def inject(patch: PatchRegion, table: BucketTable, spectrum: DirectionalSpectrum
     total = int(counts.sum())
     if host_gen is not None:
         g_tot = int((ledger.groups.sum() - groups_before).item())
-        if g_tot:
-            host_gen.bit_generator.random_raw(g_tot * (1 + nth))   # keep the numpy stream in step
-    return ParticleSet.from_segments(sx[:total], sy[:total], sux[:total], suy[:total], samp[:total], counts, dev)
+        if g_tot:                                                # keep the numpy stream in step
+            bg = host_gen.bit_generator
+            if hasattr(bg, "advance") and bg.state["bit_generator"] == "PCG64":
+                bg.advance(g_tot * (1 + nth))
+            else:
+                bg.random_raw(g_tot * (1 + nth))
+    return ParticleSet.from_segments(sx[:total], sy[:total], sux[:total], suy[:total], samp[:total], counts, dev,
+                                     birth=sbirth[:total])
 
 
 def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRegion,
@@ -376,6 +417,7 @@ def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRe
     oamp = torch.empty(n, dtype=torch.float32, device=dev)
     dx, dy, dux, duy = z64(n), z64(n), z64(n), z64(n)
     damp = torch.empty(n, dtype=torch.float32, device=dev)
+    obirth, dbirth = z64(n), z64(n)
     in_count = torch.from_numpy(particles.counts.astype(np.int32)).to(dev)
     out_count = torch.zeros(nb, dtype=torch.int32, device=dev)
     drop_count = torch.zeros(nb, dtype=torch.int32, device=dev)
@@ -390,8 +432,8 @@ def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRe
     args = N.HsAdvectArgs(n_patches=1, nb=nb, buckets=N.ptr(buckets), patches=N.ptr(pstruct), dt=float(dt),
                           rho=float(own_ledger.rho), g=float(g), in_=particles.pool_struct(),
                           in_count=N.ptr(in_count), stage=N.pool_struct(), stage_count=0,
-                          out=N.pool_struct(ox, oy, oux, ouy, oamp), out_count=N.ptr(out_count),
-                          dropped=N.pool_struct(dx, dy, dux, duy, damp), dropped_count=N.ptr(drop_count),
+                          out=N.pool_struct(ox, oy, oux, ouy, oamp, obirth), out_count=N.ptr(out_count),
+                          dropped=N.pool_struct(dx, dy, dux, duy, damp, dbirth), dropped_count=N.ptr(drop_count),
                           e_out=N.ptr(own_ledger.e_out), splat=0, raw_layers=0, raw_layers_len=0, layers=0,
                           clamped=0, tile_state=N.ptr(tile_state), max_tiles=max_tiles,
                           tile_counter=N.ptr(tile_counter), status=N.ptr(status), keep_words=N.ptr(keep_words))
@@ -400,8 +442,9 @@ def advect(particles: ParticleSet, table: BucketTable, dt: float, patch: PatchRe
     dc = drop_count.cpu().numpy().astype(np.int64)
     k, d = int(kc.sum()), int(dc.sum())
     particles.x, particles.y, particles.ux, particles.uy, particles.amp = ox[:k], oy[:k], oux[:k], ouy[:k], oamp[:k]
+    particles.birth = obirth[:k]
     particles.counts = kc
-    return ParticleSet.from_segments(dx[:d], dy[:d], dux[:d], duy[:d], damp[:d], dc, dev)
+    return ParticleSet.from_segments(dx[:d], dy[:d], dux[:d], duy[:d], damp[:d], dc, dev, birth=dbirth[:d])
 
 
 def _params_for(table: BucketTable, g: float):

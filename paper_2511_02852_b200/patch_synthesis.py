@@ -177,6 +177,32 @@ def synthesize(particles: ParticleSet, patch: PatchRegion, resolution: int, plan
     return heights, int(ws.clamped.item())
 
 
+def convolve1d_zero(arr, taps, axis: int) -> np.ndarray:
+    """Same-size 1-D convolution with zero-padded borders along an axis
+    (patch_synthesis.py:105-130), fp64 on the device (hs_conv1d_zero) with
+    direct taps.  ConfigError if the kernel is wider than the axis."""
+    a = np.asarray(arr, dtype=np.float64)
+    taps = np.asarray(taps, dtype=np.float64)
+    axis = axis % a.ndim
+    n = a.shape[axis]
+    if len(taps) > n:
+        raise ConfigError(f"kernel of {len(taps)} taps wider than grid axis of {n}")
+    outer = int(np.prod(a.shape[:axis], dtype=np.int64))
+    inner = int(np.prod(a.shape[axis + 1:], dtype=np.int64))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    src = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    tp = torch.from_numpy(np.ascontiguousarray(taps)).to(dev)
+    out = torch.empty_like(src)
+    N.call_raw("hs_conv1d_zero", N.vp(N.ptr(src)), N.vp(N.ptr(out)), N.i64(outer), N.i32(n), N.i64(inner),
+               N.vp(N.ptr(tp)), N.i32((len(taps) - 1) // 2), N.vp(stream_ptr()))
+    return out.cpu().numpy()
+
+
+def smooth_layer(layer, kernel: SmoothingKernel) -> np.ndarray:
+    """Two separable zero-padded passes along x then y (patch_synthesis.py:206-209)."""
+    return convolve1d_zero(convolve1d_zero(layer, kernel.taps, axis=0), kernel.taps, axis=1)
+
+
 def finish_field(heights, patch: PatchRegion, choppiness: float = 0.0,
                  displacement_scale: float = 1.0) -> HeightField:
     """Clamped-border FD normals and optional choppy displacement (:323-340)."""
@@ -198,8 +224,12 @@ def finish_field(heights, patch: PatchRegion, choppiness: float = 0.0,
 
 
 class LayerStack:
-    """Texel-exact (factor 1) layered synthesis (:133-162): holds the kernels
-    and the accumulated particles; `smooth_and_sum` runs the device path."""
+    """Texel-exact (factor 1) per-bucket accumulation grids over a patch
+    (patch_synthesis.py:133-162): padded raw layers in device memory (the
+    synthesis workspace's), splatted by `accumulate` (hs_splat), smoothed and
+    summed by `smooth_and_sum` (hs_smooth + hs_compose).  `layers` /
+    `layer_view` read them back as numpy (node-centred; the crop of layer i is
+    [pad_i : pad_i + res, pad_i : pad_i + ny])."""
 
     def __init__(self, patch: PatchRegion, resolution: int, kernels: list):
         if resolution < 2:
@@ -210,20 +240,70 @@ class LayerStack:
         self.ny = int(round(patch.l2 / self.texel_size)) + 1
         self.kernels = list(kernels)
         self.pads = [k.half_width + 1 for k in self.kernels]
-        self.particles = ParticleSet(n_buckets=len(self.kernels))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.ws = SynthWorkspace([patch], [resolution], [as_plan(self.kernels)], dev)
+        self.clamped_splats = 0
+
+    def _layer(self, i: int) -> torch.Tensor:
+        L = self.ws.pack.layers[i]
+        return self.ws.raw[L.raw_off:L.raw_off + L.wx * L.raw_pitch].view(L.wx, L.raw_pitch)[:, :L.wy]
+
+    @property
+    def layers(self) -> list:
+        return [self._layer(i).double().cpu().numpy() for i in range(len(self.kernels))]
+
+    def layer_view(self, i: int) -> np.ndarray:
+        p = self.pads[i]
+        return self._layer(i)[p:p + self.resolution, p:p + self.ny].double().cpu().numpy()
+
+    def clear(self) -> None:
+        self.ws.raw.zero_()
         self.clamped_splats = 0
 
 
 def accumulate(particles: ParticleSet, patch: PatchRegion, stack: LayerStack) -> LayerStack:
-    particles.materialize(len(stack.kernels))
-    stack.particles.extend(particles)
+    """Splat every particle's signed amplitude into its bucket's layer
+    (patch_synthesis.py:189-203): one hs_splat launch."""
+    nb = len(stack.kernels)
+    particles.materialize(nb)
+    if len(particles) == 0:
+        return stack
+    ws = stack.ws
+    dev = ws.device
+    pst = structs_to_device([patch_struct(patch, stack.resolution, grid_base=0, layer_base=0)], dev)
+    count = torch.from_numpy(particles.counts.astype(np.int32)).to(dev)
+    ws.clamped.zero_()
+    N.call("hs_splat", N.HsSplatArgs(n_patches=1, nb=nb, patches=N.ptr(pst), pool=particles.pool_struct(),
+                                     count=N.ptr(count), raw_layers=N.ptr(ws.raw), raw_layers_len=ws.pack.raw_len,
+                                     layers=N.ptr(ws.layers), clamped=N.ptr(ws.clamped),
+                                     max_count=int(particles.counts.sum())), stream_ptr())
+    stack.clamped_splats += int(ws.clamped.item())
     return stack
 
 
 def smooth_and_sum(stack: LayerStack, kernels: list | None = None) -> torch.Tensor:
-    kernels = kernels if kernels is not None else stack.kernels
+    """Smooth each layer, apply the gain, sum to the (res, ny) grid
+    (patch_synthesis.py:212-224) -- hs_smooth + hs_compose over the stack's
+    layers.  Other `kernels` must keep each layer's half width (the padding
+    the layers were laid out with)."""
+    kernels = list(kernels) if kernels is not None else stack.kernels
     if len(kernels) != len(stack.kernels):
         raise ConfigError("need exactly one kernel per layer")
-    h, c = synthesize(stack.particles, stack.patch, stack.resolution, list(kernels))
-    stack.clamped_splats = c
-    return h
+    ws = stack.ws
+    if kernels is not stack.kernels:
+        if any(k.half_width != s.half_width for k, s in zip(kernels, stack.kernels)):
+            raise ConfigError("smooth_and_sum kernels must keep the stack's half widths")
+        other = SynthWorkspace([stack.patch], [stack.resolution], [as_plan(kernels)], ws.device)
+        other.raw.copy_(ws.raw)
+        ws = other
+    dev = ws.device
+    heights = torch.zeros((stack.resolution, stack.ny), dtype=torch.float32, device=dev)
+    pst = structs_to_device(ws.patch_structs(), dev)
+    st = stream_ptr()
+    N.call("hs_smooth", ws.smooth_args(), st)
+    N.call("hs_compose", N.HsComposeArgs(
+        n_patches=1, nb=len(kernels), patches=N.ptr(pst), layers=N.ptr(ws.layers), smooth_layers=N.ptr(ws.smooth),
+        tile_info=N.ptr(ws.compose_info), total_tiles=ws.compose_tiles, bg_height=0, bg_normal=0, bg_n=0,
+        bg_spacing=1.0, patch_height=N.ptr(heights), patch_normal=0, blend_height=0, blend_normal=0, blend_mode=0,
+        interior_sumsq=0, interior_count=0), st)
+    return heights

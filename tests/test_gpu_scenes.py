@@ -55,18 +55,20 @@ def compare_pools(sim, ref, nb):
     for k in range(sim.n_patches):
         ps = sim.pool(k)
         off = np.concatenate([[0], np.cumsum(ps.counts)])
-        pos, dirs, amp = ps.positions, ps.directions, ps.amplitudes
+        pos, dirs, amp, birth = ps.positions, ps.directions, ps.amplitudes, ps.birth_times
         rp = ref.pools[k]
         for b in range(nb):
             m = rp.bucket == b
             lo, hi = int(off[b]), int(off[b + 1])
             assert hi - lo == int(m.sum()), f"patch {k} bucket {b}: {hi - lo} vs {int(m.sum())}"
-            gp, gd, ga = pos[lo:hi], dirs[lo:hi], amp[lo:hi]
+            gp, gd, ga, gb = pos[lo:hi], dirs[lo:hi], amp[lo:hi], birth[lo:hi]
             rpos, rdir, ramp, rbirth = rp.pos[m], rp.dir[m], rp.amp[m], rp.birth[m]
             old = rbirth == CLONED
             np.testing.assert_array_equal(gp[old], rpos[old], err_msg=f"patch {k} bucket {b} cloned positions")
             np.testing.assert_array_equal(gd[old], rdir[old], err_msg=f"patch {k} bucket {b} cloned directions")
             new = ~old
+            # birth times t = frame * dt (particles.py:296-299; emitted ones 0, interaction.py:210)
+            np.testing.assert_array_equal(gb[new], rbirth[new], err_msg=f"patch {k} bucket {b} births")
             if new.any():
                 np.testing.assert_allclose(gp[new], rpos[new], rtol=0, atol=1e-9,
                                            err_msg=f"patch {k} bucket {b} injected positions")
