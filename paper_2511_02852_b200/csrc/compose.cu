@@ -110,7 +110,10 @@ __device__ __forceinline__ int4 bg_footprint(const HsPatch& P, int i0, int j0, d
 //            blend against the periodic background at the patch nodes
 //            (coupling.py:37-40, 120-141); the background bilinear is done
 //            separably from per-row x-lerped tables
-__global__ void __launch_bounds__(NT, 9) compose_kernel(HsComposeArgs a) {
+#ifndef HS_COMPOSE_MINB
+#define HS_COMPOSE_MINB 9         // one wave of 30x30 tiles at C3 (9 x 148 >= 1225); 6..8 measured slower
+#endif
+__global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& W = *reinterpret_cast<TileSmem*>(smem_raw);
     const int nb = a.nb;
