@@ -105,7 +105,7 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
                                     float(k.gain), mid_off if wide else -1, pitch, 0))
             taps.append(np.asarray(k.taps, dtype=np.float32))
             raw_off += wx * pitch                     # stays a multiple of 4
-            sm_off += ncx * ncy
+            sm_off += -(-(ncx * ncy) // 4) * 4          # 16-byte aligned crops (vector stores)
             tap_off += len(k.taps)
             if wide:
                 mid_off += ncx * wy

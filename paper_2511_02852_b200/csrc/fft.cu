@@ -249,15 +249,17 @@ __global__ void normals_periodic_kernel(const float* __restrict__ h, float* __re
 // ------------------------------------------------ register-FFT kernels --
 // n >= 64: each transform is N/16 threads x 16 register elements per pass
 // (fft_reg.cuh).  Same data flow as the radix-2/4 kernels above.
+// om_row: this CTA's row |i| of the host omega table staged in shared memory
+// (or NULL: formed from kf); kxi, kxip = kf[i], kf[ip]; dk = kf[1]
 __device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0, const float2* r1, int i, int ip,
-                                              int j, double t, float2& A0, float2& A1, float2& B0) {
+                                              int j, double t, const double* om_row, double kxi, double kxip,
+                                              double dk, float2& A0, float2& A1, float2& B0) {
     const int n = d.n, half = n >> 1;
     const int jm = (n - j) & (n - 1);
-    const double kxi = d.kf[i], kxip = d.kf[ip], kyj = d.kf[j];
+    const double kyj = dk * (double)(j <= half ? j : j - n);     // the chop factors use it in fp32
     double w;
-    if (d.omega) {   // host table, numpy's sqrt(g hypot(kx, ky)) (fft_background.py:40-47)
-        const int ia = i <= half ? i : n - i, ja = j <= half ? j : n - j;
-        w = __ldg(d.omega + (size_t)ia * (half + 1) + ja);
+    if (om_row) {    // host table, numpy's sqrt(g hypot(kx, ky)) (fft_background.py:40-47)
+        w = om_row[j <= half ? j : n - j];
     } else {
         w = sqrt(d.g * sqrt(fma(kxi, kxi, kyj * kyj)));
     }
@@ -307,21 +309,29 @@ __global__ void fft_rows_reg_kernel(FftDev d) {
     float2* r0 = tw + N;        // h0 row i
     float2* r1 = r0 + N;        // h0 row i'
     float2* buf = r1 + N;       // 3 transforms of NP: A(i), A(i'), B(i)
+    double* om = reinterpret_cast<double*>(buf + 3 * NP);   // omega row |i| (N/2 + 1)
     const int i = blockIdx.x, ip = (N - i) & (N - 1);
     const bool self = (i == ip);
     if (d.sumsq_zero && i == 0 && threadIdx.x == 0) *d.sumsq_zero = 0.0;
+    // every input of the row pair in one cp.async batch: twiddles, h0 rows i and
+    // -i, the dispersion row; the frame counter and wavenumbers load meanwhile
     for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
         cp_async16(tw + 2 * k, d.tw + 2 * k);
         cp_async16(r0 + 2 * k, d.h0 + (size_t)i * N + 2 * k);
         cp_async16(r1 + 2 * k, d.h0 + (size_t)ip * N + 2 * k);
     }
+    if (d.omega) {
+        const double* orow = d.omega + (size_t)(i <= N / 2 ? i : N - i) * (N / 2 + 1);
+        for (int k = threadIdx.x; k <= N / 2; k += blockDim.x) cp_async8(om + k, orow + k, true);
+    }
+    const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame * dt
+    const double kxi = __ldg(d.kf + i), kxip = __ldg(d.kf + ip), dk = __ldg(d.kf + 1);
     cp_async_wait_all();
     __syncthreads();
     FTRACE(1);
-    const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame * dt
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
         float2 A0, A1, B0;
-        spectrum_pair(d, r0, r1, i, ip, j, t, A0, A1, B0);
+        spectrum_pair(d, r0, r1, i, ip, j, t, d.omega ? om : nullptr, kxi, kxip, dk, A0, A1, B0);
         buf[fpad(j)] = A0;
         buf[NP + fpad(j)] = A1;
         buf[2 * NP + fpad(j)] = B0;
@@ -428,7 +438,7 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
     constexpr int CT0 = (256 / T) < 1 ? 1 : ((256 / T) < N / 2 ? (256 / T) : N / 2);
     constexpr int CT = (CT0 < HS_FFT_COLS_MIN_CT && HS_FFT_COLS_MIN_CT * T <= 512) ? HS_FFT_COLS_MIN_CT : CT0;
     const int rows_threads = 3 * T < 32 ? 32 : 3 * T;
-    const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2);
+    const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2) + (size_t)(N / 2 + 1) * sizeof(double);
     const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
     static bool attr = false;
     if (!attr) {

@@ -27,16 +27,52 @@ constexpr int SM_RB = 8;                 // outputs per thread along the convolu
 // x pass of one tile, register-blocked: thread item = (column c, block of 8
 // output rows); the K taps live in registers and each input value is loaded
 // once and feeds up to 8 accumulators.
+#ifdef HS_SMOOTH_TRACE
+__device__ unsigned long long g_strace[4096 * 4];
+__device__ __forceinline__ unsigned long long sgtime() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+#define STRACE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_strace[blockIdx.x * 4 + (k)] = sgtime(); } while (0)
+#else
+#define STRACE(k) do {} while (0)
+#endif
+
 template <int H>
-__device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ in, int IS, float* __restrict__ mid,
-                                                     const float* __restrict__ taps_sm, int W, int MS,
-                                                     float* __restrict__ out, long long out_base, int ncy,
-                                                     int rows_valid, int cols_valid, float* __restrict__ ot) {
+__device__ __forceinline__ void smooth_tile_unrolled(const HsSmoothArgs& a, const HsLayer& L, int cx0, int cy0,
+                                                     float* __restrict__ smem) {
     constexpr int K = 2 * H + 1;
+    constexpr int W = SM_TY + 2 * H;           // staged columns (y halo)
+    constexpr int MS = W | 1;                  // odd row stride: conflict-free column walks
+    constexpr int NV = (W + 1 + 3) >> 2;       // float4s per staged row
+    constexpr int IS = 4 * NV;                 // staged row stride (floats)
+    constexpr int ROWS = SM_TX + 2 * H;
+    float* const in0 = smem;                   // ROWS x IS
+    float* const mid = in0 + ROWS * IS;        // SM_TX x MS
+    float* const ot = in0;                     // the y pass's output reuses the staging rows
+    // the halo's first column ry0 = cy0 + pad - H = cy0 + 1 (pad = H + 1); loading
+    // from cy0 instead makes every staged row 16-byte aligned in global memory
+    // (raw_off and raw_pitch are multiples of 4 floats), so rows move as float4s
+    {
+        const float* raw = a.raw_layers + L.raw_off;
+        const int rx0 = cx0 + L.pad - H;
+        for (int e = threadIdx.x; e < ROWS * NV; e += blockDim.x) {
+            const int r = e / NV, c4 = e - r * NV;
+            const int gx = rx0 + r, gy = cy0 + 4 * c4;
+            // columns in [wy, raw_pitch) are zero; beyond the pitch is the next row
+            const bool ok = gx >= 0 && gx < L.wx && gy < L.raw_pitch;
+            cp_async16z(in0 + r * IS + 4 * c4, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
+        }
+    }
     float t[K];
 #pragma unroll
-    for (int m = 0; m < K; ++m) t[m] = taps_sm[m];
-    // x pass (axis 0): mid[r][c] = sum_m t[m] in[r + m][c]
+    for (int m = 0; m < K; ++m) t[m] = __ldg(a.taps + L.taps_off + m);
+    cp_async_wait_all();
+    __syncthreads();
+    STRACE(1);
+    const float* in = in0 + 1;                 // staged column 1 = halo column 0
+    // x pass (axis 0): mid[r][c] = sum_m t[m] in[r + m][c]; thread item =
+    // (column c, block of 8 output rows): each input value is loaded once and
+    // feeds up to 8 accumulators
     for (int item = threadIdx.x; item < W * (SM_TX / SM_RB); item += blockDim.x) {
         const int c = item % W, rb = item / W;
         float acc[SM_RB];
@@ -72,15 +108,27 @@ __device__ __forceinline__ void smooth_tile_unrolled(const float* __restrict__ i
                 if (m >= 0 && m < K) acc[k] = fmaf(t[m], v, acc[k]);
             }
         }
-        // through shared memory (row stride SM_TY + 1: conflict-free) so the
-        // global stores below are whole coalesced row segments
+        // through shared memory (row stride SM_TY + 4: 16-byte rows) so the global
+        // stores below are whole coalesced row segments
 #pragma unroll
-        for (int k = 0; k < SM_RB; ++k) ot[r * (SM_TY + 1) + cb * SM_RB + k] = acc[k];
+        for (int k = 0; k < SM_RB; ++k) ot[r * (SM_TY + 4) + cb * SM_RB + k] = acc[k];
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < SM_TX * SM_TY; e += blockDim.x) {
-        const int r = e / SM_TY, c = e - r * SM_TY;
-        if (r < rows_valid && c < cols_valid) out[out_base + (long long)r * ncy + c] = ot[r * (SM_TY + 1) + c];
+    float* out = a.smooth_layers + L.sm_off + (long long)cx0 * L.ncy + cy0;
+    const int rv = min(SM_TX, L.ncx - cx0), cv = min(SM_TY, L.ncy - cy0);
+    if ((((uintptr_t)out | (uintptr_t)L.ncy * 4u) & 15u) == 0 && cv == SM_TY) {
+        // float4 rows (the full-size layers: 16-byte aligned crop rows)
+        for (int e = threadIdx.x; e < SM_TX * (SM_TY / 4); e += blockDim.x) {
+            const int r = e / (SM_TY / 4), c4 = e - r * (SM_TY / 4);
+            if (r < rv)
+                *reinterpret_cast<float4*>(out + (long long)r * L.ncy + 4 * c4) =
+                    *reinterpret_cast<const float4*>(ot + r * (SM_TY + 4) + 4 * c4);
+        }
+    } else {
+        for (int e = threadIdx.x; e < SM_TX * SM_TY; e += blockDim.x) {
+            const int r = e / SM_TY, c = e - r * SM_TY;
+            if (r < rv && c < cv) out[(long long)r * L.ncy + c] = ot[r * (SM_TY + 4) + c];
+        }
     }
 }
 
@@ -107,56 +155,44 @@ __device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in
     }
 }
 
-#ifdef HS_SMOOTH_TRACE
-__device__ unsigned long long g_strace[4096 * 4];
-__device__ __forceinline__ unsigned long long sgtime() {
-    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
-}
-#define STRACE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_strace[blockIdx.x * 4 + (k)] = sgtime(); } while (0)
-#else
-#define STRACE(k) do {} while (0)
-#endif
 
 __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     STRACE(0);
     const int* ti = a.tile_info + 3 * blockIdx.x;
     const HsLayer L = a.layers[ti[0]];
     const int cx0 = ti[1], cy0 = ti[2];
-    const int H = L.H, K = 2 * H + 1, W = SM_TY + 2 * H;   // W: staged columns (y halo)
-    const int MS = W | 1;                      // odd row stride: conflict-free column walks
-    // the halo's first column ry0 = cy0 + pad - H = cy0 + 1 (pad = H + 1); loading
-    // from cy0 instead makes every staged row 16-byte aligned in global memory
-    // (raw_off and raw_pitch are multiples of 4 floats), so rows move as float4s
-    const int NV = (W + 1 + 3) >> 2;           // float4s per staged row
-    const int IS = 4 * NV;                     // staged row stride (floats)
-    float* taps = smem;                        // K (padded to 4)
-    float* in = taps + ((K + 3) & ~3);         // (SM_TX + 2H) x IS
-    float* mid = in + (SM_TX + 2 * H) * IS;    // SM_TX x MS
-    for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
-    const float* raw = a.raw_layers + L.raw_off;
-    const int rx0 = cx0 + L.pad - H;
-    for (int e = threadIdx.x; e < (SM_TX + 2 * H) * NV; e += blockDim.x) {
-        const int r = e / NV, c4 = e - r * NV;
-        const int gx = rx0 + r, gy = cy0 + 4 * c4;
-        // columns in [wy, raw_pitch) are zero; beyond the pitch is the next row
-        const bool ok = gx >= 0 && gx < L.wx && gy < L.raw_pitch;
-        cp_async16z(in + r * IS + 4 * c4, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    STRACE(1);
-    in += 1;                                   // staged column 1 = halo column 0
-    float* out = a.smooth_layers + L.sm_off;
-    const long long ob = (long long)cx0 * L.ncy + cy0;
-    const int rv = min(SM_TX, L.ncx - cx0), cv = min(SM_TY, L.ncy - cy0);
+    const int H = L.H;
     switch (H) {
-#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(in, IS, mid, taps, W, MS, out, ob, L.ncy, rv, cv, in - 1); break;
+#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(a, L, cx0, cy0, smem); break;
         HS_SM_CASE(1) HS_SM_CASE(2) HS_SM_CASE(3) HS_SM_CASE(4) HS_SM_CASE(5) HS_SM_CASE(6) HS_SM_CASE(7)
         HS_SM_CASE(8) HS_SM_CASE(9) HS_SM_CASE(10) HS_SM_CASE(11) HS_SM_CASE(12) HS_SM_CASE(13)
         HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16)
 #undef HS_SM_CASE
-        default: smooth_tile_generic(in, IS, mid, taps, H, W, MS, out, ob, L.ncy, rv, cv);
+        default: {
+            const int K = 2 * H + 1, W = SM_TY + 2 * H;
+            const int MS = W | 1;
+            const int NV = (W + 1 + 3) >> 2;
+            const int IS = 4 * NV;
+            float* taps = smem;                        // K (padded to 4)
+            float* in = taps + ((K + 3) & ~3);         // (SM_TX + 2H) x IS
+            float* mid = in + (SM_TX + 2 * H) * IS;    // SM_TX x MS
+            for (int m = threadIdx.x; m < K; m += blockDim.x) taps[m] = a.taps[L.taps_off + m];
+            const float* raw = a.raw_layers + L.raw_off;
+            const int rx0 = cx0 + L.pad - H;
+            for (int e = threadIdx.x; e < (SM_TX + 2 * H) * NV; e += blockDim.x) {
+                const int r = e / NV, c4 = e - r * NV;
+                const int gx = rx0 + r, gy = cy0 + 4 * c4;
+                const bool ok = gx >= 0 && gx < L.wx && gy < L.raw_pitch;
+                cp_async16z(in + r * IS + 4 * c4, ok ? raw + (long long)gx * L.raw_pitch + gy : raw, ok);
+            }
+            cp_async_wait_all();
+            __syncthreads();
+            STRACE(1);
+            const long long ob = (long long)cx0 * L.ncy + cy0;
+            const int rv = min(SM_TX, L.ncx - cx0), cv = min(SM_TY, L.ncy - cy0);
+            smooth_tile_generic(in + 1, IS, mid, taps, H, W, MS, a.smooth_layers + L.sm_off, ob, L.ncy, rv, cv);
+        }
     }
     STRACE(2);
 }
