@@ -116,7 +116,15 @@ typedef struct {
     int mid_off;         /* float offset into HsSmoothArgs.mid (wide kernels), -1 otherwise */
     int raw_pitch;       /* raw row pitch in floats: >= wy, multiple of 4 (16-byte rows for
                             the splat's vector reductions); columns >= wy stay zero */
-    int pad1;
+    int group;           /* layer groups (consecutive fused layers with one factor f > 1, hence
+                            one coarse grid): n > 1 on the first layer of a group of n, -k on
+                            the k-th following member, 0 or 1 on a lone layer.  hs_smooth
+                            folds a group's smoothed crops into the FIRST layer's crop as
+                            sum_m gain_m smooth_m (fixed member order); hs_compose then reads
+                            that crop with gain 1 and skips the members */
+    int ticket;          /* group layers: first of the group's per-tile completion tickets in
+                            HsSmoothArgs.tickets (one per 32x64 smooth tile); -1 otherwise */
+    int pad2;
 } HsLayer;
 
 /* Structure-of-arrays particle pool.  Pools of all patches live in one set of
@@ -472,6 +480,9 @@ typedef struct {
     const int* ytile_prefix;  /* [n_layers+1] y-pass tiles of wide layers (ncx x ncy) */
     int total_ytiles;
     int max_H_wide;           /* max H over wide layers (<= 780) */
+    int* tickets;             /* zeroed per-tile group tickets (HsLayer.ticket); the kernel
+                                 re-arms them, so one zeroing serves every frame.  Required
+                                 when any layer has group != 0/1 */
 } HsSmoothArgs;
 HS_API int hs_smooth(const HsSmoothArgs* a, void* stream);
 

@@ -7,6 +7,7 @@ only passes the resulting device pointers.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -76,33 +77,68 @@ class LayerPack:
     xtile_prefix: np.ndarray = None
     ytile_prefix: np.ndarray = None
     max_H_wide: int = 0
+    n_tickets: int = 0         # layer-group tile tickets (HsSmoothArgs.tickets)
 
 
 def _tiles(a: int, b: int) -> int:
     return (-(-a // TILE)) * (-(-b // TILE))
 
 
+GROUP_LAYERS = os.environ.get("HS_GROUP_LAYERS", "1") != "0"
+
+
+def _groups(factors: list, wide: list) -> list[int]:
+    """HsLayer.group per layer: runs of consecutive fused coarse layers with
+    one factor (hence one coarse grid): n on the first, -k on the k-th
+    following member, 1 on lone layers.  Full-resolution (f = 1) layers stay
+    apart: the compose reads them as plain coalesced rows anyway."""
+    out = [1] * len(factors)
+    if not GROUP_LAYERS:
+        return out
+    i = 0
+    while i < len(factors):
+        j = i + 1
+        while j < len(factors) and factors[j] == factors[i] > 1 and not wide[i] and not wide[j]:
+            j += 1
+        if j - i > 1:
+            out[i] = j - i
+            out[i + 1:j] = [-k for k in range(1, j - i)]
+        i = j
+    return out
+
+
 def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
     """Lay out the per-bucket decimated layers of every patch (LayerPlan,
     patch_synthesis.py:227-258; layer dims :306-308).  Kernels wider than
-    HS_SMOOTH_FUSED_MAX_H take the two-pass path through a scratch layer."""
+    HS_SMOOTH_FUSED_MAX_H take the two-pass path through a scratch layer.
+    Consecutive fused coarse layers with one factor form a group
+    (HsLayer.group): hs_smooth folds them into the first layer's crop, which
+    the compose upsamples once."""
     layers, taps, prefix, xpre, ypre = [], [], [0], [0], [0]
-    raw_off = sm_off = tap_off = mid_off = 0
+    raw_off = sm_off = tap_off = mid_off = tickets = 0
     max_h, max_hw = 1, 0
     for plan, (res, ny) in zip(plans, grids):
-        for k, f in zip(plan.kernels, plan.factors):
+        factors = list(plan.factors)
+        wides = [k.half_width > N.HS_SMOOTH_FUSED_MAX_H for k in plan.kernels]
+        groups = _groups(factors, wides)
+        ticket = -1
+        for k, f, wide, grp in zip(plan.kernels, factors, wides, groups):
             pad = k.half_width + 1
             ncx = -((res - 1) // -f) + 1
             ncy = -((ny - 1) // -f) + 1
             wx, wy = ncx + 2 * pad, ncy + 2 * pad
             if len(k.taps) > min(wx, wy):
                 raise ConfigError(f"kernel of {len(k.taps)} taps wider than grid axis of {min(wx, wy)}")
-            wide = k.half_width > N.HS_SMOOTH_FUSED_MAX_H
             if wide and k.half_width > 780:
                 raise ConfigError(f"kernel half width {k.half_width} exceeds the device limit of 780 texels")
             pitch = -(-wy // 4) * 4                  # 16-byte rows (vector splat reductions)
+            tiles = (-(-ncx // TILE_X)) * (-(-ncy // TILE_Y))
+            if grp > 1:                               # a group's tickets: one per tile
+                ticket, tickets = tickets, tickets + tiles
+            elif grp == 1:
+                ticket = -1
             layers.append(N.HsLayer(raw_off, sm_off, f, k.half_width, pad, ncx, ncy, wx, wy, tap_off,
-                                    float(k.gain), mid_off if wide else -1, pitch, 0))
+                                    float(k.gain), mid_off if wide else -1, pitch, grp, ticket, 0))
             taps.append(np.asarray(k.taps, dtype=np.float32))
             raw_off += wx * pitch                     # stays a multiple of 4
             sm_off += -(-(ncx * ncy) // 4) * 4          # 16-byte aligned crops (vector stores)
@@ -112,16 +148,18 @@ def pack_layers(plans: list, grids: list[tuple[int, int]]) -> LayerPack:
                 max_hw = max(max_hw, k.half_width)
             else:
                 max_h = max(max_h, k.half_width)
-            prefix.append(prefix[-1] + (0 if wide else (-(-ncx // TILE_X)) * (-(-ncy // TILE_Y))))
+            prefix.append(prefix[-1] + (0 if wide else tiles))
             xpre.append(xpre[-1] + (_tiles(ncx, wy) if wide else 0))
             ypre.append(ypre[-1] + (_tiles(ncx, ncy) if wide else 0))
     info = [(l, tx * TILE_X, ty * TILE_Y) for l, L in enumerate(layers) if L.mid_off < 0
             for tx in range(-(-L.ncx // TILE_X)) for ty in range(-(-L.ncy // TILE_Y))]
-    # largest kernels first: the long-tap tiles start earliest
-    info.sort(key=lambda t: -layers[t[0]].H)
+    # group tiles first (their last member folds the group), then the largest
+    # kernels: the long-tap tiles start earliest
+    info.sort(key=lambda t: (layers[t[0]].group in (0, 1), -layers[t[0]].H))
     return LayerPack(layers, np.concatenate(taps) if taps else np.zeros(0, np.float32), raw_off, sm_off,
                      np.array(prefix, dtype=np.int32), max_h, np.array(info, dtype=np.int32).reshape(-1, 3),
-                     mid_off, np.array(xpre, dtype=np.int32), np.array(ypre, dtype=np.int32), max_hw)
+                     mid_off, np.array(xpre, dtype=np.int32), np.array(ypre, dtype=np.int32), max_hw,
+                     n_tickets=tickets)
 
 
 def compose_tile_info(grids: list[tuple[int, int]]) -> np.ndarray:

@@ -45,7 +45,8 @@ class HsPatch(C.Structure):
 class HsLayer(C.Structure):
     _fields_ = [("raw_off", i64), ("sm_off", i64), ("f", i32), ("H", i32), ("pad", i32), ("ncx", i32),
                 ("ncy", i32), ("wx", i32), ("wy", i32), ("taps_off", i32), ("gain", C.c_float),
-                ("mid_off", i32), ("raw_pitch", i32), ("pad1", i32)]
+                ("mid_off", i32), ("raw_pitch", i32), ("group", i32), ("ticket", i32),
+                ("pad2", i32)]
 
 
 class HsPool(C.Structure):
@@ -145,7 +146,7 @@ class HsSmoothArgs(C.Structure):
     _fields_ = [("n_layers", i32), ("layers", vp), ("taps", vp), ("raw_layers", vp),
                 ("smooth_layers", vp), ("tile_info", vp), ("total_tiles", i32), ("max_H", i32),
                 ("mid", vp), ("xtile_prefix", vp), ("total_xtiles", i32), ("ytile_prefix", vp),
-                ("total_ytiles", i32), ("max_H_wide", i32)]
+                ("total_ytiles", i32), ("max_H_wide", i32), ("tickets", vp)]
 
 
 class HsComposeArgs(C.Structure):
@@ -196,7 +197,7 @@ ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAd
                HsSmoothArgs, HsComposeArgs, HsSampleArgs, HsCompositeArgs, HsFinishArgs, HsResidentArgs,
                HsLayoutArgs, HsSource, HsEmitArgs, HsBody, HsBodyArgs, HsInitArgs, HsBoxArgs]
 
-EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 64, HsPool: 48, HsSource: 80}
+EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 72, HsPool: 48, HsSource: 80}
 
 # every symbol include/hybridsea_b200.h declares
 EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",

@@ -78,6 +78,7 @@ struct TileSmem {
     int col_p0[CT];
     double red[NW];
     int redc[NW];
+    int nbe;                          // layers with a crop (group members folded)
     // dynamic tail, nb entries each:
     //   LayerPlan pl[nb];
 };
@@ -153,13 +154,17 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
 
     if (wid == 0) {
         // layer plans (lane b: layer b); footprint offsets by warp scans
+        // layer-group members (HsLayer.group < 0) have no crop of their own: their
+        // smoothed sum sits in the group's first layer, already gain-weighted
         LayerPlan pl{};
         int need_cs = 0, need_tc = 0;
+        bool use = false;
         if (lane < nb) {
             const HsLayer L = a.layers[P.layer_base + lane];
+            use = L.group >= 0;
             pl.sm_off = L.sm_off; pl.f = L.f; pl.ncx = L.ncx; pl.ncy = L.ncy;
-            pl.inv_f = 1.f / (float)L.f; pl.gain = L.gain;
-            if (L.f > 1) {
+            pl.inv_f = 1.f / (float)L.f; pl.gain = L.group > 1 ? 1.f : L.gain;
+            if (use && L.f > 1) {
                 pl.cr0 = ilo / L.f;
                 pl.nr = min(ihi / L.f + 1, L.ncx - 1) - pl.cr0 + 1;
                 pl.cc0 = jlo / L.f;
@@ -174,7 +179,9 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
         const bool fits = need_cs > 0 && inc_cs <= CS_CTA && inc_tc <= TC_CAP;
         pl.cs_off = fits ? inc_cs - need_cs : -1;
         pl.tc_off = fits ? inc_tc - need_tc : -1;
-        if (lane < nb) Wpl[lane] = pl;
+        const unsigned used = __ballot_sync(0xffffffffu, use);
+        if (use) Wpl[__popc(used & ((1u << lane) - 1u))] = pl;
+        if (lane == 0) W.nbe = __popc(used);
     } else if (wid == 1 && lane < CT) {
         // per output row / column (fp64 world coordinates, coupling.py:57-59): boundary
         // depth (coupling.py:27-34) and the column-side background lerp
@@ -209,8 +216,9 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     }
     __syncthreads();
     TRACE(1);
+    const int nl = W.nbe;
     // every coarse footprint, one batch
-    for (int b = 0; b < nb; ++b) {
+    for (int b = 0; b < nl; ++b) {
         const LayerPlan& L = Wpl[b];
         if (L.cs_off < 0) continue;
         const float* Sg = a.smooth_layers + L.sm_off + (long long)L.cr0 * L.ncy + L.cc0;
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     float acc[RPW];
 #pragma unroll
     for (int k = 0; k < RPW; ++k) acc[k] = 0.f;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = 0; b < nl; ++b) {
         const LayerPlan& L = Wpl[b];
         if (L.f != 1) continue;
         const float* Sg = a.smooth_layers + L.sm_off;
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
         }
     }
     // tc[b][r][c] = coarse row r of layer b lerped at haloed column c (x-first bilinear, :270-273)
-    for (int b = 0; b < nb; ++b) {
+    for (int b = 0; b < nl; ++b) {
         const LayerPlan& L = Wpl[b];
         if (L.tc_off < 0) continue;
         const int jj = min(max(jb + (tid & 31), 0), P.ny - 1);
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
         float h[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) h[k] = W.hs[q][c0 + k];
-        for (int b = 0; b < nb; ++b) {
+        for (int b = 0; b < nl; ++b) {
             const LayerPlan& L = Wpl[b];
             if (L.f == 1) continue;
             const int ci = fdiv(ii, L.inv_f);

@@ -156,18 +156,63 @@ __device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in
 }
 
 
-__global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
+// Layer groups (HsLayer.group): every member smooths into its own crop in
+// its own CTA; the CTA that finishes a group's tile last (ticket) folds the
+// members' tiles, in member order, into the first layer's crop as
+// sum_m gain_m smooth_m -- so the compose upsamples the group once
+// (bilinear upsampling is linear, patch_synthesis.py:261-274, 301-313), the
+// members still run in parallel, and the sum is order-fixed (deterministic).
+__device__ __forceinline__ void group_sum_tile(const HsSmoothArgs& a, int l, const HsLayer& L, int cx0, int cy0) {
+    __shared__ int s_last;
+    const int lead = L.group > 1 ? l : l + L.group;
+    const int n = a.layers[lead].group;
+    __threadfence();                           // this CTA's crop stores, device-visible
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int tix = L.ticket + (cx0 / SM_TX) * ((L.ncy + SM_TY - 1) / SM_TY) + cy0 / SM_TY;
+        const int prev = atomicAdd(&a.tickets[tix], 1);
+        s_last = prev == n - 1;
+        if (s_last) a.tickets[tix] = 0;        // re-armed for the next frame / graph replay
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int rv = min(SM_TX, L.ncx - cx0), cv = min(SM_TY, L.ncy - cy0);
+    for (int e = threadIdx.x; e < rv * cv; e += blockDim.x) {
+        const int r = e / cv, c = e - r * cv;
+        const long long o = (long long)(cx0 + r) * L.ncy + cy0 + c;
+        // eight members' values in flight at once, summed in member order
+        float s = 0.f;
+        for (int m0 = 0; m0 < n; m0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (m0 + m < n) v[m] = __ldcg(a.smooth_layers + a.layers[lead + m0 + m].sm_off + o);
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (m0 + m < n) s = fmaf(a.layers[lead + m0 + m].gain, v[m], s);
+        }
+        a.smooth_layers[a.layers[lead].sm_off + o] = s;
+    }
+}
+
+#ifndef HS_SMOOTH_MINB
+#define HS_SMOOTH_MINB 4
+#endif
+__global__ void __launch_bounds__(256, HS_SMOOTH_MINB) smooth_kernel(HsSmoothArgs a) {
     extern __shared__ __align__(16) float smem[];
     STRACE(0);
     const int* ti = a.tile_info + 3 * blockIdx.x;
-    const HsLayer L = a.layers[ti[0]];
+    const int l = ti[0];
+    const HsLayer L = a.layers[l];
     const int cx0 = ti[1], cy0 = ti[2];
     const int H = L.H;
     switch (H) {
 #define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(a, L, cx0, cy0, smem); break;
         HS_SM_CASE(1) HS_SM_CASE(2) HS_SM_CASE(3) HS_SM_CASE(4) HS_SM_CASE(5) HS_SM_CASE(6) HS_SM_CASE(7)
         HS_SM_CASE(8) HS_SM_CASE(9) HS_SM_CASE(10) HS_SM_CASE(11) HS_SM_CASE(12) HS_SM_CASE(13)
-        HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16)
+        HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16) HS_SM_CASE(17) HS_SM_CASE(18) HS_SM_CASE(19)
+        HS_SM_CASE(20) HS_SM_CASE(21) HS_SM_CASE(22) HS_SM_CASE(23) HS_SM_CASE(24)
 #undef HS_SM_CASE
         default: {
             const int K = 2 * H + 1, W = SM_TY + 2 * H;
@@ -194,6 +239,7 @@ __global__ void __launch_bounds__(256) smooth_kernel(HsSmoothArgs a) {
             smooth_tile_generic(in + 1, IS, mid, taps, H, W, MS, a.smooth_layers + L.sm_off, ob, L.ncy, rv, cv);
         }
     }
+    if (L.group > 1 || L.group < 0) group_sum_tile(a, l, L, cx0, cy0);
     STRACE(2);
 }
 

@@ -127,6 +127,7 @@ class SynthWorkspace:
         self.xtile_prefix = torch.from_numpy(self.pack.xtile_prefix).to(device)
         self.ytile_prefix = torch.from_numpy(self.pack.ytile_prefix).to(device)
         self.mid = torch.zeros(self.pack.mid_len, dtype=torch.float32, device=device) if self.pack.mid_len else None
+        self.tickets = torch.zeros(max(1, self.pack.n_tickets), dtype=torch.int32, device=device)
         self.compose_info_np = compose_tile_info(self.grids)
         self.compose_info = torch.from_numpy(self.compose_info_np).to(device)
         self.compose_tiles = int(self.compose_info_np.shape[0])
@@ -144,7 +145,8 @@ class SynthWorkspace:
                               total_tiles=int(self.pack.smooth_tile_info.shape[0]), max_H=self.pack.max_H,
                               mid=N.ptr(self.mid), xtile_prefix=N.ptr(self.xtile_prefix),
                               total_xtiles=int(self.pack.xtile_prefix[-1]), ytile_prefix=N.ptr(self.ytile_prefix),
-                              total_ytiles=int(self.pack.ytile_prefix[-1]), max_H_wide=self.pack.max_H_wide)
+                              total_ytiles=int(self.pack.ytile_prefix[-1]), max_H_wide=self.pack.max_H_wide,
+                              tickets=N.ptr(self.tickets))
 
 
 def synthesize(particles: ParticleSet, patch: PatchRegion, resolution: int, plan) -> tuple:

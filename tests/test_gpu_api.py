@@ -183,3 +183,50 @@ def test_integration_stub_runs_as_written(cuda):
     assert np.abs(f.height - h).max() <= 1e-4 * hs
     assert np.abs(f.displacement[..., 0] - dx).max() <= 1e-4 * hs
     assert not math.isnan(float(f.normal.sum()))
+
+
+def test_layer_groups_fold_equal_factor_layers(cuda, monkeypatch):
+    """C3's plan has five f=63 layers: hs_smooth folds them into one crop
+    (HsLayer.group, tickets) that the compose upsamples once.  Heights equal
+    the ungrouped path to fp32 reordering, repeat runs are bitwise identical
+    (the tickets re-arm), and the oracle bar holds."""
+    import torch
+    from bench import scene_config
+    from paper_2511_02852_b200 import ParticleSet, PatchRegion, _layout, synthesize
+    from paper_2511_02852_b200 import _native as N
+    from paper_2511_02852_b200 import harness as Hm
+    from paper_2511_02852_b200._layout import stream_ptr
+    from paper_2511_02852_b200.patch_synthesis import SynthWorkspace, plan_layers
+    cfg, _, _, _ = scene_config("C3", 0, 1)
+    params = Hm.derive_params(cfg.u10, cfg.fetch, cfg.g, gamma=cfg.gamma, spread_s=cfg.spread_s)
+    table = Hm.build_table(cfg, params)
+    res = 257
+    patch = PatchRegion((0.0, 0.0), 256.0, 256.0, 10.0)
+    plan = plan_layers(table, 256.0 / (res - 1), res, convention=cfg.amplitude_convention,
+                       trough_fraction=cfg.trough_fraction)
+    assert len(set(plan.factors)) < len(plan.factors)
+    rng = np.random.default_rng(11)
+    n = 100000
+    pos = rng.uniform(-5.0, 261.0, size=(n, 2))
+    ang = rng.uniform(0, 2 * np.pi, n)
+    d = np.stack([np.cos(ang), np.sin(ang)], 1)
+    amp, b = rng.normal(0, 0.05, n), rng.integers(0, table.n_omega, n)
+    ps = ParticleSet.from_arrays(pos, d, amp, b, table.n_omega, device=cuda)
+    ws = SynthWorkspace([patch], [res], [plan], cuda)
+    assert any(L.group > 1 for L in ws.pack.layers) and ws.pack.n_tickets > 0
+    for _ in range(2):                            # the kernel re-arms its tickets
+        ws.raw.zero_()
+        N.call("hs_smooth", ws.smooth_args(), stream_ptr())
+        torch.cuda.synchronize()
+        assert int(ws.tickets.count_nonzero()) == 0
+    h1, _ = synthesize(ps, patch, res, plan)
+    monkeypatch.setattr(_layout, "GROUP_LAYERS", False)
+    h0, _ = synthesize(ps, patch, res, plan)
+    h0, h1 = h0.double().cpu().numpy(), h1.double().cpu().numpy()
+    np.testing.assert_allclose(h1, h0, rtol=0, atol=2e-6 * np.abs(h0).max())
+    pool = particles_ref.Pool(pos, d, amp, b.astype(np.int32), np.zeros(n))
+    opl = synth_ref.Plan(tuple(synth_ref.Kernel(np.asarray(k.taps, np.float64), k.half_width, float(k.gain))
+                               for k in plan.kernels), tuple(plan.factors))
+    ref, _ = synth_ref.synthesize(pool, particles_ref.Patch(0.0, 0.0, 256.0, 256.0, 10.0), res, opl)
+    hs = 4.0 * np.sqrt(np.mean(ref ** 2))
+    assert np.abs(h1 - ref).max() <= 1e-4 * hs
