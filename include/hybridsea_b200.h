@@ -249,7 +249,7 @@ typedef struct {
     unsigned long long* rng;       /* [n_patches*8] */
     HsPool stage;                  /* staging arrays (per-patch regions) */
     int* stage_count;              /* [n_patches*nb] out */
-    double* scratch;               /* [n_patches*member_capacity*2] */
+    double* scratch;               /* [n_patches*member_capacity*6]: per-member records */
     int member_capacity;           /* per patch: >= max groups * n_theta */
     int* status;
     int* zero_words;               /* optional: 4-byte words zeroed by this launch (per-frame */

@@ -1,5 +1,6 @@
 // C ABI bookkeeping: error strings, ABI version, device properties.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "hs_common.cuh"
@@ -14,6 +15,13 @@ void set_error(const char* fmt, ...) {
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
 }
+
+#ifdef HS_EXP_SKIP
+bool hs_exp_skip(const char* tag) {
+    const char* e = getenv("HS_EXP_SKIP");
+    return e && strstr(e, tag) != nullptr;
+}
+#endif
 
 int num_sms() {
     static int cached[64] = {0};

@@ -532,6 +532,7 @@ extern "C" HS_API int hs_debug_trace(void* dst) {
 #endif
 
 extern "C" int hs_compose(const HsComposeArgs* a, void* stream) {
+    HS_EXP_SKIP_POINT("compose");
     HS_CHECK_ARG(a != nullptr, "hs_compose: null args");
     HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "hs_compose: nb out of range");
     if (a->total_tiles == 0) {

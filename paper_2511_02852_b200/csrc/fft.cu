@@ -475,6 +475,7 @@ extern "C" int hs_periodic_normals(const float* height, float* normal, int n, do
 }
 
 extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
+    HS_EXP_SKIP_POINT("fft");
     HS_CHECK_ARG(a != nullptr, "hs_fft_evolve: null args");
     const int n = a->n;
     HS_CHECK_ARG(n >= 4 && n <= 4096 && (n & (n - 1)) == 0, "hs_fft_evolve: n=%d must be a power of two in [4, 4096]", n);

@@ -51,6 +51,15 @@ __device__ __forceinline__ void sumsq_add(double* dst, double v, int fixed_point
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Experiment builds only (-DHS_EXP_SKIP): HS_EXP_SKIP=<stage>[,<stage>...]
+// makes that stage's entry point return without launching, to measure how
+// much of the frame a stage holds (tools/gpu/skip.sh).  Never in the product.
+#ifdef HS_EXP_SKIP
+bool hs_exp_skip(const char* tag);
+#define HS_EXP_SKIP_POINT(tag) do { if (hs_exp_skip(tag)) return 0; } while (0)
+#else
+#define HS_EXP_SKIP_POINT(tag) do {} while (0)
+#endif
 int num_sms();
 
 // ---------------------------------------------------------------- complex --

@@ -114,9 +114,19 @@ __device__ __forceinline__ int find_cell(const int* gstart, int ncell, int g) {
     return lo;
 }
 
-constexpr int INJ_SMEM_MEMBERS = 1536;
+#ifdef HS_INJECT_TRACE
+__device__ unsigned long long g_itrace[16];
+#define ITRACE(k) do { if (threadIdx.x == 0 && blockIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_itrace[k] = t_; } } while (0)
+#else
+#define ITRACE(k) do {} while (0)
+#endif
+
+constexpr int INJ_SMEM_MEMBERS = 640;   // member records held in shared memory
+constexpr int INJ_REC = 6;              // e, amp, x, y, ux, uy per member (doubles)
 
 __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
+    ITRACE(0);
     const int p = blockIdx.x;
     const int nb = a.nb, nth = a.n_theta, ncell = nb * 4;
     __shared__ int n_emit[HS_MAX_BUCKETS * 4];
@@ -147,6 +157,11 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
                               L.raw_pitch, L.pad};
         if (b == 0) ap_clamp = 0;
     }
+    // the bucket table, cached for the member passes (warps 2.., beside the ledger)
+    __shared__ HsBucket Bs[HS_MAX_BUCKETS];
+    if (threadIdx.x >= 64)
+        for (int e = threadIdx.x - 64; e < nb * (int)(sizeof(HsBucket) / 8); e += blockDim.x - 64)
+            reinterpret_cast<double*>(Bs)[e] = reinterpret_cast<const double*>(a.buckets)[e];
     double* acc = a.acc + (size_t)p * ncell;
     const double* hr = a.half_rate + (size_t)p * ncell;
     unsigned long long* rng = a.rng + (size_t)p * 8;
@@ -174,7 +189,8 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
             gstart[4 * lane + 1] = g0 + e0;
             gstart[4 * lane + 2] = g0 + e0 + e1;
             gstart[4 * lane + 3] = g0 + e0 + e1 + e2;
-            a.groups[(size_t)p * nb + lane] += sb;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.groups[(size_t)p * nb + lane]),
+                      (unsigned long long)sb);            // result unused: no round trip
         }
         const int tot = __shfl_sync(0xffffffffu, inc, 31);
         if (lane == 0) {
@@ -184,6 +200,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         }
     }
     __syncthreads();
+    ITRACE(1);
     const int g_tot = gstart[ncell];
     int* scount = a.stage_count + (size_t)p * nb;
     if (g_tot == 0 || abort_s) {     // no groups: no RNG draws (particles.py:248-249)
@@ -199,16 +216,19 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     const double dth = dmul(2.0, pi) / (double)nth;
     const double j_lo = dmul(-0.5, dth), j_range = dsub(dmul(0.5, dth), j_lo);
     const unsigned long long D = rng[6];
-    // member (energy, amplitude) pairs: shared memory when they fit (the
-    // per-bucket sums below walk them serially), global scratch otherwise
-    __shared__ __align__(16) double scr_sm[2 * INJ_SMEM_MEMBERS];
-    double* scr = M <= INJ_SMEM_MEMBERS ? scr_sm : a.scratch + (size_t)p * a.member_capacity * 2;
+    // member records (energy, amplitude, position, direction): shared memory
+    // when they fit (the per-bucket sums below walk them serially), global
+    // scratch otherwise
+    __shared__ __align__(16) double scr_sm[INJ_REC * INJ_SMEM_MEMBERS];
+    double* scr = M <= INJ_SMEM_MEMBERS ? scr_sm : a.scratch + (size_t)p * a.member_capacity * INJ_REC;
 
-    // 2. amplitudes + booked energy for every member  (particles.py:256-264, 291-292)
+    // 2. every member: amplitude + booked energy (particles.py:256-264, 291-292)
+    //    and its entry point and direction (:266-290), in one pass
     for (int m = threadIdx.x; m < M; m += blockDim.x) {
         const int g = m / nth, k = m - g * nth;
         const int cell = find_cell(gstart, ncell, g);
-        const HsBucket B = a.buckets[cell >> 2];
+        const int s = cell & 3;
+        const HsBucket& B = Bs[cell >> 2];
         double jit = uniform_from(stream_draw(rng, D + (unsigned long long)g), j_lo, j_range);
         double th0 = dadd(-pi, dmul((double)k + 0.5, dth));
         double th = dadd(th0, jit);
@@ -216,10 +236,21 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         double dv = dmul(B.spread_c, pow(cv, dmul(2.0, B.spread_s)));
         double amp = sqrt(dmul(dmul(dmul(dmul(2.0, B.s1d), dv), B.width), dth));
         double e = dmul(dmul(dmul(dmul(dmul(0.125, a.rho), a.g), dmul(amp, amp)), pi), dmul(B.radius, B.radius));
-        scr[2 * m] = e;
-        scr[2 * m + 1] = amp;
+        double thw = dadd(th, a.mean_dir);
+        double dx = cos(thw), dy = sin(thw);
+        double dot = (s == 0) ? dx : (s == 1) ? -dx : (s == 2) ? dy : -dy;
+        int side = dot > 0.0 ? s : (s ^ 1);
+        double u = uniform_from(stream_draw(rng, D + (unsigned long long)g_tot + (unsigned long long)m), 0.0, 1.0);
+        double px, py;
+        if (side == 0)      { px = P.x0;                 py = dadd(P.y0, dmul(u, P.l2)); }
+        else if (side == 1) { px = dadd(P.x0, P.l1);     py = dadd(P.y0, dmul(u, P.l2)); }
+        else if (side == 2) { px = dadd(P.x0, dmul(u, P.l1)); py = P.y0; }
+        else                { px = dadd(P.x0, dmul(u, P.l1)); py = dadd(P.y0, P.l2); }
+        double* r = scr + INJ_REC * m;
+        r[0] = e; r[1] = amp; r[2] = px; r[3] = py; r[4] = dx; r[5] = dy;
     }
     __syncthreads();
+    ITRACE(2);
     // 3. per-bucket energy in member order (bincount order, a serial fp64 sum per
     //    bucket: lane b walks bucket b, loads four ahead) and live counts; prefixes
     const int per_live = a.beta != 0.0 ? 2 : 1;
@@ -231,18 +262,20 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
             const int m0 = gstart[4 * lane] * nth, m1 = gstart[4 * lane + 4] * nth;
             int m = m0;
             for (; m + 4 <= m1; m += 4) {
-                const double2 v0 = *reinterpret_cast<const double2*>(scr + 2 * m);
-                const double2 v1 = *reinterpret_cast<const double2*>(scr + 2 * m + 2);
-                const double2 v2 = *reinterpret_cast<const double2*>(scr + 2 * m + 4);
-                const double2 v3 = *reinterpret_cast<const double2*>(scr + 2 * m + 6);
+                const double2 v0 = *reinterpret_cast<const double2*>(scr + INJ_REC * m);
+                const double2 v1 = *reinterpret_cast<const double2*>(scr + INJ_REC * (m + 1));
+                const double2 v2 = *reinterpret_cast<const double2*>(scr + INJ_REC * (m + 2));
+                const double2 v3 = *reinterpret_cast<const double2*>(scr + INJ_REC * (m + 3));
                 s = dadd(dadd(dadd(dadd(s, v0.x), v1.x), v2.x), v3.x);
                 live += (v0.y > 0.0) + (v1.y > 0.0) + (v2.y > 0.0) + (v3.y > 0.0);
             }
             for (; m < m1; ++m) {
-                s = dadd(s, scr[2 * m]);
-                live += scr[2 * m + 1] > 0.0;
+                s = dadd(s, scr[INJ_REC * m]);
+                live += scr[INJ_REC * m + 1] > 0.0;
             }
-            a.e_in[(size_t)p * nb + lane] = dadd(a.e_in[(size_t)p * nb + lane], s);
+            // e_in += s (one IEEE add, as the reference's ledger update); the
+            // result is unused, so this is a fire-and-forget reduction
+            atomicAdd(&a.e_in[(size_t)p * nb + lane], s);
             live_cnt[lane] = live;
         }
         const int inc = warp_incl_scan(live, lane);
@@ -259,6 +292,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         }
     }
     __syncthreads();
+    ITRACE(3);
     if (abort_s) {
         for (int b = threadIdx.x; b < nb; b += blockDim.x) {
             scount[b] = 0;
@@ -273,27 +307,16 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
     for (int base = 0; base < M; base += blockDim.x) {
         const int m = base + threadIdx.x;
         double amp = 0.0;
-        if (m < M) amp = scr[2 * m + 1];
+        if (m < M) amp = scr[INJ_REC * m + 1];
         int live = (m < M) && amp > 0.0;
         int tot;
         int ex = block_excl_scan(live, scan_sm, &tot) + carry;
         if (live) {
-            const int g = m / nth, k = m - g * nth;
-            const int cell = find_cell(gstart, ncell, g);
-            const int b = cell >> 2, s = cell & 3;
-            const HsBucket B = a.buckets[b];
-            double jit = uniform_from(stream_draw(rng, D + (unsigned long long)g), j_lo, j_range);
-            double th = dadd(dadd(-pi, dmul((double)k + 0.5, dth)), jit);
-            double thw = dadd(th, a.mean_dir);
-            double dx = cos(thw), dy = sin(thw);
-            double dot = (s == 0) ? dx : (s == 1) ? -dx : (s == 2) ? dy : -dy;
-            int side = dot > 0.0 ? s : (s ^ 1);
-            double u = uniform_from(stream_draw(rng, D + (unsigned long long)g_tot + (unsigned long long)m), 0.0, 1.0);
-            double px, py;
-            if (side == 0)      { px = P.x0;                 py = dadd(P.y0, dmul(u, P.l2)); }
-            else if (side == 1) { px = dadd(P.x0, P.l1);     py = dadd(P.y0, dmul(u, P.l2)); }
-            else if (side == 2) { px = dadd(P.x0, dmul(u, P.l1)); py = P.y0; }
-            else                { px = dadd(P.x0, dmul(u, P.l1)); py = dadd(P.y0, P.l2); }
+            const int g = m / nth;
+            const int b = find_cell(gstart, ncell, g) >> 2;
+            const HsBucket& B = Bs[b];
+            const double* r = scr + INJ_REC * m;
+            const double px = r[2], py = r[3], dx = r[4], dy = r[5];
             const int rank = ex - live_before[b];
             if (a.append) {
                 // advected in their birth frame (harness.py:142-152), culled, appended
@@ -344,6 +367,7 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         }
         carry += tot;
     }
+    ITRACE(4);
     for (int b = threadIdx.x; b < nb; b += blockDim.x) scount[b] = per_live * live_cnt[b];
     if (threadIdx.x == 0) rng[6] = D + (unsigned long long)g_tot * (1 + nth);
     if (a.append) {
@@ -359,7 +383,14 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         }
         if (threadIdx.x == 0 && ap_clamp && a.res.clamped) atomicAdd(&a.res.clamped[p], ap_clamp);
     }
+    ITRACE(5);
 }
+
+#ifdef HS_INJECT_TRACE
+extern "C" HS_API int hs_debug_itrace(void* dst) {
+    return (int)cudaMemcpyFromSymbol(dst, g_itrace, sizeof(g_itrace));
+}
+#endif
 
 // ============================================================== advect ==
 constexpr int ADV_THREADS = 256;
@@ -1387,6 +1418,7 @@ __global__ void emit_commit_kernel(HsEmitArgs a) {
 using namespace hs;
 
 extern "C" int hs_inject(const HsInjectArgs* a, void* stream) {
+    HS_EXP_SKIP_POINT("inject");
     HS_CHECK_ARG(a != nullptr, "hs_inject: null args");
     HS_CHECK_ARG(a->nb >= 1 && a->nb <= HS_MAX_BUCKETS, "hs_inject: nb=%d out of range", a->nb);
     HS_CHECK_ARG(a->n_theta >= 1, "hs_inject: n_theta must be >= 1");
@@ -1470,6 +1502,7 @@ static int check_resident(const HsResidentArgs* a, const char* who) {
 }
 
 extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
+    HS_EXP_SKIP_POINT("advect");
     if (int rc = check_resident(a, "hs_advect_resident")) return rc;
     if (a->n_patches == 0) return 0;
     HS_CHECK_ARG(a->tile_map && a->max_tiles > 0, "hs_advect_resident: missing tile map");

@@ -451,6 +451,7 @@ extern "C" HS_API int hs_debug_strace(void* dst) {
 #endif
 
 extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
+    HS_EXP_SKIP_POINT("smooth");
     HS_CHECK_ARG(a != nullptr, "hs_smooth: null args");
     HS_CHECK_ARG(a->layers && a->taps && a->raw_layers && a->smooth_layers && a->tile_info, "hs_smooth: missing buffer");
     cudaStream_t st = as_stream(stream);

@@ -323,7 +323,7 @@ class Simulation:
             self.stage = [f64(total_stage), f64(total_stage), f64(total_stage), f64(total_stage), f32(total_stage),
                           f64(total_stage)]
             self.stage_count = torch.zeros(self.n_patches * self.nb, dtype=torch.int32, device=dev)
-            self.scratch = f64(2 * self.member_cap * self.n_patches)
+            self.scratch = f64(6 * self.member_cap * self.n_patches)   # member records (HsInjectArgs.scratch)
             self.acc = torch.zeros(self.n_patches * self.nb * 4, dtype=torch.float64, device=dev)
             self.groups = torch.zeros(self.n_patches * self.nb, dtype=torch.int64, device=dev)
             self.e_in = torch.zeros(self.n_patches * self.nb, dtype=torch.float64, device=dev)
@@ -720,6 +720,7 @@ class Simulation:
                 k += 2 + (1 if self._tracking else 0)      # emit + commit (+ track)
             k += (1 if pk.smooth_tile_info.shape[0] > 0 else 0) + (2 if pk.xtile_prefix[-1] > 0 else 0)
             k += 1 if self.det else 0                 # fixed-point raw layers -> float
+            k += 1                                    # compose
             if self.fft_state is not None and (self.composite_each_frame or self.post_frame is not None):
                 k += 1 if len(self.cascades) > 1 else 0   # composite background (cascade sum; else a copy)
         return max(k, 1.0)

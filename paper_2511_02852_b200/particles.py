@@ -366,7 +366,7 @@ def inject(patch: PatchRegion, table: BucketTable, spectrum: DirectionalSpectrum
     samp = torch.empty(stage_cap, dtype=torch.float32, device=dev)
     sbirth = z64(stage_cap)
     scount = torch.zeros(nb, dtype=torch.int32, device=dev)
-    scratch = z64(2 * members)
+    scratch = z64(6 * members)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     # S_J(w_b) through this module's evaluate_1d (particles.py:262), the hook
     # the reference tests monkeypatch
