@@ -23,11 +23,15 @@ bool hs_exp_skip(const char* tag) {
 }
 #endif
 
-int num_sms() {
-    static int cached[64] = {0};
+int current_device() {
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) dev = 0;
+    return dev >= 0 && dev < HS_MAX_DEVICES ? dev : 0;
+}
+
+int num_sms() {
+    static int cached[HS_MAX_DEVICES] = {0};
+    const int dev = current_device();
     if (!cached[dev]) {
         int v = 0;
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);

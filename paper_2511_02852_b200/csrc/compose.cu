@@ -31,7 +31,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 constexpr int CT = 30;            // output tile edge
 constexpr int CH = CT + 2;        // haloed height tile (32): lane = haloed column
-constexpr int NW = 4;             // warps per tile (CTA)
+#ifndef HS_COMPOSE_NW
+#define HS_COMPOSE_NW 4
+#endif
+constexpr int NW = HS_COMPOSE_NW;  // warps per tile (CTA)
 constexpr int NT = 32 * NW;
 constexpr int RPW = CH / NW;      // haloed rows per warp in the height pass
 constexpr int BG_CAP = 8;         // staged background footprint per axis (+1 halo each side)
@@ -542,7 +545,8 @@ extern "C" int hs_compose(const HsComposeArgs* a, void* stream) {
     HS_CHECK_ARG(a->patches && a->layers && a->smooth_layers && a->tile_info, "hs_compose: missing buffer");
     HS_CHECK_ARG(!a->blend_mode || a->bg_height == nullptr || (a->bg_n >= 2 && (a->bg_n & (a->bg_n - 1)) == 0),
                  "hs_compose: background size must be a power of two");
-    static bool carve = false;
+    static PerDevice<bool> carve_done{};
+    bool& carve = carve_done.get();
     if (!carve) {   // the whole 228 KB as shared memory: 9 tiles per SM
         HS_CUDA(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         carve = true;

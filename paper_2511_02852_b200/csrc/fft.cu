@@ -440,7 +440,8 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
     const int rows_threads = 3 * T < 32 ? 32 : 3 * T;
     const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2) + (size_t)(N / 2 + 1) * sizeof(double);
     const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
-    static bool attr = false;
+    static PerDevice<bool> attr_done{};
+    bool& attr = attr_done.get();
     if (!attr) {
         HS_CUDA(cudaFuncSetAttribute(fft_rows_reg_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows));
         HS_CUDA(cudaFuncSetAttribute(fft_cols_reg_kernel<N, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cols));
@@ -521,7 +522,9 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     }
 
     size_t sm_rows = (size_t)(n / 2 + 5 * n) * sizeof(float2);
-    static size_t rows_attr = 48 * 1024;   // attribute calls stay out of graph capture after the first frame
+    static PerDevice<size_t> rows_attr_d{};   // attribute calls stay out of graph capture after the first frame
+    size_t& rows_attr = rows_attr_d.get();
+    if (rows_attr == 0) rows_attr = 48 * 1024;
     if (sm_rows > rows_attr) {
         HS_CUDA(cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows));
         rows_attr = sm_rows;
@@ -535,11 +538,12 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
         int n_a = n / ca;
         int n_b = n / (2 * cbp);
         size_t sm = (size_t)(n / 2 + (size_t)(ca > cbp ? ca : cbp) * (n + 1)) * sizeof(float2);
-        static size_t cols_attr[2] = {48 * 1024, 48 * 1024};
-        const int slot = ca == 8 ? 0 : 1;
-        if (sm > cols_attr[slot]) {
+        static PerDevice<size_t> cols_attr_d[2]{};
+        size_t& cols_attr = cols_attr_d[ca == 8 ? 0 : 1].get();
+        if (cols_attr == 0) cols_attr = 48 * 1024;
+        if (sm > cols_attr) {
             HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            cols_attr[slot] = sm;
+            cols_attr = sm;
         }
         kern<<<n_a + n_b, 256, sm, st>>>(d, o, n_a);
         HS_LAUNCH_CHECK();

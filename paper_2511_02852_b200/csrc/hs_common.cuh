@@ -60,6 +60,15 @@ bool hs_exp_skip(const char* tag);
 #else
 #define HS_EXP_SKIP_POINT(tag) do {} while (0)
 #endif
+// Launch state kept per device (function attributes and occupancy are per
+// device), so one process may drive several GPUs.
+constexpr int HS_MAX_DEVICES = 64;
+int current_device();   // cudaGetDevice, clamped to [0, HS_MAX_DEVICES)
+template <typename T>
+struct PerDevice {
+    T v[HS_MAX_DEVICES];
+    T& get() { return v[current_device()]; }
+};
 int num_sms();
 
 // ---------------------------------------------------------------- complex --

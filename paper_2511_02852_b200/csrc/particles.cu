@@ -1465,7 +1465,8 @@ extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
     HS_CUDA(cudaMemsetAsync(a->tile_state, 0, sizeof(unsigned long long) * (size_t)a->max_tiles, st));
     HS_CUDA(cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st));
     if (a->splat) HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
-    static int occ = 0;
+    static PerDevice<int> occ_d{};
+    int& occ = occ_d.get();
     if (occ == 0) {
         HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_kernel<1>, ADV_THREADS, 0));
         if (occ < 1) occ = 1;
@@ -1507,7 +1508,8 @@ extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
     if (a->n_patches == 0) return 0;
     HS_CHECK_ARG(a->tile_map && a->max_tiles > 0, "hs_advect_resident: missing tile map");
     HS_CHECK_ARG(((size_t)a->tile_map & 15) == 0, "hs_advect_resident: tile_map must be 16-byte aligned");
-    static int occ = 0;
+    static PerDevice<int> occ_d{};
+    int& occ = occ_d.get();
     if (!occ) {
         HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel<false>, RES_THREADS, 0));
         if (occ < 1) occ = 1;

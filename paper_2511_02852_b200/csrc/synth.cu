@@ -459,7 +459,9 @@ extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
         HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= HS_SMOOTH_FUSED_MAX_H, "hs_smooth: max_H=%d out of range", a->max_H);
         const int W = SM_TY + 2 * a->max_H, K = 2 * a->max_H + 1, IS = 4 * ((W + 4) >> 2);
         size_t sm = (size_t)(((K + 3) & ~3) + (SM_TX + 2 * a->max_H) * IS + SM_TX * (W | 1)) * sizeof(float);
-        static size_t smooth_attr = 48 * 1024;
+        static PerDevice<size_t> smooth_attr_d{};
+        size_t& smooth_attr = smooth_attr_d.get();
+        if (smooth_attr == 0) smooth_attr = 48 * 1024;
         if (sm > smooth_attr) {
             HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             smooth_attr = sm;
@@ -472,7 +474,9 @@ extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
         HS_CHECK_ARG(a->max_H_wide >= 1 && a->max_H_wide <= 780, "hs_smooth: max_H_wide=%d out of range", a->max_H_wide);
         const int K = 2 * a->max_H_wide + 1, R = SM_TILE + 2 * a->max_H_wide;
         size_t sm = (size_t)(((K + 3) & ~3) + R * SM_TILE) * sizeof(float);
-        static size_t wide_attr = 48 * 1024;
+        static PerDevice<size_t> wide_attr_d{};
+        size_t& wide_attr = wide_attr_d.get();
+        if (wide_attr == 0) wide_attr = 48 * 1024;
         if (sm > wide_attr) {
             HS_CUDA(cudaFuncSetAttribute(smooth_wide_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             HS_CUDA(cudaFuncSetAttribute(smooth_wide_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
