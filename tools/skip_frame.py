@@ -26,8 +26,8 @@ def main() -> int:
     sim.run_frames(int(round(WARM_SECONDS / WARM_DT)), dt=WARM_DT)
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
-    sets = ["", "fft", "inject", "advect", "smooth", "compose", "inject,advect", "fft,inject",
-            "smooth,compose", "fft,smooth,compose", ""]
+    sets = os.environ.get("SKIP_SETS", "|fft|inject|advect|smooth|compose|inject,advect|fft,inject|"
+                          "smooth,compose|fft,smooth,compose|").split("|")
     if os.environ.get("FORK_AT_START"):
         sim.fft_fork_at_start = True
     for tag in sets:
