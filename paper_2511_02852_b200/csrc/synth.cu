@@ -502,6 +502,7 @@ extern "C" int hs_sample(const HsSampleArgs* a, void* stream) {
 }
 
 extern "C" int hs_composite(const HsCompositeArgs* a, void* stream) {
+    HS_EXP_SKIP_POINT("composite");
     HS_CHECK_ARG(a != nullptr, "hs_composite: null args");
     cudaStream_t st = as_stream(stream);
     HS_CHECK_ARG(a->out, "hs_composite: missing output");

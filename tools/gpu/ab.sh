@@ -1,2 +1,2 @@
-mkdir -p gpurun_out
-timeout 600 python tools/ab_sched.py ${@} > gpurun_out/ab_sched.log 2>&1; echo rc=$?; tail -8 gpurun_out/ab_sched.log
+# A/B of Simulation attributes on the C3 frame: bash tools/gpu/ab.sh "attr=v1|attr=v2" [config]
+AB_ATTR="$1" timeout 600 python tools/skip_frame.py ${2:-C3} 2>&1 | tail -8

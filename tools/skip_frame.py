@@ -30,6 +30,28 @@ def main() -> int:
                           "smooth,compose|fft,smooth,compose|").split("|")
     if os.environ.get("FORK_AT_START"):
         sim.fft_fork_at_start = True
+    # AB_ATTR="name=v1|name=v2": time frames with a Simulation attribute set to each value
+    # (graphs re-captured per value), instead of the skip sets
+    ab = os.environ.get("AB_ATTR")
+    if ab:
+        for spec in ab.split("|") * 2:
+            k, v = spec.split("=")
+            setattr(sim, k, eval(v))
+            sim._graphs = {}
+            sim.prepare_graphs()
+            for _ in range(5):
+                sim.step(stats=False)
+            ts = []
+            for _ in range(300):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                sim.step(stats=False)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+            print(f"{spec:30s} frame median {np.median(ts):7.2f} us  p10 {np.percentile(ts, 10):7.2f}", flush=True)
+        return 0
     for tag in sets:
         os.environ["HS_EXP_SKIP"] = tag
         sim._graphs = {}
