@@ -907,8 +907,11 @@ __global__ void __launch_bounds__(256) splat_kernel(HsSplatArgs a) {
 // 1024 consecutive slots of ONE (patch, bucket) segment, so every CTA works
 // on a single bucket: one step, one support radius, one splat layer, and one
 // atomic per counter at the end.
-constexpr int RES_THREADS = 256;
-constexpr int RES_ITEMS = 4;
+#ifndef HS_RES_THREADS
+#define HS_RES_THREADS 256
+#endif
+constexpr int RES_THREADS = HS_RES_THREADS;
+constexpr int RES_ITEMS = 1024 / RES_THREADS;   // a tile is 1024 slots (harness.RES_TILE)
 constexpr int RES_TILE = RES_THREADS * RES_ITEMS;
 
 // Slots k = k0 + it * STRIDE + lane_k (it < ITEMS) of the resident tile m =
