@@ -66,6 +66,17 @@ HS_API const char* hs_last_error(void);
  * 4..12 the args structs in declaration order); -1 if unknown */
 HS_API int hs_struct_size(int which);
 
+/* One-time configuration of the current device's kernels (shared-memory
+ * limits, carve-out, persistent-grid occupancy).  Entry points do this
+ * lazily on first use, but attribute calls made inside a CUDA-graph capture
+ * invalidate the capture: call this once per device before capturing.       */
+HS_API int hs_configure_device(void);
+
+/* A non-blocking stream of the given priority on the current device (and its
+ * destruction): the streams a frame graph forks onto and is captured on. */
+HS_API int hs_stream_create(void** stream, int priority);
+HS_API int hs_stream_destroy(void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Per-bucket constants (replaces the BucketTable array views,
  * reference spectrum.py:233-257).                                           */

@@ -200,7 +200,8 @@ ABI_STRUCTS = [HsBucket, HsPatch, HsLayer, HsPool, HsFftArgs, HsInjectArgs, HsAd
 EXPECTED_SIZES = {HsBucket: 64, HsPatch: 128, HsLayer: 72, HsPool: 48, HsSource: 80}
 
 # every symbol include/hybridsea_b200.h declares
-EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
+EXPORTS = ["hs_abi_version", "hs_last_error", "hs_struct_size", "hs_configure_device", "hs_stream_create",
+           "hs_stream_destroy", "hs_fft_evolve", "hs_inject", "hs_advect", "hs_splat",
            "hs_smooth", "hs_compose", "hs_sample", "hs_composite", "hs_finish", "hs_sumsq",
            "hs_advance_frame", "hs_periodic_normals", "hs_advect_resident", "hs_append_resident",
            "hs_resident_layout", "hs_track", "hs_emit", "hs_bodies", "hs_init_h0",
@@ -243,12 +244,57 @@ def lib() -> C.CDLL:
     L.hs_clear.argtypes = [vp, i64, vp]
     L.hs_spectral_at.argtypes = [vp, vp, i32, dbl, vp, vp]
     L.hs_conv1d_zero.argtypes = [vp, vp, i64, i32, i64, vp, i32, vp]
+    L.hs_stream_create.argtypes = [C.POINTER(vp), C.c_int]
+    L.hs_stream_destroy.argtypes = [vp]
     L.hs_init_workspace_bytes.restype = i64
     L.hs_init_workspace_bytes.argtypes = [C.c_int]
     if L.hs_abi_version() != 1:
         raise RuntimeError("hybridsea_b200 ABI version mismatch")
     _lib = L
     return L
+
+
+_configured: set = set()
+
+
+def configure_device(device) -> None:
+    """hs_configure_device once per device (kernel attributes and occupancy):
+    must run before the first graph capture, since attribute calls inside a
+    capture invalidate it."""
+    import torch
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx in _configured:
+        return
+    with torch.cuda.device(idx):
+        L = lib()
+        if L.hs_configure_device() != 0:
+            raise RuntimeError(f"hs_configure_device failed: {L.hs_last_error().decode(errors='replace')}")
+    _configured.add(idx)
+
+
+class OwnedStream:
+    """A CUDA stream created by the library (hs_stream_create), exposed to
+    torch as an ExternalStream and destroyed with this object."""
+
+    def __init__(self, device, priority: int = 0):
+        import torch
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        ptr = vp()
+        with torch.cuda.device(idx):
+            L = lib()
+            if L.hs_stream_create(C.byref(ptr), int(priority)) != 0:
+                raise RuntimeError(f"hs_stream_create failed: {L.hs_last_error().decode(errors='replace')}")
+        self.ptr = ptr.value
+        self.stream = torch.cuda.ExternalStream(self.ptr, device=torch.device("cuda", idx))
+
+    def __del__(self):
+        try:
+            if self.ptr and _lib is not None:
+                _lib.hs_stream_destroy(vp(self.ptr))
+        except Exception:
+            pass
 
 
 def call(name: str, args, stream) -> None:

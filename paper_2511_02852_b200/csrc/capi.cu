@@ -73,3 +73,28 @@ extern "C" HS_API int hs_struct_size(int which) {
         default: return -1;
     }
 }
+
+extern "C" HS_API int hs_configure_device(void) {
+    int rc = 0;
+    if (!rc) rc = hs::fft_configure();
+    if (!rc) rc = hs::smooth_configure();
+    if (!rc) rc = hs::compose_configure();
+    if (!rc) rc = hs::particles_configure();
+    return rc;
+}
+
+// Streams owned by one Simulation (side branches, graph capture), created
+// here rather than taken from a framework's shared round-robin pool, so no
+// other component (e.g. a collective library) ever issues work on them.
+extern "C" HS_API int hs_stream_create(void** stream, int priority) {
+    HS_CHECK_ARG(stream != nullptr, "hs_stream_create: null output");
+    cudaStream_t s = nullptr;
+    HS_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
+    *stream = (void*)s;
+    return 0;
+}
+
+extern "C" HS_API int hs_stream_destroy(void* stream) {
+    if (stream) HS_CUDA(cudaStreamDestroy((cudaStream_t)stream));
+    return 0;
+}

@@ -425,6 +425,21 @@ __global__ void fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
     }
 }
 
+// kernel attributes, once per device: set by hs_configure_device before any
+// graph capture (attribute calls inside a capture invalidate it), or lazily
+// here on first eager use
+template <int N, int CT>
+int fft_reg_attrs(size_t sm_rows, size_t sm_cols) {
+    static PerDevice<bool> attr_done{};
+    bool& attr = attr_done.get();
+    if (!attr) {
+        HS_CUDA(cudaFuncSetAttribute(fft_rows_reg_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows));
+        HS_CUDA(cudaFuncSetAttribute(fft_cols_reg_kernel<N, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cols));
+        attr = true;
+    }
+    return 0;
+}
+
 template <int N>
 int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
     constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
@@ -440,13 +455,7 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
     const int rows_threads = 3 * T < 32 ? 32 : 3 * T;
     const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2) + (size_t)(N / 2 + 1) * sizeof(double);
     const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
-    static PerDevice<bool> attr_done{};
-    bool& attr = attr_done.get();
-    if (!attr) {
-        HS_CUDA(cudaFuncSetAttribute(fft_rows_reg_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows));
-        HS_CUDA(cudaFuncSetAttribute(fft_cols_reg_kernel<N, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cols));
-        attr = true;
-    }
+    if (int rc = fft_reg_attrs<N, CT>(sm_rows, sm_cols)) return rc;
     fft_rows_reg_kernel<N><<<N / 2 + 1, rows_threads, sm_rows, st>>>(d);
     HS_LAUNCH_CHECK();
     const int n_a = N / CT, n_b = N / (2 * CT);
@@ -454,6 +463,28 @@ int launch_fft_reg(const FftDev& d, const ColOut& o, cudaStream_t st) {
     fft_cols_reg_kernel<N, CT><<<n_a + n_b, cols_threads, sm_cols, st>>>(d, o, n_a);
     HS_LAUNCH_CHECK();
     return 0;
+}
+
+template <int N>
+int fft_reg_configure() {
+    constexpr int T = N / 16, NP = N + 4;
+    constexpr int CT0 = (256 / T) < 1 ? 1 : ((256 / T) < N / 2 ? (256 / T) : N / 2);
+    constexpr int CT = (CT0 < HS_FFT_COLS_MIN_CT && HS_FFT_COLS_MIN_CT * T <= 512) ? HS_FFT_COLS_MIN_CT : CT0;
+    const size_t sm_rows = (size_t)(3 * N + 3 * NP) * sizeof(float2) + (size_t)(N / 2 + 1) * sizeof(double);
+    const size_t sm_cols = (size_t)(N + CT * NP) * sizeof(float2);
+    return fft_reg_attrs<N, CT>(sm_rows, sm_cols);
+}
+
+int fft_configure() {
+    int rc = 0;
+    if (!rc) rc = fft_reg_configure<64>();
+    if (!rc) rc = fft_reg_configure<128>();
+    if (!rc) rc = fft_reg_configure<256>();
+    if (!rc) rc = fft_reg_configure<512>();
+    if (!rc) rc = fft_reg_configure<1024>();
+    if (!rc) rc = fft_reg_configure<2048>();
+    if (!rc) rc = fft_reg_configure<4096>();
+    return rc;
 }
 
 }  // namespace hs

@@ -69,6 +69,12 @@ struct PerDevice {
     T v[HS_MAX_DEVICES];
     T& get() { return v[current_device()]; }
 };
+// one-time per-device kernel configuration (attributes, occupancy), run by
+// hs_configure_device before graph capture and lazily on first eager use
+int fft_configure();
+int smooth_configure();
+int compose_configure();
+int particles_configure();
 int num_sms();
 
 // ---------------------------------------------------------------- complex --

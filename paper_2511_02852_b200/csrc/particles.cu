@@ -1420,6 +1420,24 @@ __global__ void emit_commit_kernel(HsEmitArgs a) {
 
 using namespace hs;
 
+namespace hs {
+// persistent grids: resident CTAs per SM of the advect kernels, once per device
+static PerDevice<int> adv_occ_d{}, res_occ_d{};
+int particles_configure() {
+    int& a = adv_occ_d.get();
+    if (a == 0) {
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, advect_kernel<1>, ADV_THREADS, 0));
+        if (a < 1) a = 1;
+    }
+    int& r = res_occ_d.get();
+    if (r == 0) {
+        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, advect_resident_kernel<false>, RES_THREADS, 0));
+        if (r < 1) r = 1;
+    }
+    return 0;
+}
+}  // namespace hs
+
 extern "C" int hs_inject(const HsInjectArgs* a, void* stream) {
     HS_EXP_SKIP_POINT("inject");
     HS_CHECK_ARG(a != nullptr, "hs_inject: null args");
@@ -1468,12 +1486,8 @@ extern "C" int hs_advect(const HsAdvectArgs* a, void* stream) {
     HS_CUDA(cudaMemsetAsync(a->tile_state, 0, sizeof(unsigned long long) * (size_t)a->max_tiles, st));
     HS_CUDA(cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st));
     if (a->splat) HS_CUDA(cudaMemsetAsync(a->raw_layers, 0, sizeof(float) * (size_t)a->raw_layers_len, st));
-    static PerDevice<int> occ_d{};
-    int& occ = occ_d.get();
-    if (occ == 0) {
-        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_kernel<1>, ADV_THREADS, 0));
-        if (occ < 1) occ = 1;
-    }
+    if (int rc = particles_configure()) return rc;
+    const int occ = adv_occ_d.get();
     advect_kernel<1><<<num_sms() * occ, ADV_THREADS, 0, st>>>(*a);
     HS_LAUNCH_CHECK();
     return 0;
@@ -1511,12 +1525,8 @@ extern "C" int hs_advect_resident(const HsResidentArgs* a, void* stream) {
     if (a->n_patches == 0) return 0;
     HS_CHECK_ARG(a->tile_map && a->max_tiles > 0, "hs_advect_resident: missing tile map");
     HS_CHECK_ARG(((size_t)a->tile_map & 15) == 0, "hs_advect_resident: tile_map must be 16-byte aligned");
-    static PerDevice<int> occ_d{};
-    int& occ = occ_d.get();
-    if (!occ) {
-        HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, advect_resident_kernel<false>, RES_THREADS, 0));
-        if (occ < 1) occ = 1;
-    }
+    if (int rc = particles_configure()) return rc;
+    const int occ = res_occ_d.get();
     const int grid = min(a->max_tiles, num_sms() * occ);
     cudaStream_t st = as_stream(stream);
     if (a->fixed_point) advect_resident_kernel<true><<<grid, RES_THREADS, 0, st>>>(*a);

@@ -450,6 +450,43 @@ extern "C" HS_API int hs_debug_strace(void* dst) {
 }
 #endif
 
+namespace hs {
+// dynamic shared-memory limits of the smooth kernels, raised once per device
+// (hs_configure_device raises them to the largest size any layout needs, so
+// no attribute call lands inside a graph capture)
+static PerDevice<size_t> smooth_attr_d{}, wide_attr_d{};
+
+static size_t smooth_fused_smem(int max_H) {
+    const int W = SM_TY + 2 * max_H, K = 2 * max_H + 1, IS = 4 * ((W + 4) >> 2);
+    return (size_t)(((K + 3) & ~3) + (SM_TX + 2 * max_H) * IS + SM_TX * (W | 1)) * sizeof(float);
+}
+static size_t smooth_wide_smem(int max_H_wide) {
+    const int K = 2 * max_H_wide + 1, R = SM_TILE + 2 * max_H_wide;
+    return (size_t)(((K + 3) & ~3) + R * SM_TILE) * sizeof(float);
+}
+
+int smooth_attrs(size_t fused, size_t wide) {
+    size_t& fa = smooth_attr_d.get();
+    size_t& wa = wide_attr_d.get();
+    if (fa == 0) fa = 48 * 1024;
+    if (wa == 0) wa = 48 * 1024;
+    if (fused > fa) {
+        HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused));
+        fa = fused;
+    }
+    if (wide > wa) {
+        HS_CUDA(cudaFuncSetAttribute(smooth_wide_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide));
+        HS_CUDA(cudaFuncSetAttribute(smooth_wide_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide));
+        wa = wide;
+    }
+    return 0;
+}
+
+int smooth_configure() {
+    return smooth_attrs(smooth_fused_smem(HS_SMOOTH_FUSED_MAX_H), smooth_wide_smem(780));
+}
+}  // namespace hs
+
 extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     HS_EXP_SKIP_POINT("smooth");
     HS_CHECK_ARG(a != nullptr, "hs_smooth: null args");
@@ -457,31 +494,16 @@ extern "C" int hs_smooth(const HsSmoothArgs* a, void* stream) {
     cudaStream_t st = as_stream(stream);
     if (a->total_tiles > 0) {
         HS_CHECK_ARG(a->max_H >= 1 && a->max_H <= HS_SMOOTH_FUSED_MAX_H, "hs_smooth: max_H=%d out of range", a->max_H);
-        const int W = SM_TY + 2 * a->max_H, K = 2 * a->max_H + 1, IS = 4 * ((W + 4) >> 2);
-        size_t sm = (size_t)(((K + 3) & ~3) + (SM_TX + 2 * a->max_H) * IS + SM_TX * (W | 1)) * sizeof(float);
-        static PerDevice<size_t> smooth_attr_d{};
-        size_t& smooth_attr = smooth_attr_d.get();
-        if (smooth_attr == 0) smooth_attr = 48 * 1024;
-        if (sm > smooth_attr) {
-            HS_CUDA(cudaFuncSetAttribute(smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            smooth_attr = sm;
-        }
+        const size_t sm = smooth_fused_smem(a->max_H);
+        if (int rc = smooth_attrs(sm, 0)) return rc;
         smooth_kernel<<<a->total_tiles, 256, sm, st>>>(*a);
         HS_LAUNCH_CHECK();
     }
     if (a->total_xtiles > 0) {
         HS_CHECK_ARG(a->mid && a->xtile_prefix && a->ytile_prefix, "hs_smooth: wide layers need mid + tile prefixes");
         HS_CHECK_ARG(a->max_H_wide >= 1 && a->max_H_wide <= 780, "hs_smooth: max_H_wide=%d out of range", a->max_H_wide);
-        const int K = 2 * a->max_H_wide + 1, R = SM_TILE + 2 * a->max_H_wide;
-        size_t sm = (size_t)(((K + 3) & ~3) + R * SM_TILE) * sizeof(float);
-        static PerDevice<size_t> wide_attr_d{};
-        size_t& wide_attr = wide_attr_d.get();
-        if (wide_attr == 0) wide_attr = 48 * 1024;
-        if (sm > wide_attr) {
-            HS_CUDA(cudaFuncSetAttribute(smooth_wide_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            HS_CUDA(cudaFuncSetAttribute(smooth_wide_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            wide_attr = sm;
-        }
+        const size_t sm = smooth_wide_smem(a->max_H_wide);
+        if (int rc = smooth_attrs(0, sm)) return rc;
         smooth_wide_x_kernel<<<a->total_xtiles, 256, sm, st>>>(*a);
         HS_LAUNCH_CHECK();
         smooth_wide_y_kernel<<<a->total_ytiles, 256, sm, st>>>(*a);

@@ -674,21 +674,28 @@ class Simulation:
             self._sides = {}
         if name not in self._sides:
             prio = self.STREAM_PRIORITY.get(name, self.CRITICAL_PRIORITY) if self.sched_priorities else 0
-            self._sides[name] = torch.cuda.Stream(device=self.device, priority=prio)
-        return self._sides[name]
+            # streams of this Simulation alone (not torch's shared round-robin pool,
+            # whose streams a collective library may also be handed)
+            self._sides[name] = N.OwnedStream(self.device, prio)
+        return self._sides[name].stream
 
     def _capture_stream(self):
-        return torch.cuda.Stream(device=self.device, priority=self.CRITICAL_PRIORITY if self.sched_priorities else 0)
+        if not hasattr(self, "_capture_owned"):
+            self._capture_owned = N.OwnedStream(self.device, self.CRITICAL_PRIORITY if self.sched_priorities else 0)
+        return self._capture_owned.stream
 
     def _graph(self, state: tuple):
         g = self._graphs.get(state)
         if g is None:
             if self.n_patches:
                 self._hr(self.config.dt)        # host->device uploads must precede capture
+            N.configure_device(self.device)     # so must the kernels' attribute calls
             g = torch.cuda.CUDAGraph()
             s = self._capture_stream()
             s.wait_stream(torch.cuda.current_stream(self.device))
-            with torch.cuda.graph(g, stream=s):
+            # thread_local: CUDA calls other threads make meanwhile (the NCCL
+            # watchdog of a multi-GPU run) must not invalidate this capture
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                 self._enqueue_frame(state, self.config.dt)
             torch.cuda.current_stream(self.device).wait_stream(s)
             self._graphs[state] = g
@@ -738,6 +745,7 @@ class Simulation:
         if key not in self._graphs:
             if self.n_patches:
                 self._hr(self.config.dt)
+            N.configure_device(self.device)
             evs = []
 
             def mark(name):
@@ -748,7 +756,7 @@ class Simulation:
             g = torch.cuda.CUDAGraph()
             s = self._capture_stream()
             s.wait_stream(torch.cuda.current_stream(self.device))
-            with torch.cuda.graph(g, stream=s):
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                 self._enqueue_frame(state, self.config.dt, mark)
             torch.cuda.current_stream(self.device).wait_stream(s)
             self._graphs[key] = (g, evs)
