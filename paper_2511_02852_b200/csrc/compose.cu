@@ -81,7 +81,6 @@ struct TileSmem {
     int col_p0[CT];
     double red[NW];
     int redc[NW];
-    int4 comp_box;                    // composite nodes of the tile: rows [x, y), columns [z, w)
     int nbe;                          // layers with a crop (group members folded)
     // dynamic tail, nb entries each:
     //   LayerPlan pl[nb];
@@ -186,15 +185,6 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
         const unsigned used = __ballot_sync(0xffffffffu, use);
         if (use) Wpl[__popc(used & ((1u << lane) - 1u))] = pl;
         if (lane == 0) W.nbe = __popc(used);
-    } else if (wid == 2 && lane == 0 && a.composite && a.bg_height) {
-        // composite nodes whose patch-grid row / column falls in this tile
-        // (tile-uniform: one lane, four fp64 divisions, read after the barrier)
-        const double sp = a.bg_spacing;
-        const int n = a.bg_n;
-        const double xa = P.x0 + (double)i0 * P.texel, xb = P.x0 + (double)(i0 + CT) * P.texel;
-        const double ya = P.y0 + (double)j0 * P.texel, yb = P.y0 + (double)(j0 + CT) * P.texel;
-        W.comp_box = make_int4(max((int)ceil(xa / sp), 0), min((int)ceil(xb / sp), n),
-                               max((int)ceil(ya / sp), 0), min((int)ceil(yb / sp), n));
     } else if (wid == 1 && lane < CT) {
         // per output row / column (fp64 world coordinates, coupling.py:57-59): boundary
         // depth (coupling.py:27-34) and the column-side background lerp
@@ -491,8 +481,10 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     if (a.composite && a.bg_height) {
         const double sp = a.bg_spacing;
         const int n = a.bg_n;
-        const int4 cb = W.comp_box;
-        const int ga0 = cb.x, ga1 = cb.y, gb0 = cb.z, gb1 = cb.w;
+        const double xa = P.x0 + (double)i0 * P.texel, xb = P.x0 + (double)(i0 + CT) * P.texel;
+        const double ya = P.y0 + (double)j0 * P.texel, yb = P.y0 + (double)(j0 + CT) * P.texel;
+        const int ga0 = max((int)ceil(xa / sp), 0), ga1 = min((int)ceil(xb / sp), n);
+        const int gb0 = max((int)ceil(ya / sp), 0), gb1 = min((int)ceil(yb / sp), n);
         const int cols = gb1 - gb0, tot = max(ga1 - ga0, 0) * max(cols, 0);
         for (int e = tid; e < tot; e += NT) {
             const int gi = ga0 + e / cols, gj = gb0 + e % cols;
