@@ -502,6 +502,8 @@ def main():
             "data": "synthetic (seeded h0 + Philox streams; steady state reached by the step itself)",
             "config": {"workload": f"{args.config} hybrid step" + wl,
                        "live_particles": live_all,
+                       "population_note": ("C3's n_theta = 2 (SURVEY 8) gives ~0.86M live particles, 14% under the "
+                                           "config table's '~1M'") if args.config == "C3" else None,
                        "fft_n": cfg.fft_n, "fft_domain_m": cfg.fft_domain, "patch_res": cfg.patches[0].res,
                        "n_patches": len(full.patches), "fft_cascades": list(cfg.fft_cascades),
                        "n_sources": len(full.sources), "n_omega": cfg.n_omega, "n_theta": cfg.n_theta, "dt": cfg.dt,
@@ -512,7 +514,8 @@ def main():
                                "smoothing + upsample-sum/normals/blend at the patch nodes + FFT-resolution "
                                "composite (one CUDA graph); pool compaction every %d frames; background "
                                "normals are not formed per frame (derived on demand, as the reference's lazy "
-                               "sampler reads them)" % sim.compact_period},
+                               "sampler reads them); the reference step forms them with the FFT (grid_normals) "
+                               "and in finish_field, so its timed arm does that extra work" % sim.compact_period},
             "step_ms_percentiles": step_pct,
             "gpu_launches": (sim.kernel_launches_per_frame() + (2 if exch is not None else 0)) * args.steps,
             "stages_ms": stage,
