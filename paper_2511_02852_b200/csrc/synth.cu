@@ -637,6 +637,7 @@ __global__ void advance_frame_kernel(long long* f) { *f += 1; }
 }  // namespace hs
 
 extern "C" int hs_clear(void* p, long long bytes, void* stream) {
+    HS_EXP_SKIP_POINT("clear");
     HS_CHECK_ARG(bytes >= 0 && (bytes == 0 || p), "hs_clear: bad buffer");
     if (bytes) HS_CUDA(cudaMemsetAsync(p, 0, (size_t)bytes, as_stream(stream)));
     return 0;
