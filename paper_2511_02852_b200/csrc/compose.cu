@@ -358,7 +358,29 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     int cnt = 0;
     const long long gb = P.grid_base;
     const int bn = a.bg_n;
-    if (!have_bg && a.blend_mode) {
+    const bool pure = !in_band && a.bg_height != nullptr && a.blend_mode && i0 >= inset && j0 >= inset &&
+                      i0 + CT <= P.res - inset && j0 + CT <= P.ny - inset;
+    if (pure) {
+        // deep interior tile: every texel deeper than the margin (blend weight
+        // 1: the blend is the patch), inside the variance inset, and off the
+        // border (central differences) -- no per-texel tests at all
+        for (int e = tid; e < CT * CT; e += NT) {
+            const int rr = e / CT, cc = e - rr * CT;
+            const int ii = i0 + rr, jj = j0 + cc;
+            const float h = W.hs[rr + 1][cc + 1];
+            const float hx = (W.hs[rr + 2][cc + 1] - W.hs[rr][cc + 1]) * inv_2s;
+            const float hy = (W.hs[rr + 1][cc + 2] - W.hs[rr + 1][cc]) * inv_2s;
+            const float rn = rsqrtf(hx * hx + hy * hy + 1.f);
+            const float pnx = -hx * rn, pny = -hy * rn, pnz = rn;
+            const int o = (int)gb + ii * P.ny + jj;
+            if (a.patch_height) a.patch_height[o] = h;
+            if (a.patch_normal) { a.patch_normal[3 * o] = pnx; a.patch_normal[3 * o + 1] = pny; a.patch_normal[3 * o + 2] = pnz; }
+            accv = fma((double)h, (double)h, accv);
+            ++cnt;
+            if (a.blend_height) a.blend_height[o] = h;
+            if (a.blend_normal) { a.blend_normal[3 * o] = pnx; a.blend_normal[3 * o + 1] = pny; a.blend_normal[3 * o + 2] = pnz; }
+        }
+    } else if (!have_bg && a.blend_mode) {
         // interior tile (every texel deeper than the margin, or no background):
         // the blend is the patch itself -- a light loop without the background
         // state, so the common case carries no spilled registers
