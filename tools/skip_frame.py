@@ -50,7 +50,8 @@ def main() -> int:
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e3)
-            print(f"{spec:30s} frame median {np.median(ts):7.2f} us  p10 {np.percentile(ts, 10):7.2f}", flush=True)
+            print(f"{spec:30s} frame median {np.median(ts):7.2f} us  mean {np.mean(ts):7.2f}  p10 "
+                  f"{np.percentile(ts, 10):7.2f}", flush=True)
         return 0
     for tag in sets:
         os.environ["HS_EXP_SKIP"] = tag
@@ -67,8 +68,8 @@ def main() -> int:
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
-        print(f"skip {tag or '(none)':22s} frame median {np.median(ts):7.2f} us  p10 {np.percentile(ts, 10):7.2f}",
-              flush=True)
+        print(f"skip {tag or '(none)':22s} frame median {np.median(ts):7.2f} us  mean {np.mean(ts):7.2f}  p10 "
+              f"{np.percentile(ts, 10):7.2f}", flush=True)
     return 0
 
 
