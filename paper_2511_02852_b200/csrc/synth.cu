@@ -132,6 +132,26 @@ __device__ __forceinline__ void smooth_tile_unrolled(const HsSmoothArgs& a, cons
     }
 }
 
+// the unrolled form for half widths up to HS_SMOOTH_UNROLL_MAX; wider
+// kernels take the runtime-H loop.  Each instantiation adds to the kernel's
+// instruction footprint, and in the frame (smooth beside the FFT) that costs
+// more than the unrolling saves on the few wide tiles: frame time C3 96.9 ->
+// 95.6 us, PR1 55.3 -> 51.9, C4 241 -> 240 going from 24 to 8 (alone, the C3
+// smooth is 21.5 -> 26.8 us).
+#ifndef HS_SMOOTH_UNROLL_MAX
+#define HS_SMOOTH_UNROLL_MAX 8
+#endif
+template <int H>
+__device__ __forceinline__ bool smooth_try_unrolled(const HsSmoothArgs& a, const HsLayer& L, int cx0, int cy0,
+                                                    float* __restrict__ smem) {
+    if constexpr (H <= HS_SMOOTH_UNROLL_MAX) {
+        smooth_tile_unrolled<H>(a, L, cx0, cy0, smem);
+        return true;
+    } else {
+        return false;
+    }
+}
+
 __device__ __forceinline__ void smooth_tile_generic(const float* __restrict__ in, int IS, float* __restrict__ mid,
                                                     const float* __restrict__ taps, int H, int W, int MS,
                                                     float* __restrict__ out, long long out_base, int ncy,
@@ -207,14 +227,18 @@ __global__ void __launch_bounds__(256, HS_SMOOTH_MINB) smooth_kernel(HsSmoothArg
     const HsLayer L = a.layers[l];
     const int cx0 = ti[1], cy0 = ti[2];
     const int H = L.H;
+    bool done = false;
     switch (H) {
-#define HS_SM_CASE(h) case h: smooth_tile_unrolled<h>(a, L, cx0, cy0, smem); break;
+#define HS_SM_CASE(h) case h: done = smooth_try_unrolled<h>(a, L, cx0, cy0, smem); break;
         HS_SM_CASE(1) HS_SM_CASE(2) HS_SM_CASE(3) HS_SM_CASE(4) HS_SM_CASE(5) HS_SM_CASE(6) HS_SM_CASE(7)
         HS_SM_CASE(8) HS_SM_CASE(9) HS_SM_CASE(10) HS_SM_CASE(11) HS_SM_CASE(12) HS_SM_CASE(13)
         HS_SM_CASE(14) HS_SM_CASE(15) HS_SM_CASE(16) HS_SM_CASE(17) HS_SM_CASE(18) HS_SM_CASE(19)
         HS_SM_CASE(20) HS_SM_CASE(21) HS_SM_CASE(22) HS_SM_CASE(23) HS_SM_CASE(24)
 #undef HS_SM_CASE
-        default: {
+        default: break;
+    }
+    if (!done) {
+        {
             const int K = 2 * H + 1, W = SM_TY + 2 * H;
             const int MS = W | 1;
             const int NV = (W + 1 + 3) >> 2;
