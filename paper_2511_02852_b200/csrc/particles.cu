@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(512) inject_kernel(HsInjectArgs a) {
         double amp = sqrt(dmul(dmul(dmul(dmul(2.0, B.s1d), dv), B.width), dth));
         double e = dmul(dmul(dmul(dmul(dmul(0.125, a.rho), a.g), dmul(amp, amp)), pi), dmul(B.radius, B.radius));
         double thw = dadd(th, a.mean_dir);
-        double dx = cos(thw), dy = sin(thw);
+        double dx, dy;
+        sincos(thw, &dy, &dx);                  // one argument reduction for both
         double dot = (s == 0) ? dx : (s == 1) ? -dx : (s == 2) ? dy : -dy;
         int side = dot > 0.0 ? s : (s ^ 1);
         double u = uniform_from(stream_draw(rng, D + (unsigned long long)g_tot + (unsigned long long)m), 0.0, 1.0);
