@@ -35,8 +35,9 @@ def main() -> int:
     ab = os.environ.get("AB_ATTR")
     if ab:
         for spec in ab.split("|") * 2:
-            k, v = spec.split("=")
-            setattr(sim, k, eval(v))
+            for kv in spec.split(","):              # "a=1,b=2": several attributes at once
+                k, v = kv.split("=")
+                setattr(sim, k, eval(v))
             sim._graphs = {}
             sim.prepare_graphs()
             for _ in range(5):
