@@ -137,9 +137,10 @@ __device__ __forceinline__ void smooth_tile_unrolled(const HsSmoothArgs& a, cons
 // instruction footprint, and in the frame (smooth beside the FFT) that costs
 // more than the unrolling saves on the few wide tiles: frame time C3 96.9 ->
 // 95.6 us, PR1 55.3 -> 51.9, C4 241 -> 240 going from 24 to 8 (alone, the C3
-// smooth is 21.5 -> 26.8 us).
+// smooth is 21.5 -> 26.8 us); 6 takes PR1 to 51.2 with C3 unchanged, 5 or 4
+// send C3's H = 6 full-resolution layer to the loop (101 us).
 #ifndef HS_SMOOTH_UNROLL_MAX
-#define HS_SMOOTH_UNROLL_MAX 8
+#define HS_SMOOTH_UNROLL_MAX 6
 #endif
 template <int H>
 __device__ __forceinline__ bool smooth_try_unrolled(const HsSmoothArgs& a, const HsLayer& L, int cx0, int cy0,
