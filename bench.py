@@ -352,7 +352,7 @@ def main():
     sim = Simulation(cfg, device=dev, rng_seed_keys=keys)
     exch = None
     if world > 1 or args.exchange:
-        if len(sim.cascades) > 1 and world > 1:
+        if len(sim.cascades) > 1:              # (at one rank --exchange runs the same path: it owns all)
             sim.shard_cascades(CascadeShard(cfg.fft_n, len(sim.cascades), world, rank, device=dev))
         if sim.n_patches and sim.fft_state is not None:
             exch = BoxExchange.for_scene(full, sim, world, rank)
