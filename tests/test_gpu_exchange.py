@@ -11,6 +11,8 @@
 * Two shards of C2 on one device (no collective: the test moves the payload
   chunks itself, as the all-gather would): both shards' composites after the
   paste equal the single-process scene's composite.
+* C4's cascades through sharding.CascadeShard at one rank equal the
+  unsharded scene bit for bit (deterministic mode).
 """
 import os
 import socket
@@ -96,3 +98,29 @@ def test_two_shards_paste_to_the_single_process_composite(cuda):
     for sim, _ in shards:
         got = sim.composite_frame.cpu().numpy()
         assert np.abs(got - want).max() <= 1e-5 * scale     # float splat atomics: order-free sums
+
+
+def test_cascade_shard_one_rank_matches_the_unsharded_scene(cuda):
+    """C4's summed cascades through sharding.CascadeShard (the N > 1 path:
+    owned transforms into the shard buffer, the background read from its
+    views) at one rank: the frame's background sum, blended tiles and
+    composite equal the unsharded scene's bit for bit."""
+    import torch
+    from paper_2511_02852_b200 import Simulation, scenes
+    from paper_2511_02852_b200.sharding import CascadeShard
+    # deterministic mode: the splat's fixed-point sums make both runs bitwise comparable
+    cfg = scenes.c4(frames=12, patches=scenes.c4().patches[:2], deterministic=True)
+    sims = [Simulation(cfg, device=cuda) for _ in range(2)]
+    sims[1].shard_cascades(CascadeShard(cfg.fft_n, len(sims[1].cascades), 1, 0, device=cuda))
+    for sim in sims:
+        sim.prepare_graphs()
+        for _ in range(cfg.frames):
+            sim.step(stats=False)
+    torch.cuda.synchronize()
+    a, b = sims
+    assert torch.equal(a.composite_frame, b.composite_frame)
+    for p in range(a.n_patches):
+        ha, _ = a.blended_tile(p)
+        hb, _ = b.blended_tile(p)
+        assert torch.equal(ha, hb)
+    np.testing.assert_array_equal(a.counts_host(), b.counts_host())
