@@ -100,13 +100,18 @@ def build(cfg, ref=None):
     return sim
 
 
-def warm(sim, frames: int, dt: float) -> None:
+def warm(sim, frames: int, dt: float, budget_s: float | None = None) -> int:
     """Steady state with the reference's own inject + advect (the pool's
     population dynamics; synthesis does not feed back), as SURVEY App. C
-    warmed its C3 pools."""
+    warmed its C3 pools.  Stops early after `budget_s` seconds; returns the
+    frames run."""
+    import time
     from hybridsea.particles import advect, inject
     cfg = sim.config
-    for _ in range(frames):
+    t0 = time.perf_counter()
+    for k in range(frames):
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            return k
         t = sim.frame * dt
         for ps in sim.patches:
             ps.pool.extend(inject(ps.region, sim.table, sim.spectrum, ps.ledger, dt, sim.rng, t=t,
@@ -114,6 +119,7 @@ def warm(sim, frames: int, dt: float) -> None:
         for ps in sim.patches:
             advect(ps.pool, sim.table, dt, ps.region, ps.ledger, g=cfg.g)
         sim.frame += 1
+    return frames
 
 
 def load_state(sim, pools, ledgers, rng_words, frame: int) -> None:

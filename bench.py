@@ -246,25 +246,37 @@ def reference_arm(args):
     n_warm = int(round(args.warm_seconds / WARM_DT))
     n_w = min(max(3, args.warmup), 20)            # W >= 3 untimed full frames (~1 s each at C3: capped at 20)
     budget = 90.0
+    warm_budget, w_budget = 80.0, 30.0            # the whole arm stays within ~3.5 min (C4's port: 4M particles)
     why = refchain.expressible(cfg) if refchain.load() is not None else "reference not installed in baseline/_ref"
     t_warm = time.perf_counter()
     if why is None:
         sim = refchain.build(cfg)
-        refchain.warm(sim, n_warm, WARM_DT)       # the reference's own inject + advect at dt = 0.1
+        n_warm = refchain.warm(sim, n_warm, WARM_DT, warm_budget)   # the reference's own inject + advect
         warm_s = time.perf_counter() - t_warm
-        for _ in range(n_w):
+        t_w = time.perf_counter()
+        for k in range(n_w):
             refchain.frame(sim)
+            if time.perf_counter() - t_w > w_budget:
+                n_w = k + 1
+                break
         frame_s, live, n = time_reference_frames(sim, budget, min_frames=1, max_frames=max(1, args.steps))
         kind = "reference"
         what = "the unmodified reference package (baseline/_ref): Simulation.step + stitched_heights"
     else:
         from oracle import scene_ref
         sc = scene_ref.OracleScene(cfg.scene_dict())
-        for _ in range(n_warm):                   # same warm-up as the GPU arm, no synthesis
+        for k in range(n_warm):                   # same warm-up as the GPU arm, no synthesis
+            if time.perf_counter() - t_warm > warm_budget:
+                n_warm = k
+                break
             sc.step(dt=WARM_DT, synth=False, fft=False)
         warm_s = time.perf_counter() - t_warm
-        for _ in range(n_w):
+        t_w = time.perf_counter()
+        for k in range(n_w):
             sc.step()
+            if time.perf_counter() - t_w > w_budget:
+                n_w = k + 1
+                break
         frame_s, live, n = time_port_frames(sc, budget, min_frames=1, max_frames=max(1, args.steps))
         kind = "port"
         what = f"the numpy oracle port of the reference algorithm (reference not run: {why})"
