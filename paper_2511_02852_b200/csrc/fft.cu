@@ -300,8 +300,18 @@ __device__ __forceinline__ unsigned long long fgtime() {
 #define FTRACE(k) do {} while (0)
 #endif
 
+#ifdef HS_FFT_ROWS_MINB
+#define HS_FFT_ROWS_LB(n) __launch_bounds__(3 * ((n) / 16) < 32 ? 32 : 3 * ((n) / 16), HS_FFT_ROWS_MINB)
+#else
+#define HS_FFT_ROWS_LB(n)
+#endif
+#ifdef HS_FFT_COLS_MINB
+#define HS_FFT_COLS_LB(n, ct) __launch_bounds__((ct) * ((n) / 16) < 32 ? 32 : (ct) * ((n) / 16), HS_FFT_COLS_MINB)
+#else
+#define HS_FFT_COLS_LB(n, ct)
+#endif
 template <int N>
-__global__ void fft_rows_reg_kernel(FftDev d) {
+__global__ void HS_FFT_ROWS_LB(N) fft_rows_reg_kernel(FftDev d) {
     FTRACE(0);
     constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
     extern __shared__ float2 sm[];
@@ -354,7 +364,7 @@ __global__ void fft_rows_reg_kernel(FftDev d) {
 // columns: CT transforms per CTA; blocks < n_a_tiles do A (height + i dx),
 // the rest do B (two real dy columns per transform)
 template <int N, int CT>
-__global__ void fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
+__global__ void HS_FFT_COLS_LB(N, CT) fft_cols_reg_kernel(FftDev d, ColOut o, int n_a_tiles) {
     constexpr int T = N / 16, NP = N + 4;   // transform stride: lanes on different transforms hit different banks
     extern __shared__ float2 sm[];
     __shared__ double red[32];
