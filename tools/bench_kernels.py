@@ -50,7 +50,7 @@ def main() -> int:
     sim.step(stats=False)
     torch.cuda.synchronize()
     N.call = real_call
-    groups = {"compose": ["hs_compose"], "interior": ["hs_compose_interior"], "smooth": ["hs_smooth"], "fft": ["hs_fft_evolve"],
+    groups = {"compose": ["hs_compose"], "smooth": ["hs_smooth"], "fft": ["hs_fft_evolve"],
               "advect": ["hs_advect_resident"], "inject": ["hs_inject"]}
     out = {}
     for st in args.stages.split(","):
