@@ -38,12 +38,20 @@ constexpr int NW = HS_COMPOSE_NW;  // warps per tile (CTA)
 constexpr int NT = 32 * NW;
 constexpr int RPW = CH / NW;      // haloed rows per warp in the height pass
 constexpr int BG_CAP = 8;         // staged background footprint per axis (+1 halo each side)
-constexpr int CS_CTA = 1536;      // floats of staged coarse footprints per tile
-constexpr int TCP = CH + 1;       // tc row pitch: lanes on different coarse rows, same column -> distinct banks
-constexpr int TC_CAP = 88 * TCP;  // floats of row-interpolated coarse rows per tile (88 rows)
+constexpr int TCP = 36;           // tc row pitch: float4 rows; 8 lanes on distinct rows -> distinct 4-bank groups
+constexpr int TC_ROWS = 72;       // row-interpolated coarse rows per tile, all coarse layers (C3: <= 64)
+constexpr int TC_CAP = TC_ROWS * TCP;
 constexpr int CPT = CH / NW;      // haloed columns per thread in the coarse pass (thread = haloed row)
 
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
+
+// 16-byte shared load from a 32-bit shared-window address (keeps the tile's
+// table base a plain register instead of a generic pointer)
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 
 // floor(x / f) for 0 <= x < 2^22, f >= 1, from the fp32 reciprocal: the
 // quotient of x + 1/2 sits >= 1/(2f) from an integer, far above the rounding
@@ -62,32 +70,45 @@ __device__ __forceinline__ float3 bg_node_normal(const float* H, int n, long lon
 struct LayerPlan {
     long long sm_off;
     int f, ncx, ncy;
-    int cs_off;                       // staged footprint offset in cs (-1: layer read from global)
-    int cr0, cc0, ncol, nr;           // coarse footprint: first row / column, extents
-    int tc_off;                       // row-interpolated rows offset in tc
+    int cr0, cc0;                     // coarse footprint origin (f > 1)
+    int tc_off;                       // row table offset in tc (-1: not tabulated, rows read from global)
     float inv_f, gain;
 };
 
+// one row of the tc table: a coarse layer's footprint row (shared-window byte
+// addresses, so the per-row work decodes nothing)
+struct RowEnt {
+    unsigned src;                     // first footprint element of the row in smooth_layers (< 2^32 floats)
+    unsigned tca;                     // tc row
+    unsigned cola;                    // the layer's column table | ncol << 24
+    float inv_f;
+};
+
 struct TileSmem {
-    float cs[CS_CTA];                 // staged coarse footprints (until the tc table is built)
-    float hs[CH][CH + 1];             // haloed patch heights
     union {
         float tc[TC_CAP];             // coarse rows of every layer interpolated at the 32 haloed columns
         float4 trow[CT][BG_CAP];      // background (h, nx, ny, nz) x-lerped per output row (epilogue)
     } u2;
+    float hs[CH][CH + 1];             // haloed patch heights
     float bgh[(BG_CAP + 2) * (BG_CAP + 2)];   // background heights (+1 halo)
     float bgn[BG_CAP * BG_CAP * 3];           // background node normals (given ones)
     float row_d[CT], col_d[CT], col_fv[CT];
     int col_p0[CT];
     double red[NW];
     int redc[NW];
-    int nbe;                          // layers with a crop (group members folded)
-    // dynamic tail, nb entries each:
-    //   LayerPlan pl[nb];
+    int nc, n1, nrows;                // coarse layers, f == 1 layers (group members folded), tc rows
+    // dynamic tail:
+    //   LayerPlan pl[nb]       coarse layers from the front, f == 1 layers at the back (layer order)
+    //   RowEnt rows[TC_ROWS]
+    //   unsigned col[nb][32]   per coarse layer and haloed column: byte offsets in the footprint row of
+    //                          its two columns (4 col | 4 (col + d1) << 8) | in-cell remainder << 16
+    //   int2 rowp[nb][32]      per coarse layer and haloed row: tc offset of its coarse row | next-row step << 16
+    //                          (-1: not tabulated), row weight g1
 };
 
 __host__ __device__ constexpr size_t compose_smem_bytes(int nb) {
-    return sizeof(TileSmem) + (size_t)nb * sizeof(LayerPlan);
+    return sizeof(TileSmem) + (size_t)nb * sizeof(LayerPlan) + TC_ROWS * sizeof(RowEnt) + (size_t)nb * 32 * 4 +
+           (size_t)nb * 32 * 8;
 }
 
 // background footprint of an output tile: first node and node count per
@@ -122,6 +143,9 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     TileSmem& W = *reinterpret_cast<TileSmem*>(smem_raw);
     const int nb = a.nb;
     LayerPlan* const Wpl = reinterpret_cast<LayerPlan*>(smem_raw + sizeof(TileSmem));
+    RowEnt* const Wrow = reinterpret_cast<RowEnt*>(Wpl + nb);
+    unsigned* const Wcol = reinterpret_cast<unsigned*>(Wrow + TC_ROWS);
+    int2* const Wrowp = reinterpret_cast<int2*>(Wcol + nb * 32);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int tile = blockIdx.x;
     TRACE(0);
@@ -155,37 +179,71 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     const int ilo = min(max(ib, 0), P.res - 1), ihi = min(max(ib + CH - 1, 0), P.res - 1);
     const int jlo = min(max(jb, 0), P.ny - 1), jhi = min(max(jb + CH - 1, 0), P.ny - 1);
 
-    if (wid == 0) {
-        // layer plans (lane b: layer b); footprint offsets by warp scans
-        // layer-group members (HsLayer.group < 0) have no crop of their own: their
-        // smoothed sum sits in the group's first layer, already gain-weighted
+    if (wid == 0 || wid >= 2) {
+        // layer plans (lane b: layer b).  Layer-group members (HsLayer.group < 0)
+        // have no crop of their own: their smoothed sum sits in the group's
+        // first layer, already gain-weighted
         LayerPlan pl{};
-        int need_cs = 0, need_tc = 0;
-        bool use = false;
+        int nr = 0, ncol = 0;
+        bool coarse = false, fine = false;
         if (lane < nb) {
             const HsLayer L = a.layers[P.layer_base + lane];
-            use = L.group >= 0;
+            coarse = L.group >= 0 && L.f > 1;
+            fine = L.group >= 0 && L.f == 1;
             pl.sm_off = L.sm_off; pl.f = L.f; pl.ncx = L.ncx; pl.ncy = L.ncy;
             pl.inv_f = 1.f / (float)L.f; pl.gain = L.group > 1 ? 1.f : L.gain;
-            if (use && L.f > 1) {
+            if (coarse) {
                 pl.cr0 = ilo / L.f;
-                pl.nr = min(ihi / L.f + 1, L.ncx - 1) - pl.cr0 + 1;
+                nr = min(ihi / L.f + 1, L.ncx - 1) - pl.cr0 + 1;
                 pl.cc0 = jlo / L.f;
-                pl.ncol = min(jhi / L.f + 1, L.ncy - 1) - pl.cc0 + 1;
-                need_cs = pl.nr * pl.ncol;
-                need_tc = pl.nr * TCP;
+                ncol = min(jhi / L.f + 1, L.ncy - 1) - pl.cc0 + 1;
             }
         }
-        const int inc_cs = warp_incl_scan(need_cs, lane);
-        const int inc_tc = warp_incl_scan(need_tc, lane);
-        // a layer is tabulated only if every layer before it was (prefix offsets stay valid)
-        const bool fits = need_cs > 0 && inc_cs <= CS_CTA && inc_tc <= TC_CAP;
-        pl.cs_off = fits ? inc_cs - need_cs : -1;
-        pl.tc_off = fits ? inc_tc - need_tc : -1;
-        const unsigned used = __ballot_sync(0xffffffffu, use);
-        if (use) Wpl[__popc(used & ((1u << lane) - 1u))] = pl;
-        if (lane == 0) W.nbe = __popc(used);
-    } else if (wid == 1 && lane < CT) {
+        const unsigned mc = __ballot_sync(0xffffffffu, coarse);
+        const unsigned lt = (1u << lane) - 1u;
+        const int cix = __popc(mc & lt);
+        if (wid == 0) {
+            // a layer is tabulated only if every coarse layer before it was
+            const int inc = warp_incl_scan(nr, lane);
+            const bool fits = coarse && inc <= TC_ROWS;
+            pl.tc_off = fits ? (inc - nr) * TCP : -1;
+            const unsigned m1 = __ballot_sync(0xffffffffu, fine);
+            if (coarse) Wpl[cix] = pl;
+            if (fine) Wpl[nb - __popc(m1) + __popc(m1 & lt)] = pl;
+            const int nrows = __reduce_max_sync(0xffffffffu, fits ? inc : 0);
+            if (lane == 0) { W.nc = __popc(mc); W.n1 = __popc(m1); W.nrows = nrows; }
+            if (fits) {
+                RowEnt e;
+                e.inv_f = pl.inv_f;
+                e.cola = (unsigned)__cvta_generic_to_shared(Wcol + cix * 32) | ((unsigned)ncol << 24);
+                const unsigned tca = (unsigned)__cvta_generic_to_shared(W.u2.tc + pl.tc_off);
+                for (int r = 0; r < nr; ++r) {
+                    e.src = (unsigned)(pl.sm_off + (long long)(pl.cr0 + r) * pl.ncy + pl.cc0);
+                    e.tca = tca + (unsigned)(4 * TCP * r);
+                    Wrow[inc - nr + r] = e;
+                }
+            }
+        } else {
+            // column table (warps 2 and 3: alternate coarse layers; lane = haloed
+            // column): the footprint column, the clamped step to the next one and
+            // the in-cell remainder (x-first bilinear, patch_synthesis.py:270-273)
+            const int jj = min(max(jb + lane, 0), P.ny - 1);
+            unsigned m = mc;
+            for (int k = 0; m; ++k) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int f = __shfl_sync(0xffffffffu, pl.f, b), ncy = __shfl_sync(0xffffffffu, pl.ncy, b);
+                const int cc0 = __shfl_sync(0xffffffffu, pl.cc0, b);
+                const float inv_f = __shfl_sync(0xffffffffu, pl.inv_f, b);
+                if ((k & 1) == (wid & 1)) {
+                    const int cj = fdiv(jj, inv_f);
+                    const int d1 = min(cj + 1, ncy - 1) - cj;
+                    Wcol[k * 32 + lane] = (unsigned)(4 * (cj - cc0)) | ((unsigned)(4 * (cj - cc0 + d1)) << 8) |
+                                          ((unsigned)(jj - cj * f) << 16);
+                }
+            }
+        }
+    } else if (lane < CT) {
         // per output row / column (fp64 world coordinates, coupling.py:57-59): boundary
         // depth (coupling.py:27-34) and the column-side background lerp
         const double yy = P.y0 + (double)(j0 + lane) * P.texel;
@@ -219,40 +277,46 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     }
     __syncthreads();
     TRACE(1);
-    const int nl = W.nbe;
-    // every coarse footprint, one batch
-    for (int b = 0; b < nl; ++b) {
-        const LayerPlan& L = Wpl[b];
-        if (L.cs_off < 0) continue;
-        const float* Sg = a.smooth_layers + L.sm_off + (long long)L.cr0 * L.ncy + L.cc0;
-        const float inv_nc = 1.f / (float)L.ncol;
-        for (int e = tid; e < L.nr * L.ncol; e += NT) {
-            const int rr = fdiv(e, inv_nc) , cc = e - rr * L.ncol;
-            cp_async4(W.cs + L.cs_off + e, Sg + (rr * L.ncy + cc), true);
+    const int nc = W.nc, n1 = W.n1, nrows = W.nrows;
+    const float* __restrict__ SL = a.smooth_layers;
+    // tc rows of this warp (wid, wid + NW, ...): each footprint row is staged
+    // by cp.async into the start of its own tc row (lane = footprint column),
+    // then lerped in place at the 32 haloed columns:
+    //   tc[row][c] = lerp(row[col(c)], row[col(c) + d1], rem(c) / f)
+    const unsigned lane4 = 4u * (unsigned)lane;
+    for (int g = wid; g < nrows; g += NW) {
+        const RowEnt e = Wrow[g];
+        if (lane < (int)(e.cola >> 24)) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(e.tca + lane4), "l"(SL + e.src + lane));
         }
     }
-    // f == 1 layers straight into the accumulators (lane = haloed column, coalesced rows)
-    const int c = lane;
-    const int j = min(max(jb + c, 0), P.ny - 1);
-    const int qb = RPW * wid;                      // first haloed row of this warp
-    float acc[RPW];
-#pragma unroll
-    for (int k = 0; k < RPW; ++k) acc[k] = 0.f;
-    for (int b = 0; b < nl; ++b) {
-        const LayerPlan& L = Wpl[b];
-        if (L.f != 1) continue;
-        const float* Sg = a.smooth_layers + L.sm_off;
-        float v[RPW];
-#pragma unroll
-        for (int k = 0; k < RPW; ++k) v[k] = Sg[min(max(ib + qb + k, 0), P.res - 1) * L.ncy + j];
-#pragma unroll
-        for (int k = 0; k < RPW; ++k) acc[k] = fmaf(L.gain, v[k], acc[k]);
+    // row table: per coarse layer and haloed row, the tc row offset, the clamped
+    // step to the next coarse row and the row weight
+    for (int e = tid; e < nc * 32; e += NT) {
+        const LayerPlan& L = Wpl[e >> 5];
+        const int ii = min(max(ib + (e & 31), 0), P.res - 1);
+        const int ci = fdiv(ii, L.inv_f);
+        const float g1 = L.gain * ((float)(ii - ci * L.f) * L.inv_f);
+        const int d1 = min(ci + 1, L.ncx - 1) - ci;
+        Wrowp[e] = make_int2(L.tc_off >= 0 ? (L.tc_off + (ci - L.cr0) * TCP) | (d1 << 16) : -1, __float_as_int(g1));
     }
-    cp_async_wait_all();
-    __syncthreads();
-    TRACE(2);
-    // f == 1 sum to shared memory; the coarse pass below picks it up transposed
+    // f == 1 layers straight into the haloed heights (lane = haloed column, coalesced rows)
     {
+        const int c = lane;
+        const int j = min(max(jb + c, 0), P.ny - 1);
+        const int qb = RPW * wid;                  // first haloed row of this warp
+        float acc[RPW];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) acc[k] = 0.f;
+        for (int b = nb - n1; b < nb; ++b) {
+            const LayerPlan& L = Wpl[b];
+            const float* Sg = SL + L.sm_off;
+            float u[RPW];
+#pragma unroll
+            for (int k = 0; k < RPW; ++k) u[k] = Sg[min(max(ib + qb + k, 0), P.res - 1) * L.ncy + j];
+#pragma unroll
+            for (int k = 0; k < RPW; ++k) acc[k] = fmaf(L.gain, u[k], acc[k]);
+        }
         const int jr = jb + c;
         const bool jok = jr >= 0 && jr < P.ny;
 #pragma unroll
@@ -261,43 +325,46 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
             W.hs[qb + k][c] = (jok && ii >= 0 && ii < P.res) ? acc[k] : 0.f;
         }
     }
-    // tc[b][r][c] = coarse row r of layer b lerped at haloed column c (x-first bilinear, :270-273)
-    for (int b = 0; b < nl; ++b) {
-        const LayerPlan& L = Wpl[b];
-        if (L.tc_off < 0) continue;
-        const int jj = min(max(jb + (tid & 31), 0), P.ny - 1);
-        const int cj = fdiv(jj, L.inv_f);
-        const int d1 = min(cj + 1, L.ncy - 1) - cj;
-        const float wj = (float)(jj - cj * L.f) * L.inv_f;
-        const float* src = W.cs + L.cs_off + (cj - L.cc0);
-        for (int r = tid >> 5; r < L.nr; r += NW)
-            W.u2.tc[L.tc_off + r * TCP + (tid & 31)] = lerpf(src[r * L.ncol], src[r * L.ncol + d1], wj);
+    cp_async_wait_all();                           // this warp's rows (and the background footprint)
+    __syncwarp();
+    for (int g = wid; g < nrows; g += NW) {
+        const RowEnt e = Wrow[g];
+        unsigned pk;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pk) : "r"((e.cola & 0xffffffu) + lane4));
+        float x0, x1;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x0) : "r"(e.tca + (pk & 0xffu)));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x1) : "r"(e.tca + ((pk >> 8) & 0xffu)));
+        __syncwarp();
+        const float v = lerpf(x0, x1, (float)(pk >> 16) * e.inv_f);
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(e.tca + lane4), "f"(v) : "memory");
     }
     __syncthreads();
     TRACE(3);
-    // ---- coarse layers: thread = haloed row q, columns c0 .. c0+7; per layer the
-    // row weights are formed once and each texel costs two table reads ----
+    // ---- coarse layers: thread = haloed row q, columns c0 .. c0+7; per layer
+    // two float4 pairs of table reads and 16 FMAs ----
     {
         const int q = lane, c0 = CPT * wid;
-        const int ii = min(max(ib + q, 0), P.res - 1);
+        const unsigned tcs = (unsigned)__cvta_generic_to_shared(W.u2.tc) + 4u * (unsigned)c0;
         float h[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) h[k] = W.hs[q][c0 + k];
-        for (int b = 0; b < nl; ++b) {
-            const LayerPlan& L = Wpl[b];
-            if (L.f == 1) continue;
-            const int ci = fdiv(ii, L.inv_f);
-            const float g1 = L.gain * ((float)(ii - ci * L.f) * L.inv_f);
-            const float g0 = L.gain - g1;
-            const int ci1 = min(ci + 1, L.ncx - 1);
-            if (L.tc_off >= 0) {
-                const float* T0 = W.u2.tc + L.tc_off + (ci - L.cr0) * TCP + c0;
-                const float* T1 = W.u2.tc + L.tc_off + (ci1 - L.cr0) * TCP + c0;
+        for (int b = 0; b < nc; ++b) {
+            const int2 rp = Wrowp[b * 32 + q];
+            const float gain = Wpl[b].gain;
+            const float g1 = __int_as_float(rp.y), g0 = gain - g1;
+            if (rp.x >= 0) {
+                const unsigned s0 = tcs + 4u * (unsigned)(rp.x & 0xffff), s1 = s0 + (unsigned)(4 * TCP) * (unsigned)(rp.x >> 16);
+                const float4 a0 = lds128(s0), a1 = lds128(s0 + 16u), b0 = lds128(s1), b1 = lds128(s1 + 16u);
+                const float t0[CPT] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float t1[CPT] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-                for (int k = 0; k < CPT; ++k) h[k] = fmaf(g0, T0[k], fmaf(g1, T1[k], h[k]));
+                for (int k = 0; k < CPT; ++k) h[k] = fmaf(g0, t0[k], fmaf(g1, t1[k], h[k]));
             } else {                               // layer not tabulated: rows from global (rare)
-                const float* R0 = a.smooth_layers + L.sm_off + (long long)ci * L.ncy;
-                const float* R1 = a.smooth_layers + L.sm_off + (long long)ci1 * L.ncy;
+                const LayerPlan& L = Wpl[b];
+                const int ii = min(max(ib + q, 0), P.res - 1);
+                const int ci = fdiv(ii, L.inv_f), ci1 = min(ci + 1, L.ncx - 1);
+                const float* R0 = SL + L.sm_off + (long long)ci * L.ncy;
+                const float* R1 = SL + L.sm_off + (long long)ci1 * L.ncy;
 #pragma unroll
                 for (int k = 0; k < CPT; ++k) {
                     const int jj = min(max(jb + c0 + k, 0), P.ny - 1);
