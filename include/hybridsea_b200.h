@@ -179,6 +179,7 @@ typedef struct {
     int fixed_point;          /* 1: deterministic mode (HS_FIXED_*): float sums go through
                                  int64 fixed point, see hs_fixed_to_float */
 } HsFftArgs;
+/* height, dx, dy, work_a and work_b must be 16-byte aligned (rows move as float4). */
 HS_API int hs_fft_evolve(const HsFftArgs* a, void* stream);
 
 /* ------------------------------------------------------------------------ */

@@ -376,9 +376,20 @@ __global__ void HS_FFT_COLS_LB(N, CT) fft_cols_reg_kernel(FftDev d, ColOut o, in
     double acc = 0.0;
     if (is_a) {
         const int j0 = blockIdx.x * CT;
-        for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
-            const int i = e / CT, c = e - i * CT;
-            cp_async8(buf + c * NP + fpad(i), d.wa + (size_t)i * N + j0 + c, true);
+        if constexpr (CT % 2 == 0) {
+            // two adjacent columns per 16-byte load, scattered to their transforms
+            for (int e = threadIdx.x; e < N * (CT / 2); e += blockDim.x) {
+                const int i = e / (CT / 2), c = 2 * (e - i * (CT / 2));
+                const float4 w = __ldg(reinterpret_cast<const float4*>(d.wa + (size_t)i * N + j0 + c));
+                const int pi = fpad(i);
+                buf[c * NP + pi] = make_float2(w.x, w.y);
+                buf[(c + 1) * NP + pi] = make_float2(w.z, w.w);
+            }
+        } else {
+            for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
+                const int i = e / CT, c = e - i * CT;
+                cp_async8(buf + c * NP + fpad(i), d.wa + (size_t)i * N + j0 + c, true);
+            }
         }
     } else if (d.chop_on) {
         const int j0 = (blockIdx.x - n_a_tiles) * (2 * CT);
@@ -386,8 +397,9 @@ __global__ void HS_FFT_COLS_LB(N, CT) fft_cols_reg_kernel(FftDev d, ColOut o, in
         for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
             const int i = e / CT, q = e - i * CT;
             const int src = i <= half ? i : N - i;
-            float2 y1 = d.wb[(size_t)src * N + j0 + 2 * q];
-            float2 y2 = d.wb[(size_t)src * N + j0 + 2 * q + 1];
+            const float4 w = __ldg(reinterpret_cast<const float4*>(d.wb + (size_t)src * N + j0 + 2 * q));
+            float2 y1 = make_float2(w.x, w.y);
+            float2 y2 = make_float2(w.z, w.w);
             if (i == 0 || i == half) { y1.y = 0.f; y2.y = 0.f; }      // rows 0, n/2 are real
             else if (i > half) { y1.y = -y1.y; y2.y = -y2.y; }        // Y[-i] = conj(Y[i])
             buf[q * NP + fpad(i)] = make_float2(y1.x - y2.y, y1.y + y2.x);
@@ -407,20 +419,48 @@ __global__ void HS_FFT_COLS_LB(N, CT) fft_cols_reg_kernel(FftDev d, ColOut o, in
     fft_inplace<N>(buf + (f < CT ? f : 0) * NP, tw, tt, f < CT);
     if (is_a) {
         const int j0 = blockIdx.x * CT;
-        for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
-            const int i = e / CT, c = e - i * CT;
-            const float2 v = buf[c * NP + fpad(out_pos<N>(i))];
-            const size_t oi = (size_t)i * N + j0 + c;
-            o.h[oi] = v.x;
-            o.dx[oi] = d.chop_on ? v.y : 0.f;
-            acc += (double)v.x * (double)v.x;
+        if constexpr (CT % 4 == 0) {
+            // one output row position per 4 columns: 16-byte height and dx stores
+            for (int e = threadIdx.x; e < N * (CT / 4); e += blockDim.x) {
+                const int i = e / (CT / 4), c = 4 * (e - i * (CT / 4));
+                const int pos = fpad(out_pos<N>(i));
+                const float2 v0 = buf[c * NP + pos], v1 = buf[(c + 1) * NP + pos];
+                const float2 v2 = buf[(c + 2) * NP + pos], v3 = buf[(c + 3) * NP + pos];
+                const size_t oi = (size_t)i * N + j0 + c;
+                *reinterpret_cast<float4*>(o.h + oi) = make_float4(v0.x, v1.x, v2.x, v3.x);
+                *reinterpret_cast<float4*>(o.dx + oi) =
+                    d.chop_on ? make_float4(v0.y, v1.y, v2.y, v3.y) : make_float4(0.f, 0.f, 0.f, 0.f);
+                acc += (double)v0.x * (double)v0.x;
+                acc += (double)v1.x * (double)v1.x;
+                acc += (double)v2.x * (double)v2.x;
+                acc += (double)v3.x * (double)v3.x;
+            }
+        } else {
+            for (int e = threadIdx.x; e < N * CT; e += blockDim.x) {
+                const int i = e / CT, c = e - i * CT;
+                const float2 v = buf[c * NP + fpad(out_pos<N>(i))];
+                const size_t oi = (size_t)i * N + j0 + c;
+                o.h[oi] = v.x;
+                o.dx[oi] = d.chop_on ? v.y : 0.f;
+                acc += (double)v.x * (double)v.x;
+            }
         }
     } else {
         const int j0 = (blockIdx.x - n_a_tiles) * (2 * CT);
-        for (int e = threadIdx.x; e < N * 2 * CT; e += blockDim.x) {
-            const int i = e / (2 * CT), c = e - i * (2 * CT);
-            const float2 v = buf[(c >> 1) * NP + fpad(out_pos<N>(i))];
-            o.dy[(size_t)i * N + j0 + c] = (c & 1) ? v.y : v.x;
+        if constexpr (CT % 2 == 0) {
+            // two transforms (four dy columns) per 16-byte store
+            for (int e = threadIdx.x; e < N * (CT / 2); e += blockDim.x) {
+                const int i = e / (CT / 2), q = 2 * (e - i * (CT / 2));
+                const int pos = fpad(out_pos<N>(i));
+                const float2 v0 = buf[q * NP + pos], v1 = buf[(q + 1) * NP + pos];
+                *reinterpret_cast<float4*>(o.dy + (size_t)i * N + j0 + 2 * q) = make_float4(v0.x, v0.y, v1.x, v1.y);
+            }
+        } else {
+            for (int e = threadIdx.x; e < N * 2 * CT; e += blockDim.x) {
+                const int i = e / (2 * CT), c = e - i * (2 * CT);
+                const float2 v = buf[(c >> 1) * NP + fpad(out_pos<N>(i))];
+                o.dy[(size_t)i * N + j0 + c] = (c & 1) ? v.y : v.x;
+            }
         }
     }
     if (o.sumsq) {
@@ -526,6 +566,8 @@ extern "C" int hs_fft_evolve(const HsFftArgs* a, void* stream) {
     const int chop_on = a->choppiness != 0.0;
     HS_CHECK_ARG(!chop_on || a->work_b, "hs_fft_evolve: work_b required when choppiness != 0");
     HS_CHECK_ARG(!a->emit_normals || a->normal, "hs_fft_evolve: normal buffer required");
+    HS_CHECK_ARG((((uintptr_t)a->height | (uintptr_t)a->dx | (uintptr_t)a->dy | (uintptr_t)a->work_a |
+                   (uintptr_t)a->work_b) & 15u) == 0, "hs_fft_evolve: field and work buffers must be 16-byte aligned");
     cudaStream_t st = as_stream(stream);
     FftDev d;
     d.n = n;
