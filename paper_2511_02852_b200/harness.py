@@ -335,7 +335,15 @@ class Simulation:
                 raise ConfigError(f"patch grids hold {n_grid} texels; at most {(2 ** 31 - 1) // 3} per GPU")
             self.patch_h = f32(n_grid)
             self.patch_n = f32(3 * n_grid)
-            self.blend_h = f32(n_grid)
+            # blended heights per length parity (which flips every frame): frame
+            # f writes one buffer while the other still holds frame f - 1, so a
+            # host copy of a finished frame (HostFramePipe) reads it in place;
+            # `blend_h` is the latest frame's
+            self._blend_h2 = (f32(n_grid), f32(n_grid))
+            self.blend_h = self._blend_h2[0]
+            # the live counts as of each frame's end, per length parity likewise
+            # (copied beside the raw-layer clear, off the critical path)
+            self._live_snap2 = (torch.zeros_like(self.live), torch.zeros_like(self.live))
             self.blend_n = f32(3 * n_grid)
             # per-frame accumulators in one block of 4-byte words per frame parity:
             # frame f accumulates into set f & 1 while its hs_inject zeroes the other
@@ -605,6 +613,7 @@ class Simulation:
             clr = self._side_stream("clear")
             clr.wait_stream(main)
             with torch.cuda.stream(clr):        # raw layers are consumed: clear them for the next splat
+                self._live_snap2[lp].copy_(self.live)
                 raw = self.raw_fixed if self.det else self.synth.raw
                 N.call_raw("hs_clear", N.vp(N.ptr(raw)), N.i64(raw.numel() * raw.element_size()), N.vp(stream_ptr()))
             if fork:
@@ -620,7 +629,7 @@ class Simulation:
                 bg_n=self.config.fft_n if bg is not None else 0,
                 bg_spacing=self.config.fft_domain / self.config.fft_n if bg is not None else 1.0,
                 patch_height=N.ptr(self.patch_h), patch_normal=0,
-                blend_height=N.ptr(self.blend_h), blend_normal=N.ptr(self.blend_n), blend_mode=1,
+                blend_height=N.ptr(self._blend_h2[state[1]]), blend_normal=N.ptr(self.blend_n), blend_mode=1,
                 interior_sumsq=N.ptr(stats[1]), interior_count=N.ptr(stats[2]),
                 frame_advance=N.ptr(self.frame_dev), fixed_point=int(self.det),
                 composite=N.ptr(self.composite_frame) if frame_composite else 0, **self._extra_bg()), stream_ptr())
@@ -653,9 +662,11 @@ class Simulation:
         return (self._buf, self._lp, self._since == self.compact_period - 1)
 
     def _advance_state(self, state: tuple) -> None:
+        """After the frame of `state` ran (never during a capture)."""
         if not self.n_patches:
             return
         buf, lp, compact = state
+        self.blend_h = self._blend_h2[lp]
         self._lp = lp ^ 1
         if compact:
             self._buf = buf ^ 1
@@ -1008,24 +1019,25 @@ class Simulation:
 
 class HostFramePipe:
     """Streams every frame's blended patch tiles and live counts to pinned host
-    memory while the next frame computes: at the end of each frame a
-    device-side snapshot (D2D, on the frame's stream) frees the live buffers,
-    and a copy stream moves the snapshot to the host, `depth`-buffered.  A
-    frame waits only for the host copy of frame k - depth (long finished), so
+    memory while the next frame computes.  Both are copied straight from the
+    frame's own buffers (blended heights and a live-count snapshot, one of
+    each per length parity, so frame k + 1 writes the other ones): no device
+    copy sits between frames.  A frame waits only for the host copy that last
+    read its buffers (frame k - 2) and for the host slot it reuses, so
     end-to-end throughput is max(frame time, transfer time) instead of their
-    sum.  `step()` returns the slot whose host buffers `result(slot)` fills."""
+    sum.  `step()` returns the slot whose host buffers
+    `result(slot)` fills."""
 
     def __init__(self, sim: "Simulation", depth: int = 2):
         self.sim = sim
         self.depth = depth
         self.n = int(sim.synth.grid_base[-1])
         dev = sim.device
-        self.stage = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(depth)]
-        self.stage_cnt = [torch.empty_like(sim.live) for _ in range(depth)]
         self.host = [torch.empty(self.n, dtype=torch.float32, pin_memory=True) for _ in range(depth)]
         self.host_cnt = [torch.empty(sim.live.numel(), dtype=torch.int32, pin_memory=True) for _ in range(depth)]
         self.copy = torch.cuda.Stream(device=dev)
         self.done = [torch.cuda.Event() for _ in range(depth)]
+        self.buf_read = [torch.cuda.Event(), torch.cuda.Event()]     # last host copy out of parity p's buffers
         self.k = 0
 
     @property
@@ -1034,17 +1046,19 @@ class HostFramePipe:
 
     def step(self, dt: float | None = None) -> int:
         i = self.k % self.depth
-        main = torch.cuda.current_stream(self.sim.device)
+        sim = self.sim
+        main = torch.cuda.current_stream(sim.device)
+        lp = sim._state()[1]                      # the blend buffer this frame writes
         main.wait_event(self.done[i])            # slot i's previous host copy has landed
-        self.sim.step(dt, stats=False)
-        self.stage[i].copy_(self.sim.blend_h[: self.n])
-        self.stage_cnt[i].copy_(self.sim.live)
+        main.wait_event(self.buf_read[lp])       # and so has the last copy out of parity lp's buffers
+        sim.step(dt, stats=False)
         ready = torch.cuda.Event()
         ready.record(main)
         with torch.cuda.stream(self.copy):
             self.copy.wait_event(ready)
-            self.host[i].copy_(self.stage[i], non_blocking=True)
-            self.host_cnt[i].copy_(self.stage_cnt[i], non_blocking=True)
+            self.host[i].copy_(sim.blend_h[: self.n], non_blocking=True)
+            self.host_cnt[i].copy_(sim._live_snap2[lp], non_blocking=True)
+            self.buf_read[lp].record(self.copy)
             self.done[i].record(self.copy)
         self.k += 1
         return i
