@@ -251,16 +251,19 @@ __global__ void normals_periodic_kernel(const float* __restrict__ h, float* __re
 // (fft_reg.cuh).  Same data flow as the radix-2/4 kernels above.
 // om_row: this CTA's row |i| of the host omega table staged in shared memory
 // (or NULL: formed from kf); kxi, kxip = kf[i], kf[ip]; dk = kf[1]
-__device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0, const float2* r1, int i, int ip,
-                                              int j, double t, const double* om_row, double kxi, double kxip,
-                                              double dk, float2& A0, float2& A1, float2& B0) {
+// The dispersion w depends on |j| only, so columns j and -j share the phase
+// and its sincos: one call forms both (jm = -j mod n; j == jm writes once).
+// Every output is the same arithmetic as a per-column formation.
+__device__ __forceinline__ void spectrum_cols(const FftDev& d, const float2* r0, const float2* r1, int i, int j,
+                                              double t, const double* om_row, double kxi, double kxip, double dk,
+                                              float2* A0, float2* A1, float2* B0) {
     const int n = d.n, half = n >> 1;
     const int jm = (n - j) & (n - 1);
-    const double kyj = dk * (double)(j <= half ? j : j - n);     // the chop factors use it in fp32
     double w;
     if (om_row) {    // host table, numpy's sqrt(g hypot(kx, ky)) (fft_background.py:40-47)
         w = om_row[j <= half ? j : n - j];
     } else {
+        const double kyj = dk * (double)(j <= half ? j : j - n);
         w = sqrt(d.g * sqrt(fma(kxi, kxi, kyj * kyj)));
     }
     const double two_pi = 6.283185307179586476925286766559;
@@ -269,24 +272,36 @@ __device__ __forceinline__ void spectrum_pair(const FftDev& d, const float2* r0,
     float s, c;
     __sincosf((float)ph, &s, &c);                   // |err| < 4e-7 on [-pi, pi]
     const float2 rot = make_float2(c, -s), rotc = make_float2(c, s);
-    const float2 hh0 = cadd(cmul(r0[j], rot), cmul(cconj(r1[jm]), rotc));
-    const float2 hh1 = cadd(cmul(r1[j], rot), cmul(cconj(r0[jm]), rotc));
-    const bool sc = ((i == 0) || (i == half)) && (j == 0 || j == half);   // self-conjugate bin
-    if (d.chop_on) {
-        // lambda k / |k| only scales fp32 values: fp32 reciprocal
-        const float wf = (float)w;
-        const float kinv = wf > 0.f ? (float)d.g / (wf * wf) : 1.f;    // 1/|k| = g / w^2
-        const float ch = (float)d.chop;
-        const float fa = sc ? 1.f : 1.f + ch * (float)kxi * kinv;
-        A0 = make_float2(hh0.x * fa, hh0.y * fa);
-        const float fb = sc ? 0.f : ch * (float)kyj * kinv;
-        B0 = make_float2(fb * hh0.y, -fb * hh0.x);
-        const float fa1 = 1.f + ch * (float)kxip * kinv;
-        A1 = make_float2(hh1.x * fa1, hh1.y * fa1);
-    } else {
-        A0 = hh0;
-        A1 = hh1;
-        B0 = make_float2(0.f, 0.f);
+    // lambda k / |k| only scales fp32 values: fp32 reciprocal
+    const float wf = (float)w;
+    const float kinv = wf > 0.f ? (float)d.g / (wf * wf) : 1.f;    // 1/|k| = g / w^2
+    const float ch = (float)d.chop;
+    const float2 a0 = r0[j], a1 = r1[j], m0 = r0[jm], m1 = r1[jm];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int jj = q ? jm : j;
+        if (q && jm == j) break;
+        const double kyj = dk * (double)(jj <= half ? jj : jj - n);     // the chop factors use it in fp32
+        const float2 hh0 = q ? cadd(cmul(m0, rot), cmul(cconj(a1), rotc)) : cadd(cmul(a0, rot), cmul(cconj(m1), rotc));
+        const float2 hh1 = q ? cadd(cmul(m1, rot), cmul(cconj(a0), rotc)) : cadd(cmul(a1, rot), cmul(cconj(m0), rotc));
+        const bool sc = ((i == 0) || (i == half)) && (jj == 0 || jj == half);   // self-conjugate bin
+        float2 x0, x1, y0;
+        if (d.chop_on) {
+            const float fa = sc ? 1.f : 1.f + ch * (float)kxi * kinv;
+            x0 = make_float2(hh0.x * fa, hh0.y * fa);
+            const float fb = sc ? 0.f : ch * (float)kyj * kinv;
+            y0 = make_float2(fb * hh0.y, -fb * hh0.x);
+            const float fa1 = 1.f + ch * (float)kxip * kinv;
+            x1 = make_float2(hh1.x * fa1, hh1.y * fa1);
+        } else {
+            x0 = hh0;
+            x1 = hh1;
+            y0 = make_float2(0.f, 0.f);
+        }
+        const int o = fpad(jj);
+        A0[o] = x0;
+        A1[o] = x1;
+        B0[o] = y0;
     }
 }
 
@@ -339,13 +354,8 @@ __global__ void HS_FFT_ROWS_LB(N) fft_rows_reg_kernel(FftDev d) {
     cp_async_wait_all();
     __syncthreads();
     FTRACE(1);
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        float2 A0, A1, B0;
-        spectrum_pair(d, r0, r1, i, ip, j, t, d.omega ? om : nullptr, kxi, kxip, dk, A0, A1, B0);
-        buf[fpad(j)] = A0;
-        buf[NP + fpad(j)] = A1;
-        buf[2 * NP + fpad(j)] = B0;
-    }
+    for (int j = threadIdx.x; j <= N / 2; j += blockDim.x)
+        spectrum_cols(d, r0, r1, i, j, t, d.omega ? om : nullptr, kxi, kxip, dk, buf, buf + NP, buf + 2 * NP);
     __syncthreads();
     FTRACE(2);
     const int f = threadIdx.x / T, tt = threadIdx.x - f * T;
