@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
     }
     cp_async_wait_all();                           // this warp's rows (and the background footprint)
     __syncwarp();
+    TRACE(2);
     for (int g = wid; g < nrows; g += NW) {
         const RowEnt e = Wrow[g];
         unsigned pk;
@@ -562,6 +563,7 @@ __global__ void __launch_bounds__(NT, HS_COMPOSE_MINB) compose_kernel(HsComposeA
             if (a.blend_normal) { a.blend_normal[3 * o] = nx; a.blend_normal[3 * o + 1] = ny; a.blend_normal[3 * o + 2] = nz; }
         }
     }
+    TRACE(7);
     // FFT-resolution composite (stitched_heights, harness.py:219-241): the
     // composite nodes whose patch-grid row/column falls in this tile, strictly
     // inside the patch, get w h_patch + (1 - w) h_bg (the patch step of

@@ -19,21 +19,26 @@ torch.cuda.synchronize()
 buf = np.zeros(4096 * 8, np.uint64)
 N.lib().hs_debug_trace(C.c_void_p(buf.ctypes.data))
 n = sim.synth.compose_tiles
-t = buf.reshape(4096, 8)[:n, :7].astype(np.float64)
+t8 = buf.reshape(4096, 8)[:n, :8].astype(np.float64)
+t = t8[:, :7]
 t0 = t[:, 0].min()
 t = (t - t0) / 1000.0
-names = ["start", "plans", "loads", "hs+tc", "coarse", "bgprep", "epilogue"]
+t7 = (t8[:, 7] - t0) / 1000.0          # after the texel loops, before the composite nodes
+names = ["start", "plans", "stage+f1", "tc", "coarse", "bgprep", "epilogue"]
 print("tiles", n, "kernel span us", t[:, 6].max())
 print("start times: min %.2f p50 %.2f max %.2f" % (t[:, 0].min(), np.median(t[:, 0]), t[:, 0].max()))
 for k in range(1, 7):
     d = t[:, k] - t[:, k - 1]
     print(f"{names[k]:9s} p10 {np.percentile(d,10):6.2f} p50 {np.median(d):6.2f} p90 {np.percentile(d,90):6.2f} max {d.max():6.2f}")
+for lbl, d in (("texels", t7 - t[:, 5]), ("composite", t[:, 6] - t7)):
+    print(f"  {lbl:9s} p10 {np.percentile(d,10):6.2f} p50 {np.median(d):6.2f} p90 {np.percentile(d,90):6.2f} max {d.max():6.2f}")
 print("end times: p10 %.2f p50 %.2f max %.2f" % (np.percentile(t[:, 6], 10), np.median(t[:, 6]), t[:, 6].max()))
 info = sim.synth.compose_info.cpu().numpy().reshape(-1, 3)[:n]
 res = cfg.patches[0].res
 band = 40   # margin / texel
 edge = (info[:, 1] < band) | (info[:, 2] < band) | (info[:, 1] + 30 > res - band) | (info[:, 2] + 30 > res - band)
-print("band tiles", edge.sum(), "end p50 %.2f max %.2f" % (np.median(t[edge, 6]), t[edge, 6].max()))
+print("band tiles", edge.sum(), "end p50 %.2f max %.2f" % (np.median(t[edge, 6]), t[edge, 6].max()),
+      "texels p50 %.2f composite p50 %.2f" % (np.median((t7 - t[:, 5])[edge]), np.median((t[:, 6] - t7)[edge])))
 print("interior tiles", (~edge).sum(), "end p50 %.2f max %.2f" % (np.median(t[~edge, 6]), t[~edge, 6].max()))
 slow = np.argsort(-t[:, 6])[:12]
 for k in slow:
