@@ -338,12 +338,17 @@ __global__ void HS_FFT_ROWS_LB(N) fft_rows_reg_kernel(FftDev d) {
     const int i = blockIdx.x, ip = (N - i) & (N - 1);
     const bool self = (i == ip);
     if (d.sumsq_zero && i == 0 && threadIdx.x == 0) *d.sumsq_zero = 0.0;
-    // every input of the row pair in one cp.async batch: twiddles, h0 rows i and
-    // -i, the dispersion row; the frame counter and wavenumbers load meanwhile
-    for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
-        cp_async16(tw + 2 * k, d.tw + 2 * k);
-        cp_async16(r0 + 2 * k, d.h0 + (size_t)i * N + 2 * k);
-        cp_async16(r1 + 2 * k, d.h0 + (size_t)ip * N + 2 * k);
+    // every input of the row pair at once: twiddles and h0 rows i and -i as three
+    // bulk copies (one thread, completion on an mbarrier), the dispersion row by
+    // cp.async (its rows are only 8-byte aligned); the frame counter and
+    // wavenumbers load meanwhile
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, 3u * N * (unsigned)sizeof(float2));
+        bulk_g2s(tw, d.tw, N * sizeof(float2), &bar);
+        bulk_g2s(r0, d.h0 + (size_t)i * N, N * sizeof(float2), &bar);
+        bulk_g2s(r1, d.h0 + (size_t)ip * N, N * sizeof(float2), &bar);
     }
     if (d.omega) {
         const double* orow = d.omega + (size_t)(i <= N / 2 ? i : N - i) * (N / 2 + 1);
@@ -352,7 +357,8 @@ __global__ void HS_FFT_ROWS_LB(N) fft_rows_reg_kernel(FftDev d) {
     const double t = d.frame_ptr ? dmul((double)(*d.frame_ptr), d.dt) : d.t;   // t = frame * dt
     const double kxi = __ldg(d.kf + i), kxip = __ldg(d.kf + ip), dk = __ldg(d.kf + 1);
     cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();                                // (also publishes the barrier's init)
+    mbar_wait(&bar, 0);
     FTRACE(1);
     for (int j = threadIdx.x; j <= N / 2; j += blockDim.x)
         spectrum_cols(d, r0, r1, i, j, t, d.omega ? om : nullptr, kxi, kxip, dk, buf, buf + NP, buf + 2 * NP);
