@@ -387,7 +387,12 @@ __global__ void HS_FFT_COLS_LB(N, CT) fft_cols_reg_kernel(FftDev d, ColOut o, in
     float2* tw = sm;
     float2* buf = tw + N;       // CT transforms of NP
     if (o.frame_advance && blockIdx.x == 0 && threadIdx.x == 0) *o.frame_advance += 1;
-    for (int k = threadIdx.x; k < N / 2; k += blockDim.x) cp_async16(tw + 2 * k, d.tw + 2 * k);
+    __shared__ __align__(8) unsigned long long bar;  // the twiddles: one bulk copy
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, N * (unsigned)sizeof(float2));
+        bulk_g2s(tw, d.tw, N * sizeof(float2), &bar);
+    }
     const bool is_a = (int)blockIdx.x < n_a_tiles;
     double acc = 0.0;
     if (is_a) {
@@ -422,7 +427,8 @@ __global__ void HS_FFT_COLS_LB(N, CT) fft_cols_reg_kernel(FftDev d, ColOut o, in
         }
     }
     cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();                                // (also publishes the barrier's init)
+    mbar_wait(&bar, 0);                             // before any exit: the copy targets this CTA's smem
     if (!is_a && !d.chop_on) {
         const int j0 = (blockIdx.x - n_a_tiles) * (2 * CT);
         for (int e = threadIdx.x; e < N * 2 * CT; e += blockDim.x) {
